@@ -1,0 +1,179 @@
+/*
+ * pa.h -- C ABI of the B200-native MMH-MH privacy-amplification hash
+ *         (hybrid multilinear-modular hashing + modular arithmetic hashing,
+ *          arXiv 2105.13678, Algorithm 1).
+ *
+ * What a context computes (readings A1-A13 are listed in DESIGN.md):
+ *   key bits kappa_0..kappa_{n-1}, MSB-first within each byte
+ *       (reading A4), bits >= n ignored;
+ *   k = ceil(n/r) blocks x_i = big-endian integer of key bits [i r, (i+1) r),
+ *       the last block zero-padded at its end (reading A3);
+ *   p = 2^gamma - 1, a Mersenne prime with gamma > r (reading A2);
+ *   y = sum_i a_i x_i mod p                       (MMH, Eq. 2),
+ *       canonical in [0, p-1] (reading A6);
+ *   z = ((b y + c) mod 2^alpha) >> (alpha - m),  alpha = max(gamma, m)
+ *                                                 (MH, Eq. 4, PAPER.md:99-101;
+ *                                                  readings A1, A8);
+ *   out = z, MSB-first in ceil(m/8) bytes, pad bits 0 (reading A5).
+ * The hash keys a_i in [0, p-1], b odd < 2^alpha, c < 2^alpha are drawn from a
+ * 64-bit seed with Philox4x64-10 (reading A7), or
+ * supplied explicitly through pa_ctx_create_ex.
+ *
+ * Error behaviour: every int-returning call returns PA_OK (0) or a negative
+ * PA_E_* code; pa_ctx_create returns NULL on failure.  The code and a message of
+ * the last failure on the calling thread are available from pa_last_error().
+ * No call aborts the process.  CUDA failures are reported as PA_E_CUDA.
+ *
+ * Threading / streams: a context is not re-entrant (one pa_hash at a time);
+ * distinct contexts are independent.  All device work of a
+ * context is enqueued on its stream (pa_params.stream, default: the legacy
+ * default stream); pa_hash / pa_mmh_partial / pa_mh_merge are asynchronous
+ * with respect to the host, pa_hash_host is synchronous.
+ *
+ * Ownership: the context owns its precomputed transforms and scratch (device
+ * memory allocated with cudaMalloc on the device current at creation); the
+ * caller owns every key / output buffer passed in.
+ */
+#ifndef PA_H_
+#define PA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PA_OK                    0
+#define PA_E_PARAM              -1   /* invalid parameter */
+#define PA_E_INSUFFICIENT_INPUT -2   /* reserved for reload mode */
+#define PA_E_BOUND              -3   /* no transform plan covers the coefficient bound */
+#define PA_E_NOMEM              -4   /* device or host allocation failed */
+#define PA_E_CUDA               -5   /* a CUDA runtime call or kernel failed */
+#define PA_E_STATE              -6   /* call not valid for this context (e.g. shard) */
+
+typedef struct pa_ctx pa_ctx;
+
+/* Transform plan of one big-integer product stage (MMH or MH).  The product
+ * is computed exactly as a cyclic convolution of B-bit limbs, modulo each of
+ * `nprimes` 30-bit NTT primes, recombined by CRT: `bound_log2` is log2 of the
+ * largest possible convolution coefficient, `modulus_log2` of the prime
+ * product (bound_log2 < modulus_log2 always holds for an accepted plan). */
+typedef struct {
+    uint32_t limb_bits;      /* B */
+    uint32_t nprimes;        /* P */
+    uint32_t log2_len;       /* L = 2^log2_len */
+    uint32_t n_col;          /* column (first) pass length N2 */
+    uint32_t n_row;          /* row (second) pass length N1; L = N1 * N2 */
+    uint32_t primes[8];
+    double   bound_log2;
+    double   modulus_log2;
+} pa_stage_plan;
+
+typedef struct {
+    uint64_t n, r, m;
+    uint64_t gamma;          /* Mersenne exponent, p = 2^gamma - 1 */
+    uint64_t alpha;          /* MH modulus width, max(gamma, m) */
+    uint64_t k;              /* total number of blocks ceil(n/r) */
+    uint64_t block_begin;    /* this context's shard [block_begin, block_end) */
+    uint64_t block_end;
+    pa_stage_plan mmh;
+    pa_stage_plan mh;
+    uint64_t device_bytes;   /* device memory held by the context */
+    uint32_t kernels_per_hash; /* kernel launches enqueued by one pa_hash */
+    uint32_t reserved;
+} pa_info;
+
+typedef struct {
+    uint64_t n;              /* key bits, >= 1 */
+    uint64_t r;              /* block bits, >= 16 and a multiple of 16 */
+    uint64_t m;              /* output bits, >= 1 */
+    uint64_t gamma;          /* Mersenne exponent (gamma > r), 0 = smallest table entry > r */
+    uint64_t seed;           /* hash-key seed (ignored for keys given explicitly) */
+    uint64_t block_begin;    /* shard: blocks [block_begin, block_end); both 0 = all */
+    uint64_t block_end;
+    /* Optional explicit hash keys (host pointers, little-endian 32-bit words).
+     * a_words: (block_end-block_begin) * ceil(gamma/32) words, a_i < p each;
+     * b_words, c_words: ceil(alpha/32) words each, b odd, both < 2^alpha.
+     * NULL = expand from `seed` (reading A7). */
+    const uint32_t *a_words;
+    const uint32_t *b_words;
+    const uint32_t *c_words;
+    void *stream;            /* cudaStream_t, NULL = legacy default stream */
+    int32_t limb_bits;       /* 0 = planner's choice, else force B (multiple of 8, 16..64) */
+    int32_t strict;          /* nonzero: reject m >= gamma ("gamma > beta") */
+} pa_params;
+
+/* Create a context on the current CUDA device.  `p` is the Mersenne EXPONENT
+ * gamma (p = 2^gamma - 1), or 0 for the smallest known exponent > r (reading A2).
+ * Validates n >= 1; r >= 16, r % 16 == 0; gamma in the SPEC.md:33 table, gamma > r;
+ * m >= 1.  Expands a_i, b, c from `seed`, precomputes the transforms of a_i and b
+ * in device memory.  Returns NULL on failure (see pa_last_error). */
+pa_ctx *pa_ctx_create(uint64_t n, uint64_t r, uint64_t m, uint64_t p, uint64_t seed);
+
+/* Same with every option; *out = context.  Returns PA_OK or PA_E_*. */
+int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out);
+
+/* Hash one key.  key_bits: DEVICE pointer to ceil(n/8) bytes (bits >= n ignored).
+ * For a shard context it points to the shard's slice: key bytes
+ * [block_begin*r/8, min(block_end*r/8, ceil(n/8))) -- and pa_hash then fails with
+ * PA_E_STATE: shards use pa_mmh_partial + pa_mh_merge.
+ * out_bits: DEVICE pointer to ceil(m/8) bytes (written MSB-first, pad bits 0).
+ * Asynchronous on the context stream. */
+int pa_hash(pa_ctx *ctx, const uint8_t *key_bits, uint8_t *out_bits);
+
+/* End-to-end variant with HOST buffers: copies the key host->device, hashes,
+ * copies the output device->host and synchronizes the stream before returning.
+ * Pinned host memory gives full PCIe bandwidth; the copy is split in chunks that
+ * overlap the first pass of the transform. */
+int pa_hash_host(pa_ctx *ctx, const uint8_t *key_host, uint8_t *out_host);
+
+/* Stages S1-S5 on this context's blocks: y_part = sum_{i in shard} a_i x_i mod p,
+ * canonical, as ceil(gamma/32) little-endian 32-bit words at DEVICE pointer y_out.
+ * key_slice: DEVICE pointer to the shard's key bytes (see pa_hash). Asynchronous. */
+int pa_mmh_partial(pa_ctx *ctx, const uint8_t *key_slice, uint32_t *y_out);
+
+/* Stages S6-S7: y = sum_{g<G} y_parts[g] mod p (each part ceil(gamma/32) words,
+ * DEVICE, contiguous), then MH into out_bits (DEVICE, ceil(m/8) bytes). */
+int pa_mh_merge(pa_ctx *ctx, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits);
+
+/* Free everything the context owns; NULL is a no-op. */
+void pa_ctx_destroy(pa_ctx *ctx);
+
+/* Describe a context (plans, shard, memory). */
+int pa_ctx_query(const pa_ctx *ctx, pa_info *info);
+
+/* Change the stream later work of the context is enqueued on. */
+int pa_ctx_set_stream(pa_ctx *ctx, void *stream);
+
+/* Stage timing: when enabled, pa_hash records CUDA events around each kernel
+ * on the context stream; pa_ctx_stage_times accumulates milliseconds per named
+ * stage since the last reset (names are static strings).  Returns the number of
+ * stages written (<= max). */
+int pa_ctx_set_profiling(pa_ctx *ctx, int enable);
+int pa_ctx_stage_times(pa_ctx *ctx, const char **names, double *ms, uint32_t *launches, int max);
+
+/* ---- host-only helpers (no GPU needed) ---------------------------------- */
+
+/* Validate parameters and compute the plan without a GPU.  Returns PA_OK and
+ * fills *info (device_bytes = projected), or PA_E_*. */
+int pa_plan(const pa_params *prm, pa_info *info);
+
+/* The Philox4x64-10 generator of reading A7 (numpy's convention): writes words
+ * w = 0..nwords-1 of stream key (key0, key1), word w = block(counter =
+ * floor(w/4) + 1)[w mod 4]. */
+int pa_philox4x64_10(uint64_t key0, uint64_t key1, uint64_t nwords, uint64_t *out);
+
+/* Hash-key expansion of reading A7 into little-endian 32-bit words:
+ * a_i (ceil(gamma/32) words), b and c (ceil(alpha/32) words each). */
+int pa_expand_a(uint64_t seed, uint64_t i, uint64_t gamma, uint32_t *out);
+int pa_expand_bc(uint64_t seed, uint64_t alpha, uint32_t *b_out, uint32_t *c_out);
+
+/* Code of the last failure on this thread; copies its message into buf. */
+int pa_last_error(char *buf, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PA_H_ */

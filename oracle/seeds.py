@@ -22,6 +22,12 @@ STREAM_B = 1 << 63
 STREAM_C = (1 << 63) + 1
 
 
+def _philox(seed: int, stream: int) -> np.random.Philox:
+    # explicit uint64 array: a Python list key is converted through float64 by numpy,
+    # which silently rounds 2^63 + 1 to 2^63
+    return np.random.Philox(key=np.array([seed & (2**64 - 1), stream], dtype=np.uint64))
+
+
 def _draw(bg: np.random.Philox, bits: int) -> int:
     nw = (bits + 63) // 64
     words = bg.random_raw(nw).astype("<u8")
@@ -30,7 +36,7 @@ def _draw(bg: np.random.Philox, bits: int) -> int:
 
 def expand_a(seed: int, i: int, gamma: int) -> int:
     """a_i in [0, 2^gamma - 2] (uniform on Z_p), stream (seed, i)."""
-    bg = np.random.Philox(key=[seed & (2**64 - 1), i])
+    bg = _philox(seed, i)
     allones = (1 << gamma) - 1
     while True:
         v = _draw(bg, gamma)
@@ -40,13 +46,13 @@ def expand_a(seed: int, i: int, gamma: int) -> int:
 
 def expand_b(seed: int, alpha: int) -> int:
     """b odd in [1, 2^alpha), stream (seed, 2^63)."""
-    bg = np.random.Philox(key=[seed & (2**64 - 1), STREAM_B])
+    bg = _philox(seed, STREAM_B)
     return _draw(bg, alpha) | 1
 
 
 def expand_c(seed: int, alpha: int) -> int:
     """c in [0, 2^alpha), stream (seed, 2^63 + 1)."""
-    bg = np.random.Philox(key=[seed & (2**64 - 1), STREAM_C])
+    bg = _philox(seed, STREAM_C)
     return _draw(bg, alpha)
 
 

@@ -1,0 +1,58 @@
+// Modular arithmetic for 30-bit NTT primes p < 2^30 on 32-bit integer pipes.
+//
+// Why 30-bit primes: the MMH/MH products ("its main part is large
+// number multiplications") are exact integer convolutions.  On sm_100a the integer
+// datapath is 32 bits wide; a butterfly mod a 30-bit prime is ~7 IMAD/ALU
+// instructions (Shoup multiply + lazy Harvey reduction), against ~35 for a 64-bit
+// Goldilocks butterfly.  Several primes are recombined by CRT (crt_carry.cuh).
+//
+// Value ranges ("lazy" representation): residues live in [0, 2p) between
+// operations; 4p < 2^32 so a sum of two never overflows.
+#pragma once
+#include <cstdint>
+
+namespace pa {
+
+struct PrimeK {            // per-prime constants passed to kernels
+    uint32_t p;            // prime, < 2^30
+    uint32_t p2;           // 2p
+    uint32_t pinv;         // p^{-1} mod 2^32   (Montgomery, R = 2^32)
+    uint32_t r2;           // R^2 mod p         (to Montgomery form)
+};
+
+// s in [0, 4p) -> [0, 2p)
+__device__ __forceinline__ uint32_t red2p(uint32_t s, uint32_t p2) { return min(s, s - p2); }
+// s in [0, 2p) -> [0, p)
+__device__ __forceinline__ uint32_t red1p(uint32_t s, uint32_t p) { return min(s, s - p); }
+
+// Shoup multiplication by a constant w < p with wp = floor(w 2^32 / p):
+// returns x*w mod p in [0, 2p) for any 32-bit x.
+__device__ __forceinline__ uint32_t mul_shoup(uint32_t x, uint32_t w, uint32_t wp, uint32_t p) {
+    uint32_t q = __umulhi(x, wp);
+    return x * w - q * p;
+}
+
+// Montgomery product x*y*2^-32 mod p in (0, 2p), valid for any 32-bit x and y < p.
+__device__ __forceinline__ uint32_t mul_mont(uint32_t x, uint32_t y, uint32_t p, uint32_t pinv) {
+    uint64_t t = (uint64_t)x * y;
+    uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);
+    uint32_t q = lo * pinv;
+    return hi - __umulhi(q, p) + p;
+}
+
+// Gentleman-Sande (DIF) butterfly: (a, b) -> (a + b, (a - b) w), inputs/outputs in [0, 2p).
+__device__ __forceinline__ void bfly_dif(uint32_t &a, uint32_t &b, uint32_t w, uint32_t wp,
+                                         uint32_t p, uint32_t p2) {
+    uint32_t s = red2p(a + b, p2);
+    uint32_t d = a - b + p2;
+    b = mul_shoup(d, w, wp, p);
+    a = s;
+}
+__device__ __forceinline__ void bfly_dif1(uint32_t &a, uint32_t &b, uint32_t p2) {
+    uint32_t s = red2p(a + b, p2);
+    uint32_t d = red2p(a - b + p2, p2);
+    a = s;
+    b = d;
+}
+
+}  // namespace pa

@@ -1,0 +1,192 @@
+// Number-theoretic transforms of length L = N1 * N2 modulo 30-bit primes (sm_100a).
+//
+// Role in the method: the MMH products a_i * x_i (Eq. 2) and the MH
+// product b * y (Eq. 4) are exact big-integer multiplications: "its main
+// part is large number multiplications, which means it can be accelerated by
+// algorithms such as the Schonhage and Strassen algorithm".  Each
+// product is a cyclic convolution of B-bit limb vectors computed with NTTs; the MMH
+// sum over blocks is accumulated in the transform domain so that one inverse
+// transform serves all blocks.
+//
+// Four-step structure (no explicit transposes, no bit reversal):
+//   column pass: for each column j1 < N1, an N2-point DFT over j2 of x[j1 + N1 j2],
+//                times omega_L^(j1 k2), stored at j1 + N1 k2;
+//   row pass:    for each row k2, an N1-point DFT of the contiguous row; the result
+//                X[k2 + N2 k1] is stored at k2 N1 + k1.
+// The inverse runs row pass (omega^-1, then times omega_L^(-j1 k2)) and column pass
+// (omega^-1) and lands in natural order; 1/L is folded into the precomputed operand.
+// Each pass is a sub-DFT of S = 2^S_LOG points: a thread holds E = 2^E_LOG elements
+// in registers and runs radix-2^r DIF networks (Shoup butterflies), with one shared
+// memory exchange and one twiddle multiply per additional round.  The sub-DFT maps
+// natural order to natural order (positions g + G l).
+#pragma once
+#include <cstdint>
+#include "modarith.cuh"
+
+namespace pa {
+
+constexpr int kMaxRounds = 4;
+
+struct NttArgs {
+    const PrimeK *pk;          // [P]
+    const uint32_t *regtw;     // [P][E/2] omega_E^j of this direction
+    const uint32_t *regtwp;    // [P][E/2] Shoup companions
+    uint32_t regtw_stride;     // E/2 entries per prime in the table (allocated for E=32)
+    const uint32_t *rtw;       // round twiddles (Montgomery form): [P][rtw_stride]
+    uint32_t rtw_stride;
+    uint32_t rtw_off[kMaxRounds];
+    const uint32_t *ltw_lo;    // omega_L^(+-e_lo), e_lo < 2^h   (Montgomery form)
+    const uint32_t *ltw_hi;    // omega_L^(+-e_hi 2^h)
+    uint32_t ltw_lo_stride, ltw_hi_stride, ltw_h;
+    uint32_t log2L;
+    uint32_t n1;               // row length (number of columns)
+    uint32_t n2;               // column length (number of rows)
+    uint32_t nprimes;
+};
+
+template <int S_LOG, int E_LOG>
+struct SubPlan {
+    static constexpr int S = 1 << S_LOG;
+    static constexpr int E = 1 << E_LOG;
+    static constexpr int Q = (S_LOG + E_LOG - 1) / E_LOG;     // radix rounds
+    static constexpr int TPV = S / E;                          // threads per vector
+    __host__ __device__ static constexpr int rlog(int rho) { return (rho < Q - 1) ? E_LOG : (S_LOG - E_LOG * (Q - 1)); }
+    __host__ __device__ static constexpr int glog(int rho) { return rho == 0 ? 0 : glog(rho - 1) + rlog(rho - 1); }
+};
+
+template <int R>
+__host__ __device__ constexpr int bitrev(int q) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1) { r = (r << 1) | (q & 1); q >>= 1; }
+    return r;
+}
+
+// In-register DIF DFT of radix R = 2^RLOG on x[0..R): natural order in, X[bitrev(q)]
+// in x[q] out.  tw[j] = omega_E^j, twp[j] its Shoup companion (j < E/2).
+template <int RLOG, int E>
+__device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const uint32_t *twp,
+                                        uint32_t p, uint32_t p2) {
+    constexpr int R = 1 << RLOG;
+#pragma unroll
+    for (int h = R / 2; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int s = 0; s < R; s += 2 * h) {
+#pragma unroll
+            for (int i = 0; i < h; i++) {
+                if (i == 0) {
+                    bfly_dif1(x[s], x[s + h], p2);
+                } else {
+                    const int j = i * (E / (2 * h));
+                    bfly_dif(x[s + i], x[s + i + h], tw[j], twp[j], p, p2);
+                }
+            }
+        }
+    }
+}
+
+// omega_L^e (direction of the tables) in Montgomery form, canonical (< p).
+__device__ __forceinline__ uint32_t ltw_mont(const NttArgs &a, int pi, uint32_t e, uint32_t p,
+                                             uint32_t pinv) {
+    const uint32_t lo = __ldg(a.ltw_lo + (size_t)pi * a.ltw_lo_stride + (e & ((1u << a.ltw_h) - 1)));
+    const uint32_t hi = __ldg(a.ltw_hi + (size_t)pi * a.ltw_hi_stride + (e >> a.ltw_h));
+    return red1p(mul_mont(lo, hi, p, pinv), p);
+}
+
+struct Ctx32 {  // per-prime constants held in registers by a thread
+    uint32_t p, p2, pinv;
+};
+
+// Round rho >= 1 of a sub-DFT (recursive over rho).  Round rho-1 left its outputs in
+// shared memory; the last round leaves its outputs in x[] (group h, register mm <->
+// position v + TPV h + G_last * bitrev(mm)).
+template <int S_LOG, int E_LOG, int RHO, class SIdx>
+__device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SIdx &sidx, int v,
+                                            const uint32_t *tw, const uint32_t *twp,
+                                            const uint32_t *rtw_p, const NttArgs &a,
+                                            const Ctx32 &c) {
+    using SP = SubPlan<S_LOG, E_LOG>;
+    if constexpr (RHO < SP::Q) {
+        constexpr int S = SP::S, E = SP::E;
+        constexpr int RL = SP::rlog(RHO);
+        constexpr int R = 1 << RL;
+        constexpr int G = 1 << SP::glog(RHO);
+        constexpr int T = S / (G * R);
+        constexpr int NG = E / R;
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < NG; h++) {
+            const int q = v + SP::TPV * h;
+#pragma unroll
+            for (int m = 0; m < R; m++) x[h * R + m] = sm[sidx(q + (S / R) * m)];
+        }
+#pragma unroll
+        for (int h = 0; h < NG; h++) dft_reg<RL, E>(x + h * R, tw, twp, c.p, c.p2);
+        if constexpr (RHO < SP::Q - 1) {
+            __syncthreads();
+#pragma unroll
+            for (int h = 0; h < NG; h++) {
+                const int q = v + SP::TPV * h;
+                const int g = q % G, t = q / G;
+#pragma unroll
+                for (int mm = 0; mm < R; mm++) {
+                    const int k = bitrev<R>(mm);
+                    uint32_t val = x[h * R + mm];
+                    if (T > 1 && k != 0)
+                        val = mul_mont(val, __ldg(rtw_p + a.rtw_off[RHO] + k * T + t), c.p, c.pinv);
+                    sm[sidx(g + G * k + G * R * t)] = val;
+                }
+            }
+        }
+        rounds_rest<S_LOG, E_LOG, RHO + 1>(x, sm, sidx, v, tw, twp, rtw_p, a, c);
+    }
+}
+
+// Round 0 post-processing: DFT of the loaded groups, twiddle, store to shared memory.
+template <int S_LOG, int E_LOG, class SIdx>
+__device__ __forceinline__ void round0_finish(uint32_t *x, uint32_t *sm, const SIdx &sidx, int v,
+                                              const uint32_t *tw, const uint32_t *twp,
+                                              const uint32_t *rtw_p, const NttArgs &a,
+                                              const Ctx32 &c) {
+    using SP = SubPlan<S_LOG, E_LOG>;
+    constexpr int S = SP::S, E = SP::E;
+    constexpr int RL = SP::rlog(0);
+    constexpr int R = 1 << RL;
+    constexpr int T = S / R;
+    constexpr int NG = E / R;
+#pragma unroll
+    for (int h = 0; h < NG; h++) dft_reg<RL, E>(x + h * R, tw, twp, c.p, c.p2);
+    if constexpr (SP::Q > 1) {
+#pragma unroll
+        for (int h = 0; h < NG; h++) {
+            const int t = v + SP::TPV * h;
+#pragma unroll
+            for (int mm = 0; mm < R; mm++) {
+                const int k = bitrev<R>(mm);
+                uint32_t val = x[h * R + mm];
+                if (T > 1 && k != 0)
+                    val = mul_mont(val, __ldg(rtw_p + a.rtw_off[0] + k * T + t), c.p, c.pinv);
+                sm[sidx(k + R * t)] = val;
+            }
+        }
+    }
+}
+
+// Position of register (h, mm) after the last round.
+template <int S_LOG, int E_LOG>
+__device__ __forceinline__ int out_pos(int v, int h, int mm) {
+    using SP = SubPlan<S_LOG, E_LOG>;
+    constexpr int RL = SP::rlog(SP::Q - 1);
+    constexpr int R = 1 << RL;
+    constexpr int G = 1 << SP::glog(SP::Q - 1);
+    return (v + SP::TPV * h) + G * bitrev<R>(mm);
+}
+
+// Position of register (h, m) in round 0 (input order).
+template <int S_LOG, int E_LOG>
+__device__ __forceinline__ int in_pos(int v, int h, int m) {
+    using SP = SubPlan<S_LOG, E_LOG>;
+    constexpr int R = 1 << SP::rlog(0);
+    return (v + SP::TPV * h) + (SP::S / R) * m;
+}
+
+}  // namespace pa

@@ -1,0 +1,956 @@
+// C ABI of the MMH-MH privacy-amplification library (include/pa.h): parameter
+// validation, transform planning, hash-key expansion, context lifecycle and the
+// stream-ordered orchestration of the sm_100a kernels of one hash.
+//
+// Hot path of one pa_hash (Algorithm 1), all on the ctx stream:
+//   S1+S2  col_pass<KEY>   pack key blocks into B-bit limbs, residues mod P primes,
+//                          first (column) NTT pass, four-step twiddle
+//   S2+S3  row_pass<MAC>   second NTT pass, multiply by the precomputed
+//                          transforms of a_i and accumulate over blocks
+//   S4     row_pass<INV>, col_pass<INV>   one inverse transform for all blocks
+//          crt_colsum + carry_{tiles,scan,apply}   exact Y = sum_i a_i x_i
+//   S5     fold_colsum + carry, fold_final x2, canonical zero  -> y = Y mod p
+//   S7     col_pass<WORDS>(y), row_pass<MAC>(B^), inverse, crt_colsum(+c), carry,
+//          mh_extract -> out_bits = top m bits of (b y + c) mod 2^alpha
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/pa.h"
+#include "carry.cuh"
+#include "host_math.h"
+#include "modarith.cuh"
+#include "ntt.cuh"
+#include "passes.cuh"
+
+using namespace pa;
+
+// ====================================================================== errors
+static thread_local int g_err = 0;
+static thread_local char g_msg[512];
+
+static int set_err(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+static int set_err(int code, const char *fmt, ...) {
+    g_err = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_msg, sizeof g_msg, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return set_err(PA_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                           __FILE__, __LINE__);                                             \
+    } while (0)
+
+#define TRY(expr)                      \
+    do {                               \
+        int _rc = (expr);              \
+        if (_rc != PA_OK) return _rc;  \
+    } while (0)
+
+extern "C" int pa_last_error(char *buf, size_t len) {
+    if (buf && len) {
+        strncpy(buf, g_msg, len - 1);
+        buf[len - 1] = 0;
+    }
+    return g_err;
+}
+
+// ====================================================================== planning
+static constexpr int kMinLog2L = 10;
+static constexpr int kMaxLog2L = 23;
+static constexpr int kColMaxLog = 9;
+
+static double log2_bound(uint64_t nterms, uint64_t overlap, uint32_t B) {
+    // log2(nterms * overlap * (2^B - 1)^2)  (upper bound of a convolution coefficient)
+    return std::log2((double)nterms) + std::log2((double)overlap) + 2.0 * std::log2(std::ldexp(1.0, (int)B) - 1.0);
+}
+
+// Choose (B, P, L) for the product of an `abits`-bit and a `bbits`-bit operand, summed
+// over `nterms` products; only coefficients below `need_coef` limbs... (all are needed:
+// the cyclic length must cover the full product so nothing wraps).
+static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int force_B, pa_stage_plan *out) {
+    static const uint32_t Bs[] = {16, 24, 32, 40, 48, 56, 64};
+    double best = 1e300;
+    pa_stage_plan bp{};
+    for (uint32_t B : Bs) {
+        if (force_B && (int)B != force_B) continue;
+        const uint64_t wa = (abits + B - 1) / B, wb = (bbits + B - 1) / B;
+        const uint64_t len = wa + wb - 1;
+        int lg = kMinLog2L;
+        while ((1ull << lg) < len) lg++;
+        if (lg > kMaxLog2L) continue;
+        const double bound = log2_bound(nterms, std::min(wa, wb), B);
+        // primes usable at this length, largest first
+        std::vector<uint32_t> ps;
+        for (uint32_t p : kPrimes) if (two_adic(p) >= lg) ps.push_back(p);
+        double mod = 0;
+        uint32_t P = 0;
+        while (P < ps.size() && P < (uint32_t)kMaxPrimes && mod <= bound + 0.5) { mod += std::log2((double)ps[P]); P++; }
+        if (mod <= bound + 0.5) continue;                   // not enough primes
+        const double cost = (double)P * std::ldexp(1.0, lg) * (lg + 2);
+        if (cost < best) {
+            best = cost;
+            bp = pa_stage_plan{};
+            bp.limb_bits = B;
+            bp.nprimes = P;
+            bp.log2_len = (uint32_t)lg;
+            const int cl = std::min(kColMaxLog, lg / 2);
+            bp.n_col = 1u << cl;
+            bp.n_row = 1u << (lg - cl);
+            for (uint32_t i = 0; i < P; i++) bp.primes[i] = ps[i];
+            bp.bound_log2 = bound;
+            bp.modulus_log2 = mod;
+        }
+    }
+    if (best == 1e300) return PA_E_BOUND;
+    *out = bp;
+    return PA_OK;
+}
+
+struct Plan {
+    uint64_t n, r, m, gamma, alpha, k, b0, b1, seed;
+    int strict, force_B;
+    pa_stage_plan mmh, mh;
+};
+
+static bool is_mersenne(uint64_t g) {
+    for (uint64_t e : kMersenne) if (e == g) return true;
+    return false;
+}
+
+static int make_plan(const pa_params *prm, Plan *P) {
+    if (!prm) return set_err(PA_E_PARAM, "params is NULL");
+    Plan p{};
+    p.n = prm->n; p.r = prm->r; p.m = prm->m; p.seed = prm->seed;
+    p.strict = prm->strict; p.force_B = prm->limb_bits;
+    if (p.n < 1) return set_err(PA_E_PARAM, "n must be >= 1");
+    if (p.r < 16 || p.r % 16) return set_err(PA_E_PARAM, "r must be >= 16 and a multiple of 16 (got %llu)", (unsigned long long)p.r);
+    if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
+    if (p.force_B && (p.force_B < 16 || p.force_B > 64 || p.force_B % 8))
+        return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, 64]");
+    uint64_t g = prm->gamma;
+    if (g == 0) {
+        for (uint64_t e : kMersenne) if (e > p.r) { g = e; break; }
+        if (g == 0) return set_err(PA_E_PARAM, "no known Mersenne exponent > r");
+    }
+    if (!is_mersenne(g)) return set_err(PA_E_PARAM, "gamma=%llu is not a known Mersenne exponent (SPEC.md:33)", (unsigned long long)g);
+    if (g <= p.r) return set_err(PA_E_PARAM, "gamma must exceed r so every r-bit block lies in Z_p (reading A2)");
+    if (p.strict && p.m >= g) return set_err(PA_E_PARAM, "strict: m must be < gamma (PAPER.md:143)");
+    p.gamma = g;
+    p.alpha = std::max<uint64_t>(g, p.m);
+    p.k = (p.n + p.r - 1) / p.r;
+    p.b0 = prm->block_begin; p.b1 = prm->block_end;
+    if (p.b0 == 0 && p.b1 == 0) p.b1 = p.k;
+    if (p.b0 >= p.b1 || p.b1 > p.k) return set_err(PA_E_PARAM, "bad shard [%llu, %llu) of %llu blocks",
+                                                  (unsigned long long)p.b0, (unsigned long long)p.b1, (unsigned long long)p.k);
+    if (plan_product(p.r, p.gamma, p.b1 - p.b0, p.force_B, &p.mmh) != PA_OK)
+        return set_err(PA_E_BOUND, "no transform plan covers the MMH coefficient bound");
+    if (plan_product(p.gamma, p.alpha, 1, p.force_B, &p.mh) != PA_OK)
+        return set_err(PA_E_BOUND, "no transform plan covers the MH product");
+    *P = p;
+    return PA_OK;
+}
+
+// ====================================================================== stage tables
+struct StageDev {
+    pa_stage_plan pl{};
+    uint32_t L = 0, lg = 0;
+    PrimeK *pk = nullptr;
+    LimbRed *lred = nullptr;
+    uint32_t *scale = nullptr;
+    uint32_t *regtw[2] = {}, *regtwp[2] = {};
+    uint32_t *rtw = nullptr;            // [P][stride]: col fwd, col inv, row fwd, row inv
+    uint32_t rtw_stride = 0;
+    uint32_t rtw_off[4][kMaxRounds] = {};
+    uint32_t *ltw_lo[2] = {}, *ltw_hi[2] = {};
+    uint32_t ltw_h = 0, ltw_lo_n = 0, ltw_hi_n = 0;
+    CrtK crt{};
+};
+
+struct DevAlloc {
+    std::vector<void *> ptrs;
+    uint64_t bytes = 0;
+    template <class T>
+    int alloc(T **p, size_t count) {
+        void *q = nullptr;
+        const size_t b = std::max<size_t>(count * sizeof(T), 16);
+        cudaError_t e = cudaMalloc(&q, b);
+        if (e != cudaSuccess) return set_err(PA_E_NOMEM, "cudaMalloc(%zu) failed: %s", b, cudaGetErrorString(e));
+        ptrs.push_back(q);
+        bytes += b;
+        *p = (T *)q;
+        return PA_OK;
+    }
+    void free_all() {
+        for (void *q : ptrs) cudaFree(q);
+        ptrs.clear();
+        bytes = 0;
+    }
+};
+
+// Round twiddles of a sub-DFT of 2^S_LOG points with radix 2^5 rounds: for round rho,
+// table[k][t] = omega_{S_rho}^(t k), S_rho = S / G_rho.
+static void round_tables(uint32_t p, uint32_t wL, int lg, int slog, std::vector<uint32_t> &tab,
+                         uint32_t off[kMaxRounds]) {
+    const int E_LOG = 5;
+    const int Q = (slog + E_LOG - 1) / E_LOG;
+    int glog = 0;
+    for (int rho = 0; rho < kMaxRounds; rho++) off[rho] = 0;
+    for (int rho = 0; rho < Q; rho++) {
+        const int rl = (rho < Q - 1) ? E_LOG : slog - E_LOG * (Q - 1);
+        const int srho_log = slog - glog;
+        const uint32_t R = 1u << rl, T = 1u << (srho_log - rl);
+        const uint32_t w = (uint32_t)powmod64(wL, 1ull << (lg - srho_log), p);   // omega_{S_rho}
+        off[rho] = (uint32_t)tab.size();
+        for (uint32_t k = 0; k < R; k++)
+            for (uint32_t t = 0; t < T; t++)
+                tab.push_back(to_mont((uint32_t)powmod64(w, (uint64_t)t * k, p), p));
+        glog += rl;
+    }
+}
+
+static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
+    sd.pl = pl;
+    sd.lg = pl.log2_len;
+    sd.L = 1u << sd.lg;
+    const uint32_t P = pl.nprimes;
+    const int lg = (int)sd.lg;
+    const int clog = __builtin_ctz(pl.n_col), rlog = __builtin_ctz(pl.n_row);
+    std::vector<PrimeK> pk(P);
+    std::vector<LimbRed> lr(P);
+    std::vector<uint32_t> scale(P);
+    std::vector<uint32_t> regtw[2], regtwp[2];
+    std::vector<std::vector<uint32_t>> rt(P);
+    sd.ltw_h = (uint32_t)((lg + 1) / 2);
+    sd.ltw_lo_n = 1u << sd.ltw_h;
+    sd.ltw_hi_n = 1u << (lg - sd.ltw_h);
+    std::vector<uint32_t> lo[2], hi[2];
+    for (uint32_t i = 0; i < P; i++) {
+        const uint32_t p = pl.primes[i];
+        pk[i].p = p;
+        pk[i].p2 = 2 * p;
+        uint32_t inv = 1;                             // p^{-1} mod 2^32 by Newton
+        for (int it = 0; it < 5; it++) inv *= 2 - p * inv;
+        pk[i].pinv = inv;
+        pk[i].r2 = (uint32_t)powmod64(2, 64, p);
+        const uint32_t c32 = (uint32_t)((1ull << 32) % p);
+        lr[i] = LimbRed{c32, shoup_of(c32, p), (uint32_t)((1ull << 32) / p)};
+        const uint32_t g = primitive_root(p);
+        const uint32_t wf = (uint32_t)powmod64(g, (p - 1) >> lg, p);     // omega_L
+        const uint32_t wi = inv_mod(wf, p);
+        const uint32_t Linv = inv_mod(sd.L, p);
+        scale[i] = (uint32_t)mulmod64(Linv, powmod64(2, 64, p), p);      // L^-1 R^2
+        for (int dir = 0; dir < 2; dir++) {
+            const uint32_t wL = dir ? wi : wf;
+            const uint32_t w32 = (uint32_t)powmod64(wL, sd.L / 32, p);
+            for (int j = 0; j < 16; j++) {
+                const uint32_t t = (uint32_t)powmod64(w32, j, p);
+                regtw[dir].push_back(t);
+                regtwp[dir].push_back(shoup_of(t, p));
+            }
+            for (uint32_t e = 0; e < sd.ltw_lo_n; e++) lo[dir].push_back(to_mont((uint32_t)powmod64(wL, e, p), p));
+            for (uint32_t e = 0; e < sd.ltw_hi_n; e++)
+                hi[dir].push_back(to_mont((uint32_t)powmod64(wL, (uint64_t)e << sd.ltw_h, p), p));
+        }
+        // round twiddle tables: col fwd, col inv, row fwd, row inv
+        round_tables(p, wf, lg, clog, rt[i], sd.rtw_off[0]);
+        round_tables(p, wi, lg, clog, rt[i], sd.rtw_off[1]);
+        round_tables(p, wf, lg, rlog, rt[i], sd.rtw_off[2]);
+        round_tables(p, wi, lg, rlog, rt[i], sd.rtw_off[3]);
+    }
+    sd.rtw_stride = (uint32_t)rt[0].size();
+    std::vector<uint32_t> rtall;
+    for (uint32_t i = 0; i < P; i++) rtall.insert(rtall.end(), rt[i].begin(), rt[i].end());
+
+    TRY(da.alloc(&sd.pk, P));
+    TRY(da.alloc(&sd.lred, P));
+    TRY(da.alloc(&sd.scale, P));
+    TRY(da.alloc(&sd.rtw, rtall.size()));
+    CUDA_TRY(cudaMemcpy(sd.pk, pk.data(), P * sizeof(PrimeK), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(sd.lred, lr.data(), P * sizeof(LimbRed), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(sd.scale, scale.data(), P * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(sd.rtw, rtall.data(), rtall.size() * 4, cudaMemcpyHostToDevice));
+    for (int dir = 0; dir < 2; dir++) {
+        TRY(da.alloc(&sd.regtw[dir], regtw[dir].size()));
+        TRY(da.alloc(&sd.regtwp[dir], regtwp[dir].size()));
+        TRY(da.alloc(&sd.ltw_lo[dir], lo[dir].size()));
+        TRY(da.alloc(&sd.ltw_hi[dir], hi[dir].size()));
+        CUDA_TRY(cudaMemcpy(sd.regtw[dir], regtw[dir].data(), regtw[dir].size() * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(sd.regtwp[dir], regtwp[dir].data(), regtwp[dir].size() * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(sd.ltw_lo[dir], lo[dir].data(), lo[dir].size() * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(sd.ltw_hi[dir], hi[dir].data(), hi[dir].size() * 4, cudaMemcpyHostToDevice));
+    }
+    // CRT constants
+    CrtK &K = sd.crt;
+    memset(&K, 0, sizeof K);
+    K.P = P;
+    for (uint32_t i = 0; i < P; i++) {
+        const uint32_t p = pl.primes[i];
+        K.p[i] = p;
+        K.pinv[i] = pk[i].pinv;
+        uint64_t prodmod = 1;
+        for (uint32_t l = 0; l < i; l++) {
+            K.pmod[i][l] = to_mont(pl.primes[l] % p, p);
+            prodmod = mulmod64(prodmod, pl.primes[l] % p, p);
+        }
+        K.inv[i] = to_mont(i ? inv_mod((uint32_t)prodmod, p) : 1u, p);
+    }
+    // prod[l] = p_0 ... p_{l-1}, little-endian words
+    std::vector<uint32_t> acc(kMaxPrimes, 0);
+    acc[0] = 1;
+    for (uint32_t l = 0; l <= P && l <= (uint32_t)kMaxPrimes; l++) {
+        for (int w = 0; w < kMaxPrimes; w++) K.prod[l][w] = acc[w];
+        if (l == P) break;
+        uint64_t carry = 0;
+        for (int w = 0; w < kMaxPrimes; w++) {
+            const uint64_t t = (uint64_t)acc[w] * pl.primes[l] + carry;
+            acc[w] = (uint32_t)t;
+            carry = t >> 32;
+        }
+    }
+    return PA_OK;
+}
+
+static NttArgs ntt_args(const StageDev &sd, int dir, int pass /*0 col, 1 row*/) {
+    NttArgs a{};
+    a.pk = sd.pk;
+    a.regtw = sd.regtw[dir];
+    a.regtwp = sd.regtwp[dir];
+    a.regtw_stride = 16;
+    a.rtw = sd.rtw;
+    a.rtw_stride = sd.rtw_stride;
+    for (int r = 0; r < kMaxRounds; r++) a.rtw_off[r] = sd.rtw_off[pass * 2 + dir][r];
+    a.ltw_lo = sd.ltw_lo[dir];
+    a.ltw_hi = sd.ltw_hi[dir];
+    a.ltw_lo_stride = sd.ltw_lo_n;
+    a.ltw_hi_stride = sd.ltw_hi_n;
+    a.ltw_h = sd.ltw_h;
+    a.log2L = sd.lg;
+    a.n1 = sd.pl.n_row;
+    a.n2 = sd.pl.n_col;
+    a.nprimes = sd.pl.nprimes;
+    return a;
+}
+
+// ====================================================================== launchers
+static int g_num_sms = 0;
+
+struct KInfo {
+    int threads = 0;
+    size_t smem = 0;
+    int occ = 0;
+};
+
+template <class F>
+static int kinfo(F *fn, int threads, size_t smem, KInfo &ki) {
+    if (ki.occ) return PA_OK;
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
+    if (occ < 1) return set_err(PA_E_CUDA, "kernel cannot be resident (threads=%d smem=%zu)", threads, smem);
+    ki.threads = threads;
+    ki.smem = smem;
+    ki.occ = occ;
+    return PA_OK;
+}
+
+template <int S_LOG, int MODE>
+static int launch_col_t(const ColArgs &A, cudaStream_t st) {
+    constexpr int E_LOG = 5;
+    static KInfo ki;
+    auto fn = col_pass<S_LOG, E_LOG, MODE>;
+    TRY(kinfo(fn, 32 * (1 << (S_LOG - E_LOG)), (size_t)(1 << S_LOG) * 32 * 4, ki));
+    const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
+    fn<<<grid, ki.threads, ki.smem, st>>>(A);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+template <int MODE>
+static int launch_col(int slog, const ColArgs &A, cudaStream_t st) {
+    switch (slog) {
+        case 5: return launch_col_t<5, MODE>(A, st);
+        case 6: return launch_col_t<6, MODE>(A, st);
+        case 7: return launch_col_t<7, MODE>(A, st);
+        case 8: return launch_col_t<8, MODE>(A, st);
+        case 9: return launch_col_t<9, MODE>(A, st);
+    }
+    return set_err(PA_E_PARAM, "unsupported column length 2^%d", slog);
+}
+
+constexpr int row_v(int slog) {
+    return (256 >> (slog - 5)) < 1 ? 1 : ((256 >> (slog - 5)) > 32 ? 32 : (256 >> (slog - 5)));
+}
+
+template <int S_LOG, int MODE>
+static int launch_row_t(const RowArgs &A0, cudaStream_t st) {
+    constexpr int E_LOG = 5;
+    constexpr int V = row_v(S_LOG);
+    static KInfo ki;
+    auto fn = row_pass<S_LOG, E_LOG, V, MODE>;
+    constexpr int S = 1 << S_LOG;
+    TRY(kinfo(fn, V * (S >> E_LOG), (size_t)V * (S + S / 32) * 4, ki));
+    RowArgs A = A0;
+    A.units = (A.nt.n2 / V) * A.nt.nprimes;
+    const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
+    fn<<<grid, ki.threads, ki.smem, st>>>(A);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+template <int MODE>
+static int launch_row(int slog, const RowArgs &A, cudaStream_t st) {
+    switch (slog) {
+        case 5: return launch_row_t<5, MODE>(A, st);
+        case 6: return launch_row_t<6, MODE>(A, st);
+        case 7: return launch_row_t<7, MODE>(A, st);
+        case 8: return launch_row_t<8, MODE>(A, st);
+        case 9: return launch_row_t<9, MODE>(A, st);
+        case 10: return launch_row_t<10, MODE>(A, st);
+        case 11: return launch_row_t<11, MODE>(A, st);
+        case 12: return launch_row_t<12, MODE>(A, st);
+        case 13: return launch_row_t<13, MODE>(A, st);
+        case 14: return launch_row_t<14, MODE>(A, st);
+    }
+    return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
+}
+
+// ====================================================================== context
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+
+struct pa_ctx {
+    Plan pl{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevAlloc da;
+    StageDev smmh, smh;
+    uint32_t nblk = 0;
+    // MMH buffers
+    uint32_t *ahat = nullptr, *scratch = nullptr, *acc = nullptr;
+    // MH buffers
+    uint32_t *bhat = nullptr, *scratch_mh = nullptr, *acc_mh = nullptr;
+    uint32_t *c_words = nullptr;
+    // carries / fold
+    uint64_t *S = nullptr;
+    uint32_t *Y = nullptr, *y1 = nullptr, *y2 = nullptr, *Z = nullptr;
+    uint8_t *tg = nullptr, *tp = nullptr, *tcin = nullptr;
+    uint32_t *flag = nullptr;
+    uint8_t *key_dev = nullptr;   // staging for pa_hash_host
+    uint8_t *out_dev = nullptr;
+    uint32_t *parts_dev = nullptr;
+    uint64_t W_Y = 0, Wg = 0, W_Z = 0, ncoef_mmh = 0;
+    uint32_t launches = 0;
+    // profiling
+    bool prof = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> evpool;
+    std::map<std::string, std::pair<double, uint32_t>> acc_ms;
+};
+
+static cudaEvent_t ev_get(pa_ctx *c) {
+    if (!c->evpool.empty()) { cudaEvent_t e = c->evpool.back(); c->evpool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    pa_ctx *c;
+    const char *name;
+    cudaEvent_t a = nullptr;
+    ProfScope(pa_ctx *c_, const char *n) : c(c_), name(n) {
+        if (c->prof) { a = ev_get(c); cudaEventRecord(a, c->stream); }
+    }
+    ~ProfScope() {
+        if (c->prof) {
+            cudaEvent_t b = ev_get(c);
+            cudaEventRecord(b, c->stream);
+            c->recs.push_back({name, a, b});
+        }
+    }
+};
+
+static uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ---- carry resolution of S[0..W) into out[0..W)
+static int run_carry(pa_ctx *c, uint32_t W, uint32_t *out) {
+    const uint32_t nt = (uint32_t)cdiv(W, kTile);
+    carry_tiles<<<nt, kTile, 0, c->stream>>>(c->S, W, c->tg, c->tp);
+    carry_scan<<<1, 1024, 0, c->stream>>>(c->tg, c->tp, nt, nullptr, c->tcin, nullptr);
+    carry_apply<<<nt, kTile, 0, c->stream>>>(c->S, W, c->tcin, out);
+    c->launches += 3;
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+// ---- forward + MAC + inverse of one stage; result residues (natural order) in acc
+static int stage_transform(pa_ctx *c, StageDev &sd, int col_mode, const KeySrc *ks, const WordSrc *ws,
+                           uint32_t nvec, uint32_t *scratch, const uint32_t *hat, uint32_t *acc,
+                           const char *tag_fwd1, const char *tag_fwd2, const char *tag_inv) {
+    const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
+    const uint32_t P = sd.pl.nprimes;
+    {
+        ProfScope ps(c, tag_fwd1);
+        ColArgs A{};
+        A.nt = ntt_args(sd, 0, 0);
+        if (ks) A.ks = *ks;
+        if (ws) A.ws = *ws;
+        A.lred = sd.lred;
+        A.dst = scratch;
+        A.nvec = nvec;
+        A.units = (sd.pl.n_row / 32) * P * nvec;
+        if (col_mode == COL_KEY) TRY(launch_col<COL_KEY>(clog, A, c->stream));
+        else TRY(launch_col<COL_WORDS>(clog, A, c->stream));
+        c->launches++;
+    }
+    {
+        ProfScope ps(c, tag_fwd2);
+        RowArgs R{};
+        R.nt = ntt_args(sd, 0, 1);
+        R.src = scratch;
+        R.dst = acc;
+        R.ahat = hat;
+        R.nvec = nvec;
+        TRY(launch_row<ROW_MAC>(rlog, R, c->stream));
+        c->launches++;
+    }
+    {
+        ProfScope ps(c, tag_inv);
+        RowArgs R{};
+        R.nt = ntt_args(sd, 1, 1);
+        R.src = acc;
+        R.dst = acc;
+        R.nvec = 1;
+        TRY(launch_row<ROW_INV>(rlog, R, c->stream));
+        ColArgs A{};
+        A.nt = ntt_args(sd, 1, 0);
+        A.src = acc;
+        A.dst = acc;
+        A.nvec = 1;
+        A.units = (sd.pl.n_row / 32) * P;
+        TRY(launch_col<COL_INV>(clog, A, c->stream));
+        c->launches += 2;
+    }
+    return PA_OK;
+}
+
+// ---- precompute transforms of word vectors (a_i or b) into hat (Montgomery, x 1/L)
+static int precompute_hat(pa_ctx *c, StageDev &sd, const WordSrc &ws, uint32_t nvec, uint32_t *scratch, uint32_t *hat) {
+    const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
+    ColArgs A{};
+    A.nt = ntt_args(sd, 0, 0);
+    A.ws = ws;
+    A.lred = sd.lred;
+    A.dst = scratch;
+    A.nvec = nvec;
+    A.units = (sd.pl.n_row / 32) * sd.pl.nprimes * nvec;
+    TRY(launch_col<COL_WORDS>(clog, A, c->stream));
+    RowArgs R{};
+    R.nt = ntt_args(sd, 0, 1);
+    R.src = scratch;
+    R.dst = hat;
+    R.scale = sd.scale;
+    R.nvec = nvec;
+    TRY(launch_row<ROW_STORE>(rlog, R, c->stream));
+    return PA_OK;
+}
+
+static int expand_words(uint64_t key0, uint64_t key1, uint64_t bits, std::vector<uint32_t> &w, bool reject_allones) {
+    const uint64_t nw64 = cdiv(bits, 64), nw32 = cdiv(bits, 32);
+    std::vector<uint64_t> raw(nw64);
+    uint64_t off = 0;
+    for (;;) {
+        Philox4x64::words(key0, key1, off, nw64, raw.data());
+        off += nw64;
+        w.assign(nw32, 0);
+        for (uint64_t i = 0; i < nw32; i++) w[i] = (uint32_t)(raw[i / 2] >> (32 * (i & 1)));
+        if (bits % 32) w[nw32 - 1] &= (uint32_t)((1ull << (bits % 32)) - 1);
+        if (!reject_allones) return PA_OK;
+        bool all = true;
+        for (uint64_t i = 0; i < nw32 && all; i++) {
+            const uint32_t want = (i == nw32 - 1 && bits % 32) ? (uint32_t)((1ull << (bits % 32)) - 1) : 0xFFFFFFFFu;
+            all = (w[i] == want);
+        }
+        if (!all) return PA_OK;
+    }
+}
+
+static const uint64_t kStreamB = 1ull << 63, kStreamC = (1ull << 63) + 1;
+
+static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
+    Plan &p = c->pl;
+    TRY(setup_stage(c->da, p.mmh, c->smmh));
+    TRY(setup_stage(c->da, p.mh, c->smh));
+    c->nblk = (uint32_t)(p.b1 - p.b0);
+    const uint32_t Lm = c->smmh.L, Pm = p.mmh.nprimes;
+    const uint32_t Lh = c->smh.L, Ph = p.mh.nprimes;
+    const uint32_t Bm = p.mmh.limb_bits, Bh = p.mh.limb_bits;
+    const uint64_t wx = cdiv(p.r, Bm), wa = cdiv(p.gamma, Bm);
+    c->ncoef_mmh = wx + wa - 1;
+    c->W_Y = cdiv(Bm * (c->ncoef_mmh - 1) + 32 * Pm, 32) + 1;
+    c->Wg = cdiv(p.gamma, 32);
+    c->W_Z = cdiv(p.alpha, 32);
+    const uint64_t Wa32 = cdiv(p.gamma, 32), Wal32 = cdiv(p.alpha, 32);
+    TRY(c->da.alloc(&c->ahat, (size_t)c->nblk * Pm * Lm));
+    TRY(c->da.alloc(&c->scratch, (size_t)c->nblk * Pm * Lm));
+    TRY(c->da.alloc(&c->acc, (size_t)Pm * Lm));
+    TRY(c->da.alloc(&c->bhat, (size_t)Ph * Lh));
+    TRY(c->da.alloc(&c->scratch_mh, (size_t)Ph * Lh));
+    TRY(c->da.alloc(&c->acc_mh, (size_t)Ph * Lh));
+    TRY(c->da.alloc(&c->c_words, Wal32));
+    const uint64_t Smax = std::max<uint64_t>(std::max<uint64_t>(c->W_Y, c->W_Z), c->Wg + 2);
+    TRY(c->da.alloc(&c->S, Smax));
+    TRY(c->da.alloc(&c->Y, c->W_Y));
+    TRY(c->da.alloc(&c->y1, c->Wg + 2));
+    TRY(c->da.alloc(&c->y2, c->Wg + 2));
+    TRY(c->da.alloc(&c->Z, c->W_Z));
+    const uint64_t ntmax = cdiv(Smax, kTile);
+    TRY(c->da.alloc(&c->tg, ntmax));
+    TRY(c->da.alloc(&c->tp, ntmax));
+    TRY(c->da.alloc(&c->tcin, ntmax));
+    TRY(c->da.alloc(&c->flag, 4));
+
+    // ---- hash keys (reading A7): a_i for the shard's blocks, b, c
+    std::vector<uint32_t> aw((size_t)c->nblk * Wa32), bw, cw, tmp;
+    for (uint32_t i = 0; i < c->nblk; i++) {
+        if (prm->a_words) {
+            memcpy(&aw[(size_t)i * Wa32], prm->a_words + (size_t)i * Wa32, Wa32 * 4);
+        } else {
+            TRY(expand_words(p.seed, p.b0 + i, p.gamma, tmp, true));
+            memcpy(&aw[(size_t)i * Wa32], tmp.data(), Wa32 * 4);
+        }
+    }
+    if (prm->b_words) bw.assign(prm->b_words, prm->b_words + Wal32);
+    else { TRY(expand_words(p.seed, kStreamB, p.alpha, bw, false)); bw[0] |= 1u; }
+    if (prm->c_words) cw.assign(prm->c_words, prm->c_words + Wal32);
+    else TRY(expand_words(p.seed, kStreamC, p.alpha, cw, false));
+    if (!(bw[0] & 1u)) return set_err(PA_E_PARAM, "b must be odd (PAPER.md:97)");
+    if (p.alpha % 32) {
+        const uint32_t mask = (uint32_t)((1ull << (p.alpha % 32)) - 1);
+        if ((bw[Wal32 - 1] & ~mask) || (cw[Wal32 - 1] & ~mask)) return set_err(PA_E_PARAM, "b, c must be < 2^alpha");
+    }
+    // a_i < p check for explicit keys (all-ones over gamma bits is p itself)
+    if (prm->a_words) {
+        for (uint32_t i = 0; i < c->nblk; i++) {
+            bool all = true;
+            for (uint64_t w = 0; w < Wa32 && all; w++) {
+                const uint32_t want = (w == Wa32 - 1 && p.gamma % 32) ? (uint32_t)((1ull << (p.gamma % 32)) - 1) : 0xFFFFFFFFu;
+                const uint32_t got = aw[(size_t)i * Wa32 + w];
+                if (w == Wa32 - 1 && p.gamma % 32 && (got & ~want)) return set_err(PA_E_PARAM, "a_i must be < p");
+                all = (got == want);
+            }
+            if (all) return set_err(PA_E_PARAM, "a_i must be < p (got p)");
+        }
+    }
+    uint32_t *a_dev = nullptr, *b_dev = nullptr;
+    CUDA_TRY(cudaMalloc(&a_dev, std::max<size_t>(aw.size() * 4, 16)));
+    CUDA_TRY(cudaMalloc(&b_dev, Wal32 * 4));
+    CUDA_TRY(cudaMemcpyAsync(a_dev, aw.data(), aw.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(b_dev, bw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->c_words, cw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
+    WordSrc wsa{a_dev, (uint32_t)Wa32, Bm, (uint32_t)wa};
+    int rc = precompute_hat(c, c->smmh, wsa, c->nblk, c->scratch, c->ahat);
+    WordSrc wsb{b_dev, (uint32_t)Wal32, Bh, (uint32_t)cdiv(p.alpha, Bh)};
+    if (rc == PA_OK) rc = precompute_hat(c, c->smh, wsb, 1, c->scratch_mh, c->bhat);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(a_dev);
+    cudaFree(b_dev);
+    if (rc != PA_OK) return rc;
+    if (e != cudaSuccess) return set_err(PA_E_CUDA, "precompute failed: %s", cudaGetErrorString(e));
+    return PA_OK;
+}
+
+extern "C" int pa_plan(const pa_params *prm, pa_info *info) {
+    Plan p;
+    TRY(make_plan(prm, &p));
+    if (info) {
+        memset(info, 0, sizeof *info);
+        info->n = p.n; info->r = p.r; info->m = p.m; info->gamma = p.gamma; info->alpha = p.alpha;
+        info->k = p.k; info->block_begin = p.b0; info->block_end = p.b1;
+        info->mmh = p.mmh; info->mh = p.mh;
+        const uint64_t nb = p.b1 - p.b0;
+        info->device_bytes = 4ull * (2 * nb + 1) * p.mmh.nprimes * (1ull << p.mmh.log2_len) +
+                             4ull * 3 * p.mh.nprimes * (1ull << p.mh.log2_len);
+    }
+    return PA_OK;
+}
+
+extern "C" int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out) {
+    if (!out) return set_err(PA_E_PARAM, "out is NULL");
+    *out = nullptr;
+    Plan p;
+    TRY(make_plan(prm, &p));
+    pa_ctx *c = new (std::nothrow) pa_ctx();
+    if (!c) return set_err(PA_E_NOMEM, "host allocation failed");
+    c->pl = p;
+    c->stream = (cudaStream_t)prm->stream;
+    int rc = PA_OK;
+    if (cudaGetDevice(&c->device) != cudaSuccess) rc = set_err(PA_E_CUDA, "no CUDA device");
+    if (rc == PA_OK && !g_num_sms) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, c->device) != cudaSuccess) rc = set_err(PA_E_CUDA, "cudaGetDeviceProperties failed");
+        else g_num_sms = prop.multiProcessorCount;
+    }
+    if (rc == PA_OK) rc = ctx_alloc_and_precompute(c, prm);
+    if (rc != PA_OK) {
+        c->da.free_all();
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return PA_OK;
+}
+
+extern "C" pa_ctx *pa_ctx_create(uint64_t n, uint64_t r, uint64_t m, uint64_t p, uint64_t seed) {
+    pa_params prm{};
+    prm.n = n; prm.r = r; prm.m = m; prm.gamma = p; prm.seed = seed;
+    pa_ctx *c = nullptr;
+    if (pa_ctx_create_ex(&prm, &c) != PA_OK) return nullptr;
+    return c;
+}
+
+extern "C" void pa_ctx_destroy(pa_ctx *c) {
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    else cudaDeviceSynchronize();
+    for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : c->evpool) cudaEventDestroy(e);
+    if (c->key_dev) cudaFree(c->key_dev);
+    if (c->out_dev) cudaFree(c->out_dev);
+    if (c->parts_dev) cudaFree(c->parts_dev);
+    c->da.free_all();
+    delete c;
+}
+
+extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
+    if (!c || !info) return set_err(PA_E_PARAM, "NULL argument");
+    memset(info, 0, sizeof *info);
+    const Plan &p = c->pl;
+    info->n = p.n; info->r = p.r; info->m = p.m; info->gamma = p.gamma; info->alpha = p.alpha;
+    info->k = p.k; info->block_begin = p.b0; info->block_end = p.b1;
+    info->mmh = p.mmh; info->mh = p.mh;
+    info->device_bytes = c->da.bytes;
+    info->kernels_per_hash = c->launches;
+    return PA_OK;
+}
+
+extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
+    if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    c->stream = (cudaStream_t)stream;
+    return PA_OK;
+}
+
+// ---- S1-S5 on this ctx's blocks -> canonical y in c->y1 (Wg words, +1 zero word)
+static int run_mmh(pa_ctx *c, const uint8_t *key_slice) {
+    const Plan &p = c->pl;
+    const uint64_t slice_bytes_total = cdiv(p.n, 8);
+    const uint64_t off = p.b0 * (p.r / 8);
+    const uint64_t nbytes = std::min<uint64_t>(slice_bytes_total - std::min(off, slice_bytes_total), (p.b1 - p.b0) * (p.r / 8));
+    KeySrc ks{};
+    ks.key = key_slice;
+    ks.nbytes = nbytes;
+    // bits >= n ignored: if this slice holds the last key byte, mask its pad bits
+    const bool has_last = (off + nbytes == slice_bytes_total);
+    ks.last_mask = (has_last && (p.n % 8)) ? ((0xFFu << (8 - p.n % 8)) & 0xFFu) : 0xFFu;
+    ks.blk_bytes = (uint32_t)(p.r / 8);
+    ks.limb_bytes = p.mmh.limb_bits / 8;
+    ks.wx = (uint32_t)cdiv(p.r, p.mmh.limb_bits);
+    ks.aligned = (((uintptr_t)key_slice) & 3) == 0;
+    TRY(stage_transform(c, c->smmh, COL_KEY, &ks, nullptr, c->nblk, c->scratch, c->ahat, c->acc,
+                        "mmh_fwd_col_pack", "mmh_fwd_row_mac", "mmh_inverse"));
+    {
+        ProfScope ps(c, "mmh_crt_carry");
+        const uint32_t W = (uint32_t)c->W_Y;
+        crt_colsum<<<(uint32_t)cdiv(W, 256), 256, 0, c->stream>>>(c->acc, c->smmh.L, (uint32_t)c->ncoef_mmh,
+                                                                   p.mmh.limb_bits, c->smmh.crt, nullptr, 0, c->S, W);
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+        TRY(run_carry(c, W, c->Y));
+    }
+    {
+        ProfScope ps(c, "mmh_fold");
+        const uint32_t Wf = (uint32_t)c->Wg + 1;
+        fold_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->Y, c->W_Y, p.gamma, c->S, Wf);
+        c->launches++;
+        TRY(run_carry(c, Wf, c->y1));
+        for (int it = 0; it < 2; it++) {
+            fold_final_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, p.gamma, c->S, Wf);
+            c->launches++;
+            TRY(run_carry(c, Wf, c->y1));
+        }
+        CUDA_TRY(cudaMemsetAsync(c->flag, 0, 4, c->stream));
+        allones_check<<<std::max(1, g_num_sms), 256, 0, c->stream>>>(c->y1, p.gamma, c->flag);
+        zero_if_allones<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, Wf, c->flag);
+        c->launches += 2;
+        CUDA_TRY(cudaGetLastError());
+    }
+    return PA_OK;
+}
+
+// ---- S7 on canonical y (Wg words + zero word) -> out_bits
+static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
+    const Plan &p = c->pl;
+    const uint32_t Bh = p.mh.limb_bits;
+    WordSrc ws{y, (uint32_t)c->Wg, Bh, (uint32_t)cdiv(p.gamma, Bh)};
+    TRY(stage_transform(c, c->smh, COL_WORDS, nullptr, &ws, 1, c->scratch_mh, c->bhat, c->acc_mh,
+                        "mh_fwd_col", "mh_fwd_row_mac", "mh_inverse"));
+    {
+        ProfScope ps(c, "mh_crt_carry_extract");
+        const uint32_t W = (uint32_t)c->W_Z;
+        const uint64_t ncoef = std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1);
+        crt_colsum<<<(uint32_t)cdiv(W, 256), 256, 0, c->stream>>>(c->acc_mh, c->smh.L, (uint32_t)ncoef, Bh,
+                                                                   c->smh.crt, c->c_words, W, c->S, W);
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+        TRY(run_carry(c, W, c->Z));
+        const uint64_t nb = cdiv(p.m, 8);
+        mh_extract<<<(uint32_t)cdiv(nb, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+    }
+    return PA_OK;
+}
+
+extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
+    if (!c || !key_bits || !out_bits) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
+    c->launches = 0;
+    TRY(run_mmh(c, key_bits));
+    TRY(run_mh(c, c->y1, out_bits));
+    return PA_OK;
+}
+
+__global__ void copy_words(const uint32_t *__restrict__ a, uint32_t *__restrict__ b, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+
+extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
+    if (!c || !key_slice || !y_out) return set_err(PA_E_PARAM, "NULL argument");
+    c->launches = 0;
+    TRY(run_mmh(c, key_slice));
+    CUDA_TRY(cudaMemcpyAsync(y_out, c->y1, c->Wg * 4, cudaMemcpyDeviceToDevice, c->stream));
+    return PA_OK;
+}
+
+__global__ void sum_parts_colsum(const uint32_t *__restrict__ parts, uint32_t G, uint32_t Wg,
+                                 uint64_t *__restrict__ S, uint32_t Wout) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= Wout) return;
+    uint64_t s = 0;
+    if (u < Wg)
+        for (uint32_t g = 0; g < G; g++) s += parts[(size_t)g * Wg + u];
+    S[u] = s;
+}
+
+extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits) {
+    if (!c || !y_parts || !out_bits || G == 0) return set_err(PA_E_PARAM, "bad argument");
+    if (G > (1u << 24)) return set_err(PA_E_PARAM, "too many parts");
+    c->launches = 0;
+    const Plan &p = c->pl;
+    const uint32_t Wf = (uint32_t)c->Wg + 1;
+    {
+        ProfScope ps(c, "merge_sum_fold");
+        sum_parts_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(y_parts, G, (uint32_t)c->Wg, c->S, Wf);
+        c->launches++;
+        TRY(run_carry(c, Wf, c->y1));
+        // sum < G 2^gamma: fold the high part (< G) back until < 2^gamma
+        for (int it = 0; it < 2; it++) {
+            fold_final_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, p.gamma, c->S, Wf);
+            c->launches++;
+            TRY(run_carry(c, Wf, c->y1));
+        }
+        CUDA_TRY(cudaMemsetAsync(c->flag, 0, 4, c->stream));
+        allones_check<<<std::max(1, g_num_sms), 256, 0, c->stream>>>(c->y1, p.gamma, c->flag);
+        zero_if_allones<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, Wf, c->flag);
+        c->launches += 2;
+        CUDA_TRY(cudaGetLastError());
+    }
+    TRY(run_mh(c, c->y1, out_bits));
+    return PA_OK;
+}
+
+extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
+    if (!c || !key_host || !out_host) return set_err(PA_E_PARAM, "NULL argument");
+    const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
+    if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
+    if (!c->out_dev) CUDA_TRY(cudaMalloc(&c->out_dev, mb));
+    CUDA_TRY(cudaMemcpyAsync(c->key_dev, key_host, nb, cudaMemcpyHostToDevice, c->stream));
+    TRY(pa_hash(c, c->key_dev, c->out_dev));
+    CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return PA_OK;
+}
+
+extern "C" int pa_ctx_set_profiling(pa_ctx *c, int enable) {
+    if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    c->prof = enable != 0;
+    return PA_OK;
+}
+
+extern "C" int pa_ctx_stage_times(pa_ctx *c, const char **names, double *ms, uint32_t *launches, int max) {
+    if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (auto &r : c->recs) {
+        float t = 0;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        auto &slot = c->acc_ms[r.name];
+        slot.first += t;
+        slot.second += 1;
+        c->evpool.push_back(r.a);
+        c->evpool.push_back(r.b);
+    }
+    c->recs.clear();
+    if (max < 0) { c->acc_ms.clear(); return 0; }
+    int i = 0;
+    for (auto &kv : c->acc_ms) {
+        if (i >= max) break;
+        if (names) names[i] = kv.first.c_str();   // map keys: stable while the ctx lives
+        if (ms) ms[i] = kv.second.first;
+        if (launches) launches[i] = kv.second.second;
+        i++;
+    }
+    return i;
+}
+
+// ---------------------------------------------------------------- host helpers
+extern "C" int pa_philox4x64_10(uint64_t key0, uint64_t key1, uint64_t nwords, uint64_t *out) {
+    if (!out && nwords) return set_err(PA_E_PARAM, "NULL out");
+    Philox4x64::words(key0, key1, 0, nwords, out);
+    return PA_OK;
+}
+
+extern "C" int pa_expand_a(uint64_t seed, uint64_t i, uint64_t gamma, uint32_t *out) {
+    if (!out || !gamma) return set_err(PA_E_PARAM, "bad argument");
+    std::vector<uint32_t> w;
+    TRY(expand_words(seed, i, gamma, w, true));
+    memcpy(out, w.data(), w.size() * 4);
+    return PA_OK;
+}
+
+extern "C" int pa_expand_bc(uint64_t seed, uint64_t alpha, uint32_t *b_out, uint32_t *c_out) {
+    if (!b_out || !c_out || !alpha) return set_err(PA_E_PARAM, "bad argument");
+    std::vector<uint32_t> w;
+    TRY(expand_words(seed, kStreamB, alpha, w, false));
+    w[0] |= 1u;
+    memcpy(b_out, w.data(), w.size() * 4);
+    TRY(expand_words(seed, kStreamC, alpha, w, false));
+    memcpy(c_out, w.data(), w.size() * 4);
+    return PA_OK;
+}

@@ -1,0 +1,309 @@
+// Column and row pass kernels of the four-step NTT (see ntt.cuh), with the hot-path
+// fusions:  S1 pack (key bits -> B-bit limbs -> residues) inside the forward column
+// pass, S3 multiply-accumulate against the precomputed transforms of the a_i inside
+// the forward row pass (Eq. 2's sum done in the transform domain), and
+// the inverse four-step twiddle inside the inverse row pass.
+#pragma once
+#include <cstdint>
+#include "modarith.cuh"
+#include "ntt.cuh"
+
+namespace pa {
+
+// ---------------------------------------------------------------- limb sources
+// S1 ("split the input bit sequence and map it to a prime field"):
+// block i of the key = bytes [i R, (i+1) R) of the slice, a big-endian integer
+// (MSB-first bits, reading A4); limb j = bits [B j, B j + B) of that integer.
+struct KeySrc {
+    const uint8_t *key;     // slice base
+    uint64_t nbytes;        // valid bytes in the slice (bytes beyond read as 0)
+    uint32_t last_mask;     // mask of the byte nbytes-1 (bits >= n ignored)
+    uint32_t blk_bytes;     // R = r / 8
+    uint32_t limb_bytes;    // B / 8
+    uint32_t wx;            // limbs per block = ceil(r / B)
+    uint32_t aligned;       // key pointer 4-byte aligned
+};
+
+__device__ __forceinline__ uint32_t key_word(const KeySrc &s, int64_t widx) {
+    const int64_t base = widx * 4;
+    if (base < 0) return 0;
+    if (s.aligned && base + 4 < (int64_t)s.nbytes)
+        return __ldg(reinterpret_cast<const uint32_t *>(s.key) + widx);
+    uint32_t w = 0;
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+        const int64_t pos = base + b;
+        if (pos < (int64_t)s.nbytes) {
+            uint32_t v = s.key[pos];
+            if (pos == (int64_t)s.nbytes - 1) v &= s.last_mask;
+            w |= v << (8 * b);
+        }
+    }
+    return w;
+}
+
+__device__ __forceinline__ uint64_t key_limb(const KeySrc &s, uint32_t blk, uint32_t j) {
+    if (j >= s.wx) return 0;
+    const int64_t start = (int64_t)blk * s.blk_bytes;
+    const int64_t end = start + s.blk_bytes;
+    int64_t lo = end - (int64_t)(j + 1) * s.limb_bytes;
+    const int64_t hi = end - (int64_t)j * s.limb_bytes;
+    if (lo < start) lo = start;
+    const int nb = (int)(hi - lo);                          // 1..8 bytes
+    const int64_t w0 = lo >> 2;
+    const int sh = (int)(lo & 3) * 8;
+    const uint32_t a0 = key_word(s, w0), a1 = key_word(s, w0 + 1), a2 = key_word(s, w0 + 2);
+    const uint32_t lo32 = __funnelshift_r(a0, a1, sh);      // bytes lo..lo+3 (memory order)
+    const uint32_t hi32 = __funnelshift_r(a1, a2, sh);      // bytes lo+4..lo+7
+    // big-endian value of the first nb bytes
+    const uint64_t be = ((uint64_t)__byte_perm(lo32, 0, 0x0123) << 32) | __byte_perm(hi32, 0, 0x0123);
+    return be >> (64 - 8 * nb);
+}
+
+// Little-endian 32-bit word vectors (a_i, b, y): limb j = bits [B j, B j + B).
+struct WordSrc {
+    const uint32_t *w;
+    uint32_t words;         // words per vector (stride); words beyond are read as 0
+    uint32_t limb_bits;     // B
+    uint32_t nlimbs;        // limbs per vector
+};
+
+__device__ __forceinline__ uint64_t word_limb(const WordSrc &s, uint32_t vec, uint32_t j) {
+    if (j >= s.nlimbs) return 0;
+    const uint64_t bit = (uint64_t)j * s.limb_bits;
+    const uint32_t wi = (uint32_t)(bit >> 5);
+    const int sh = (int)(bit & 31);
+    const uint32_t *base = s.w + (size_t)vec * s.words;
+    const uint32_t a0 = wi < s.words ? __ldg(base + wi) : 0u;
+    const uint32_t a1 = wi + 1 < s.words ? __ldg(base + wi + 1) : 0u;
+    const uint32_t a2 = wi + 2 < s.words ? __ldg(base + wi + 2) : 0u;
+    const uint64_t v = ((uint64_t)__funnelshift_r(a1, a2, sh) << 32) | __funnelshift_r(a0, a1, sh);
+    return s.limb_bits >= 64 ? v : (v & ((1ull << s.limb_bits) - 1));
+}
+
+// x mod p in [0, 2p) for a 64-bit limb value (c32 = 2^32 mod p, Shoup companions).
+struct LimbRed {
+    uint32_t c32, c32p, c1p;
+};
+__device__ __forceinline__ uint32_t limb_mod(uint64_t v, const LimbRed &lr, uint32_t p, uint32_t p2) {
+    const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+    const uint32_t rlo = mul_shoup(lo, 1u, lr.c1p, p);
+    const uint32_t rhi = mul_shoup(hi, lr.c32, lr.c32p, p);
+    return red2p(rlo + rhi, p2);
+}
+
+// ---------------------------------------------------------------- column pass
+enum ColMode { COL_KEY = 0, COL_WORDS = 1, COL_INV = 2 };
+
+struct ColArgs {
+    NttArgs nt;
+    KeySrc ks;
+    WordSrc ws;
+    const LimbRed *lred;     // [P]
+    const uint32_t *src;     // COL_INV: residues [P][L]
+    uint32_t *dst;           // forward: [nvec][P][L]; inverse: [P][L]
+    uint32_t nvec;           // vectors (blocks) per prime
+    uint32_t units;          // (N1/32) * P * nvec
+};
+
+// One CTA = 32 adjacent columns (one lane each) x S/E threads per column.
+template <int S_LOG, int E_LOG, int MODE>
+__global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)))
+col_pass(const ColArgs A) {
+    using SP = SubPlan<S_LOG, E_LOG>;
+    constexpr int E = SP::E;
+    extern __shared__ uint32_t sm[];
+    const int c = threadIdx.x & 31;
+    const int v = threadIdx.x >> 5;
+    const NttArgs &a = A.nt;
+    const uint32_t L = 1u << a.log2L;
+    const uint32_t P = a.nprimes;
+    const uint32_t ncg = a.n1 >> 5;
+    const uint32_t u0 = (uint32_t)(((uint64_t)blockIdx.x * A.units) / gridDim.x);
+    const uint32_t u1 = (uint32_t)(((uint64_t)(blockIdx.x + 1) * A.units) / gridDim.x);
+    auto sidx = [c](int pos) { return pos * 32 + c; };
+
+    uint32_t tw[E / 2], twp[E / 2], pw[E];
+    int cur_pair = -1;
+    Ctx32 cx{};
+    LimbRed lr{};
+    const uint32_t *rtw_p = nullptr;
+
+    for (uint32_t u = u0; u < u1; u++) {
+        const uint32_t iv = u % A.nvec;
+        const uint32_t pair = u / A.nvec;           // (cg, pi)
+        const uint32_t pi = pair % P;
+        const uint32_t cg = pair / P;
+        const uint32_t j1 = cg * 32 + c;
+        (void)ncg;
+        if ((int)pair != cur_pair) {
+            cur_pair = (int)pair;
+            const PrimeK pk = a.pk[pi];
+            cx.p = pk.p; cx.p2 = pk.p2; cx.pinv = pk.pinv;
+#pragma unroll
+            for (int j = 0; j < E / 2; j++) {
+                tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j);
+                twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j);
+            }
+            rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
+            if constexpr (MODE != COL_INV) {
+                lr = A.lred[pi];
+#pragma unroll
+                for (int h = 0; h < E / (1 << SP::rlog(SP::Q - 1)); h++) {
+                    constexpr int R = 1 << SP::rlog(SP::Q - 1);
+#pragma unroll
+                    for (int mm = 0; mm < R; mm++) {
+                        const uint32_t k2 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
+                        const uint32_t e = (uint32_t)(((uint64_t)j1 * k2) & (L - 1));
+                        pw[h * R + mm] = ltw_mont(a, pi, e, cx.p, cx.pinv);
+                    }
+                }
+            }
+        }
+        uint32_t x[E];
+        // ---- round 0 loads
+        {
+            constexpr int R = 1 << SP::rlog(0);
+#pragma unroll
+            for (int h = 0; h < E / R; h++) {
+#pragma unroll
+                for (int m = 0; m < R; m++) {
+                    const uint32_t j2 = (uint32_t)in_pos<S_LOG, E_LOG>(v, h, m);
+                    uint32_t val;
+                    if constexpr (MODE == COL_KEY) {
+                        val = limb_mod(key_limb(A.ks, iv, j1 + a.n1 * j2), lr, cx.p, cx.p2);
+                    } else if constexpr (MODE == COL_WORDS) {
+                        val = limb_mod(word_limb(A.ws, iv, j1 + a.n1 * j2), lr, cx.p, cx.p2);
+                    } else {
+                        val = A.src[(size_t)pi * L + (size_t)j2 * a.n1 + j1];
+                    }
+                    x[h * R + m] = val;
+                }
+            }
+        }
+        __syncthreads();    // previous unit's last-round smem reads are done
+        round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+        rounds_rest<S_LOG, E_LOG, 1>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+        // ---- outputs
+        {
+            constexpr int R = 1 << SP::rlog(SP::Q - 1);
+            uint32_t *dst = (MODE == COL_INV) ? A.dst + (size_t)pi * L
+                                              : A.dst + ((size_t)iv * P + pi) * L;
+#pragma unroll
+            for (int h = 0; h < E / R; h++) {
+#pragma unroll
+                for (int mm = 0; mm < R; mm++) {
+                    const uint32_t k2 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
+                    uint32_t val = x[h * R + mm];
+                    if constexpr (MODE != COL_INV) val = mul_mont(val, pw[h * R + mm], cx.p, cx.pinv);
+                    else val = red1p(val, cx.p);
+                    dst[(size_t)k2 * a.n1 + j1] = val;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- row pass
+enum RowMode { ROW_MAC = 0, ROW_STORE = 1, ROW_INV = 2 };
+
+struct RowArgs {
+    NttArgs nt;
+    const uint32_t *src;      // MAC/STORE: [nvec][P][L];  INV: [P][L]
+    uint32_t *dst;            // MAC: [P][L] accumulators;  STORE: [nvec][P][L];  INV: [P][L]
+    const uint32_t *ahat;     // MAC: [nvec][P][L] (Montgomery form, times 1/L)
+    const uint32_t *scale;    // STORE: [P] Montgomery constant multiplied into outputs
+    uint32_t nvec;
+    uint32_t units;           // (N2 / V) * P
+};
+
+template <int S_LOG, int E_LOG, int V, int MODE>
+__global__ void __launch_bounds__(V * (1 << (S_LOG - E_LOG)))
+row_pass(const RowArgs A) {
+    using SP = SubPlan<S_LOG, E_LOG>;
+    constexpr int S = SP::S, E = SP::E;
+    constexpr int RS = S + S / 32;                       // padded row stride in smem
+    extern __shared__ uint32_t sm[];
+    const int w = threadIdx.x / SP::TPV;
+    const int v = threadIdx.x % SP::TPV;
+    const NttArgs &a = A.nt;
+    const uint32_t L = 1u << a.log2L;
+    const uint32_t P = a.nprimes;
+    auto sidx = [w](int pos) { return w * RS + pos + (pos >> 5); };
+
+    for (uint32_t u = blockIdx.x; u < A.units; u += gridDim.x) {
+        const uint32_t pi = u % P;
+        const uint32_t rg = u / P;
+        const uint32_t k2 = rg * V + w;                  // row index
+        const PrimeK pk = a.pk[pi];
+        const Ctx32 cx{pk.p, pk.p2, pk.pinv};
+        uint32_t tw[E / 2], twp[E / 2];
+#pragma unroll
+        for (int j = 0; j < E / 2; j++) {
+            tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j);
+            twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j);
+        }
+        const uint32_t *rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
+        uint32_t acc[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) acc[e] = 0;
+        const uint32_t nv = (MODE == ROW_INV) ? 1u : A.nvec;
+        for (uint32_t iv = 0; iv < nv; iv++) {
+            const size_t vbase = (MODE == ROW_INV) ? (size_t)pi * L : ((size_t)iv * P + pi) * L;
+            const uint32_t *src = A.src + vbase + (size_t)k2 * S;
+            uint32_t x[E];
+            {
+                constexpr int R = 1 << SP::rlog(0);
+#pragma unroll
+                for (int h = 0; h < E / R; h++)
+#pragma unroll
+                    for (int m = 0; m < R; m++) x[h * R + m] = src[in_pos<S_LOG, E_LOG>(v, h, m)];
+            }
+            __syncthreads();
+            round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+            rounds_rest<S_LOG, E_LOG, 1>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+            constexpr int R = 1 << SP::rlog(SP::Q - 1);
+            if constexpr (MODE == ROW_MAC) {
+                const uint32_t *ah = A.ahat + vbase + (size_t)k2 * S;
+#pragma unroll
+                for (int h = 0; h < E / R; h++)
+#pragma unroll
+                    for (int mm = 0; mm < R; mm++) {
+                        const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
+                        acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], __ldg(ah + k1), cx.p, cx.pinv), cx.p2);
+                    }
+            } else if constexpr (MODE == ROW_STORE) {
+                const uint32_t sc = A.scale[pi];
+                uint32_t *dst = A.dst + vbase + (size_t)k2 * S;
+#pragma unroll
+                for (int h = 0; h < E / R; h++)
+#pragma unroll
+                    for (int mm = 0; mm < R; mm++) {
+                        const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
+                        dst[k1] = red1p(mul_mont(x[h * R + mm], sc, cx.p, cx.pinv), cx.p);
+                    }
+            } else {
+                uint32_t *dst = A.dst + vbase + (size_t)k2 * S;
+#pragma unroll
+                for (int h = 0; h < E / R; h++)
+#pragma unroll
+                    for (int mm = 0; mm < R; mm++) {
+                        const uint32_t j1 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
+                        const uint32_t e = (uint32_t)(((uint64_t)j1 * k2) & (L - 1));
+                        dst[j1] = mul_mont(x[h * R + mm], ltw_mont(a, pi, e, cx.p, cx.pinv), cx.p, cx.pinv);
+                    }
+            }
+        }
+        if constexpr (MODE == ROW_MAC) {
+            constexpr int R = 1 << SP::rlog(SP::Q - 1);
+            uint32_t *dst = A.dst + (size_t)pi * L + (size_t)k2 * S;
+#pragma unroll
+            for (int h = 0; h < E / R; h++)
+#pragma unroll
+                for (int mm = 0; mm < R; mm++) dst[out_pos<S_LOG, E_LOG>(v, h, mm)] = acc[h * R + mm];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace pa

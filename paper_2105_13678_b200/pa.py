@@ -1,0 +1,204 @@
+"""Python surface of the library: a context object over include/pa.h.
+
+Marshalling only: torch tensors give device memory and the CUDA stream, the C ABI
+does the work.  Shard planning for multi-GPU ("split and separately
+handle"; SPEC.md:161 split-merge) is host logic and lives here too.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _binding as B
+
+
+def _words(v: int, bits: int) -> np.ndarray:
+    nw = (bits + 31) // 32
+    return np.frombuffer(int(v).to_bytes(4 * nw, "little"), dtype="<u4").copy()
+
+
+def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
+            stream=None, limb_bits=0, strict=False, keep=None) -> B.pa_params:
+    prm = B.pa_params()
+    prm.n, prm.r, prm.m, prm.gamma, prm.seed = n, r, m, gamma, seed & (2**64 - 1)
+    if block_range is not None:
+        prm.block_begin, prm.block_end = block_range
+    prm.limb_bits = limb_bits
+    prm.strict = 1 if strict else 0
+    prm.stream = stream
+    keep = [] if keep is None else keep
+    if a is not None or b is not None or c is not None:
+        info = plan(n, r, m, gamma, block_range=block_range, limb_bits=limb_bits)
+        g, alpha = info["gamma"], info["alpha"]
+        if a is not None:
+            aw = np.concatenate([_words(v, g) for v in a]).astype("<u4")
+            keep.append(aw)
+            prm.a_words = aw.ctypes.data
+        if b is not None:
+            bw = _words(b, alpha)
+            keep.append(bw)
+            prm.b_words = bw.ctypes.data
+        if c is not None:
+            cw = _words(c, alpha)
+            keep.append(cw)
+            prm.c_words = cw.ctypes.data
+    return prm
+
+
+def plan(n: int, r: int, m: int, gamma: int = 0, block_range=None, limb_bits: int = 0,
+         strict: bool = False) -> dict:
+    """Validate parameters and return the transform plan (host only, no GPU)."""
+    prm = _params(n, r, m, gamma, 0, block_range, limb_bits=limb_bits, strict=strict)
+    info = B.pa_info()
+    B.check(B.pa_plan(ctypes.byref(prm), ctypes.byref(info)))
+    return info.as_dict()
+
+
+def shard_ranges(k: int, G: int) -> list[tuple[int, int]]:
+    """Rank g owns blocks [floor(k g / G), floor(k (g+1) / G))."""
+    return [(k * g // G, k * (g + 1) // G) for g in range(G)]
+
+
+class PAContext:
+    """One MMH-MH hash function (a_i, b, c fixed by `seed` or given explicitly) on the
+    current CUDA device; see include/pa.h for the exact semantics."""
+
+    def __init__(self, n: int, r: int, m: int, gamma: int = 0, seed: int = 0, *,
+                 block_range=None, a=None, b=None, c=None, stream=None, limb_bits: int = 0,
+                 strict: bool = False):
+        import torch
+        if not torch.cuda.is_available():
+            raise B.PAError(B.PA_E_CUDA, "no CUDA device: the library has no CPU path")
+        self._torch = torch
+        st = stream if stream is not None else torch.cuda.current_stream()
+        self.stream = st
+        keep: list = []
+        prm = _params(n, r, m, gamma, seed, block_range, a, b, c, ctypes.c_void_p(st.cuda_stream),
+                      limb_bits, strict, keep)
+        h = ctypes.c_void_p()
+        B.check(B.pa_ctx_create_ex(ctypes.byref(prm), ctypes.byref(h)))
+        self._h = h
+        self.info = self.query()
+        self.n, self.r, self.m = n, r, m
+        self.gamma, self.alpha, self.k = self.info["gamma"], self.info["alpha"], self.info["k"]
+        self.block_range = (self.info["block_begin"], self.info["block_end"])
+        self.nbytes_in = (n + 7) // 8
+        self.nbytes_out = (m + 7) // 8
+        self.y_words = (self.gamma + 31) // 32
+
+    # ------------------------------------------------------------------ queries
+    def query(self) -> dict:
+        info = B.pa_info()
+        B.check(B.pa_ctx_query(self._h, ctypes.byref(info)))
+        return info.as_dict()
+
+    def set_profiling(self, on: bool) -> None:
+        B.check(B.pa_ctx_set_profiling(self._h, 1 if on else 0))
+
+    def stage_times(self, reset: bool = False) -> dict:
+        names = (ctypes.c_char_p * 32)()
+        ms = (ctypes.c_double * 32)()
+        cnt = (ctypes.c_uint32 * 32)()
+        k = B.pa_ctx_stage_times(self._h, names, ms, cnt, 32)
+        if k < 0:
+            B.check(k)
+        out = {names[i].decode(): (ms[i], cnt[i]) for i in range(k)}
+        if reset:
+            B.pa_ctx_stage_times(self._h, None, None, None, -1)
+        return out
+
+    # ------------------------------------------------------------------ hashing
+    def _dev_u8(self, t, nbytes: int):
+        torch = self._torch
+        if not isinstance(t, torch.Tensor):
+            t = torch.as_tensor(np.asarray(t, dtype=np.uint8))
+        if t.device.type != "cuda":
+            t = t.to("cuda", non_blocking=False)
+        if t.dtype != torch.uint8 or not t.is_contiguous():
+            raise ValueError("expected a contiguous uint8 tensor")
+        if t.numel() < nbytes:
+            raise ValueError(f"buffer has {t.numel()} bytes, need {nbytes}")
+        return t
+
+    def hash(self, key, out=None):
+        """pa_hash: key = CUDA uint8 tensor of ceil(n/8) bytes -> CUDA uint8 tensor ceil(m/8)."""
+        torch = self._torch
+        key = self._dev_u8(key, self.nbytes_in)
+        if out is None:
+            out = torch.empty(self.nbytes_out, dtype=torch.uint8, device=key.device)
+        B.check(B.pa_hash(self._h, ctypes.c_void_p(key.data_ptr()), ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def hash_host(self, key_host, out_host=None):
+        """pa_hash_host: host buffers (numpy uint8 / pinned torch CPU tensor), synchronous."""
+        torch = self._torch
+        if isinstance(key_host, torch.Tensor):
+            kp = key_host.data_ptr()
+        else:
+            key_host = np.ascontiguousarray(key_host, dtype=np.uint8)
+            kp = key_host.ctypes.data
+        if out_host is None:
+            out_host = np.zeros(self.nbytes_out, dtype=np.uint8)
+        op = out_host.data_ptr() if isinstance(out_host, torch.Tensor) else out_host.ctypes.data
+        B.check(B.pa_hash_host(self._h, ctypes.c_void_p(kp), ctypes.c_void_p(op)))
+        return out_host
+
+    def mmh_partial(self, key_slice, y_out=None):
+        """pa_mmh_partial: this shard's residue as ceil(gamma/32) words (int32 CUDA tensor)."""
+        torch = self._torch
+        b0, b1 = self.block_range
+        key_slice = self._dev_u8(key_slice, 1)
+        if y_out is None:
+            y_out = torch.empty(self.y_words, dtype=torch.int32, device=key_slice.device)
+        B.check(B.pa_mmh_partial(self._h, ctypes.c_void_p(key_slice.data_ptr()), ctypes.c_void_p(y_out.data_ptr())))
+        return y_out
+
+    def mh_merge(self, y_parts, out=None):
+        """pa_mh_merge: y_parts = int32 CUDA tensor [G, ceil(gamma/32)] -> output bytes."""
+        torch = self._torch
+        y_parts = y_parts.contiguous()
+        G = y_parts.shape[0] if y_parts.dim() == 2 else 1
+        if out is None:
+            out = torch.empty(self.nbytes_out, dtype=torch.uint8, device=y_parts.device)
+        B.check(B.pa_mh_merge(self._h, ctypes.c_void_p(y_parts.data_ptr()), G, ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            B.pa_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def key_slice_bytes(n: int, r: int, block_range) -> tuple[int, int]:
+    """Byte range [lo, hi) of the key a shard context reads (include/pa.h, pa_hash)."""
+    b0, b1 = block_range
+    nb = (n + 7) // 8
+    return min(b0 * r // 8, nb), min(b1 * r // 8, nb)
+
+
+def distributed_hash(ctx: PAContext, key_slice, group=None, root: int = 0):
+    """Multi-GPU hash of one key (S6): every rank computes its shard residue, the
+    residues are all-gathered with torch.distributed (NCCL over NVLink on B200), and
+    `root` merges them mod p and runs MH.  Returns the output on root, else None."""
+    import torch
+    import torch.distributed as dist
+    y = ctx.mmh_partial(key_slice)
+    G = dist.get_world_size(group)
+    parts = torch.empty((G, y.numel()), dtype=y.dtype, device=y.device)
+    dist.all_gather_into_tensor(parts, y, group=group)
+    if dist.get_rank(group) == root:
+        return ctx.mh_merge(parts)
+    return None

@@ -62,7 +62,7 @@ def key_bytes(n_bits: int, key_seed: int) -> np.ndarray:
     last byte are left random on purpose: the hash must ignore them."""
     nbytes = (n_bits + 7) // 8
     nwords = (nbytes + 7) // 8
-    bg = np.random.Philox(key=[key_seed & (2**64 - 1), 0])
+    bg = np.random.Philox(key=np.array([key_seed & (2**64 - 1), 0], dtype=np.uint64))
     words = bg.random_raw(nwords).astype("<u8")
     return np.frombuffer(words.tobytes(), dtype=np.uint8)[:nbytes].copy()
 

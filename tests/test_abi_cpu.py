@@ -1,0 +1,133 @@
+"""CPU-side checks of the C ABI (-m "not gpu"): the library loads, exports every symbol
+include/pa.h declares, validates parameters, plans transforms whose CRT modulus covers
+the coefficient bound, and expands hash keys exactly as the oracle does (reading A7)."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2105_13678_b200 import _binding as B
+from paper_2105_13678_b200 import pa as P
+from oracle import seeds as oseeds
+from synth import CONFIGS
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_symbols_exported():
+    hdr = open(os.path.join(ROOT, "include", "pa.h")).read()
+    declared = set(re.findall(r"\b(pa_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    lib = ctypes.CDLL(B.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared in include/pa.h but not exported"
+    assert declared == set(B.EXPORTED)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(n=0, r=16, m=8), B.PA_E_PARAM),
+    (dict(n=100, r=15, m=8), B.PA_E_PARAM),
+    (dict(n=100, r=24, m=8), B.PA_E_PARAM),            # r % 16 != 0
+    (dict(n=100, r=16, m=0), B.PA_E_PARAM),
+    (dict(n=100, r=64, m=8, gamma=61), B.PA_E_PARAM),   # gamma <= r
+    (dict(n=100, r=64, m=8, gamma=67), B.PA_E_PARAM),   # not a Mersenne exponent
+    (dict(n=1000, r=64, m=100, gamma=89, strict=True), B.PA_E_PARAM),  # m >= gamma
+    (dict(n=1000, r=64, m=8, block_range=(3, 3)), B.PA_E_PARAM),
+    (dict(n=1000, r=64, m=8, block_range=(0, 17)), B.PA_E_PARAM),
+    (dict(n=1000, r=64, m=8, limb_bits=12), B.PA_E_PARAM),
+])
+def test_plan_rejects(kw, code):
+    with pytest.raises(B.PAError) as ei:
+        P.plan(**kw)
+    assert ei.value.code == code
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_plan_configs(name):
+    w = CONFIGS[name]
+    info = P.plan(w.n, w.r, w.m)
+    from oracle.hashes import plan_params
+    pp = plan_params(w.n, w.r, w.m)
+    assert info["gamma"] == pp["gamma"] and info["alpha"] == pp["alpha"] and info["k"] == pp["k"]
+    for st in ("mmh", "mh"):
+        s = info[st]
+        assert s["bound_log2"] < s["modulus_log2"]
+        # independent recomputation of the coefficient bound and the CRT modulus
+        Bl = s["limb_bits"]
+        if st == "mmh":
+            wa, wb, terms = -(-w.r // Bl), -(-pp["gamma"] // Bl), pp["k"]
+        else:
+            wa, wb, terms = -(-pp["gamma"] // Bl), -(-pp["alpha"] // Bl), 1
+        bound = terms * min(wa, wb) * (2 ** Bl - 1) ** 2
+        modulus = math.prod(s["primes"])
+        assert bound < modulus
+        assert (1 << s["log2_len"]) >= wa + wb - 1        # no cyclic wrap-around
+        assert s["n_col"] * s["n_row"] == 1 << s["log2_len"]
+        for p in s["primes"]:
+            assert p < 2 ** 30 and (p - 1) % (1 << s["log2_len"]) == 0
+            assert pow(3, p - 1, p) == 1 and all(p % d for d in range(2, 1000))
+
+
+def test_plan_forced_limb_bits():
+    for Bl in (16, 24, 32, 40, 48, 56, 64):
+        info = P.plan(1 << 20, 1 << 16, 100_000, limb_bits=Bl)
+        assert info["mmh"]["limb_bits"] == Bl and info["mh"]["limb_bits"] == Bl
+
+
+def test_philox_matches_numpy():
+    # T1: product-side Philox4x64-10 == numpy.random.Philox (library routine)
+    for key in [(0, 0), (5, 7), (2**64 - 1, 2**63), (0x5EED0004, 13)]:
+        out = np.zeros(37, dtype=np.uint64)
+        B.check(B.pa_philox4x64_10(key[0], key[1], 37, out.ctypes.data))
+        want = np.random.Philox(key=np.array(key, dtype=np.uint64)).random_raw(37)
+        assert np.array_equal(out, want)
+
+
+@pytest.mark.parametrize("seed,gamma,alpha", [(1234, 89, 200), (0x5EED0001, 86243, 104858), (7, 17, 40)])
+def test_expand_keys_match_oracle(seed, gamma, alpha):
+    for i in (0, 1, 5, 1000):
+        w = np.zeros((gamma + 31) // 32, dtype="<u4")
+        B.check(B.pa_expand_a(seed, i, gamma, w.ctypes.data))
+        assert int.from_bytes(w.tobytes(), "little") == oseeds.expand_a(seed, i, gamma)
+    bw = np.zeros((alpha + 31) // 32, dtype="<u4")
+    cw = np.zeros_like(bw)
+    B.check(B.pa_expand_bc(seed, alpha, bw.ctypes.data, cw.ctypes.data))
+    assert int.from_bytes(bw.tobytes(), "little") == oseeds.expand_b(seed, alpha)
+    assert int.from_bytes(cw.tobytes(), "little") == oseeds.expand_c(seed, alpha)
+
+
+def test_expand_a_rejection_matches_oracle():
+    # gamma = 17: an all-ones first draw is rare; search streams where it happens
+    found = 0
+    for i in range(300_000):
+        w = np.random.Philox(key=np.array([3, i], dtype=np.uint64)).random_raw(1)
+        if int(w[0]) & ((1 << 17) - 1) == (1 << 17) - 1:
+            out = np.zeros(1, dtype="<u4")
+            B.check(B.pa_expand_a(3, i, 17, out.ctypes.data))
+            assert int(out[0]) == oseeds.expand_a(3, i, 17) != (1 << 17) - 1
+            found += 1
+            if found == 2:
+                break
+    assert found >= 1
+
+
+def test_shard_ranges():
+    assert P.shard_ranges(31, 8) == [(0, 3), (3, 7), (7, 11), (11, 15), (15, 19), (19, 23), (23, 27), (27, 31)]
+    for k in (1, 7, 31, 2048):
+        for G in (1, 2, 3, 8):
+            rs = P.shard_ranges(k, G)
+            assert rs[0][0] == 0 and rs[-1][1] == k
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+    assert P.key_slice_bytes(1000, 64, (3, 16)) == (24, 125)
+
+
+def test_ctx_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(B.PAError):
+        P.PAContext(1 << 12, 256, 100)
+    assert not B.pa_ctx_create(1 << 12, 256, 100, 0, 1)

@@ -185,7 +185,7 @@ def test_seed_expansion_contract():
     assert all(0 <= v < (1 << 89) - 1 for v in a)
     assert b % 2 == 1 and 0 < b < (1 << 200) and 0 <= c < (1 << 200)
     # raw Philox words, little-endian, masked: numpy stream key (seed, i)
-    w = np.random.Philox(key=[1234, 3]).random_raw(2)
+    w = np.random.Philox(key=np.array([1234, 3], dtype=np.uint64)).random_raw(2)
     assert a[3] == (int(w[0]) | (int(w[1]) << 64)) & ((1 << 89) - 1)
 
 
@@ -193,7 +193,7 @@ def test_seed_rejection_of_all_ones():
     # an all-ones draw is rejected and the next draw taken
     hits = 0
     for i in range(400):
-        bg = np.random.Philox(key=[99, i])
+        bg = np.random.Philox(key=np.array([99, i], dtype=np.uint64))
         first = int(bg.random_raw(1)[0]) & 7
         second = int(bg.random_raw(1)[0]) & 7
         a = seeds.expand_a(99, i, 3)
