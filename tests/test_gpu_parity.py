@@ -1,0 +1,185 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Sizes are chosen so the oracle finishes in seconds while the transforms still span
+several tiles and ragged tails (n not a multiple of r or of 8, partial last limbs,
+m not a multiple of 8, m < gamma and m > gamma).  Full BASELINE.json sizes are checked
+against SHA-256 digests written by scripts/gen_golden.py from oracle/ only.
+"""
+import hashlib
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import hashes, seeds  # noqa: E402
+from synth import CONFIGS, key_bytes, special_key  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _pa():
+    from paper_2105_13678_b200 import PAContext
+    return PAContext
+
+
+def oracle_seeded(key, n, r, m, seed, gamma=None):
+    return hashes.pa_hash_seeded(key, n, r, m, seed, gamma)
+
+
+def gpu_hash(key, n, r, m, seed, **kw):
+    ctx = _pa()(n, r, m, seed=seed, **kw)
+    out = ctx.hash(torch.from_numpy(np.asarray(key)).cuda())
+    torch.cuda.synchronize()
+    res = bytes(out.cpu().numpy())
+    ctx.close()
+    return res
+
+
+CASES = [
+    # n, r, m
+    (4096, 256, 500),
+    (100_003, 1024, 5_000),          # ragged: n % r, n % 8, m % 8
+    (262_157, 2048, 30_001),          # m > gamma (2281)
+    (300_000, 4096, 4_000),           # m < gamma (4423)
+    (1 << 20, 1 << 16, 104_858),      # C1
+    (2_000_001, 1 << 14, 150_000),
+]
+
+
+@pytest.mark.parametrize("n,r,m", CASES)
+def test_parity_seeded(n, r, m):
+    key = key_bytes(n, n ^ 0xABC)
+    seed = (n * 7 + r) & 0xFFFFFFFF
+    assert gpu_hash(key, n, r, m, seed) == oracle_seeded(key, n, r, m, seed)
+
+
+def test_parity_C2():
+    w = CONFIGS["C2"]
+    key = key_bytes(w.n, w.key_seed)
+    assert gpu_hash(key, w.n, w.r, w.m, w.hash_seed) == oracle_seeded(key, w.n, w.r, w.m, w.hash_seed)
+
+
+@pytest.mark.parametrize("B", [16, 24, 32, 40, 48, 56, 64])
+def test_limb_width_invariance(B):
+    # reading A11: the limb width is internal and must not change the output
+    n, r, m = 70_001, 2048, 9_999
+    key = key_bytes(n, 5)
+    assert gpu_hash(key, n, r, m, 77, limb_bits=B) == oracle_seeded(key, n, r, m, 77)
+
+
+@pytest.mark.parametrize("kind,pos", [("zero", 0), ("ones", 0), ("alt", 0), ("bit", 0), ("bit", 2047),
+                                      ("bit", 2048), ("bit", 65_535)])
+def test_special_keys(kind, pos):
+    n, r, m = 65_536, 2048, 3_000
+    key = special_key(kind, n, pos)
+    assert gpu_hash(key, n, r, m, 3) == oracle_seeded(key, n, r, m, 3)
+
+
+def test_explicit_identity_and_rotation():
+    # a = (2^j, 0, ...), b = 1, c = 0, m = gamma: z = gamma-bit rotation of x_0 by j
+    n, r = 40_000, 4096
+    g = 4423
+    key = key_bytes(n, 11)
+    k = -(-n // r)
+    x0 = hashes.key_blocks(key, n, r)[0]
+    for j in (0, 1, 17, 4422):
+        a = [1 << j] + [0] * (k - 1)
+        out = gpu_hash(key, n, r, g, 0, gamma=g, a=a, b=1, c=0)
+        s = format(x0, f"0{g}b")
+        want = int(s[j:] + s[:j], 2)
+        assert int.from_bytes(out, "big") >> (8 * len(out) - g) == want
+
+
+def test_canonical_zero():
+    # reading A6: a_0 = p - 1, a_1 = 1, x_0 = x_1 = 1 -> Y = p -> y = 0 -> z = top bits of c
+    r, g, m = 256, 521, 300
+    p = (1 << g) - 1
+    key = np.zeros(2 * r // 8, np.uint8)
+    key[r // 8 - 1] = 1
+    key[2 * r // 8 - 1] = 1
+    c = random.Random(2).getrandbits(g)
+    b = random.Random(3).getrandbits(g) | 1
+    out = gpu_hash(key, 2 * r, r, m, 0, gamma=g, a=[p - 1, 1], b=b, c=c)
+    assert out == hashes.pack_output(c >> (g - m), m)
+    # and y = p - 1 (largest residue) is kept: a_0 = p - 1, x_0 = 1, x_1 = 0
+    key[2 * r // 8 - 1] = 0
+    out = gpu_hash(key, 2 * r, r, m, 0, gamma=g, a=[p - 1, 1], b=b, c=c)
+    assert out == hashes.mh_output(p - 1, b, c, g, m)
+
+
+def test_explicit_keys_random():
+    rng = random.Random(9)
+    n, r, m = 123_457, 1024, 2_000
+    g = 1279
+    k = -(-n // r)
+    p = (1 << g) - 1
+    a = [rng.randrange(p) for _ in range(k)]
+    alpha = max(g, m)
+    b, c = rng.getrandbits(alpha) | 1, rng.getrandbits(alpha)
+    key = key_bytes(n, 12)
+    assert gpu_hash(key, n, r, m, 0, gamma=g, a=a, b=b, c=c) == hashes.pa_hash(key, n, r, m, g, a, b, c)
+
+
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_shard_merge_equals_single(G):
+    # split-merge: per-shard residues summed mod p == unsharded hash
+    from paper_2105_13678_b200.pa import key_slice_bytes, shard_ranges
+    PAContext = _pa()
+    n, r, m, seed = 500_001, 4096, 20_000, 99
+    key = key_bytes(n, 21)
+    kd = torch.from_numpy(key).cuda()
+    k = -(-n // r)
+    parts = []
+    ctxs = []
+    for (b0, b1) in shard_ranges(k, G):
+        ctx = PAContext(n, r, m, seed=seed, block_range=(b0, b1))
+        lo, hi = key_slice_bytes(n, r, (b0, b1))
+        parts.append(ctx.mmh_partial(kd[lo:hi].clone()))
+        ctxs.append(ctx)
+        # each partial equals the oracle's residue of that block range
+        gamma = ctx.gamma
+        y_or = hashes.mmh_partial(key, n, r, gamma, seeds.expand_hash_keys(seed, k, gamma, gamma)[0], range(b0, b1))
+        y_gpu = int.from_bytes(parts[-1].cpu().numpy().astype("<u4").tobytes(), "little")
+        assert y_gpu == y_or
+    out = ctxs[0].mh_merge(torch.stack(parts))
+    torch.cuda.synchronize()
+    assert bytes(out.cpu().numpy()) == oracle_seeded(key, n, r, m, seed)
+
+
+def test_hash_host_and_determinism():
+    PAContext = _pa()
+    n, r, m = 200_000, 2048, 10_000
+    key = key_bytes(n, 31)
+    ctx = PAContext(n, r, m, seed=5)
+    o1 = bytes(ctx.hash_host(key))
+    o2 = bytes(ctx.hash(torch.from_numpy(key).cuda()).cpu().numpy())
+    o3 = bytes(ctx.hash_host(torch.from_numpy(key).pin_memory()))
+    assert o1 == o2 == o3 == oracle_seeded(key, n, r, m, 5)
+
+
+def _golden():
+    path = os.path.join(ROOT, "tests", "golden", "digests.json")
+    return json.load(open(path)) if os.path.exists(path) else {}
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5a", "C5b", "C5c"])
+def test_full_size_golden(name):
+    db = _golden()
+    if name not in db:
+        pytest.skip(f"no golden digest for {name}")
+    rec = db[name]
+    w = CONFIGS[name]
+    PAContext = _pa()
+    key = key_bytes(w.n, w.key_seed)
+    ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed)
+    out = ctx.hash(torch.from_numpy(key).cuda())
+    torch.cuda.synchronize()
+    got = bytes(out.cpu().numpy())
+    ctx.close()
+    assert got[:16].hex() == rec["out_head"]
+    assert hashlib.sha256(got).hexdigest() == rec["out_sha256"]
