@@ -1,0 +1,343 @@
+"""Benchmark of the MMH-MH privacy-amplification hot path on B200 (one JSON line).
+
+Metric (BASELINE.json): PA throughput in Mbps of INPUT key at n = 2.6e8 bits (config C4),
+= n / t_step / 1e6, one step = one full pa_hash (S1..S7: pack, forward NTTs of all 31
+blocks, transform-domain multiply-accumulate, inverse, CRT + carries, Mersenne fold, MH).
+
+    python bench.py                               # N=1, C4
+    python bench.py --impl reference              # the CPU oracle on a bounded sample
+    torchrun --nproc-per-node N bench.py --gpus N # blocks sharded over N ranks, NCCL gather
+
+Timing rules followed: W >= 3 untimed warm-up steps; every timed step is bracketed by
+CUDA events on the context stream and preceded (outside the events) by an L2 flush
+(a 256 MiB write, > 126 MB L2); device time, max over ranks; nvidia-smi clocks sampled
+during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PA throughput, Mbps of input key at n=2.6e8 bits, 1/2/4/8 B200; % HBM roofline"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+INT_OPS_PER_BFLY = 6     # Shoup butterfly: 3 multiplies + 3 add/sub/correct
+INT_OPS_PER_MAC = 6      # Montgomery product (4) + lazy add/correct (2)
+
+
+def load_peaks() -> dict:
+    try:
+        return json.load(open(PEAKS))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 600] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- roofline
+def stage_ops(info: dict, stage: str) -> float:
+    """Algorithmic int32 lane-operations of one launch of a stage:
+    radix-2 butterflies of the pass times 6, plus 6 per transform-domain MAC."""
+    mmh, mh = info["mmh"], info["mh"]
+    nblk = info["block_end"] - info["block_begin"]
+
+    def bfly(pl, nvec, npass_len):
+        L = 1 << pl["log2_len"]
+        import math
+        return nvec * pl["nprimes"] * (L / 2) * math.log2(npass_len)
+
+    if stage == "mmh_fwd_col_pack":
+        return INT_OPS_PER_BFLY * bfly(mmh, nblk, mmh["n_col"])
+    if stage == "mmh_fwd_row_mac":
+        L = 1 << mmh["log2_len"]
+        return INT_OPS_PER_BFLY * bfly(mmh, nblk, mmh["n_row"]) + INT_OPS_PER_MAC * nblk * mmh["nprimes"] * L
+    if stage == "mmh_inverse":
+        return INT_OPS_PER_BFLY * bfly(mmh, 1, 1 << mmh["log2_len"])
+    if stage == "mh_fwd_col":
+        return INT_OPS_PER_BFLY * bfly(mh, 1, mh["n_col"])
+    if stage == "mh_fwd_row_mac":
+        return INT_OPS_PER_BFLY * bfly(mh, 1, mh["n_row"]) + INT_OPS_PER_MAC * mh["nprimes"] * (1 << mh["log2_len"])
+    if stage == "mh_inverse":
+        return INT_OPS_PER_BFLY * bfly(mh, 1, 1 << mh["log2_len"])
+    return 0.0
+
+
+def roofline(info: dict, stages: dict, peaks: dict, steps: int) -> dict:
+    """Dominant kernel stage -> achieved int32 Gop/s vs the issue-rate peak."""
+    name, (ms, cnt) = max(stages.items(), key=lambda kv: kv[1][0])
+    per_launch_ms = ms / max(cnt, 1)
+    ops = stage_ops(info, name)
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = 148
+    peak = nsm * 4 * 32 * sm_mhz * 1e6 / 1e9          # Gop/s: 1 warp-instr/clk/SMSP x 32 lanes
+    achieved = ops / (per_launch_ms * 1e-3) / 1e9 if ops else None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    share = ms / sum(v[0] for v in stages.values())
+    return {"bound": "alu", "kernel": name, "achieved": achieved, "peak": peak, "unit": "Gop/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "ms_per_launch": per_launch_ms, "share_of_step": share,
+            "peak_note": f"int32 lane-ops: {nsm} SMs x 4 SMSP x 32 lanes x 1 instr/clk x {sm_mhz:.0f} MHz "
+                         "(B300_MICROARCH.md issue model; IMAD and ALU pipes each half rate)"}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_sample(w, nblocks: int = 2) -> dict:
+    """Time the CPU oracle (oracle/, as it stands) on a bounded sample of the workload:
+    the MMH products + fold of the first `nblocks` blocks."""
+    from oracle import hashes, seeds
+    from synth import key_bytes
+    pp = hashes.plan_params(w.n, w.r, w.m)
+    key = key_bytes(w.n, w.key_seed)
+    a = [seeds.expand_a(w.hash_seed, i, pp["gamma"]) for i in range(nblocks)]
+    x = hashes.key_blocks(key, w.n, w.r)[:nblocks]
+    t0 = time.perf_counter()
+    hashes.mmh_eval(a, x, pp["gamma"])
+    dt = time.perf_counter() - t0
+    bits = nblocks * w.r
+    return {"value": bits / dt / 1e6, "unit": "Mbps", "cores": 1, "kind": "oracle",
+            "sample": f"MMH sum_i a_i x_i mod p + fold over blocks 0..{nblocks - 1} of {w.name} "
+                      f"({bits} key bits), CPython-int oracle (oracle/hashes.py), 1 thread",
+            "seconds": dt}
+
+
+def run_reference(args, w) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_oracle_sample(w, 1)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = cpu_oracle_sample(w, 1)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mbps", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(secs) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int (Python bignum)",
+            "data": "synthetic", "config": {"workload": w.name, "n": w.n, "r": w.r, "m": w.m,
+                                             "sample": "one block product per step"},
+            "cpu_baseline": {"value": v, "unit": "Mbps", "cores": 1, "kind": "oracle",
+                             "sample": f"MMH product + fold of block 0 of {w.name} ({w.r} key bits) per step, "
+                                       "CPython-int oracle, 1 thread"},
+            "e2e": {"value": v, "unit": "Mbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU run
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from synth import CONFIGS, key_bytes
+    w = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, w)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2105_13678_b200 import PAContext
+    from paper_2105_13678_b200.pa import key_slice_bytes, shard_ranges
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+
+    k = w.k
+    b0, b1 = shard_ranges(k, world)[rank]
+    key_full = key_bytes(w.n, w.key_seed)
+    lo, hi = key_slice_bytes(w.n, w.r, (b0, b1))
+    key_dev = torch.from_numpy(key_full[lo:hi].copy()).to(dev)
+    ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None)
+    info = ctx.query()
+    out = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
+    yw = ctx.y_words
+    parts = torch.empty((world, yw), dtype=torch.int32, device=dev) if world > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        if world == 1:
+            ctx.hash(key_dev, out)
+        else:
+            y = ctx.mmh_partial(key_dev)
+            dist.all_gather_into_tensor(parts, y)
+            if rank == 0:
+                ctx.mh_merge(parts, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = ctx.query()["kernels_per_hash"] + (ctx.query()["kernels_per_hash"] if False else 0)
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = []
+    for _ in range(args.steps):
+        if not args.no_flush:
+            flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    times = [a.elapsed_time(b) for a, b in evs]
+    tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = tot.item() / args.steps
+
+    # ---- per-stage times (profiling pass, untimed), e2e through the host-buffer API
+    ctx.set_profiling(True)
+    ctx.stage_times(reset=True)
+    for _ in range(3):
+        if not args.no_flush:
+            flush.fill_(1)
+        step()
+    stages = ctx.stage_times()
+    ctx.set_profiling(False)
+    nsteps_prof = 3
+    stages = {kname: (v[0], v[1]) for kname, v in stages.items()}
+
+    e2e = None
+    if world == 1:
+        host_key = torch.from_numpy(key_full).pin_memory()
+        host_out = torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory()
+        for _ in range(2):
+            ctx.hash_host(host_key, host_out)
+        t = []
+        for _ in range(max(3, args.steps // 2)):
+            if not args.no_flush:
+                flush.fill_(1)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.hash_host(host_key, host_out)
+            bb.record(stream)
+            bb.synchronize()
+            t.append(a.elapsed_time(bb))
+        e2e_ms = statistics.median(t)
+        e2e = {"value": w.n / (e2e_ms * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": (w.n + 7) // 8, "d2h_bytes_per_step": (w.m + 7) // 8,
+               "api": "pa_hash_host (pinned host buffers, H2D + hash + D2H + sync)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = load_peaks()
+    roof = roofline(info, {kk: (v[0] / nsteps_prof, v[1] // nsteps_prof) for kk, v in stages.items()}, peaks, 1)
+    line = {
+        "metric": METRIC, "value": w.n / (ms_per_step * 1e-3) / 1e6, "unit": "Mbps", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (i.i.d. Bernoulli(0.5) key bits from Philox4x64-10; hash keys from seed)",
+        "config": {"workload": w.name, "n": w.n, "r": w.r, "m": w.m, "k": k, "gamma": info["gamma"],
+                   "alpha": info["alpha"],
+                   "mmh_plan": {kk: info["mmh"][kk] for kk in ("limb_bits", "nprimes", "log2_len", "n_col", "n_row")},
+                   "mh_plan": {kk: info["mh"][kk] for kk in ("limb_bits", "nprimes", "log2_len", "n_col", "n_row")},
+                   "parallelism": f"blocks sharded over {world} rank(s), residues all-gathered (NCCL), MH on rank 0",
+                   "l2": "flushed (256 MiB write) before every timed step" if not args.no_flush else "not flushed"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "roofline": roof,
+        "stages_ms_per_step": {kk: v[0] / nsteps_prof for kk, v in sorted(stages.items())},
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_oracle_sample(w, 2)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,16 +1,20 @@
 // Exact reconstruction of the product integers and the Mersenne / power-of-two
 // reductions of the MMH-MH pipeline.
 //
-//  * CRT (Garner) turns the P residues of every convolution coefficient into the
-//    exact coefficient c_j < prod p_i (the plan guarantees the bound).
-//  * Column sums: word u of  sum_j c_j 2^(B j)  (+ an optional addend, MH's c) is
-//    gathered as a 64-bit sum of 32-bit windows of the coefficients.
-//  * Carry resolution: the 64-bit column sums become 32-bit words with a
-//    generate/propagate carry-lookahead scan (warp ballots, block, grid).
-//  * Fold: y = Y mod (2^gamma - 1) = sum of gamma-bit chunks of Y, folded again
-//    (PAPER.md:130-132), canonical zero (reading A6).
-//  * MH extract: bits [alpha - m, alpha) of (b y + c) mod 2^alpha, MSB-first bytes
-//    (Eq. 4; readings A5, A8).
+//  * CRT (Garner) turns the P residues of every convolution coefficient into the exact
+//    coefficient c_j < prod p_i (the plan guarantees the bound).  One CTA owns a tile of
+//    output words, reconstructs the coefficients that touch it into shared memory once,
+//    and forms the 64-bit column sums of its words.
+//  * MMH (S4+S5): the column sums are taken on the gamma-bit ring directly: coefficient j
+//    sits at bit (B j) mod gamma, and a piece that crosses bit gamma wraps to bit 0 --
+//    this is the fold x mod M_gamma = floor(x / 2^gamma) + x mod 2^gamma
+//    applied to each coefficient before the carries.
+//  * MH (S7): plain column sums of b*y plus the addend c, words below alpha
+//    (Eq. 4).
+//  * Carry resolution: 64-bit column sums -> 32-bit words with a generate/propagate
+//    carry-lookahead: warp ballots inside a tile, single-pass decoupled look-back between
+//    tiles (a tile that does not propagate ends the look-back).
+//  * Final folds + canonical zero (reading A6), MH bit extraction (readings A5, A8).
 #pragma once
 #include <cstdint>
 #include "modarith.cuh"
@@ -23,36 +27,36 @@ struct CrtK {
     uint32_t P;
     uint32_t p[kMaxPrimes];
     uint32_t pinv[kMaxPrimes];
-    // inv[i][l] = (p_0 ... p_{l-1})^{-1} mod p_i   for l <= i, Montgomery form
-    // pm[i][l]  = (p_0 ... p_{l-1}) mod p_i        Montgomery form (l < i)
-    uint32_t inv[kMaxPrimes];         // (p_0 ... p_{i-1})^{-1} mod p_i  (Montgomery form)
-    uint32_t pmod[kMaxPrimes][kMaxPrimes];  // pmod[i][l] = p_l mod p_i (Montgomery form)
-    // prod[l] = p_0 ... p_{l-1} as little-endian 32-bit words (l <= P), P words each
-    uint32_t prod[kMaxPrimes + 1][kMaxPrimes];
+    uint32_t inv[kMaxPrimes];                 // (p_0 ... p_{i-1})^{-1} mod p_i, Montgomery form
+    uint32_t pmod[kMaxPrimes][kMaxPrimes];    // p_l mod p_i (l < i), Montgomery form
+    uint32_t prod[kMaxPrimes + 1][kMaxPrimes];// p_0 ... p_{l-1}, little-endian words
 };
 
-// Garner: exact c (P 32-bit words, little-endian) from canonical residues r[i].
-// u_0 = r_0; u_i = (r_i - (u_0 + p_0 (u_1 + p_1 (...)))) * (p_0...p_{i-1})^{-1} mod p_i;
-// c = u_0 + p_0 u_1 + p_0 p_1 u_2 + ...
+// Garner: exact c (P words) from canonical residues r[i].
+// u_0 = r_0;  u_i = (r_i - (u_0 + p_0 (u_1 + p_1 (... u_{i-1})))) (p_0...p_{i-1})^{-1} mod p_i;
+// c = sum_i u_i p_0 ... p_{i-1}.
+template <int P>
 __device__ __forceinline__ void garner(const CrtK &K, const uint32_t *r, uint32_t *c) {
-    uint32_t u[kMaxPrimes];
-    for (uint32_t i = 0; i < K.P; i++) {
+    uint32_t u[P];
+#pragma unroll
+    for (int i = 0; i < P; i++) {
         const uint32_t p = K.p[i], pinv = K.pinv[i];
-        // partial = u_0 + p_0 (u_1 + p_1 (... u_{i-1})) mod p_i, Horner from the inside
         uint32_t acc = 0;
-        for (int l = (int)i - 1; l >= 0; l--) {
-            // acc = u_l + p_l * acc
+#pragma unroll
+        for (int l = i - 1; l >= 0; l--) {
             acc = red1p(mul_mont(acc, K.pmod[i][l], p, pinv), p);
-            acc = red1p(acc + (u[l] >= p ? u[l] - p : u[l]) % p, p);  // u_l < p_l may exceed p_i
+            acc = red1p(acc + red1p(u[l], p), p);      // u_l < p_l < 2 p_i
         }
-        uint32_t d = r[i] + p - acc;            // in (0, 2p)
-        d = red1p(d, p);
-        u[i] = (i == 0) ? r[0] : red1p(mul_mont(d, K.inv[i], p, pinv), p);
+        if (i == 0) u[0] = r[0];
+        else u[i] = red1p(mul_mont(red1p(r[i] + p - acc, p), K.inv[i], p, pinv), p);
     }
-    for (uint32_t w = 0; w < K.P; w++) c[w] = 0;
-    for (uint32_t i = 0; i < K.P; i++) {       // c += u_i * prod[i]
+#pragma unroll
+    for (int w = 0; w < P; w++) c[w] = 0;
+#pragma unroll
+    for (int i = 0; i < P; i++) {
         uint64_t carry = 0;
-        for (uint32_t w = 0; w < K.P; w++) {
+#pragma unroll
+        for (int w = 0; w < P; w++) {
             const uint64_t t = (uint64_t)c[w] + (uint64_t)u[i] * K.prod[i][w] + carry;
             c[w] = (uint32_t)t;
             carry = t >> 32;
@@ -60,57 +64,117 @@ __device__ __forceinline__ void garner(const CrtK &K, const uint32_t *r, uint32_
     }
 }
 
-// 32-bit window of a multiword value x (nw words) starting at bit offset `off`
-// (may be negative: the value starts inside the window).
-__device__ __forceinline__ uint32_t window32(const uint32_t *x, int nw, int off) {
-    if (off <= -32) return 0;
-    if (off < 0) return x[0] << (-off);
-    const int wi = off >> 5, sh = off & 31;
-    if (wi >= nw) return 0;
-    const uint32_t lo = x[wi];
-    const uint32_t hi = (wi + 1 < nw) ? x[wi + 1] : 0u;
-    return __funnelshift_r(lo, hi, sh);
+// 32-bit window [off, off+32) of the multiword value x (NW words; negative off allowed),
+// restricted to the value's bits [0, len).
+template <int NW>
+__device__ __forceinline__ uint32_t window_masked(const uint32_t *x, int off, int len) {
+    if (off <= -32 || off >= len) return 0;
+    uint32_t v;
+    if (off < 0) {
+        v = x[0] << (-off);
+    } else {
+        const int wi = off >> 5, sh = off & 31;
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) { if (w == wi) lo = x[w]; if (w == wi + 1) hi = x[w]; }
+        v = __funnelshift_r(lo, hi, sh);
+    }
+    // bits of the window at or above len (value-relative) are cleared
+    const int top = len - off;                     // window bits [0, top) are inside
+    if (top < 32) v &= (top <= 0) ? 0u : ((1u << top) - 1u);
+    return v;
 }
 
-// Column sums of Y = sum_{j < ncoef} c_j 2^(B j) (+ addend) for words [0, W).
-// res: [P][L] canonical residues (natural coefficient order).
-__global__ void crt_colsum(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
-                           uint32_t B, const CrtK K, const uint32_t *__restrict__ addend,
-                           uint32_t n_addend, uint64_t *__restrict__ S, uint32_t W) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= W) return;
-    const int64_t cbits = 32 * (int64_t)K.P;
-    const int64_t lo_bit = 32 * (int64_t)u, hi_bit = lo_bit + 32;
-    int64_t jlo = (lo_bit - cbits + 1 + B - 1);
-    jlo = jlo <= 0 ? 0 : jlo / B;
-    int64_t jhi = (hi_bit - 1) / B;
-    if (jhi >= (int64_t)ncoef) jhi = (int64_t)ncoef - 1;
-    uint64_t s = (addend && u < n_addend) ? addend[u] : 0ull;
-    for (int64_t j = jlo; j <= jhi; j++) {
-        uint32_t r[kMaxPrimes], c[kMaxPrimes];
-        for (uint32_t i = 0; i < K.P; i++) r[i] = res[(size_t)i * L + j];
-        garner(K, r, c);
-        s += window32(c, (int)K.P, (int)(lo_bit - (int64_t)B * j));
+// Column sums over a tile of words [u0, u0 + blockDim.x).
+//   RING = true : positions e_j = (B j) mod gamma on the gamma-bit ring (MMH, S4+S5);
+//   RING = false: positions B j, plus addend words (MH, S7).
+// res: [P][L] canonical residues in natural coefficient order.
+template <int P, bool RING>
+__global__ void __launch_bounds__(256) crt_colsum_tile(const uint32_t *__restrict__ res, uint32_t L,
+                                                       uint32_t ncoef, uint32_t B, uint64_t gamma,
+                                                       const CrtK K, const uint32_t *__restrict__ addend,
+                                                       uint32_t n_addend, uint64_t *__restrict__ S, uint32_t W) {
+    extern __shared__ uint32_t sc[];               // [cap][P] coefficients
+    const uint32_t U = blockDim.x;
+    const uint32_t u0 = blockIdx.x * U;
+    const uint32_t u = u0 + threadIdx.x;
+    const int64_t cbits = 32 * P;
+    const uint32_t cap = (32 * U + cbits) / B + 3;
+    uint64_t s = (!RING && addend && u < n_addend) ? addend[u] : 0ull;
+
+    // chunk t covers coefficients with t gamma <= B j < (t+1) gamma (ring); one chunk (linear)
+    const uint64_t span = RING ? gamma : ~0ull >> 2;
+    const uint64_t nchunks = RING ? ((uint64_t)B * ncoef + gamma - 1) / gamma : 1;
+    const int64_t lo_bit = 32 * (int64_t)u0, hi_bit = 32 * (int64_t)(u0 + U);
+    for (uint64_t t = 0; t < nchunks; t++) {
+        const int64_t base = (int64_t)(t * span);                 // ring position 0 of this chunk
+        // coefficients whose piece [B j - base, B j - base + cbits) meets [lo_bit, hi_bit)
+        int64_t ja = (lo_bit - cbits + base) / (int64_t)B;        // may be one too small: harmless
+        if (ja < 0) ja = 0;
+        const int64_t jc0 = (base + B - 1) / B;                   // first j of the chunk
+        if (ja < jc0) ja = jc0;
+        int64_t jb = (hi_bit - 1 + base) / (int64_t)B;            // inclusive
+        const int64_t jc1 = RING ? (int64_t)(((t + 1) * span + B - 1) / B) - 1 : (int64_t)ncoef - 1;
+        if (jb > jc1) jb = jc1;
+        if (jb > (int64_t)ncoef - 1) jb = (int64_t)ncoef - 1;
+        if (jb < ja) continue;                                    // uniform across the CTA
+        const uint32_t cnt = (uint32_t)(jb - ja + 1);
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < cnt && q < cap; q += U) {
+            uint32_t r[P], c[P];
+#pragma unroll
+            for (int i = 0; i < P; i++) r[i] = res[(size_t)i * L + (ja + q)];
+            garner<P>(K, r, c);
+#pragma unroll
+            for (int w = 0; w < P; w++) sc[q * P + w] = c[w];
+        }
+        __syncthreads();
+        if (u < W) {
+            const int64_t me = 32 * (int64_t)u;
+            int64_t j0 = (me - cbits + base) / (int64_t)B;
+            if (j0 < ja) j0 = ja;
+            int64_t j1e = (me + 31 + base) / (int64_t)B;
+            if (j1e > jb) j1e = jb;
+            for (int64_t j = j0; j <= j1e; j++) {
+                const int64_t pos = (int64_t)B * j - base;        // piece start on the ring
+                int len = (int)cbits;
+                if (RING && pos + len > (int64_t)gamma) len = (int)((int64_t)gamma - pos);
+                s += window_masked<P>(&sc[(j - ja) * P], (int)(me - pos), len);
+            }
+        }
     }
-    S[u] = s;
+    if (RING && u0 * 32ull < (uint64_t)cbits + 32) {
+        // wrapped pieces: the bits of a coefficient above the ring top land at bit 0
+        for (uint64_t t = 0; t < nchunks; t++) {
+            const int64_t base = (int64_t)(t * gamma);
+            const int64_t top = base + (int64_t)gamma;                // chunk end (ring bit gamma)
+            int64_t ja = (top - cbits) / (int64_t)B;
+            const int64_t jc0 = (base + B - 1) / B;
+            if (ja < jc0) ja = jc0;
+            int64_t jb = (top - 1) / (int64_t)B;
+            if (jb > (int64_t)ncoef - 1) jb = (int64_t)ncoef - 1;
+            if (u < W) {
+                for (int64_t j = ja; j <= jb; j++) {
+                    const int64_t pos = (int64_t)B * j - base;
+                    if (pos + cbits <= (int64_t)gamma) continue;
+                    uint32_t r[P], c[P];
+#pragma unroll
+                    for (int i = 0; i < P; i++) r[i] = res[(size_t)i * L + j];
+                    garner<P>(K, r, c);
+                    // high part c >> (gamma - pos) placed at ring bit 0
+                    const int cut = (int)((int64_t)gamma - pos);
+                    s += window_masked<P>(c, 32 * (int)u + cut, (int)cbits);
+                }
+            }
+        }
+    }
+    if (u < W) S[u] = s;
 }
 
 // ---------------------------------------------------------------- carry resolution
-// Words t_u = lo(S_u) + hi(S_{u-1}) < 2^32 + 2^31: generate g_u = t_u >> 32,
-// propagate p_u = (uint32)t_u == 0xFFFFFFFF.  Final word = (uint32)t_u + carry_in_u.
 constexpr int kTile = 1024;
 
-__device__ __forceinline__ void word_gp(const uint64_t *S, uint32_t W, uint32_t u, uint32_t &w, int &g, int &pp) {
-    uint64_t t = 0;
-    if (u < W) {
-        t = (S[u] & 0xFFFFFFFFull) + (u > 0 ? (S[u - 1] >> 32) : 0ull);
-    }
-    w = (uint32_t)t;
-    g = (int)(t >> 32);
-    pp = (u < W) && (w == 0xFFFFFFFFu);
-}
-
-// (g, p) of a whole warp / block given bit masks: carry-in to each lane and carry out.
+// (g, p) over 32 lanes given ballot masks: per-lane carry-in (bit i) and carry out.
 __device__ __forceinline__ uint32_t lane_carries(uint32_t Gm, uint32_t Pm, uint32_t cin, uint32_t &cout) {
     const uint64_t A = (uint64_t)(Gm | Pm), Bm = Gm;
     const uint64_t sum = A + Bm + cin;
@@ -118,129 +182,127 @@ __device__ __forceinline__ uint32_t lane_carries(uint32_t Gm, uint32_t Pm, uint3
     return (uint32_t)sum ^ (uint32_t)A ^ (uint32_t)Bm;
 }
 
-// Block-level carry resolution of one tile of kTile words with block carry-in `cin`
-// (uniform).  Returns this thread's word carry-in; block carry-out in *bcout.
-__device__ __forceinline__ uint32_t block_carries(int g, int pp, uint32_t cin, uint32_t *bcout) {
+// Carry-in of this thread's word within a block of kTile words with block carry-in
+// `cin`; block aggregate (generate with cin = 0) in *bg.
+__device__ __forceinline__ uint32_t block_carries(int g, int pp, uint32_t cin, uint32_t *bg) {
     __shared__ uint32_t wg[32], wp[32], wc[32];
-    __shared__ uint32_t s_cout;
+    __shared__ uint32_t s_bg;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t Gm = __ballot_sync(0xFFFFFFFFu, g), Pm = __ballot_sync(0xFFFFFFFFu, pp);
     uint32_t co0;
-    (void)lane_carries(Gm, Pm, 0, co0);            // warp generate (cin = 0)
+    (void)lane_carries(Gm, Pm, 0, co0);
+    __syncthreads();
     if (lane == 0) { wg[wid] = co0; wp[wid] = (Pm == 0xFFFFFFFFu); }
     __syncthreads();
     if (wid == 0) {
         const int nw = blockDim.x >> 5;
         const uint32_t G2 = __ballot_sync(0xFFFFFFFFu, lane < nw ? wg[lane] : 0);
-        const uint32_t P2 = __ballot_sync(0xFFFFFFFFu, lane < nw ? wp[lane] : 0);
+        const uint32_t P2 = __ballot_sync(0xFFFFFFFFu, lane < nw ? wp[lane] : 1);
         uint32_t co;
         const uint32_t C2 = lane_carries(G2, P2, cin, co);
         wc[lane] = (C2 >> lane) & 1;
-        if (lane == 0) {
-            // carry out of the last active warp
-            uint32_t c = cin;
-            for (int i = 0; i < nw; i++) c = ((G2 >> i) & 1) | (((P2 >> i) & 1) & c);
-            s_cout = c;
-        }
+        uint32_t co_g;
+        (void)lane_carries(G2, P2, 0, co_g);
+        if (lane == 0) s_bg = co_g;
     }
     __syncthreads();
     uint32_t co;
     const uint32_t C = lane_carries(Gm, Pm, wc[wid], co);
-    if (bcout) *bcout = s_cout;
+    if (bg) *bg = s_bg;
     return (C >> lane) & 1;
 }
 
-// Phase A: (g, p) summary per tile.
-__global__ void carry_tiles(const uint64_t *__restrict__ S, uint32_t W, uint8_t *__restrict__ tg,
-                            uint8_t *__restrict__ tp) {
-    const uint32_t u = blockIdx.x * kTile + threadIdx.x;
-    uint32_t w; int g, pp;
-    word_gp(S, W, u, w, g, pp);
-    // tile propagate = all words propagate (out-of-range words count as propagate so
-    // the last partial tile passes carries through; they are never written)
-    const int pfull = (u < W) ? pp : 1;
-    const int allp = __syncthreads_and(pfull);
-    uint32_t cout;
-    (void)block_carries(g, pp, 0, &cout);
-    if (threadIdx.x == 0) { tg[blockIdx.x] = (uint8_t)cout; tp[blockIdx.x] = (uint8_t)allp; }
-}
+// Sources of 64-bit column sums for the carry kernel.
+struct SrcArr {
+    const uint64_t *S;
+    __device__ __forceinline__ uint64_t operator()(uint32_t u) const { return S[u]; }
+};
+// Mersenne fold of y (W words) by chunks (PAPER.md:130-132 applied to all chunks at once):
+// S_u = sum_t word u of bits [t gamma, (t+1) gamma) of y, for u < ceil(gamma/32); 0 above.
+struct SrcFoldChunks {
+    const uint32_t *y;
+    uint64_t gamma;
+    uint32_t W;            // words of y
+    __device__ __forceinline__ uint32_t bits32(uint64_t start) const {
+        const uint64_t wi = start >> 5;
+        const int sh = (int)(start & 31);
+        const uint32_t lo = wi < W ? y[wi] : 0u, hi = wi + 1 < W ? y[wi + 1] : 0u;
+        return __funnelshift_r(lo, hi, sh);
+    }
+    __device__ __forceinline__ uint64_t operator()(uint32_t u) const {
+        const uint64_t off = 32 * (uint64_t)u;
+        if (off >= gamma) return 0;
+        const uint32_t mask = (off + 32 > gamma) ? (uint32_t)((1ull << (gamma - off)) - 1) : 0xFFFFFFFFu;
+        const uint64_t nch = (32ull * W + gamma - 1) / gamma;
+        uint64_t s = 0;
+        for (uint64_t t = 0; t < nch; t++) s += bits32(t * gamma + off) & mask;
+        return s;
+    }
+};
+// Sum of G residues (S6): S_u = sum_g parts[g][u].
+struct SrcParts {
+    const uint32_t *parts;
+    uint32_t G, Wg;
+    __device__ __forceinline__ uint64_t operator()(uint32_t u) const {
+        uint64_t s = 0;
+        if (u < Wg)
+            for (uint32_t g = 0; g < G; g++) s += parts[(size_t)g * Wg + u];
+        return s;
+    }
+};
 
-// Phase B: carry-in of every tile (single block, sequential chunks + block scan).
-__global__ void carry_scan(const uint8_t *__restrict__ tg, const uint8_t *__restrict__ tp, uint32_t ntiles,
-                           const uint32_t *__restrict__ cin0, uint8_t *__restrict__ tcin,
-                           uint32_t *__restrict__ carry_out) {
-    const uint32_t T = blockDim.x;
-    const uint32_t per = (ntiles + T - 1) / T;
-    const uint32_t b0 = threadIdx.x * per;
-    const uint32_t b1 = min(ntiles, b0 + per);
-    int G = 0, Pp = 1;
-    for (uint32_t t = b0; t < b1; t++) { G = tg[t] | (tp[t] & G); Pp &= tp[t]; }
-    const uint32_t cin = cin0 ? (*cin0 & 1u) : 0u;
-    uint32_t bcout;
-    uint32_t c = block_carries(G, (b0 < b1) ? Pp : 1, cin, &bcout);
-    for (uint32_t t = b0; t < b1; t++) { tcin[t] = (uint8_t)c; c = tg[t] | (tp[t] & c); }
-    if (threadIdx.x == 0 && carry_out) *carry_out = bcout;
-}
-
-// Phase C: final words.
-__global__ void carry_apply(const uint64_t *__restrict__ S, uint32_t W, const uint8_t *__restrict__ tcin,
-                            uint32_t *__restrict__ out) {
-    const uint32_t u = blockIdx.x * kTile + threadIdx.x;
-    uint32_t w; int g, pp;
-    word_gp(S, W, u, w, g, pp);
-    const uint32_t c = block_carries(g, pp, tcin[blockIdx.x], nullptr);
+// Single-pass carry resolution: out[u] = word u of sum_u S_u 2^(32u), u < W.
+// state[ntiles] and ticket must be zero before the launch.  state encoding:
+// bit0 aggregate ready, bit1 g, bit2 p, bit3 inclusive ready, bit4 inclusive carry-out.
+template <class Src>
+__global__ void __launch_bounds__(kTile) carry_lb(const Src src, uint32_t W, uint32_t *__restrict__ out,
+                                                  uint32_t *state, uint32_t *ticket, uint32_t *carry_out) {
+    __shared__ uint32_t s_tile, s_cin;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t ntiles = (W + kTile - 1) / kTile;
+    const uint32_t u = tile * kTile + threadIdx.x;
+    const uint64_t su = (u < W) ? src(u) : 0ull;
+    const uint64_t sp = (u > 0 && u - 1 < W) ? src(u - 1) : 0ull;
+    const uint64_t t = (su & 0xFFFFFFFFull) + (sp >> 32);
+    const uint32_t w = (uint32_t)t;
+    const int g = (int)(t >> 32);
+    const int pp = (u < W) ? (w == 0xFFFFFFFFu) : 1;
+    const int allp = __syncthreads_and(pp);
+    uint32_t bg;
+    (void)block_carries(g, pp, 0, &bg);
+    if (threadIdx.x == 0) {
+        volatile uint32_t *vs = state;
+        uint32_t cin = 0;
+        if (tile > 0) {
+            vs[tile] = 1u | (bg << 1) | ((uint32_t)allp << 2);
+            __threadfence();
+            uint32_t accG = 0, accP = 1;
+            int64_t j = (int64_t)tile - 1;
+            for (;;) {
+                if (j < 0) { cin = accG; break; }
+                const uint32_t st = vs[j];
+                if (st == 0) continue;
+                if (st & 8u) { cin = accG | (accP & ((st >> 4) & 1u)); break; }
+                accG |= accP & ((st >> 1) & 1u);
+                accP &= (st >> 2) & 1u;
+                if (!accP) { cin = accG; break; }
+                j--;
+            }
+        }
+        const uint32_t incl = bg | ((uint32_t)allp & cin);
+        __threadfence();
+        vs[tile] = 1u | (bg << 1) | ((uint32_t)allp << 2) | 8u | (incl << 4);
+        s_cin = cin;
+        if (tile == ntiles - 1 && carry_out) *carry_out = incl;
+    }
+    __syncthreads();
+    const uint32_t c = block_carries(g, pp, s_cin, nullptr);
     if (u < W) out[u] = w + c;
 }
 
-// ---------------------------------------------------------------- fold mod 2^gamma - 1
-// bits [start, start + 32) of X (nw words), zero beyond nw words.
-__device__ __forceinline__ uint32_t bits32(const uint32_t *X, uint64_t nw, uint64_t start) {
-    const uint64_t wi = start >> 5;
-    const int sh = (int)(start & 31);
-    const uint32_t lo = wi < nw ? X[wi] : 0u;
-    const uint32_t hi = wi + 1 < nw ? X[wi + 1] : 0u;
-    return __funnelshift_r(lo, hi, sh);
-}
-
-// S_u = sum over gamma-bit chunks t of word u of chunk_t(X), u < Wg = ceil(gamma/32),
-// plus S_{Wg} = 0 (room for the overflow).
-__global__ void fold_colsum(const uint32_t *__restrict__ X, uint64_t nwx, uint64_t gamma,
-                            uint64_t *__restrict__ S, uint32_t Wout) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= Wout) return;
-    const uint64_t Wg = (gamma + 31) >> 5;
-    uint64_t s = 0;
-    if (u < Wg) {
-        const uint64_t nbits = 32 * nwx;
-        const uint64_t nch = (nbits + gamma - 1) / gamma;
-        const uint64_t off = 32 * (uint64_t)u;
-        uint32_t mask = 0xFFFFFFFFu;
-        if (off + 32 > gamma) mask = (uint32_t)((1ull << (gamma - off)) - 1);
-        for (uint64_t t = 0; t < nch; t++) s += bits32(X, nwx, t * gamma + off) & mask;
-    }
-    S[u] = s;
-}
-
-// y (Wout words) -> S_u = (y mod 2^gamma)_u + [u == 0] * (y >> gamma).
-__global__ void fold_final_colsum(const uint32_t *__restrict__ y, uint64_t gamma,
-                                  uint64_t *__restrict__ S, uint32_t Wout) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= Wout) return;
-    const uint64_t off = 32 * (uint64_t)u;
-    uint64_t s = 0;
-    if (off < gamma) {
-        uint32_t mask = 0xFFFFFFFFu;
-        if (off + 32 > gamma) mask = (uint32_t)((1ull << (gamma - off)) - 1);
-        s = y[u] & mask;
-    }
-    if (u == 0) {
-        // y >> gamma: at most 64 bits are ever non-zero here
-        s += bits32(y, Wout, gamma) + ((uint64_t)bits32(y, Wout, gamma + 32) << 32);
-    }
-    S[u] = s;
-}
-
-// flag = (y == 2^gamma - 1) over the low gamma bits (y < 2^gamma guaranteed).
+// flag |= 1 if y (gamma bits) differs from all ones.
 __global__ void allones_check(const uint32_t *__restrict__ y, uint64_t gamma, uint32_t *flag) {
     const uint64_t Wg = (gamma + 31) >> 5;
     int bad = 0;
@@ -252,32 +314,34 @@ __global__ void allones_check(const uint32_t *__restrict__ y, uint64_t gamma, ui
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
-// canonical zero (reading A6): if y == p, y := 0.  flag = 0 means "not all ones".
+// canonical zero (reading A6): if y == p (flag == 0), y := 0.
 __global__ void zero_if_allones(uint32_t *__restrict__ y, uint32_t W, const uint32_t *flag) {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u < W && *flag == 0) y[u] = 0;
 }
 
 // ---------------------------------------------------------------- MH output
-// out byte q = bits of z = Z mod 2^alpha >> (alpha - m), MSB-first (reading A5).
-// Each thread writes one byte (bytes are few: ceil(m/8)).
+// out word q (4 bytes, big-endian) = bits [alpha - 32(q+1), alpha - 32q) of Z, i.e. the
+// next 32 output bits MSB-first (reading A5); bits beyond m are zero.
 __global__ void mh_extract(const uint32_t *__restrict__ Z, uint64_t nwz, uint64_t alpha, uint64_t m,
                            uint8_t *__restrict__ out, uint64_t nbytes) {
     const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (q >= nbytes) return;
-    // output bits 8q .. 8q+7 are z bits m-1-8q ... m-8-8q = Z bits alpha-1-8q ... alpha-8-8q
-    const int64_t top = (int64_t)alpha - 1 - 8 * (int64_t)q;          // Z bit of the byte's MSB
-    const int64_t lowb = top - 7;
+    if (4 * q >= nbytes) return;
+    const int64_t lowb = (int64_t)alpha - 32 * (int64_t)(q + 1);   // Z bit of the word's LSB
     uint32_t v;
+    auto zw = [&](int64_t wi) -> uint32_t { return (wi >= 0 && (uint64_t)wi < nwz) ? Z[wi] : 0u; };
     if (lowb >= 0) {
-        v = (bits32(Z, nwz, (uint64_t)lowb) & 0xFFu);
+        const int64_t wi = lowb >> 5;
+        v = __funnelshift_r(zw(wi), zw(wi + 1), (int)(lowb & 31));
     } else {
-        v = (bits32(Z, nwz, 0) << (-lowb)) & 0xFFu;
+        v = zw(0) << (-lowb);
     }
-    // pad bits (output bit index >= m) are zero
-    const int64_t valid = (int64_t)m - 8 * (int64_t)q;                  // bits of this byte that exist
-    if (valid < 8) v &= (0xFFu << (8 - valid)) & 0xFFu;
-    out[q] = (uint8_t)v;
+    const int64_t valid = (int64_t)m - 32 * (int64_t)q;              // output bits present here
+    if (valid < 32) v &= valid <= 0 ? 0u : ~((1u << (32 - valid)) - 1u);
+    const uint32_t be = __byte_perm(v, 0, 0x0123);
+#pragma unroll
+    for (int b = 0; b < 4; b++)
+        if (4 * q + b < nbytes) out[4 * q + b] = (uint8_t)(be >> (8 * b));
 }
 
 }  // namespace pa

@@ -82,7 +82,7 @@ static double log2_bound(uint64_t nterms, uint64_t overlap, uint32_t B) {
 // over `nterms` products; only coefficients below `need_coef` limbs... (all are needed:
 // the cyclic length must cover the full product so nothing wraps).
 static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int force_B, pa_stage_plan *out) {
-    static const uint32_t Bs[] = {16, 24, 32, 40, 48, 56, 64};
+    static const uint32_t Bs[] = {16, 24, 32, 40, 48, 56};   // B <= 56: limb_redc needs v < p 2^32
     double best = 1e300;
     pa_stage_plan bp{};
     for (uint32_t B : Bs) {
@@ -139,8 +139,8 @@ static int make_plan(const pa_params *prm, Plan *P) {
     if (p.n < 1) return set_err(PA_E_PARAM, "n must be >= 1");
     if (p.r < 16 || p.r % 16) return set_err(PA_E_PARAM, "r must be >= 16 and a multiple of 16 (got %llu)", (unsigned long long)p.r);
     if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
-    if (p.force_B && (p.force_B < 16 || p.force_B > 64 || p.force_B % 8))
-        return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, 64]");
+    if (p.force_B && (p.force_B < 16 || p.force_B > 56 || p.force_B % 8))
+        return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, 56]");
     uint64_t g = prm->gamma;
     if (g == 0) {
         for (uint64_t e : kMersenne) if (e > p.r) { g = e; break; }
@@ -169,7 +169,6 @@ struct StageDev {
     pa_stage_plan pl{};
     uint32_t L = 0, lg = 0;
     PrimeK *pk = nullptr;
-    LimbRed *lred = nullptr;
     uint32_t *scale = nullptr;
     uint32_t *regtw[2] = {}, *regtwp[2] = {};
     uint32_t *rtw = nullptr;            // [P][stride]: col fwd, col inv, row fwd, row inv
@@ -177,6 +176,7 @@ struct StageDev {
     uint32_t rtw_off[4][kMaxRounds] = {};
     uint32_t *ltw_lo[2] = {}, *ltw_hi[2] = {};
     uint32_t ltw_h = 0, ltw_lo_n = 0, ltw_hi_n = 0;
+    uint32_t *tw4[2] = {};              // omega_L^(+-j1 k2) at k2 N1 + j1, [P][L]
     CrtK crt{};
 };
 
@@ -215,14 +215,32 @@ static void round_tables(uint32_t p, uint32_t wL, int lg, int slog, std::vector<
         const uint32_t R = 1u << rl, T = 1u << (srho_log - rl);
         const uint32_t w = (uint32_t)powmod64(wL, 1ull << (lg - srho_log), p);   // omega_{S_rho}
         off[rho] = (uint32_t)tab.size();
-        for (uint32_t k = 0; k < R; k++)
-            for (uint32_t t = 0; t < T; t++)
-                tab.push_back(to_mont((uint32_t)powmod64(w, (uint64_t)t * k, p), p));
+        for (uint32_t k = 0; k < R; k++) {
+            uint64_t wk = powmod64(w, k, p), cur = 1;
+            for (uint32_t t = 0; t < T; t++) { tab.push_back(to_mont((uint32_t)cur, p)); cur = mulmod64(cur, wk, p); }
+        }
         glog += rl;
     }
 }
 
-static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
+// tw4[pi][k2 N1 + j1] = omega_L^(j1 k2) (Montgomery form, canonical) from the two-level tables.
+__global__ void gen_tw4(const uint32_t *__restrict__ lo, const uint32_t *__restrict__ hi, uint32_t lo_n,
+                        uint32_t hi_n, uint32_t h, const PrimeK *__restrict__ pk, uint32_t P, uint32_t lg,
+                        uint32_t n1, uint32_t *__restrict__ out) {
+    const uint64_t L = 1ull << lg;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < P * L; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t pi = (uint32_t)(t >> lg);
+        const uint32_t pos = (uint32_t)(t & (L - 1));
+        const uint32_t k2 = pos / n1, j1 = pos % n1;
+        const uint32_t e = (uint32_t)(((uint64_t)j1 * k2) & (L - 1));
+        const uint32_t p = pk[pi].p, pinv = pk[pi].pinv;
+        const uint32_t a = lo[(size_t)pi * lo_n + (e & ((1u << h) - 1))];
+        const uint32_t b = hi[(size_t)pi * hi_n + (e >> h)];
+        out[t] = red1p(mul_mont(a, b, p, pinv), p);
+    }
+}
+
+static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cudaStream_t st) {
     sd.pl = pl;
     sd.lg = pl.log2_len;
     sd.L = 1u << sd.lg;
@@ -230,7 +248,6 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
     const int lg = (int)sd.lg;
     const int clog = __builtin_ctz(pl.n_col), rlog = __builtin_ctz(pl.n_row);
     std::vector<PrimeK> pk(P);
-    std::vector<LimbRed> lr(P);
     std::vector<uint32_t> scale(P);
     std::vector<uint32_t> regtw[2], regtwp[2];
     std::vector<std::vector<uint32_t>> rt(P);
@@ -246,13 +263,13 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
         for (int it = 0; it < 5; it++) inv *= 2 - p * inv;
         pk[i].pinv = inv;
         pk[i].r2 = (uint32_t)powmod64(2, 64, p);
-        const uint32_t c32 = (uint32_t)((1ull << 32) % p);
-        lr[i] = LimbRed{c32, shoup_of(c32, p), (uint32_t)((1ull << 32) / p)};
         const uint32_t g = primitive_root(p);
         const uint32_t wf = (uint32_t)powmod64(g, (p - 1) >> lg, p);     // omega_L
         const uint32_t wi = inv_mod(wf, p);
         const uint32_t Linv = inv_mod(sd.L, p);
-        scale[i] = (uint32_t)mulmod64(Linv, powmod64(2, 64, p), p);      // L^-1 R^2
+        // packed operands carry 2^-32 (limb_redc); stored hat = T(a) L^-1 R^2 needs
+        // mont(T(a) R^-1, L^-1 R^4)
+        scale[i] = (uint32_t)mulmod64(Linv, powmod64(2, 128, p), p);
         for (int dir = 0; dir < 2; dir++) {
             const uint32_t wL = dir ? wi : wf;
             const uint32_t w32 = (uint32_t)powmod64(wL, sd.L / 32, p);
@@ -261,11 +278,12 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
                 regtw[dir].push_back(t);
                 regtwp[dir].push_back(shoup_of(t, p));
             }
-            for (uint32_t e = 0; e < sd.ltw_lo_n; e++) lo[dir].push_back(to_mont((uint32_t)powmod64(wL, e, p), p));
-            for (uint32_t e = 0; e < sd.ltw_hi_n; e++)
-                hi[dir].push_back(to_mont((uint32_t)powmod64(wL, (uint64_t)e << sd.ltw_h, p), p));
+            uint64_t cur = 1;
+            for (uint32_t e = 0; e < sd.ltw_lo_n; e++) { lo[dir].push_back(to_mont((uint32_t)cur, p)); cur = mulmod64(cur, wL, p); }
+            const uint64_t step = powmod64(wL, 1ull << sd.ltw_h, p);
+            cur = 1;
+            for (uint32_t e = 0; e < sd.ltw_hi_n; e++) { hi[dir].push_back(to_mont((uint32_t)cur, p)); cur = mulmod64(cur, step, p); }
         }
-        // round twiddle tables: col fwd, col inv, row fwd, row inv
         round_tables(p, wf, lg, clog, rt[i], sd.rtw_off[0]);
         round_tables(p, wi, lg, clog, rt[i], sd.rtw_off[1]);
         round_tables(p, wf, lg, rlog, rt[i], sd.rtw_off[2]);
@@ -276,11 +294,9 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
     for (uint32_t i = 0; i < P; i++) rtall.insert(rtall.end(), rt[i].begin(), rt[i].end());
 
     TRY(da.alloc(&sd.pk, P));
-    TRY(da.alloc(&sd.lred, P));
     TRY(da.alloc(&sd.scale, P));
     TRY(da.alloc(&sd.rtw, rtall.size()));
     CUDA_TRY(cudaMemcpy(sd.pk, pk.data(), P * sizeof(PrimeK), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(sd.lred, lr.data(), P * sizeof(LimbRed), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(sd.scale, scale.data(), P * 4, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(sd.rtw, rtall.data(), rtall.size() * 4, cudaMemcpyHostToDevice));
     for (int dir = 0; dir < 2; dir++) {
@@ -288,10 +304,14 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
         TRY(da.alloc(&sd.regtwp[dir], regtwp[dir].size()));
         TRY(da.alloc(&sd.ltw_lo[dir], lo[dir].size()));
         TRY(da.alloc(&sd.ltw_hi[dir], hi[dir].size()));
+        TRY(da.alloc(&sd.tw4[dir], (size_t)P * sd.L));
         CUDA_TRY(cudaMemcpy(sd.regtw[dir], regtw[dir].data(), regtw[dir].size() * 4, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(sd.regtwp[dir], regtwp[dir].data(), regtwp[dir].size() * 4, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(sd.ltw_lo[dir], lo[dir].data(), lo[dir].size() * 4, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(sd.ltw_hi[dir], hi[dir].data(), hi[dir].size() * 4, cudaMemcpyHostToDevice));
+        gen_tw4<<<1024, 256, 0, st>>>(sd.ltw_lo[dir], sd.ltw_hi[dir], sd.ltw_lo_n, sd.ltw_hi_n, sd.ltw_h, sd.pk, P,
+                                      sd.lg, pl.n_row, sd.tw4[dir]);
+        CUDA_TRY(cudaGetLastError());
     }
     // CRT constants
     CrtK &K = sd.crt;
@@ -308,7 +328,6 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd) {
         }
         K.inv[i] = to_mont(i ? inv_mod((uint32_t)prodmod, p) : 1u, p);
     }
-    // prod[l] = p_0 ... p_{l-1}, little-endian words
     std::vector<uint32_t> acc(kMaxPrimes, 0);
     acc[0] = 1;
     for (uint32_t l = 0; l <= P && l <= (uint32_t)kMaxPrimes; l++) {
@@ -428,6 +447,33 @@ static int launch_row(int slog, const RowArgs &A, cudaStream_t st) {
     return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
 }
 
+template <int P, bool RING>
+static int launch_crt_t(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
+                        const uint32_t *addend, uint32_t n_addend, uint64_t *S, uint32_t W, cudaStream_t st) {
+    const uint32_t U = 256;
+    const uint32_t B = sd.pl.limb_bits;
+    const size_t smem = (size_t)((32 * U + 32 * P) / B + 3) * P * 4;
+    crt_colsum_tile<P, RING><<<(W + U - 1) / U, U, smem, st>>>(res, sd.L, ncoef, B, gamma, sd.crt, addend,
+                                                                n_addend, S, W);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+template <bool RING>
+static int launch_crt(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
+                      const uint32_t *addend, uint32_t n_addend, uint64_t *S, uint32_t W, cudaStream_t st) {
+    switch (sd.pl.nprimes) {
+        case 2: return launch_crt_t<2, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+        case 3: return launch_crt_t<3, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+        case 4: return launch_crt_t<4, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+        case 5: return launch_crt_t<5, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+        case 6: return launch_crt_t<6, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+        case 7: return launch_crt_t<7, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+        case 8: return launch_crt_t<8, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+    }
+    return set_err(PA_E_PARAM, "unsupported prime count %u", sd.pl.nprimes);
+}
+
 // ====================================================================== context
 struct ProfRec {
     const char *name;
@@ -441,27 +487,27 @@ struct pa_ctx {
     DevAlloc da;
     StageDev smmh, smh;
     uint32_t nblk = 0;
-    // MMH buffers
+    uint32_t rows_mmh = 0, rows_mh = 0;       // column-pass rows holding limbs
+    uint32_t *res = nullptr;                  // packed residues [nvec][P][rows N1]
     uint32_t *ahat = nullptr, *scratch = nullptr, *acc = nullptr;
-    // MH buffers
     uint32_t *bhat = nullptr, *scratch_mh = nullptr, *acc_mh = nullptr;
     uint32_t *c_words = nullptr;
-    // carries / fold
     uint64_t *S = nullptr;
-    uint32_t *Y = nullptr, *y1 = nullptr, *y2 = nullptr, *Z = nullptr;
-    uint8_t *tg = nullptr, *tp = nullptr, *tcin = nullptr;
+    uint32_t *y1 = nullptr, *y2 = nullptr, *Z = nullptr;
+    uint32_t *cstate = nullptr;               // carry look-back: [kCarrySlots][1 + ntiles]
+    uint32_t cstate_stride = 0;
+    int cslot = 0;
     uint32_t *flag = nullptr;
-    uint8_t *key_dev = nullptr;   // staging for pa_hash_host
+    uint8_t *key_dev = nullptr;               // staging for pa_hash_host
     uint8_t *out_dev = nullptr;
-    uint32_t *parts_dev = nullptr;
-    uint64_t W_Y = 0, Wg = 0, W_Z = 0, ncoef_mmh = 0;
+    uint64_t Wg = 0, W_ring = 0, W_fold = 0, W_Z = 0, ncoef_mmh = 0;
     uint32_t launches = 0;
-    // profiling
     bool prof = false;
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> evpool;
     std::map<std::string, std::pair<double, uint32_t>> acc_ms;
 };
+static constexpr int kCarrySlots = 8;
 
 static cudaEvent_t ev_get(pa_ctx *c) {
     if (!c->evpool.empty()) { cudaEvent_t e = c->evpool.back(); c->evpool.pop_back(); return e; }
@@ -488,37 +534,70 @@ struct ProfScope {
 
 static uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
-// ---- carry resolution of S[0..W) into out[0..W)
-static int run_carry(pa_ctx *c, uint32_t W, uint32_t *out) {
+// zero all look-back state slots used by one hash (one memset)
+static int carry_reset(pa_ctx *c) {
+    CUDA_TRY(cudaMemsetAsync(c->cstate, 0, (size_t)c->cstate_stride * kCarrySlots * 4, c->stream));
+    c->cslot = 0;
+    return PA_OK;
+}
+
+template <class Src>
+static int run_carry(pa_ctx *c, const Src &src, uint32_t W, uint32_t *out, uint32_t *carry_out = nullptr) {
+    if (c->cslot >= kCarrySlots) return set_err(PA_E_STATE, "carry slots exhausted");
+    uint32_t *base = c->cstate + (size_t)c->cslot * c->cstate_stride;
+    c->cslot++;
     const uint32_t nt = (uint32_t)cdiv(W, kTile);
-    carry_tiles<<<nt, kTile, 0, c->stream>>>(c->S, W, c->tg, c->tp);
-    carry_scan<<<1, 1024, 0, c->stream>>>(c->tg, c->tp, nt, nullptr, c->tcin, nullptr);
-    carry_apply<<<nt, kTile, 0, c->stream>>>(c->S, W, c->tcin, out);
-    c->launches += 3;
+    carry_lb<Src><<<nt, kTile, 0, c->stream>>>(src, W, out, base + 1, base, carry_out);
+    c->launches++;
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
 
-// ---- forward + MAC + inverse of one stage; result residues (natural order) in acc
-static int stage_transform(pa_ctx *c, StageDev &sd, int col_mode, const KeySrc *ks, const WordSrc *ws,
-                           uint32_t nvec, uint32_t *scratch, const uint32_t *hat, uint32_t *acc,
-                           const char *tag_fwd1, const char *tag_fwd2, const char *tag_inv) {
+// fold y (W_fold words) three times onto gamma bits and canonicalise into y (reading A6)
+static int mersenne_finish(pa_ctx *c, uint32_t *ya, uint32_t *yb) {
+    const uint64_t g = c->pl.gamma;
+    const uint32_t Wf = (uint32_t)c->W_fold;
+    TRY(run_carry(c, SrcFoldChunks{ya, g, Wf}, Wf, yb));
+    TRY(run_carry(c, SrcFoldChunks{yb, g, Wf}, Wf, ya));
+    TRY(run_carry(c, SrcFoldChunks{ya, g, Wf}, Wf, yb));
+    CUDA_TRY(cudaMemsetAsync(c->flag, 0, 4, c->stream));
+    allones_check<<<std::max(1, g_num_sms), 256, 0, c->stream>>>(yb, g, c->flag);
+    zero_if_allones<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(yb, Wf, c->flag);
+    c->launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+// ---- pack -> forward column pass -> row pass with MAC -> inverse; residues in acc
+template <class Src>
+static int stage_transform(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec, uint32_t rows,
+                           uint32_t *scratch, const uint32_t *hat, uint32_t *acc,
+                           const char *tag_pack, const char *tag_fwd1, const char *tag_fwd2, const char *tag_inv) {
     const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
     const uint32_t P = sd.pl.nprimes;
+    const uint32_t wxp = rows * sd.pl.n_row;
+    {
+        ProfScope ps(c, tag_pack);
+        const uint64_t total = (uint64_t)nvec * wxp;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
+        pack_residues<Src><<<grid, 256, 0, c->stream>>>(src, sd.pk, P, nvec, wxp, c->res);
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+    }
     {
         ProfScope ps(c, tag_fwd1);
         ColArgs A{};
         A.nt = ntt_args(sd, 0, 0);
-        if (ks) A.ks = *ks;
-        if (ws) A.ws = *ws;
-        A.lred = sd.lred;
+        A.src = c->res;
+        A.rows = rows;
+        A.tw4 = sd.tw4[0];
         A.dst = scratch;
         A.nvec = nvec;
         A.units = (sd.pl.n_row / 32) * P * nvec;
-        if (col_mode == COL_KEY) TRY(launch_col<COL_KEY>(clog, A, c->stream));
-        else TRY(launch_col<COL_WORDS>(clog, A, c->stream));
+        TRY(launch_col<COL_FWD>(clog, A, c->stream));
         c->launches++;
     }
+    if (!hat) return PA_OK;
     {
         ProfScope ps(c, tag_fwd2);
         RowArgs R{};
@@ -536,6 +615,7 @@ static int stage_transform(pa_ctx *c, StageDev &sd, int col_mode, const KeySrc *
         R.nt = ntt_args(sd, 1, 1);
         R.src = acc;
         R.dst = acc;
+        R.tw4 = sd.tw4[1];
         R.nvec = 1;
         TRY(launch_row<ROW_INV>(rlog, R, c->stream));
         ColArgs A{};
@@ -551,23 +631,16 @@ static int stage_transform(pa_ctx *c, StageDev &sd, int col_mode, const KeySrc *
 }
 
 // ---- precompute transforms of word vectors (a_i or b) into hat (Montgomery, x 1/L)
-static int precompute_hat(pa_ctx *c, StageDev &sd, const WordSrc &ws, uint32_t nvec, uint32_t *scratch, uint32_t *hat) {
-    const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
-    ColArgs A{};
-    A.nt = ntt_args(sd, 0, 0);
-    A.ws = ws;
-    A.lred = sd.lred;
-    A.dst = scratch;
-    A.nvec = nvec;
-    A.units = (sd.pl.n_row / 32) * sd.pl.nprimes * nvec;
-    TRY(launch_col<COL_WORDS>(clog, A, c->stream));
+static int precompute_hat(pa_ctx *c, StageDev &sd, const WordSrc &ws, uint32_t nvec, uint32_t rows,
+                          uint32_t *scratch, uint32_t *hat) {
+    TRY(stage_transform(c, sd, WordLimbs{ws}, nvec, rows, scratch, nullptr, nullptr, "pre_pack", "pre_col", "", ""));
     RowArgs R{};
     R.nt = ntt_args(sd, 0, 1);
     R.src = scratch;
     R.dst = hat;
     R.scale = sd.scale;
     R.nvec = nvec;
-    TRY(launch_row<ROW_STORE>(rlog, R, c->stream));
+    TRY(launch_row<ROW_STORE>(__builtin_ctz(sd.pl.n_row), R, c->stream));
     return PA_OK;
 }
 
@@ -593,20 +666,35 @@ static int expand_words(uint64_t key0, uint64_t key1, uint64_t bits, std::vector
 
 static const uint64_t kStreamB = 1ull << 63, kStreamC = (1ull << 63) + 1;
 
+static uint32_t rows_for(uint64_t limbs, uint32_t n1, uint32_t n2) {
+    return (uint32_t)std::min<uint64_t>(n2, cdiv(limbs, n1));
+}
+
 static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     Plan &p = c->pl;
-    TRY(setup_stage(c->da, p.mmh, c->smmh));
-    TRY(setup_stage(c->da, p.mh, c->smh));
+    TRY(setup_stage(c->da, p.mmh, c->smmh, c->stream));
+    TRY(setup_stage(c->da, p.mh, c->smh, c->stream));
     c->nblk = (uint32_t)(p.b1 - p.b0);
     const uint32_t Lm = c->smmh.L, Pm = p.mmh.nprimes;
     const uint32_t Lh = c->smh.L, Ph = p.mh.nprimes;
     const uint32_t Bm = p.mmh.limb_bits, Bh = p.mh.limb_bits;
     const uint64_t wx = cdiv(p.r, Bm), wa = cdiv(p.gamma, Bm);
     c->ncoef_mmh = wx + wa - 1;
-    c->W_Y = cdiv(Bm * (c->ncoef_mmh - 1) + 32 * Pm, 32) + 1;
     c->Wg = cdiv(p.gamma, 32);
+    c->W_ring = c->Wg + Pm + 2;              // wrapped pieces of tiny rings may pass the top
+    c->W_fold = c->W_ring;
     c->W_Z = cdiv(p.alpha, 32);
     const uint64_t Wa32 = cdiv(p.gamma, 32), Wal32 = cdiv(p.alpha, 32);
+    const uint32_t rows_x = rows_for(wx, p.mmh.n_row, p.mmh.n_col);
+    const uint32_t rows_a = rows_for(wa, p.mmh.n_row, p.mmh.n_col);
+    c->rows_mmh = rows_x;
+    const uint32_t rows_y = rows_for(cdiv(p.gamma, Bh), p.mh.n_row, p.mh.n_col);
+    const uint32_t rows_b = rows_for(cdiv(p.alpha, Bh), p.mh.n_row, p.mh.n_col);
+    c->rows_mh = rows_y;
+    const uint64_t res_words = std::max<uint64_t>(
+        (uint64_t)c->nblk * Pm * std::max(rows_x, rows_a) * p.mmh.n_row,
+        (uint64_t)Ph * std::max(rows_y, rows_b) * p.mh.n_row);
+    TRY(c->da.alloc(&c->res, res_words));
     TRY(c->da.alloc(&c->ahat, (size_t)c->nblk * Pm * Lm));
     TRY(c->da.alloc(&c->scratch, (size_t)c->nblk * Pm * Lm));
     TRY(c->da.alloc(&c->acc, (size_t)Pm * Lm));
@@ -614,16 +702,13 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     TRY(c->da.alloc(&c->scratch_mh, (size_t)Ph * Lh));
     TRY(c->da.alloc(&c->acc_mh, (size_t)Ph * Lh));
     TRY(c->da.alloc(&c->c_words, Wal32));
-    const uint64_t Smax = std::max<uint64_t>(std::max<uint64_t>(c->W_Y, c->W_Z), c->Wg + 2);
+    const uint64_t Smax = std::max<uint64_t>(c->W_ring, c->W_Z);
     TRY(c->da.alloc(&c->S, Smax));
-    TRY(c->da.alloc(&c->Y, c->W_Y));
-    TRY(c->da.alloc(&c->y1, c->Wg + 2));
-    TRY(c->da.alloc(&c->y2, c->Wg + 2));
+    TRY(c->da.alloc(&c->y1, c->W_fold));
+    TRY(c->da.alloc(&c->y2, c->W_fold));
     TRY(c->da.alloc(&c->Z, c->W_Z));
-    const uint64_t ntmax = cdiv(Smax, kTile);
-    TRY(c->da.alloc(&c->tg, ntmax));
-    TRY(c->da.alloc(&c->tp, ntmax));
-    TRY(c->da.alloc(&c->tcin, ntmax));
+    c->cstate_stride = (uint32_t)(cdiv(Smax, kTile) + 2);
+    TRY(c->da.alloc(&c->cstate, (size_t)c->cstate_stride * kCarrySlots));
     TRY(c->da.alloc(&c->flag, 4));
 
     // ---- hash keys (reading A7): a_i for the shard's blocks, b, c
@@ -645,7 +730,6 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
         const uint32_t mask = (uint32_t)((1ull << (p.alpha % 32)) - 1);
         if ((bw[Wal32 - 1] & ~mask) || (cw[Wal32 - 1] & ~mask)) return set_err(PA_E_PARAM, "b, c must be < 2^alpha");
     }
-    // a_i < p check for explicit keys (all-ones over gamma bits is p itself)
     if (prm->a_words) {
         for (uint32_t i = 0; i < c->nblk; i++) {
             bool all = true;
@@ -665,9 +749,9 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     CUDA_TRY(cudaMemcpyAsync(b_dev, bw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->c_words, cw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
     WordSrc wsa{a_dev, (uint32_t)Wa32, Bm, (uint32_t)wa};
-    int rc = precompute_hat(c, c->smmh, wsa, c->nblk, c->scratch, c->ahat);
+    int rc = precompute_hat(c, c->smmh, wsa, c->nblk, rows_a, c->scratch, c->ahat);
     WordSrc wsb{b_dev, (uint32_t)Wal32, Bh, (uint32_t)cdiv(p.alpha, Bh)};
-    if (rc == PA_OK) rc = precompute_hat(c, c->smh, wsb, 1, c->scratch_mh, c->bhat);
+    if (rc == PA_OK) rc = precompute_hat(c, c->smh, wsb, 1, rows_b, c->scratch_mh, c->bhat);
     cudaError_t e = cudaStreamSynchronize(c->stream);
     cudaFree(a_dev);
     cudaFree(b_dev);
@@ -685,8 +769,8 @@ extern "C" int pa_plan(const pa_params *prm, pa_info *info) {
         info->k = p.k; info->block_begin = p.b0; info->block_end = p.b1;
         info->mmh = p.mmh; info->mh = p.mh;
         const uint64_t nb = p.b1 - p.b0;
-        info->device_bytes = 4ull * (2 * nb + 1) * p.mmh.nprimes * (1ull << p.mmh.log2_len) +
-                             4ull * 3 * p.mh.nprimes * (1ull << p.mh.log2_len);
+        info->device_bytes = 4ull * (3 * nb + 3) * p.mmh.nprimes * (1ull << p.mmh.log2_len) +
+                             4ull * 5 * p.mh.nprimes * (1ull << p.mh.log2_len);
     }
     return PA_OK;
 }
@@ -709,6 +793,7 @@ extern "C" int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out) {
     }
     if (rc == PA_OK) rc = ctx_alloc_and_precompute(c, prm);
     if (rc != PA_OK) {
+        cudaStreamSynchronize(c->stream);
         c->da.free_all();
         delete c;
         return rc;
@@ -727,13 +812,11 @@ extern "C" pa_ctx *pa_ctx_create(uint64_t n, uint64_t r, uint64_t m, uint64_t p,
 
 extern "C" void pa_ctx_destroy(pa_ctx *c) {
     if (!c) return;
-    if (c->stream) cudaStreamSynchronize(c->stream);
-    else cudaDeviceSynchronize();
+    cudaStreamSynchronize(c->stream);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->evpool) cudaEventDestroy(e);
     if (c->key_dev) cudaFree(c->key_dev);
     if (c->out_dev) cudaFree(c->out_dev);
-    if (c->parts_dev) cudaFree(c->parts_dev);
     c->da.free_all();
     delete c;
 }
@@ -756,71 +839,51 @@ extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
     return PA_OK;
 }
 
-// ---- S1-S5 on this ctx's blocks -> canonical y in c->y1 (Wg words, +1 zero word)
-static int run_mmh(pa_ctx *c, const uint8_t *key_slice) {
+// ---- S1-S5 on this ctx's blocks -> canonical y in the returned buffer (Wg words)
+static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
     const Plan &p = c->pl;
-    const uint64_t slice_bytes_total = cdiv(p.n, 8);
+    const uint64_t total_bytes = cdiv(p.n, 8);
     const uint64_t off = p.b0 * (p.r / 8);
-    const uint64_t nbytes = std::min<uint64_t>(slice_bytes_total - std::min(off, slice_bytes_total), (p.b1 - p.b0) * (p.r / 8));
+    const uint64_t nbytes = std::min<uint64_t>(total_bytes - std::min(off, total_bytes), (p.b1 - p.b0) * (p.r / 8));
     KeySrc ks{};
     ks.key = key_slice;
     ks.nbytes = nbytes;
-    // bits >= n ignored: if this slice holds the last key byte, mask its pad bits
-    const bool has_last = (off + nbytes == slice_bytes_total);
+    const bool has_last = (off + nbytes == total_bytes);      // bits >= n ignored
     ks.last_mask = (has_last && (p.n % 8)) ? ((0xFFu << (8 - p.n % 8)) & 0xFFu) : 0xFFu;
     ks.blk_bytes = (uint32_t)(p.r / 8);
     ks.limb_bytes = p.mmh.limb_bits / 8;
     ks.wx = (uint32_t)cdiv(p.r, p.mmh.limb_bits);
     ks.aligned = (((uintptr_t)key_slice) & 3) == 0;
-    TRY(stage_transform(c, c->smmh, COL_KEY, &ks, nullptr, c->nblk, c->scratch, c->ahat, c->acc,
-                        "mmh_fwd_col_pack", "mmh_fwd_row_mac", "mmh_inverse"));
+    TRY(stage_transform(c, c->smmh, KeyLimbs{ks}, c->nblk, c->rows_mmh, c->scratch, c->ahat, c->acc,
+                        "mmh_pack", "mmh_fwd_col", "mmh_fwd_row_mac", "mmh_inverse"));
     {
-        ProfScope ps(c, "mmh_crt_carry");
-        const uint32_t W = (uint32_t)c->W_Y;
-        crt_colsum<<<(uint32_t)cdiv(W, 256), 256, 0, c->stream>>>(c->acc, c->smmh.L, (uint32_t)c->ncoef_mmh,
-                                                                   p.mmh.limb_bits, c->smmh.crt, nullptr, 0, c->S, W);
+        ProfScope ps(c, "mmh_crt_fold");
+        TRY(launch_crt<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->S,
+                             (uint32_t)c->W_ring, c->stream));
         c->launches++;
-        CUDA_TRY(cudaGetLastError());
-        TRY(run_carry(c, W, c->Y));
+        TRY(run_carry(c, SrcArr{c->S}, (uint32_t)c->W_ring, c->y1));
+        TRY(mersenne_finish(c, c->y1, c->y2));
     }
-    {
-        ProfScope ps(c, "mmh_fold");
-        const uint32_t Wf = (uint32_t)c->Wg + 1;
-        fold_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->Y, c->W_Y, p.gamma, c->S, Wf);
-        c->launches++;
-        TRY(run_carry(c, Wf, c->y1));
-        for (int it = 0; it < 2; it++) {
-            fold_final_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, p.gamma, c->S, Wf);
-            c->launches++;
-            TRY(run_carry(c, Wf, c->y1));
-        }
-        CUDA_TRY(cudaMemsetAsync(c->flag, 0, 4, c->stream));
-        allones_check<<<std::max(1, g_num_sms), 256, 0, c->stream>>>(c->y1, p.gamma, c->flag);
-        zero_if_allones<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, Wf, c->flag);
-        c->launches += 2;
-        CUDA_TRY(cudaGetLastError());
-    }
+    *y_out = c->y2;
     return PA_OK;
 }
 
-// ---- S7 on canonical y (Wg words + zero word) -> out_bits
+// ---- S7 on canonical y -> out_bits
 static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     const Plan &p = c->pl;
     const uint32_t Bh = p.mh.limb_bits;
     WordSrc ws{y, (uint32_t)c->Wg, Bh, (uint32_t)cdiv(p.gamma, Bh)};
-    TRY(stage_transform(c, c->smh, COL_WORDS, nullptr, &ws, 1, c->scratch_mh, c->bhat, c->acc_mh,
-                        "mh_fwd_col", "mh_fwd_row_mac", "mh_inverse"));
+    TRY(stage_transform(c, c->smh, WordLimbs{ws}, 1, c->rows_mh, c->scratch_mh, c->bhat, c->acc_mh,
+                        "mh_pack", "mh_fwd_col", "mh_fwd_row_mac", "mh_inverse"));
     {
         ProfScope ps(c, "mh_crt_carry_extract");
         const uint32_t W = (uint32_t)c->W_Z;
         const uint64_t ncoef = std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1);
-        crt_colsum<<<(uint32_t)cdiv(W, 256), 256, 0, c->stream>>>(c->acc_mh, c->smh.L, (uint32_t)ncoef, Bh,
-                                                                   c->smh.crt, c->c_words, W, c->S, W);
+        TRY(launch_crt<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->S, W, c->stream));
         c->launches++;
-        CUDA_TRY(cudaGetLastError());
-        TRY(run_carry(c, W, c->Z));
-        const uint64_t nb = cdiv(p.m, 8);
-        mh_extract<<<(uint32_t)cdiv(nb, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
+        TRY(run_carry(c, SrcArr{c->S}, W, c->Z));
+        const uint64_t nb = cdiv(p.m, 8), nw = cdiv(nb, 4);
+        mh_extract<<<(uint32_t)cdiv(nw, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
         c->launches++;
         CUDA_TRY(cudaGetLastError());
     }
@@ -831,58 +894,34 @@ extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     if (!c || !key_bits || !out_bits) return set_err(PA_E_PARAM, "NULL argument");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     c->launches = 0;
-    TRY(run_mmh(c, key_bits));
-    TRY(run_mh(c, c->y1, out_bits));
+    TRY(carry_reset(c));
+    uint32_t *y = nullptr;
+    TRY(run_mmh(c, key_bits, &y));
+    TRY(run_mh(c, y, out_bits));
     return PA_OK;
-}
-
-__global__ void copy_words(const uint32_t *__restrict__ a, uint32_t *__restrict__ b, uint32_t n) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) b[i] = a[i];
 }
 
 extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
     if (!c || !key_slice || !y_out) return set_err(PA_E_PARAM, "NULL argument");
     c->launches = 0;
-    TRY(run_mmh(c, key_slice));
-    CUDA_TRY(cudaMemcpyAsync(y_out, c->y1, c->Wg * 4, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(carry_reset(c));
+    uint32_t *y = nullptr;
+    TRY(run_mmh(c, key_slice, &y));
+    CUDA_TRY(cudaMemcpyAsync(y_out, y, c->Wg * 4, cudaMemcpyDeviceToDevice, c->stream));
     return PA_OK;
-}
-
-__global__ void sum_parts_colsum(const uint32_t *__restrict__ parts, uint32_t G, uint32_t Wg,
-                                 uint64_t *__restrict__ S, uint32_t Wout) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= Wout) return;
-    uint64_t s = 0;
-    if (u < Wg)
-        for (uint32_t g = 0; g < G; g++) s += parts[(size_t)g * Wg + u];
-    S[u] = s;
 }
 
 extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits) {
     if (!c || !y_parts || !out_bits || G == 0) return set_err(PA_E_PARAM, "bad argument");
     if (G > (1u << 24)) return set_err(PA_E_PARAM, "too many parts");
     c->launches = 0;
-    const Plan &p = c->pl;
-    const uint32_t Wf = (uint32_t)c->Wg + 1;
+    TRY(carry_reset(c));
     {
         ProfScope ps(c, "merge_sum_fold");
-        sum_parts_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(y_parts, G, (uint32_t)c->Wg, c->S, Wf);
-        c->launches++;
-        TRY(run_carry(c, Wf, c->y1));
-        // sum < G 2^gamma: fold the high part (< G) back until < 2^gamma
-        for (int it = 0; it < 2; it++) {
-            fold_final_colsum<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, p.gamma, c->S, Wf);
-            c->launches++;
-            TRY(run_carry(c, Wf, c->y1));
-        }
-        CUDA_TRY(cudaMemsetAsync(c->flag, 0, 4, c->stream));
-        allones_check<<<std::max(1, g_num_sms), 256, 0, c->stream>>>(c->y1, p.gamma, c->flag);
-        zero_if_allones<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(c->y1, Wf, c->flag);
-        c->launches += 2;
-        CUDA_TRY(cudaGetLastError());
+        TRY(run_carry(c, SrcParts{y_parts, G, (uint32_t)c->Wg}, (uint32_t)c->W_fold, c->y1));
+        TRY(mersenne_finish(c, c->y1, c->y2));
     }
-    TRY(run_mh(c, c->y1, out_bits));
+    TRY(run_mh(c, c->y2, out_bits));
     return PA_OK;
 }
 

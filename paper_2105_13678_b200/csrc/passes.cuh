@@ -81,27 +81,52 @@ __device__ __forceinline__ uint64_t word_limb(const WordSrc &s, uint32_t vec, ui
     return s.limb_bits >= 64 ? v : (v & ((1ull << s.limb_bits) - 1));
 }
 
-// x mod p in [0, 2p) for a 64-bit limb value (c32 = 2^32 mod p, Shoup companions).
-struct LimbRed {
-    uint32_t c32, c32p, c1p;
-};
-__device__ __forceinline__ uint32_t limb_mod(uint64_t v, const LimbRed &lr, uint32_t p, uint32_t p2) {
+// Montgomery reduction of a limb value v < 2^56 (hi < 2^24 < p): v 2^-32 mod p in (0, 2p).
+// The factor 2^-32 is common to every element of a packed vector and is compensated in
+// the scale of the precomputed operand (pa_api.cu, setup_stage).
+__device__ __forceinline__ uint32_t limb_redc(uint64_t v, uint32_t p, uint32_t pinv) {
     const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
-    const uint32_t rlo = mul_shoup(lo, 1u, lr.c1p, p);
-    const uint32_t rhi = mul_shoup(hi, lr.c32, lr.c32p, p);
-    return red2p(rlo + rhi, p2);
+    return hi - __umulhi(lo * pinv, p) + p;
 }
 
+// S1 ("split the input bit sequence and map it to a prime field"): every
+// limb of every vector is extracted once and reduced modulo all P primes.
+// res layout: [vec][prime][wxp] with wxp = rows * N1 (zero beyond the vector's limbs).
+template <class Src>
+__global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeK *__restrict__ pk,
+                                                     uint32_t P, uint32_t nvec, uint32_t wxp,
+                                                     uint32_t *__restrict__ res) {
+    const uint64_t total = (uint64_t)nvec * wxp;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t iv = (uint32_t)(t / wxp), j = (uint32_t)(t % wxp);
+        const uint64_t v = src(iv, j);
+        uint32_t *o = res + (size_t)iv * P * wxp + j;
+        for (uint32_t pi = 0; pi < P; pi++) {
+            const uint32_t p = pk[pi].p;
+            o[(size_t)pi * wxp] = v ? limb_redc(v, p, pk[pi].pinv) : 0u;
+        }
+    }
+}
+
+struct KeyLimbs {
+    KeySrc s;
+    __device__ __forceinline__ uint64_t operator()(uint32_t iv, uint32_t j) const { return key_limb(s, iv, j); }
+};
+struct WordLimbs {
+    WordSrc s;
+    __device__ __forceinline__ uint64_t operator()(uint32_t iv, uint32_t j) const { return word_limb(s, iv, j); }
+};
+
 // ---------------------------------------------------------------- column pass
-enum ColMode { COL_KEY = 0, COL_WORDS = 1, COL_INV = 2 };
+enum ColMode { COL_FWD = 0, COL_INV = 2 };
 
 struct ColArgs {
     NttArgs nt;
-    KeySrc ks;
-    WordSrc ws;
-    const LimbRed *lred;     // [P]
-    const uint32_t *src;     // COL_INV: residues [P][L]
-    uint32_t *dst;           // forward: [nvec][P][L]; inverse: [P][L]
+    const uint32_t *src;     // FWD: residues [nvec][P][rows*N1];  INV: [P][L]
+    uint32_t rows;           // FWD: rows holding non-zero limbs (<= N2)
+    const uint32_t *tw4;     // FWD: omega_L^(j1 k2) table [P][L] (Montgomery, canonical)
+    uint32_t *dst;           // FWD: [nvec][P][L];  INV: [P][L]
     uint32_t nvec;           // vectors (blocks) per prime
     uint32_t units;          // (N1/32) * P * nvec
 };
@@ -118,15 +143,13 @@ col_pass(const ColArgs A) {
     const NttArgs &a = A.nt;
     const uint32_t L = 1u << a.log2L;
     const uint32_t P = a.nprimes;
-    const uint32_t ncg = a.n1 >> 5;
     const uint32_t u0 = (uint32_t)(((uint64_t)blockIdx.x * A.units) / gridDim.x);
     const uint32_t u1 = (uint32_t)(((uint64_t)(blockIdx.x + 1) * A.units) / gridDim.x);
     auto sidx = [c](int pos) { return pos * 32 + c; };
 
-    uint32_t tw[E / 2], twp[E / 2], pw[E];
-    int cur_pair = -1;
+    uint32_t tw[E / 2], twp[E / 2];
+    int cur_pi = -1;
     Ctx32 cx{};
-    LimbRed lr{};
     const uint32_t *rtw_p = nullptr;
 
     for (uint32_t u = u0; u < u1; u++) {
@@ -135,9 +158,8 @@ col_pass(const ColArgs A) {
         const uint32_t pi = pair % P;
         const uint32_t cg = pair / P;
         const uint32_t j1 = cg * 32 + c;
-        (void)ncg;
-        if ((int)pair != cur_pair) {
-            cur_pair = (int)pair;
+        if ((int)pi != cur_pi) {
+            cur_pi = (int)pi;
             const PrimeK pk = a.pk[pi];
             cx.p = pk.p; cx.p2 = pk.p2; cx.pinv = pk.pinv;
 #pragma unroll
@@ -146,37 +168,19 @@ col_pass(const ColArgs A) {
                 twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j);
             }
             rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
-            if constexpr (MODE != COL_INV) {
-                lr = A.lred[pi];
-#pragma unroll
-                for (int h = 0; h < E / (1 << SP::rlog(SP::Q - 1)); h++) {
-                    constexpr int R = 1 << SP::rlog(SP::Q - 1);
-#pragma unroll
-                    for (int mm = 0; mm < R; mm++) {
-                        const uint32_t k2 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
-                        const uint32_t e = (uint32_t)(((uint64_t)j1 * k2) & (L - 1));
-                        pw[h * R + mm] = ltw_mont(a, pi, e, cx.p, cx.pinv);
-                    }
-                }
-            }
         }
         uint32_t x[E];
-        // ---- round 0 loads
         {
             constexpr int R = 1 << SP::rlog(0);
+            const uint32_t *src = (MODE == COL_INV) ? A.src + (size_t)pi * L
+                                                    : A.src + ((size_t)iv * P + pi) * ((size_t)A.rows * a.n1);
 #pragma unroll
             for (int h = 0; h < E / R; h++) {
 #pragma unroll
                 for (int m = 0; m < R; m++) {
                     const uint32_t j2 = (uint32_t)in_pos<S_LOG, E_LOG>(v, h, m);
-                    uint32_t val;
-                    if constexpr (MODE == COL_KEY) {
-                        val = limb_mod(key_limb(A.ks, iv, j1 + a.n1 * j2), lr, cx.p, cx.p2);
-                    } else if constexpr (MODE == COL_WORDS) {
-                        val = limb_mod(word_limb(A.ws, iv, j1 + a.n1 * j2), lr, cx.p, cx.p2);
-                    } else {
-                        val = A.src[(size_t)pi * L + (size_t)j2 * a.n1 + j1];
-                    }
+                    uint32_t val = 0;
+                    if (MODE == COL_INV || j2 < A.rows) val = src[(size_t)j2 * a.n1 + j1];
                     x[h * R + m] = val;
                 }
             }
@@ -184,20 +188,21 @@ col_pass(const ColArgs A) {
         __syncthreads();    // previous unit's last-round smem reads are done
         round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         rounds_rest<S_LOG, E_LOG, 1>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
-        // ---- outputs
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
             uint32_t *dst = (MODE == COL_INV) ? A.dst + (size_t)pi * L
                                               : A.dst + ((size_t)iv * P + pi) * L;
+            const uint32_t *tw4 = A.tw4 + (size_t)pi * L;
 #pragma unroll
             for (int h = 0; h < E / R; h++) {
 #pragma unroll
                 for (int mm = 0; mm < R; mm++) {
                     const uint32_t k2 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
+                    const size_t o = (size_t)k2 * a.n1 + j1;
                     uint32_t val = x[h * R + mm];
-                    if constexpr (MODE != COL_INV) val = mul_mont(val, pw[h * R + mm], cx.p, cx.pinv);
+                    if constexpr (MODE != COL_INV) val = mul_mont(val, __ldg(tw4 + o), cx.p, cx.pinv);
                     else val = red1p(val, cx.p);
-                    dst[(size_t)k2 * a.n1 + j1] = val;
+                    dst[o] = val;
                 }
             }
         }
@@ -213,6 +218,7 @@ struct RowArgs {
     uint32_t *dst;            // MAC: [P][L] accumulators;  STORE: [nvec][P][L];  INV: [P][L]
     const uint32_t *ahat;     // MAC: [nvec][P][L] (Montgomery form, times 1/L)
     const uint32_t *scale;    // STORE: [P] Montgomery constant multiplied into outputs
+    const uint32_t *tw4;      // INV: omega_L^(-j1 k2) table [P][L] (Montgomery, canonical)
     uint32_t nvec;
     uint32_t units;           // (N2 / V) * P
 };
@@ -289,8 +295,8 @@ row_pass(const RowArgs A) {
 #pragma unroll
                     for (int mm = 0; mm < R; mm++) {
                         const uint32_t j1 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
-                        const uint32_t e = (uint32_t)(((uint64_t)j1 * k2) & (L - 1));
-                        dst[j1] = mul_mont(x[h * R + mm], ltw_mont(a, pi, e, cx.p, cx.pinv), cx.p, cx.pinv);
+                        const uint32_t w = __ldg(A.tw4 + (size_t)pi * L + (size_t)k2 * S + j1);
+                        dst[j1] = mul_mont(x[h * R + mm], w, cx.p, cx.pinv);
                     }
             }
         }

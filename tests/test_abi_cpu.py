@@ -72,9 +72,11 @@ def test_plan_configs(name):
 
 
 def test_plan_forced_limb_bits():
-    for Bl in (16, 24, 32, 40, 48, 56, 64):
+    for Bl in (16, 24, 32, 40, 48, 56):
         info = P.plan(1 << 20, 1 << 16, 100_000, limb_bits=Bl)
         assert info["mmh"]["limb_bits"] == Bl and info["mh"]["limb_bits"] == Bl
+    with pytest.raises(B.PAError):
+        P.plan(1 << 20, 1 << 16, 100_000, limb_bits=64)     # limb_redc needs B <= 56
 
 
 def test_philox_matches_numpy():
