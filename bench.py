@@ -42,55 +42,90 @@ def load_peaks() -> dict:
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled DURING the timed region: an NVML
+    polling thread (1 ms period), falling back to `nvidia-smi -lms 100`."""
+    SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
-        self.proc = None
-        self.lines: list[str] = []
+    def __init__(self, torch_dev: int):
+        self.dev = torch_dev
+        self.sm: list[float] = []
+        self.reasons: set[str] = set()
+        self.smax = None
+        self.mode = None
+        self._stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.dev)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+
+    def _poll_nvml(self, nv, h):
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, bit in self.REASONS:
+                    if rs & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def start(self):
         try:
+            nv, h = self._nvml_handle()
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.mode = "nvml (1 ms polling thread)"
+            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            pass
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.SMI_FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.mode = "nvidia-smi -lms 100"
+            self.t = threading.Thread(target=self._read_smi, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.mode = None
 
-    def _read(self):
+    def _read_smi(self):
+        names = [n for n, _ in self.REASONS[:4]]
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
-
-    def stop(self) -> dict:
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(2)
-        except Exception:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
+            f = [x.strip() for x in ln.strip().split(",")]
             if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[1]))
-                smax = float(f[2])
+                self.sm.append(float(f[1]))
+                self.smax = float(f[2])
             except ValueError:
                 continue
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
-                    reasons.add(nm)
-        loaded = [s for s in sm if s > 600] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                    self.reasons.add(nm)
+
+    def stop(self) -> dict:
+        if self.mode is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        self._stop.set()
+        if self.mode.startswith("nvidia-smi"):
+            time.sleep(0.25)
+            self.proc.terminate()
+        self.t.join(timeout=3)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "sampler": self.mode}
 
 
 # --------------------------------------------------------------------------- roofline
@@ -105,7 +140,7 @@ def stage_ops(info: dict, stage: str) -> float:
         import math
         return nvec * pl["nprimes"] * (L / 2) * math.log2(npass_len)
 
-    if stage == "mmh_fwd_col_pack":
+    if stage == "mmh_fwd_col":
         return INT_OPS_PER_BFLY * bfly(mmh, nblk, mmh["n_col"])
     if stage == "mmh_fwd_row_mac":
         L = 1 << mmh["log2_len"]
@@ -122,7 +157,9 @@ def stage_ops(info: dict, stage: str) -> float:
 
 
 def roofline(info: dict, stages: dict, peaks: dict, steps: int) -> dict:
-    """Dominant kernel stage -> achieved int32 Gop/s vs the issue-rate peak."""
+    """Dominant kernel stage -> achieved int32 Gop/s vs the issue-rate peak.
+    `stages` maps stage -> (ms per step, launches per step), from CUDA events recorded
+    on the context stream around each launch (pa_ctx_set_profiling)."""
     name, (ms, cnt) = max(stages.items(), key=lambda kv: kv[1][0])
     per_launch_ms = ms / max(cnt, 1)
     ops = stage_ops(info, name)
@@ -192,7 +229,7 @@ def run_reference(args, w) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
@@ -210,7 +247,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2105_13678_b200 import PAContext
-    from paper_2105_13678_b200.pa import key_slice_bytes, shard_ranges
+    from paper_2105_13678_b200.pa import distributed_hash, key_slice_bytes, shard_ranges
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -231,23 +268,18 @@ def main():
     ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None)
     info = ctx.query()
     out = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
-    yw = ctx.y_words
-    parts = torch.empty((world, yw), dtype=torch.int32, device=dev) if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
         if world == 1:
             ctx.hash(key_dev, out)
         else:
-            y = ctx.mmh_partial(key_dev)
-            dist.all_gather_into_tensor(parts, y)
-            if rank == 0:
-                ctx.mh_merge(parts, out)
+            distributed_hash(ctx, key_dev)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = ctx.query()["kernels_per_hash"] + (ctx.query()["kernels_per_hash"] if False else 0)
+    launches0 = ctx.query()["launches_total"]
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local)
@@ -268,22 +300,24 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
+    launches_timed = (ctx.query()["launches_total"] - launches0) % (1 << 32)
     times = [a.elapsed_time(b) for a, b in evs]
     tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_per_step = tot.item() / args.steps
 
-    # ---- per-stage times (profiling pass, untimed), e2e through the host-buffer API
+    # ---- per-launch times: the same K steps again with CUDA events recorded on the
+    # context stream around every launch (pa_ctx_set_profiling); e2e via the host API
     ctx.set_profiling(True)
     ctx.stage_times(reset=True)
-    for _ in range(3):
+    for _ in range(args.steps):
         if not args.no_flush:
             flush.fill_(1)
         step()
     stages = ctx.stage_times()
     ctx.set_profiling(False)
-    nsteps_prof = 3
+    nsteps_prof = args.steps
     stages = {kname: (v[0], v[1]) for kname, v in stages.items()}
 
     e2e = None
@@ -326,7 +360,7 @@ def main():
                    "mh_plan": {kk: info["mh"][kk] for kk in ("limb_bits", "nprimes", "log2_len", "n_col", "n_row")},
                    "parallelism": f"blocks sharded over {world} rank(s), residues all-gathered (NCCL), MH on rank 0",
                    "l2": "flushed (256 MiB write) before every timed step" if not args.no_flush else "not flushed"},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches_timed,
         "clocks": clocks,
         "roofline": roof,
         "stages_ms_per_step": {kk: v[0] / nsteps_prof for kk, v in sorted(stages.items())},

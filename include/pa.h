@@ -81,8 +81,10 @@ typedef struct {
     pa_stage_plan mmh;
     pa_stage_plan mh;
     uint64_t device_bytes;   /* device memory held by the context */
-    uint32_t kernels_per_hash; /* kernel launches enqueued by one pa_hash */
-    uint32_t reserved;
+    uint32_t kernels_per_hash; /* kernel launches enqueued by the last pa_hash /
+                                  pa_mmh_partial / pa_mh_merge call */
+    uint32_t launches_total; /* kernel launches enqueued since creation (mod 2^32),
+                                precompute included */
 } pa_info;
 
 typedef struct {

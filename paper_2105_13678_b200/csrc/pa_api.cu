@@ -501,7 +501,8 @@ struct pa_ctx {
     uint8_t *key_dev = nullptr;               // staging for pa_hash_host
     uint8_t *out_dev = nullptr;
     uint64_t Wg = 0, W_ring = 0, W_fold = 0, W_Z = 0, ncoef_mmh = 0;
-    uint32_t launches = 0;
+    uint32_t launches = 0;            // launches of the current / last hash call
+    uint32_t launches_total = 0;      // since creation
     bool prof = false;
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> evpool;
@@ -830,6 +831,7 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
     info->mmh = p.mmh; info->mh = p.mh;
     info->device_bytes = c->da.bytes;
     info->kernels_per_hash = c->launches;
+    info->launches_total = c->launches_total;
     return PA_OK;
 }
 
@@ -896,9 +898,10 @@ extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     c->launches = 0;
     TRY(carry_reset(c));
     uint32_t *y = nullptr;
-    TRY(run_mmh(c, key_bits, &y));
-    TRY(run_mh(c, y, out_bits));
-    return PA_OK;
+    int rc = run_mmh(c, key_bits, &y);
+    if (rc == PA_OK) rc = run_mh(c, y, out_bits);
+    c->launches_total += c->launches;
+    return rc;
 }
 
 extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
@@ -906,7 +909,9 @@ extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_o
     c->launches = 0;
     TRY(carry_reset(c));
     uint32_t *y = nullptr;
-    TRY(run_mmh(c, key_slice, &y));
+    const int rc = run_mmh(c, key_slice, &y);
+    c->launches_total += c->launches;
+    TRY(rc);
     CUDA_TRY(cudaMemcpyAsync(y_out, y, c->Wg * 4, cudaMemcpyDeviceToDevice, c->stream));
     return PA_OK;
 }
@@ -916,13 +921,15 @@ extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8
     if (G > (1u << 24)) return set_err(PA_E_PARAM, "too many parts");
     c->launches = 0;
     TRY(carry_reset(c));
+    int rc;
     {
         ProfScope ps(c, "merge_sum_fold");
-        TRY(run_carry(c, SrcParts{y_parts, G, (uint32_t)c->Wg}, (uint32_t)c->W_fold, c->y1));
-        TRY(mersenne_finish(c, c->y1, c->y2));
+        rc = run_carry(c, SrcParts{y_parts, G, (uint32_t)c->Wg}, (uint32_t)c->W_fold, c->y1);
+        if (rc == PA_OK) rc = mersenne_finish(c, c->y1, c->y2);
     }
-    TRY(run_mh(c, c->y2, out_bits));
-    return PA_OK;
+    if (rc == PA_OK) rc = run_mh(c, c->y2, out_bits);
+    c->launches_total += c->launches;
+    return rc;
 }
 
 extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {

@@ -189,16 +189,32 @@ def key_slice_bytes(n: int, r: int, block_range) -> tuple[int, int]:
     return min(b0 * r // 8, nb), min(b1 * r // 8, nb)
 
 
-def distributed_hash(ctx: PAContext, key_slice, group=None, root: int = 0):
-    """Multi-GPU hash of one key (S6): every rank computes its shard residue, the
-    residues are all-gathered with torch.distributed (NCCL over NVLink on B200), and
-    `root` merges them mod p and runs MH.  Returns the output on root, else None."""
+def gather_residues(y, group=None):
+    """S6 exchange: all-gather every rank's residue words (a [W] int32 tensor) into a
+    [G, W] tensor on every rank.  NCCL over NVLink on B200; gloo on CPU for tests."""
     import torch
     import torch.distributed as dist
-    y = ctx.mmh_partial(key_slice)
     G = dist.get_world_size(group)
     parts = torch.empty((G, y.numel()), dtype=y.dtype, device=y.device)
-    dist.all_gather_into_tensor(parts, y, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(parts, y.contiguous(), group=group)
+    else:
+        dist.all_gather(list(parts.unbind(0)), y.contiguous(), group=group)
+    return parts
+
+
+def shard_gather_merge(partial_fn, merge_fn, key_slice, group=None, root: int = 0):
+    """Multi-GPU hash of one key: y_g = partial_fn(key_slice) on every
+    rank, residues all-gathered, ``merge_fn(parts)`` (sum mod p + MH) on ``root``.
+    Returns the output on root, else None."""
+    import torch.distributed as dist
+    parts = gather_residues(partial_fn(key_slice), group)
     if dist.get_rank(group) == root:
-        return ctx.mh_merge(parts)
+        return merge_fn(parts)
     return None
+
+
+def distributed_hash(ctx: PAContext, key_slice, group=None, root: int = 0):
+    """Multi-GPU hash with a shard context: pa_mmh_partial on every rank, NCCL all-gather
+    of the residues, pa_mh_merge on `root` (S6-S7)."""
+    return shard_gather_merge(ctx.mmh_partial, ctx.mh_merge, key_slice, group, root)
