@@ -12,9 +12,10 @@
 //  * MH (S7): plain column sums of b*y plus the addend c, words below alpha
 //    (Eq. 4).
 //  * Carry resolution: 64-bit column sums -> 32-bit words with a generate/propagate
-//    carry-lookahead: warp ballots inside a tile, single-pass decoupled look-back between
-//    tiles (a tile that does not propagate ends the look-back).
-//  * Final folds + canonical zero (reading A6), MH bit extraction (readings A5, A8).
+//    carry-lookahead: 8 words per thread, warp ballots inside a tile, single-pass
+//    decoupled look-back between tiles (a tile that does not propagate ends the look-back).
+//  * Mersenne finish: the residual fold (x >> gamma) + (x mod 2^gamma) and canonical zero
+//    (reading A6) in one CTA; MH bit extraction (readings A5, A8).
 #pragma once
 #include <cstdint>
 #include "modarith.cuh"
@@ -172,8 +173,6 @@ __global__ void __launch_bounds__(256) crt_colsum_tile(const uint32_t *__restric
 }
 
 // ---------------------------------------------------------------- carry resolution
-constexpr int kTile = 1024;
-
 // (g, p) over 32 lanes given ballot masks: per-lane carry-in (bit i) and carry out.
 __device__ __forceinline__ uint32_t lane_carries(uint32_t Gm, uint32_t Pm, uint32_t cin, uint32_t &cout) {
     const uint64_t A = (uint64_t)(Gm | Pm), Bm = Gm;
@@ -215,29 +214,8 @@ __device__ __forceinline__ uint32_t block_carries(int g, int pp, uint32_t cin, u
 // Sources of 64-bit column sums for the carry kernel.
 struct SrcArr {
     const uint64_t *S;
-    __device__ __forceinline__ uint64_t operator()(uint32_t u) const { return S[u]; }
-};
-// Mersenne fold of y (W words) by chunks (PAPER.md:130-132 applied to all chunks at once):
-// S_u = sum_t word u of bits [t gamma, (t+1) gamma) of y, for u < ceil(gamma/32); 0 above.
-struct SrcFoldChunks {
-    const uint32_t *y;
-    uint64_t gamma;
-    uint32_t W;            // words of y
-    __device__ __forceinline__ uint32_t bits32(uint64_t start) const {
-        const uint64_t wi = start >> 5;
-        const int sh = (int)(start & 31);
-        const uint32_t lo = wi < W ? y[wi] : 0u, hi = wi + 1 < W ? y[wi + 1] : 0u;
-        return __funnelshift_r(lo, hi, sh);
-    }
-    __device__ __forceinline__ uint64_t operator()(uint32_t u) const {
-        const uint64_t off = 32 * (uint64_t)u;
-        if (off >= gamma) return 0;
-        const uint32_t mask = (off + 32 > gamma) ? (uint32_t)((1ull << (gamma - off)) - 1) : 0xFFFFFFFFu;
-        const uint64_t nch = (32ull * W + gamma - 1) / gamma;
-        uint64_t s = 0;
-        for (uint64_t t = 0; t < nch; t++) s += bits32(t * gamma + off) & mask;
-        return s;
-    }
+    uint32_t n;            // words present; S_u = 0 for u >= n
+    __device__ __forceinline__ uint64_t operator()(uint32_t u) const { return u < n ? S[u] : 0ull; }
 };
 // Sum of G residues (S6): S_u = sum_g parts[g][u].
 struct SrcParts {
@@ -251,29 +229,48 @@ struct SrcParts {
     }
 };
 
-// Single-pass carry resolution: out[u] = word u of sum_u S_u 2^(32u), u < W.
-// state[ntiles] and ticket must be zero before the launch.  state encoding:
-// bit0 aggregate ready, bit1 g, bit2 p, bit3 inclusive ready, bit4 inclusive carry-out.
+// ---------------------------------------------------------------- multiword carry scan
+// out[u] = word u of sum_u S_u 2^(32u) for u < W (the caller sizes W so nothing is
+// lost above).  One thread owns kCarryV consecutive words; a tile is 256 threads.
+// Word u: t_u = lo32(S_u) + hi32(S_{u-1}) < 2^33 -> digit w_u = lo32(t_u) with a
+// generate bit g_u = t_u >> 32 and a propagate bit p_u = (w_u == 2^32 - 1).  Thread
+// aggregates are scanned with warp ballots; tiles chain through decoupled look-back.
+constexpr int kCarryV = 8;
+constexpr int kCarryT = 256;
+constexpr int kCarryTile = kCarryV * kCarryT;
+
 template <class Src>
-__global__ void __launch_bounds__(kTile) carry_lb(const Src src, uint32_t W, uint32_t *__restrict__ out,
-                                                  uint32_t *state, uint32_t *ticket, uint32_t *carry_out) {
+__global__ void __launch_bounds__(kCarryT) carry_mw(const Src src, uint32_t W, uint32_t *__restrict__ out,
+                                                  uint32_t *state, uint32_t *ticket) {
     __shared__ uint32_t s_tile, s_cin;
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
-    const uint32_t ntiles = (W + kTile - 1) / kTile;
-    const uint32_t u = tile * kTile + threadIdx.x;
-    const uint64_t su = (u < W) ? src(u) : 0ull;
-    const uint64_t sp = (u > 0 && u - 1 < W) ? src(u - 1) : 0ull;
-    const uint64_t t = (su & 0xFFFFFFFFull) + (sp >> 32);
-    const uint32_t w = (uint32_t)t;
-    const int g = (int)(t >> 32);
-    const int pp = (u < W) ? (w == 0xFFFFFFFFu) : 1;
-    const int allp = __syncthreads_and(pp);
+    const uint32_t u0 = tile * kCarryTile + threadIdx.x * kCarryV;
+    uint32_t w[kCarryV];
+    uint32_t gm = 0, pm = 0;                       // per-word generate / propagate bits
+    uint64_t prev = (u0 > 0 && u0 - 1 < W) ? src(u0 - 1) : 0ull;
+#pragma unroll
+    for (int j = 0; j < kCarryV; j++) {
+        const uint32_t u = u0 + j;
+        const uint64_t s = (u < W) ? src(u) : 0ull;
+        const uint64_t t = (s & 0xFFFFFFFFull) + (prev >> 32);
+        prev = s;
+        w[j] = (uint32_t)t;
+        gm |= (uint32_t)(t >> 32) << j;
+        pm |= (uint32_t)((u >= W) || (w[j] == 0xFFFFFFFFu)) << j;
+    }
+    // thread aggregate (carry out with carry-in 0; all-propagate)
+    uint32_t G = 0;
+#pragma unroll
+    for (int j = 0; j < kCarryV; j++) G = ((gm >> j) & 1u) | (((pm >> j) & 1u) & G);
+    const int Pall = (pm == (1u << kCarryV) - 1u);
+    const int allp = __syncthreads_and(Pall);
     uint32_t bg;
-    (void)block_carries(g, pp, 0, &bg);
+    (void)block_carries((int)G, Pall, 0, &bg);
     if (threadIdx.x == 0) {
         volatile uint32_t *vs = state;
+        const uint32_t ntiles = (W + kCarryTile - 1) / kCarryTile;
         uint32_t cin = 0;
         if (tile > 0) {
             vs[tile] = 1u | (bg << 1) | ((uint32_t)allp << 2);
@@ -295,29 +292,96 @@ __global__ void __launch_bounds__(kTile) carry_lb(const Src src, uint32_t W, uin
         __threadfence();
         vs[tile] = 1u | (bg << 1) | ((uint32_t)allp << 2) | 8u | (incl << 4);
         s_cin = cin;
-        if (tile == ntiles - 1 && carry_out) *carry_out = incl;
+        (void)ntiles;
     }
     __syncthreads();
-    const uint32_t c = block_carries(g, pp, s_cin, nullptr);
-    if (u < W) out[u] = w + c;
-}
-
-// flag |= 1 if y (gamma bits) differs from all ones.
-__global__ void allones_check(const uint32_t *__restrict__ y, uint64_t gamma, uint32_t *flag) {
-    const uint64_t Wg = (gamma + 31) >> 5;
-    int bad = 0;
-    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < Wg; u += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t want = 0xFFFFFFFFu;
-        if (32 * u + 32 > gamma) want = (uint32_t)((1ull << (gamma - 32 * u)) - 1);
-        if (y[u] != want) bad = 1;
+    uint32_t c = block_carries((int)G, Pall, s_cin, nullptr);
+#pragma unroll
+    for (int j = 0; j < kCarryV; j++) {
+        const uint32_t u = u0 + j;
+        if (u < W) out[u] = w[j] + c;
+        c = ((gm >> j) & 1u) | (((pm >> j) & 1u) & c);
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
-// canonical zero (reading A6): if y == p (flag == 0), y := 0.
-__global__ void zero_if_allones(uint32_t *__restrict__ y, uint32_t W, const uint32_t *flag) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u < W && *flag == 0) y[u] = 0;
+// ---------------------------------------------------------------- Mersenne finish
+// y (Wtot words, y < 2^(32 Wtot)) -> y mod (2^gamma - 1), canonical in [0, p-1]
+// (reading A6), in place, by the fold x mod M_gamma = (x >> gamma) + (x mod 2^gamma)
+// repeated until nothing is left above bit gamma.  One CTA of
+// 1024 threads: the fold adds a short number (Wtot - floor(gamma/32) words) at bit 0,
+// whose carry ripples only through a run of all-ones words -- one chunk of 1024 words
+// almost always, more chunks only for such runs (correct either way).
+constexpr int kFinT = 1024;
+
+__device__ __forceinline__ void fin_ripple(uint32_t *y, uint32_t Wtot, uint32_t from) {
+    // add 1 at word `from`, rippling through all-ones words
+    __shared__ uint32_t s_first;
+    for (uint32_t base = from; base < Wtot; base += kFinT) {
+        if (threadIdx.x == 0) s_first = 0xFFFFFFFFu;
+        __syncthreads();
+        const uint32_t u = base + threadIdx.x;
+        const uint32_t v = (u < Wtot) ? y[u] : 0u;
+        if (u < Wtot && v != 0xFFFFFFFFu) atomicMin(&s_first, u);
+        __syncthreads();
+        const uint32_t f = s_first;
+        if (u < Wtot && u < f) y[u] = 0u;
+        if (u == f) y[u] = v + 1u;
+        __syncthreads();
+        if (f != 0xFFFFFFFFu) return;     // carry absorbed (uniform)
+    }
+}
+
+__global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict__ y, uint32_t Wtot, uint64_t gamma) {
+    __shared__ uint32_t T[64];
+    __shared__ uint32_t s_nz, s_carry, s_bad;
+    const uint32_t gw = (uint32_t)(gamma >> 5);
+    const int gs = (int)(gamma & 31);
+    const uint32_t nT = Wtot - gw;                       // words of y >> gamma (<= 64)
+    for (;;) {
+        if (threadIdx.x == 0) s_nz = 0;
+        __syncthreads();
+        if (threadIdx.x < nT) {
+            const uint32_t i = gw + threadIdx.x;
+            const uint32_t lo = y[i], hi = (i + 1 < Wtot) ? y[i + 1] : 0u;
+            const uint32_t t = gs ? __funnelshift_r(lo, hi, gs) : lo;
+            T[threadIdx.x] = t;
+            if (t) atomicOr(&s_nz, 1u);
+        }
+        __syncthreads();
+        if (!s_nz) break;
+        if (threadIdx.x < nT) {                           // clear bits >= gamma
+            const uint32_t i = gw + threadIdx.x;
+            if (threadIdx.x == 0 && gs) y[i] &= (1u << gs) - 1u;
+            else y[i] = 0u;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {                           // y += T (short add)
+            uint64_t cy = 0;
+            for (uint32_t t = 0; t < nT && t < Wtot; t++) {
+                const uint64_t s = (uint64_t)y[t] + T[t] + cy;
+                y[t] = (uint32_t)s;
+                cy = s >> 32;
+            }
+            s_carry = (uint32_t)cy;
+        }
+        __syncthreads();
+        if (s_carry && nT < Wtot) fin_ripple(y, Wtot, nT);
+        __syncthreads();
+    }
+    // canonical zero: y == 2^gamma - 1 -> 0
+    const uint32_t Wg = (uint32_t)((gamma + 31) >> 5);
+    for (uint32_t base = 0; base < Wg; base += kFinT) {
+        if (threadIdx.x == 0) s_bad = 0;
+        __syncthreads();
+        const uint32_t u = base + threadIdx.x;
+        if (u < Wg) {
+            const uint32_t want = (u == Wg - 1 && gs) ? ((1u << gs) - 1u) : 0xFFFFFFFFu;
+            if (y[u] != want) atomicOr(&s_bad, 1u);
+        }
+        __syncthreads();
+        if (s_bad) return;
+    }
+    for (uint32_t u = threadIdx.x; u < Wg; u += kFinT) y[u] = 0u;
 }
 
 // ---------------------------------------------------------------- MH output

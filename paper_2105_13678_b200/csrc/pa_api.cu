@@ -493,11 +493,10 @@ struct pa_ctx {
     uint32_t *bhat = nullptr, *scratch_mh = nullptr, *acc_mh = nullptr;
     uint32_t *c_words = nullptr;
     uint64_t *S = nullptr;
-    uint32_t *y1 = nullptr, *y2 = nullptr, *Z = nullptr;
+    uint32_t *y1 = nullptr, *Z = nullptr;
     uint32_t *cstate = nullptr;               // carry look-back: [kCarrySlots][1 + ntiles]
     uint32_t cstate_stride = 0;
     int cslot = 0;
-    uint32_t *flag = nullptr;
     uint8_t *key_dev = nullptr;               // staging for pa_hash_host
     uint8_t *out_dev = nullptr;
     uint64_t Wg = 0, W_ring = 0, W_fold = 0, W_Z = 0, ncoef_mmh = 0;
@@ -543,28 +542,21 @@ static int carry_reset(pa_ctx *c) {
 }
 
 template <class Src>
-static int run_carry(pa_ctx *c, const Src &src, uint32_t W, uint32_t *out, uint32_t *carry_out = nullptr) {
+static int run_carry(pa_ctx *c, const Src &src, uint32_t W, uint32_t *out) {
     if (c->cslot >= kCarrySlots) return set_err(PA_E_STATE, "carry slots exhausted");
     uint32_t *base = c->cstate + (size_t)c->cslot * c->cstate_stride;
     c->cslot++;
-    const uint32_t nt = (uint32_t)cdiv(W, kTile);
-    carry_lb<Src><<<nt, kTile, 0, c->stream>>>(src, W, out, base + 1, base, carry_out);
+    const uint32_t nt = (uint32_t)cdiv(W, kCarryTile);
+    carry_mw<Src><<<nt, kCarryT, 0, c->stream>>>(src, W, out, base + 1, base);
     c->launches++;
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
 
-// fold y (W_fold words) three times onto gamma bits and canonicalise into y (reading A6)
-static int mersenne_finish(pa_ctx *c, uint32_t *ya, uint32_t *yb) {
-    const uint64_t g = c->pl.gamma;
-    const uint32_t Wf = (uint32_t)c->W_fold;
-    TRY(run_carry(c, SrcFoldChunks{ya, g, Wf}, Wf, yb));
-    TRY(run_carry(c, SrcFoldChunks{yb, g, Wf}, Wf, ya));
-    TRY(run_carry(c, SrcFoldChunks{ya, g, Wf}, Wf, yb));
-    CUDA_TRY(cudaMemsetAsync(c->flag, 0, 4, c->stream));
-    allones_check<<<std::max(1, g_num_sms), 256, 0, c->stream>>>(yb, g, c->flag);
-    zero_if_allones<<<(uint32_t)cdiv(Wf, 256), 256, 0, c->stream>>>(yb, Wf, c->flag);
-    c->launches += 2;
+// y (W_fold words, resolved) -> y mod p, canonical (reading A6), in place
+static int mersenne_finish(pa_ctx *c, uint32_t *y) {
+    mersenne_finish_k<<<1, kFinT, 0, c->stream>>>(y, (uint32_t)c->W_fold, c->pl.gamma);
+    c->launches++;
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
@@ -683,7 +675,7 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     c->ncoef_mmh = wx + wa - 1;
     c->Wg = cdiv(p.gamma, 32);
     c->W_ring = c->Wg + Pm + 2;              // wrapped pieces of tiny rings may pass the top
-    c->W_fold = c->W_ring;
+    c->W_fold = c->W_ring + 2;               // 64-bit column sums carry into 2 more words
     c->W_Z = cdiv(p.alpha, 32);
     const uint64_t Wa32 = cdiv(p.gamma, 32), Wal32 = cdiv(p.alpha, 32);
     const uint32_t rows_x = rows_for(wx, p.mmh.n_row, p.mmh.n_col);
@@ -703,14 +695,12 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     TRY(c->da.alloc(&c->scratch_mh, (size_t)Ph * Lh));
     TRY(c->da.alloc(&c->acc_mh, (size_t)Ph * Lh));
     TRY(c->da.alloc(&c->c_words, Wal32));
-    const uint64_t Smax = std::max<uint64_t>(c->W_ring, c->W_Z);
+    const uint64_t Smax = std::max<uint64_t>(c->W_fold, c->W_Z);
     TRY(c->da.alloc(&c->S, Smax));
     TRY(c->da.alloc(&c->y1, c->W_fold));
-    TRY(c->da.alloc(&c->y2, c->W_fold));
     TRY(c->da.alloc(&c->Z, c->W_Z));
-    c->cstate_stride = (uint32_t)(cdiv(Smax, kTile) + 2);
+    c->cstate_stride = (uint32_t)(cdiv(Smax, kCarryTile) + 2);
     TRY(c->da.alloc(&c->cstate, (size_t)c->cstate_stride * kCarrySlots));
-    TRY(c->da.alloc(&c->flag, 4));
 
     // ---- hash keys (reading A7): a_i for the shard's blocks, b, c
     std::vector<uint32_t> aw((size_t)c->nblk * Wa32), bw, cw, tmp;
@@ -859,14 +849,17 @@ static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
     TRY(stage_transform(c, c->smmh, KeyLimbs{ks}, c->nblk, c->rows_mmh, c->scratch, c->ahat, c->acc,
                         "mmh_pack", "mmh_fwd_col", "mmh_fwd_row_mac", "mmh_inverse"));
     {
-        ProfScope ps(c, "mmh_crt_fold");
+        ProfScope ps(c, "mmh_crt");
         TRY(launch_crt<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->S,
                              (uint32_t)c->W_ring, c->stream));
         c->launches++;
-        TRY(run_carry(c, SrcArr{c->S}, (uint32_t)c->W_ring, c->y1));
-        TRY(mersenne_finish(c, c->y1, c->y2));
     }
-    *y_out = c->y2;
+    {
+        ProfScope ps(c, "mmh_carry_fold");
+        TRY(run_carry(c, SrcArr{c->S, (uint32_t)c->W_ring}, (uint32_t)c->W_fold, c->y1));
+        TRY(mersenne_finish(c, c->y1));
+    }
+    *y_out = c->y1;
     return PA_OK;
 }
 
@@ -877,13 +870,16 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     WordSrc ws{y, (uint32_t)c->Wg, Bh, (uint32_t)cdiv(p.gamma, Bh)};
     TRY(stage_transform(c, c->smh, WordLimbs{ws}, 1, c->rows_mh, c->scratch_mh, c->bhat, c->acc_mh,
                         "mh_pack", "mh_fwd_col", "mh_fwd_row_mac", "mh_inverse"));
+    const uint32_t W = (uint32_t)c->W_Z;
     {
-        ProfScope ps(c, "mh_crt_carry_extract");
-        const uint32_t W = (uint32_t)c->W_Z;
+        ProfScope ps(c, "mh_crt");
         const uint64_t ncoef = std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1);
         TRY(launch_crt<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->S, W, c->stream));
         c->launches++;
-        TRY(run_carry(c, SrcArr{c->S}, W, c->Z));
+    }
+    {
+        ProfScope ps(c, "mh_carry_extract");
+        TRY(run_carry(c, SrcArr{c->S, W}, W, c->Z));
         const uint64_t nb = cdiv(p.m, 8), nw = cdiv(nb, 4);
         mh_extract<<<(uint32_t)cdiv(nw, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
         c->launches++;
@@ -925,9 +921,9 @@ extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8
     {
         ProfScope ps(c, "merge_sum_fold");
         rc = run_carry(c, SrcParts{y_parts, G, (uint32_t)c->Wg}, (uint32_t)c->W_fold, c->y1);
-        if (rc == PA_OK) rc = mersenne_finish(c, c->y1, c->y2);
+        if (rc == PA_OK) rc = mersenne_finish(c, c->y1);
     }
-    if (rc == PA_OK) rc = run_mh(c, c->y2, out_bits);
+    if (rc == PA_OK) rc = run_mh(c, c->y1, out_bits);
     c->launches_total += c->launches;
     return rc;
 }

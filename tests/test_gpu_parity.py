@@ -112,6 +112,35 @@ def test_canonical_zero():
     assert out == hashes.mh_output(p - 1, b, c, g, m)
 
 
+def _block_key(blocks, r):
+    """Key bytes (MSB-first) whose r-bit blocks are the given integers."""
+    return np.frombuffer(b"".join(int(x).to_bytes(r // 8, "big") for x in blocks), np.uint8).copy()
+
+
+@pytest.mark.parametrize("r", [1 << 15, 1 << 20])
+def test_long_carry_runs(r):
+    # carries rippling through long all-ones runs (fold PAPER.md:130-132, reading A6):
+    # (1) x_0 = 2^r - 1, a_0 = 2^j with j + r > gamma (the ones run wraps past bit gamma),
+    #     plus a_1 x_1 = 2^(gamma-1) * 2 = 2^gamma == 1 (mod p) added at bit 0;
+    # (2) x_0 = 2^r - 1, a_0 = 1, x_1 = 1, a_1 = 2^gamma - 2^r -> Y = p -> y = 0,
+    #     every word of the pre-canonical value all-ones.
+    g = {1 << 15: 44497, 1 << 20: 1257787}[r]
+    p = (1 << g) - 1
+    m = 4000
+    b = random.Random(4).getrandbits(g) | 1
+    c = random.Random(5).getrandbits(g)
+    key = _block_key([(1 << r) - 1, 2], r)
+    j = g - r + 20_000
+    a = [1 << j, 1 << (g - 1)]
+    out = gpu_hash(key, 2 * r, r, m, 0, gamma=g, a=a, b=b, c=c)
+    assert out == hashes.pa_hash(key, 2 * r, r, m, g, a, b, c)
+    key = _block_key([(1 << r) - 1, 1], r)
+    a = [1, (1 << g) - (1 << r)]
+    assert sum(ai * xi for ai, xi in zip(a, [(1 << r) - 1, 1])) == p
+    out = gpu_hash(key, 2 * r, r, m, 0, gamma=g, a=a, b=b, c=c)
+    assert out == hashes.pack_output(c >> (g - m), m)
+
+
 def test_explicit_keys_random():
     rng = random.Random(9)
     n, r, m = 123_457, 1024, 2_000
