@@ -459,6 +459,36 @@ static int launch_crt_t(const uint32_t *res, const StageDev &sd, uint32_t ncoef,
     return PA_OK;
 }
 
+template <int S_LOG>
+static int launch_mac_t(const MacArgs &A, cudaStream_t st) {
+    constexpr int E_LOG = 5;
+    static KInfo ki;
+    auto fn = row_mac<S_LOG, E_LOG>;
+    TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
+    // grid <= nunits: every CTA runs >= nvec iterations, so a unit is split between at
+    // most two CTAs and the red.add merge of two partials in [0, 2p) stays < 4p < 2^32
+    const int grid = (int)std::min<uint64_t>(A.nunits, (uint64_t)ki.occ * g_num_sms);
+    fn<<<grid, ki.threads, ki.smem, st>>>(A);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+static int launch_mac(int slog, const MacArgs &A, cudaStream_t st) {
+    switch (slog) {
+        case 5: return launch_mac_t<5>(A, st);
+        case 6: return launch_mac_t<6>(A, st);
+        case 7: return launch_mac_t<7>(A, st);
+        case 8: return launch_mac_t<8>(A, st);
+        case 9: return launch_mac_t<9>(A, st);
+        case 10: return launch_mac_t<10>(A, st);
+        case 11: return launch_mac_t<11>(A, st);
+        case 12: return launch_mac_t<12>(A, st);
+        case 13: return launch_mac_t<13>(A, st);
+        case 14: return launch_mac_t<14>(A, st);
+    }
+    return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
+}
+
 template <bool RING>
 static int launch_crt(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
                       const uint32_t *addend, uint32_t n_addend, uint64_t *S, uint32_t W, cudaStream_t st) {
@@ -561,6 +591,13 @@ static int mersenne_finish(pa_ctx *c, uint32_t *y) {
     return PA_OK;
 }
 
+static uint32_t mac_v_rt(int slog) {
+    switch (slog) {
+        case 5: return mac_v(5); case 6: return mac_v(6); case 7: return mac_v(7); case 8: return mac_v(8);
+        case 9: return mac_v(9); case 10: return mac_v(10); default: return 1;
+    }
+}
+
 // ---- pack -> forward column pass -> row pass with MAC -> inverse; residues in acc
 template <class Src>
 static int stage_transform(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec, uint32_t rows,
@@ -593,13 +630,15 @@ static int stage_transform(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nve
     if (!hat) return PA_OK;
     {
         ProfScope ps(c, tag_fwd2);
-        RowArgs R{};
-        R.nt = ntt_args(sd, 0, 1);
-        R.src = scratch;
-        R.dst = acc;
-        R.ahat = hat;
-        R.nvec = nvec;
-        TRY(launch_row<ROW_MAC>(rlog, R, c->stream));
+        CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)P * sd.L * 4, c->stream));
+        MacArgs M{};
+        M.nt = ntt_args(sd, 0, 1);
+        M.src = scratch;
+        M.ahat = hat;
+        M.dst = acc;
+        M.nvec = nvec;
+        M.nunits = (sd.pl.n_col / mac_v_rt(rlog)) * P;
+        TRY(launch_mac(rlog, M, c->stream));
         c->launches++;
     }
     {

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include "modarith.cuh"
 #include "ntt.cuh"
+#include "bulk.cuh"
 
 namespace pa {
 
@@ -263,7 +264,11 @@ row_pass(const RowArgs A) {
 #pragma unroll
                 for (int h = 0; h < E / R; h++)
 #pragma unroll
-                    for (int m = 0; m < R; m++) x[h * R + m] = src[in_pos<S_LOG, E_LOG>(v, h, m)];
+                    for (int m = 0; m < R; m++) {
+                        const uint32_t t = src[in_pos<S_LOG, E_LOG>(v, h, m)];
+                        // ROW_INV input: accumulators merged with red.add, in [0, 4p)
+                        x[h * R + m] = (MODE == ROW_INV) ? red2p(t, cx.p2) : t;
+                    }
             }
             __syncthreads();
             round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
@@ -310,6 +315,144 @@ row_pass(const RowArgs A) {
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------- row pass + MAC
+// S2+S3 (Eq. 2): second NTT pass of every block and the transform-
+// domain multiply-accumulate acc += X_i (.) A^_i, for all blocks i.
+// Iteration space (unit = V rows of one prime, block iv) flattened with iv fastest and
+// split evenly over persistent CTAs; a CTA streams its iterations' X rows and A^ rows
+// (2 x V*S contiguous words each) into an NS-stage shared-memory ring with bulk
+// asynchronous copies (cp.async.bulk, mbarrier completion), so HBM reads overlap the
+// butterflies.  A unit's accumulators are added into dst with red.add (dst zeroed by
+// the caller); a unit split between two CTAs is thereby merged, values < 4p (the
+// launcher keeps gridDim.x <= nunits so no unit spans more than two CTAs).
+struct MacArgs {
+    NttArgs nt;
+    const uint32_t *src;      // [nvec][P][L] forward column-pass output
+    const uint32_t *ahat;     // [nvec][P][L] precomputed transforms (Montgomery, x 1/L)
+    uint32_t *dst;            // [P][L] accumulators (zeroed), results in [0, 4p)
+    uint32_t nvec;
+    uint32_t nunits;          // (N2 / V) * P
+};
+
+// rows per CTA: V*S = 2048 words per operand and stage, and V <= S/2 <= N2 (planner)
+__host__ __device__ constexpr int mac_v(int slog) {
+    return (slog >= 11 ? 1 : (2048 >> slog)) < (1 << (slog - 1)) ? (slog >= 11 ? 1 : (2048 >> slog)) : (1 << (slog - 1));
+}
+__host__ __device__ constexpr int mac_ns(int slog) { return slog >= 14 ? 1 : 2; }
+template <int S_LOG>
+constexpr size_t mac_smem_bytes() {
+    return (size_t)(2 * mac_ns(S_LOG) * mac_v(S_LOG) * (1 << S_LOG) +
+                    mac_v(S_LOG) * ((1 << S_LOG) + (1 << S_LOG) / 32)) * 4 + 16 * 8;
+}
+
+template <int S_LOG, int E_LOG>
+__global__ void __launch_bounds__(mac_v(S_LOG) * (1 << (S_LOG - E_LOG)))
+row_mac(const MacArgs A) {
+    using SP = SubPlan<S_LOG, E_LOG>;
+    constexpr int S = SP::S, E = SP::E;
+    constexpr int V = mac_v(S_LOG), NS = mac_ns(S_LOG);
+    constexpr int RS = S + S / 32;
+    constexpr uint32_t SW = V * S;                       // words per operand per stage
+    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t *xs = smem;                                 // [NS][SW]
+    uint32_t *as = smem + NS * SW;                       // [NS][SW]
+    uint32_t *ex = smem + 2 * NS * SW;                   // [V][RS] exchange
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ex + V * RS);
+    const int w = threadIdx.x / SP::TPV;
+    const int v = threadIdx.x % SP::TPV;
+    const NttArgs &a = A.nt;
+    const uint32_t L = 1u << a.log2L;
+    const uint32_t P = a.nprimes;
+    const uint32_t nvec = A.nvec;
+    const uint64_t total = (uint64_t)A.nunits * nvec;
+    const uint64_t it0 = blockIdx.x * total / gridDim.x;
+    const uint64_t it1 = (blockIdx.x + 1) * total / gridDim.x;
+    auto sidx = [w](int pos) { return w * RS + pos + (pos >> 5); };
+    auto offset_of = [&](uint64_t it) -> size_t {
+        const uint32_t unit = (uint32_t)(it / nvec), iv = (uint32_t)(it % nvec);
+        const uint32_t pi = unit % P, rg = unit / P;
+        return ((size_t)iv * P + pi) * L + (size_t)rg * SW;
+    };
+    auto issue = [&](uint64_t it, int s) {
+        const size_t off = offset_of(it);
+        mbar_arrive_expect_tx(&bars[s], 2 * SW * 4);
+        bulk_g2s(xs + s * SW, A.src + off, SW * 4, &bars[s]);
+        bulk_g2s(as + s * SW, A.ahat + off, SW * 4, &bars[s]);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < NS; s++)
+            if (it0 + s < it1) issue(it0 + s, s);
+
+    uint32_t tw[E / 2], twp[E / 2];
+    uint32_t acc[E];
+    Ctx32 cx{};
+    const uint32_t *rtw_p = nullptr;
+    int64_t cur_unit = -1;
+    uint32_t cur_pi = 0;
+    auto flush = [&](uint32_t unit) {
+        constexpr int R = 1 << SP::rlog(SP::Q - 1);
+        const uint32_t pi = unit % P, rg = unit / P;
+        uint32_t *dst = A.dst + (size_t)pi * L + (size_t)(rg * V + w) * S;
+#pragma unroll
+        for (int h = 0; h < E / R; h++)
+#pragma unroll
+            for (int mm = 0; mm < R; mm++) atomicAdd(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
+    };
+    for (uint64_t it = it0; it < it1; it++) {
+        const uint32_t unit = (uint32_t)(it / nvec);
+        if ((int64_t)unit != cur_unit) {
+            if (cur_unit >= 0) flush((uint32_t)cur_unit);
+            cur_unit = unit;
+            const uint32_t pi = unit % P;
+            if (rtw_p == nullptr || pi != cur_pi) {
+                cur_pi = pi;
+                const PrimeK pk = a.pk[pi];
+                cx = Ctx32{pk.p, pk.p2, pk.pinv};
+#pragma unroll
+                for (int j = 0; j < E / 2; j++) {
+                    tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j);
+                    twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j);
+                }
+                rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
+            }
+#pragma unroll
+            for (int e = 0; e < E; e++) acc[e] = 0;
+        }
+        const int s = (int)((it - it0) % NS);
+        mbar_wait(&bars[s], (uint32_t)(((it - it0) / NS) & 1));
+        const uint32_t *xrow = xs + s * SW + w * S;
+        const uint32_t *arow = as + s * SW + w * S;
+        uint32_t x[E];
+        {
+            constexpr int R = 1 << SP::rlog(0);
+#pragma unroll
+            for (int h = 0; h < E / R; h++)
+#pragma unroll
+                for (int m = 0; m < R; m++) x[h * R + m] = xrow[in_pos<S_LOG, E_LOG>(v, h, m)];
+        }
+        round0_finish<S_LOG, E_LOG>(x, ex, sidx, v, tw, twp, rtw_p, a, cx);
+        rounds_rest<S_LOG, E_LOG, 1>(x, ex, sidx, v, tw, twp, rtw_p, a, cx);
+        {
+            constexpr int R = 1 << SP::rlog(SP::Q - 1);
+#pragma unroll
+            for (int h = 0; h < E / R; h++)
+#pragma unroll
+                for (int mm = 0; mm < R; mm++) {
+                    const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
+                    acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], arow[k1], cx.p, cx.pinv), cx.p2);
+                }
+        }
+        __syncthreads();                                 // stage s and the exchange are free
+        if (threadIdx.x == 0 && it + NS < it1) issue(it + NS, s);
+    }
+    if (cur_unit >= 0) flush((uint32_t)cur_unit);
 }
 
 }  // namespace pa
