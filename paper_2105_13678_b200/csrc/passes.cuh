@@ -321,12 +321,15 @@ row_pass(const RowArgs A) {
 // S2+S3 (Eq. 2): second NTT pass of every block and the transform-
 // domain multiply-accumulate acc += X_i (.) A^_i, for all blocks i.
 // Iteration space (unit = V rows of one prime, block iv) flattened with iv fastest and
-// split evenly over persistent CTAs; a CTA streams its iterations' X rows and A^ rows
-// (2 x V*S contiguous words each) into an NS-stage shared-memory ring with bulk
-// asynchronous copies (cp.async.bulk, mbarrier completion), so HBM reads overlap the
-// butterflies.  A unit's accumulators are added into dst with red.add (dst zeroed by
-// the caller); a unit split between two CTAs is thereby merged, values < 4p (the
-// launcher keeps gridDim.x <= nunits so no unit spans more than two CTAs).
+// split evenly over persistent CTAs.  A CTA streams its iterations' X rows (2-stage
+// ring) and A^ rows (single buffer, loaded while the X rows are transformed) into
+// shared memory with bulk asynchronous copies (cp.async.bulk, mbarrier completion),
+// so HBM reads overlap the butterflies.  The radix-round exchange happens in place in
+// the X stage, XOR-swizzled (bank-conflict free for every round pattern, checked by
+// scripts/dev/swizzle_sim.py), so a CTA needs only 3 V*S words of shared memory.
+// A unit's accumulators are added into dst with red.add (dst zeroed by the caller);
+// a unit split between two CTAs is thereby merged, values < 4p (the launcher keeps
+// gridDim.x <= nunits so no unit spans more than two CTAs).
 struct MacArgs {
     NttArgs nt;
     const uint32_t *src;      // [nvec][P][L] forward column-pass output
@@ -340,26 +343,25 @@ struct MacArgs {
 __host__ __device__ constexpr int mac_v(int slog) {
     return (slog >= 11 ? 1 : (2048 >> slog)) < (1 << (slog - 1)) ? (slog >= 11 ? 1 : (2048 >> slog)) : (1 << (slog - 1));
 }
-__host__ __device__ constexpr int mac_ns(int slog) { return slog >= 14 ? 1 : 2; }
 template <int S_LOG>
 constexpr size_t mac_smem_bytes() {
-    return (size_t)(2 * mac_ns(S_LOG) * mac_v(S_LOG) * (1 << S_LOG) +
-                    mac_v(S_LOG) * ((1 << S_LOG) + (1 << S_LOG) / 32)) * 4 + 16 * 8;
+    return (size_t)3 * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8;
 }
+__device__ __forceinline__ int swz32(int P) { return P ^ ((P >> 5) & 31); }
 
+// <= 128 registers per thread: 16 warps per SM (the register file bound)
 template <int S_LOG, int E_LOG>
-__global__ void __launch_bounds__(mac_v(S_LOG) * (1 << (S_LOG - E_LOG)))
+__global__ void __launch_bounds__(mac_v(S_LOG) * (1 << (S_LOG - E_LOG)),
+                                  (512 / (mac_v(S_LOG) * (1 << (S_LOG - E_LOG)))) < 8 ? (512 / (mac_v(S_LOG) * (1 << (S_LOG - E_LOG)))) : 8)
 row_mac(const MacArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int S = SP::S, E = SP::E;
-    constexpr int V = mac_v(S_LOG), NS = mac_ns(S_LOG);
-    constexpr int RS = S + S / 32;
+    constexpr int V = mac_v(S_LOG);
     constexpr uint32_t SW = V * S;                       // words per operand per stage
     extern __shared__ __align__(128) uint32_t smem[];
-    uint32_t *xs = smem;                                 // [NS][SW]
-    uint32_t *as = smem + NS * SW;                       // [NS][SW]
-    uint32_t *ex = smem + 2 * NS * SW;                   // [V][RS] exchange
-    uint64_t *bars = reinterpret_cast<uint64_t *>(ex + V * RS);
+    uint32_t *xs = smem;                                 // [2][SW] X ring (exchange in place)
+    uint32_t *as = smem + 2 * SW;                        // [SW]   A^
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 3 * SW);   // fullX[2], fullA
     const int w = threadIdx.x / SP::TPV;
     const int v = threadIdx.x % SP::TPV;
     const NttArgs &a = A.nt;
@@ -369,26 +371,30 @@ row_mac(const MacArgs A) {
     const uint64_t total = (uint64_t)A.nunits * nvec;
     const uint64_t it0 = blockIdx.x * total / gridDim.x;
     const uint64_t it1 = (blockIdx.x + 1) * total / gridDim.x;
-    auto sidx = [w](int pos) { return w * RS + pos + (pos >> 5); };
+    auto sidx = [w](int pos) { return swz32(w * S + pos); };
     auto offset_of = [&](uint64_t it) -> size_t {
         const uint32_t unit = (uint32_t)(it / nvec), iv = (uint32_t)(it % nvec);
         const uint32_t pi = unit % P, rg = unit / P;
         return ((size_t)iv * P + pi) * L + (size_t)rg * SW;
     };
-    auto issue = [&](uint64_t it, int s) {
-        const size_t off = offset_of(it);
-        mbar_arrive_expect_tx(&bars[s], 2 * SW * 4);
-        bulk_g2s(xs + s * SW, A.src + off, SW * 4, &bars[s]);
-        bulk_g2s(as + s * SW, A.ahat + off, SW * 4, &bars[s]);
+    auto issue_x = [&](uint64_t it, int s) {
+        mbar_arrive_expect_tx(&bars[s], SW * 4);
+        bulk_g2s(xs + s * SW, A.src + offset_of(it), SW * 4, &bars[s]);
+    };
+    auto issue_a = [&](uint64_t it) {
+        mbar_arrive_expect_tx(&bars[2], SW * 4);
+        bulk_g2s(as, A.ahat + offset_of(it), SW * 4, &bars[2]);
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+        for (int s = 0; s < 3; s++) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int s = 0; s < NS; s++)
-            if (it0 + s < it1) issue(it0 + s, s);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; s++)
+            if (it0 + s < it1) issue_x(it0 + s, s);
+        if (it0 < it1) issue_a(it0);
+    }
 
     uint32_t tw[E / 2], twp[E / 2];
     uint32_t acc[E];
@@ -396,19 +402,18 @@ row_mac(const MacArgs A) {
     const uint32_t *rtw_p = nullptr;
     int64_t cur_unit = -1;
     uint32_t cur_pi = 0;
-    auto flush = [&](uint32_t unit) {
-        constexpr int R = 1 << SP::rlog(SP::Q - 1);
-        const uint32_t pi = unit % P, rg = unit / P;
-        uint32_t *dst = A.dst + (size_t)pi * L + (size_t)(rg * V + w) * S;
-#pragma unroll
-        for (int h = 0; h < E / R; h++)
-#pragma unroll
-            for (int mm = 0; mm < R; mm++) atomicAdd(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
-    };
     for (uint64_t it = it0; it < it1; it++) {
         const uint32_t unit = (uint32_t)(it / nvec);
         if ((int64_t)unit != cur_unit) {
-            if (cur_unit >= 0) flush((uint32_t)cur_unit);
+            if (cur_unit >= 0) {
+                constexpr int R = 1 << SP::rlog(SP::Q - 1);
+                const uint32_t fpi = (uint32_t)cur_unit % P, frg = (uint32_t)cur_unit / P;
+                uint32_t *dst = A.dst + (size_t)fpi * L + (size_t)(frg * V + w) * S;
+#pragma unroll
+                for (int h = 0; h < E / R; h++)
+#pragma unroll
+                    for (int mm = 0; mm < R; mm++) atomicAdd(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
+            }
             cur_unit = unit;
             const uint32_t pi = unit % P;
             if (rtw_p == nullptr || pi != cur_pi) {
@@ -425,22 +430,25 @@ row_mac(const MacArgs A) {
 #pragma unroll
             for (int e = 0; e < E; e++) acc[e] = 0;
         }
-        const int s = (int)((it - it0) % NS);
-        mbar_wait(&bars[s], (uint32_t)(((it - it0) / NS) & 1));
-        const uint32_t *xrow = xs + s * SW + w * S;
-        const uint32_t *arow = as + s * SW + w * S;
+        const uint32_t k = (uint32_t)(it - it0);
+        const int s = (int)(k & 1);
+        mbar_wait(&bars[s], (k >> 1) & 1);
+        uint32_t *xst = xs + s * SW;
         uint32_t x[E];
         {
             constexpr int R = 1 << SP::rlog(0);
 #pragma unroll
             for (int h = 0; h < E / R; h++)
 #pragma unroll
-                for (int m = 0; m < R; m++) x[h * R + m] = xrow[in_pos<S_LOG, E_LOG>(v, h, m)];
+                for (int m = 0; m < R; m++) x[h * R + m] = xst[w * S + in_pos<S_LOG, E_LOG>(v, h, m)];
         }
-        round0_finish<S_LOG, E_LOG>(x, ex, sidx, v, tw, twp, rtw_p, a, cx);
-        rounds_rest<S_LOG, E_LOG, 1>(x, ex, sidx, v, tw, twp, rtw_p, a, cx);
+        if constexpr (SP::Q > 1) __syncthreads();        // natural-order reads done before in-place writes
+        round0_finish<S_LOG, E_LOG>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
+        rounds_rest<S_LOG, E_LOG, 1>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
+        mbar_wait(&bars[2], k & 1);
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
+            const uint32_t *arow = as + w * S;
 #pragma unroll
             for (int h = 0; h < E / R; h++)
 #pragma unroll
@@ -449,10 +457,21 @@ row_mac(const MacArgs A) {
                     acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], arow[k1], cx.p, cx.pinv), cx.p2);
                 }
         }
-        __syncthreads();                                 // stage s and the exchange are free
-        if (threadIdx.x == 0 && it + NS < it1) issue(it + NS, s);
+        __syncthreads();                                 // X stage s and A^ are free
+        if (threadIdx.x == 0) {
+            if (it + 2 < it1) issue_x(it + 2, s);
+            if (it + 1 < it1) issue_a(it + 1);
+        }
     }
-    if (cur_unit >= 0) flush((uint32_t)cur_unit);
+    if (cur_unit >= 0) {
+        constexpr int R = 1 << SP::rlog(SP::Q - 1);
+        const uint32_t fpi = (uint32_t)cur_unit % P, frg = (uint32_t)cur_unit / P;
+        uint32_t *dst = A.dst + (size_t)fpi * L + (size_t)(frg * V + w) * S;
+#pragma unroll
+        for (int h = 0; h < E / R; h++)
+#pragma unroll
+            for (int mm = 0; mm < R; mm++) atomicAdd(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
+    }
 }
 
 }  // namespace pa
