@@ -66,7 +66,7 @@ typedef struct {
     uint32_t log2_len;       /* L = 2^log2_len */
     uint32_t n_col;          /* column (first) pass length N2 */
     uint32_t n_row;          /* row (second) pass length N1; L = N1 * N2 */
-    uint32_t primes[8];
+    uint32_t primes[16];
     double   bound_log2;
     double   modulus_log2;
 } pa_stage_plan;

@@ -33,7 +33,7 @@ u64, u32, i32, vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_v
 
 class pa_stage_plan(ctypes.Structure):
     _fields_ = [("limb_bits", u32), ("nprimes", u32), ("log2_len", u32), ("n_col", u32), ("n_row", u32),
-                ("primes", u32 * 8), ("bound_log2", ctypes.c_double), ("modulus_log2", ctypes.c_double)]
+                ("primes", u32 * 16), ("bound_log2", ctypes.c_double), ("modulus_log2", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {"limb_bits": self.limb_bits, "nprimes": self.nprimes, "log2_len": self.log2_len,

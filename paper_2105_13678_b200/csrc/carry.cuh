@@ -1,10 +1,10 @@
 // Exact reconstruction of the product integers and the Mersenne / power-of-two
 // reductions of the MMH-MH pipeline.
 //
-//  * CRT (Garner) turns the P residues of every convolution coefficient into the exact
-//    coefficient c_j < prod p_i (the plan guarantees the bound).  One CTA owns a tile of
-//    output words, reconstructs the coefficients that touch it into shared memory once,
-//    and forms the 64-bit column sums of its words.
+//  * CRT (approximate-quotient form, no Garner chain) turns the P residues of every
+//    convolution coefficient into the exact coefficient c_j < prod p_i (the plan
+//    guarantees the bound), one thread per coefficient; a second kernel forms the
+//    64-bit column sums of the 32-bit output words from those coefficients.
 //  * MMH (S4+S5): the column sums are taken on the gamma-bit ring directly: coefficient j
 //    sits at bit (B j) mod gamma, and a piece that crosses bit gamma wraps to bit 0 --
 //    this is the fold x mod M_gamma = floor(x / 2^gamma) + x mod 2^gamma
@@ -22,154 +22,137 @@
 
 namespace pa {
 
-constexpr int kMaxPrimes = 8;
-
 struct CrtK {
     uint32_t P;
     uint32_t p[kMaxPrimes];
     uint32_t pinv[kMaxPrimes];
-    uint32_t inv[kMaxPrimes];                 // (p_0 ... p_{i-1})^{-1} mod p_i, Montgomery form
-    uint32_t pmod[kMaxPrimes][kMaxPrimes];    // p_l mod p_i (l < i), Montgomery form
-    uint32_t prod[kMaxPrimes + 1][kMaxPrimes];// p_0 ... p_{l-1}, little-endian words
+    uint32_t qinv[kMaxPrimes];                // (M / p_i)^{-1} mod p_i, Montgomery form
+    uint64_t G[kMaxPrimes];                   // floor(2^64 / p_i)
+    uint32_t MI[kMaxPrimes][kMaxPrimes];      // M / p_i, little-endian words
+    uint32_t M[kMaxPrimes];                   // M = p_0 ... p_{P-1}, little-endian words
 };
 
-// Garner: exact c (P words) from canonical residues r[i].
-// u_0 = r_0;  u_i = (r_i - (u_0 + p_0 (u_1 + p_1 (... u_{i-1})))) (p_0...p_{i-1})^{-1} mod p_i;
-// c = sum_i u_i p_0 ... p_{i-1}.
+// Exact coefficient c < M' (M' = 2^-0.5 M at most, the planner's margin) from its
+// residues r_i (canonical), CRT with an approximate quotient:
+//   y_i = r_i (M/p_i)^{-1} mod p_i,   c = sum_i y_i (M/p_i) - k M,
+//   k = floor(sum_i y_i / p_i) evaluated in 64-bit fixed point (q_i = y_i floor(2^64/p_i),
+//   error < P 2^-34 per unit) with a bias of 2^-24: exact because c/M <= 2^-0.5 keeps the
+//   fractional part away from 1.  All coefficients are independent (no Garner chain).
+// One thread per coefficient; coef[j][w], P words each.
 template <int P>
-__device__ __forceinline__ void garner(const CrtK &K, const uint32_t *r, uint32_t *c) {
-    uint32_t u[P];
+__global__ void __launch_bounds__(128) crt_coeffs(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
+                                                  const CrtK K, uint32_t *__restrict__ coef) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ncoef) return;
+    uint32_t y[P];
+    uint64_t slo = 1ull << 40, shi = 0;                // bias 2^-24
 #pragma unroll
     for (int i = 0; i < P; i++) {
-        const uint32_t p = K.p[i], pinv = K.pinv[i];
-        uint32_t acc = 0;
-#pragma unroll
-        for (int l = i - 1; l >= 0; l--) {
-            acc = red1p(mul_mont(acc, K.pmod[i][l], p, pinv), p);
-            acc = red1p(acc + red1p(u[l], p), p);      // u_l < p_l < 2 p_i
-        }
-        if (i == 0) u[0] = r[0];
-        else u[i] = red1p(mul_mont(red1p(r[i] + p - acc, p), K.inv[i], p, pinv), p);
+        const uint32_t r = res[(size_t)i * L + j];
+        y[i] = red1p(mul_mont(r, K.qinv[i], K.p[i], K.pinv[i]), K.p[i]);
+        const uint64_t q = (uint64_t)y[i] * K.G[i];
+        slo += q;
+        shi += (slo < q);
     }
+    const uint32_t k = (uint32_t)shi;
+    uint64_t acc[P + 1];
 #pragma unroll
-    for (int w = 0; w < P; w++) c[w] = 0;
+    for (int w = 0; w <= P; w++) acc[w] = 0;
 #pragma unroll
-    for (int i = 0; i < P; i++) {
-        uint64_t carry = 0;
+    for (int i = 0; i < P; i++)
 #pragma unroll
         for (int w = 0; w < P; w++) {
-            const uint64_t t = (uint64_t)c[w] + (uint64_t)u[i] * K.prod[i][w] + carry;
-            c[w] = (uint32_t)t;
-            carry = t >> 32;
+            const uint64_t t = (uint64_t)y[i] * K.MI[i][w];
+            acc[w] += (uint32_t)t;
+            acc[w + 1] += t >> 32;
         }
+    // words of sum_i y_i M_i (P + 1 words) minus k M
+    uint64_t carry = 0;
+    int64_t borrow = 0;
+    uint32_t *out = coef + (size_t)j * P;
+#pragma unroll
+    for (int w = 0; w < P; w++) {
+        const uint64_t v = acc[w] + carry;
+        carry = v >> 32;
+        const uint64_t km = (uint64_t)k * K.M[w];
+        // subtract low word of k M (its high part carries into the next word via `borrow`)
+        const int64_t d = (int64_t)(uint32_t)v - (int64_t)(uint32_t)km + borrow;
+        out[w] = (uint32_t)d;
+        borrow = (d >> 32) - (int64_t)(km >> 32);       // arithmetic shift: -1 on underflow
     }
 }
 
-// 32-bit window [off, off+32) of the multiword value x (NW words; negative off allowed),
-// restricted to the value's bits [0, len).
-template <int NW>
-__device__ __forceinline__ uint32_t window_masked(const uint32_t *x, int off, int len) {
+// Column sums of 32-bit output words u < W from exact coefficients coef[j] (P words):
+//   RING = true : coefficient j sits at ring bit (B j) mod gamma (MMH, S4+S5): pieces are
+//                 cut at bit gamma and their high part lands at ring bit 0 -- the fold
+//                 x mod M_gamma = floor(x / 2^gamma) + x mod 2^gamma
+//                 applied per coefficient before the carries;
+//   RING = false: coefficient j at bit B j, plus the addend words (MH, Eq. 4 b y + c).
+// S[u] = sum of the 32-bit windows of all pieces over [32u, 32u + 32), < 2^40.
+template <int P>
+__device__ __forceinline__ uint32_t coef_window(const uint32_t *__restrict__ c, int64_t off, int64_t len) {
+    // bits [off, off + 32) of the coefficient restricted to [0, len); off may be negative
     if (off <= -32 || off >= len) return 0;
     uint32_t v;
     if (off < 0) {
-        v = x[0] << (-off);
+        v = __ldg(c) << (-off);
     } else {
-        const int wi = off >> 5, sh = off & 31;
-        uint32_t lo = 0, hi = 0;
-#pragma unroll
-        for (int w = 0; w < NW; w++) { if (w == wi) lo = x[w]; if (w == wi + 1) hi = x[w]; }
+        const int wi = (int)(off >> 5), sh = (int)(off & 31);
+        const uint32_t lo = __ldg(c + wi);
+        const uint32_t hi = (wi + 1 < P) ? __ldg(c + wi + 1) : 0u;
         v = __funnelshift_r(lo, hi, sh);
     }
-    // bits of the window at or above len (value-relative) are cleared
-    const int top = len - off;                     // window bits [0, top) are inside
+    const int64_t top = len - off;
     if (top < 32) v &= (top <= 0) ? 0u : ((1u << top) - 1u);
     return v;
 }
 
-// Column sums over a tile of words [u0, u0 + blockDim.x).
-//   RING = true : positions e_j = (B j) mod gamma on the gamma-bit ring (MMH, S4+S5);
-//   RING = false: positions B j, plus addend words (MH, S7).
-// res: [P][L] canonical residues in natural coefficient order.
 template <int P, bool RING>
-__global__ void __launch_bounds__(256) crt_colsum_tile(const uint32_t *__restrict__ res, uint32_t L,
-                                                       uint32_t ncoef, uint32_t B, uint64_t gamma,
-                                                       const CrtK K, const uint32_t *__restrict__ addend,
-                                                       uint32_t n_addend, uint64_t *__restrict__ S, uint32_t W) {
-    extern __shared__ uint32_t sc[];               // [cap][P] coefficients
-    const uint32_t U = blockDim.x;
-    const uint32_t u0 = blockIdx.x * U;
-    const uint32_t u = u0 + threadIdx.x;
+__global__ void __launch_bounds__(256) crt_colsum(const uint32_t *__restrict__ coef, uint32_t ncoef, uint32_t B,
+                                                  uint64_t gamma, const uint32_t *__restrict__ addend,
+                                                  uint32_t n_addend, uint64_t *__restrict__ S, uint32_t W) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= W) return;
     const int64_t cbits = 32 * P;
-    const uint32_t cap = (32 * U + cbits) / B + 3;
+    const int64_t me = 32 * (int64_t)u;
     uint64_t s = (!RING && addend && u < n_addend) ? addend[u] : 0ull;
-
-    // chunk t covers coefficients with t gamma <= B j < (t+1) gamma (ring); one chunk (linear)
-    const uint64_t span = RING ? gamma : ~0ull >> 2;
+    const uint64_t span = RING ? gamma : (1ull << 62);
     const uint64_t nchunks = RING ? ((uint64_t)B * ncoef + gamma - 1) / gamma : 1;
-    const int64_t lo_bit = 32 * (int64_t)u0, hi_bit = 32 * (int64_t)(u0 + U);
     for (uint64_t t = 0; t < nchunks; t++) {
-        const int64_t base = (int64_t)(t * span);                 // ring position 0 of this chunk
-        // coefficients whose piece [B j - base, B j - base + cbits) meets [lo_bit, hi_bit)
-        int64_t ja = (lo_bit - cbits + base) / (int64_t)B;        // may be one too small: harmless
-        if (ja < 0) ja = 0;
-        const int64_t jc0 = (base + B - 1) / B;                   // first j of the chunk
-        if (ja < jc0) ja = jc0;
-        int64_t jb = (hi_bit - 1 + base) / (int64_t)B;            // inclusive
+        const int64_t base = (int64_t)(t * span);             // ring bit 0 of this chunk
+        const int64_t jc0 = (base + B - 1) / B;                // first j of the chunk
         const int64_t jc1 = RING ? (int64_t)(((t + 1) * span + B - 1) / B) - 1 : (int64_t)ncoef - 1;
-        if (jb > jc1) jb = jc1;
-        if (jb > (int64_t)ncoef - 1) jb = (int64_t)ncoef - 1;
-        if (jb < ja) continue;                                    // uniform across the CTA
-        const uint32_t cnt = (uint32_t)(jb - ja + 1);
-        __syncthreads();
-        for (uint32_t q = threadIdx.x; q < cnt && q < cap; q += U) {
-            uint32_t r[P], c[P];
-#pragma unroll
-            for (int i = 0; i < P; i++) r[i] = res[(size_t)i * L + (ja + q)];
-            garner<P>(K, r, c);
-#pragma unroll
-            for (int w = 0; w < P; w++) sc[q * P + w] = c[w];
-        }
-        __syncthreads();
-        if (u < W) {
-            const int64_t me = 32 * (int64_t)u;
-            int64_t j0 = (me - cbits + base) / (int64_t)B;
-            if (j0 < ja) j0 = ja;
-            int64_t j1e = (me + 31 + base) / (int64_t)B;
-            if (j1e > jb) j1e = jb;
-            for (int64_t j = j0; j <= j1e; j++) {
-                const int64_t pos = (int64_t)B * j - base;        // piece start on the ring
-                int len = (int)cbits;
-                if (RING && pos + len > (int64_t)gamma) len = (int)((int64_t)gamma - pos);
-                s += window_masked<P>(&sc[(j - ja) * P], (int)(me - pos), len);
-            }
+        int64_t j0 = (me - cbits + base) / (int64_t)B;        // pieces [B j - base, + cbits) meeting me
+        int64_t j1 = (me + 31 + base) / (int64_t)B;
+        if (j0 < jc0) j0 = jc0;
+        if (j1 > jc1) j1 = jc1;
+        if (j1 > (int64_t)ncoef - 1) j1 = (int64_t)ncoef - 1;
+        for (int64_t j = j0; j <= j1; j++) {
+            const int64_t pos = (int64_t)B * j - base;
+            int64_t len = cbits;
+            if (RING && pos + len > (int64_t)gamma) len = (int64_t)gamma - pos;
+            s += coef_window<P>(coef + (size_t)j * P, me - pos, len);
         }
     }
-    if (RING && u0 * 32ull < (uint64_t)cbits + 32) {
-        // wrapped pieces: the bits of a coefficient above the ring top land at bit 0
+    if (RING && me < cbits + 32) {
+        // wrapped pieces: bits of a coefficient above the ring top land at ring bit 0
         for (uint64_t t = 0; t < nchunks; t++) {
             const int64_t base = (int64_t)(t * gamma);
-            const int64_t top = base + (int64_t)gamma;                // chunk end (ring bit gamma)
+            const int64_t top = base + (int64_t)gamma;
             int64_t ja = (top - cbits) / (int64_t)B;
             const int64_t jc0 = (base + B - 1) / B;
             if (ja < jc0) ja = jc0;
             int64_t jb = (top - 1) / (int64_t)B;
             if (jb > (int64_t)ncoef - 1) jb = (int64_t)ncoef - 1;
-            if (u < W) {
-                for (int64_t j = ja; j <= jb; j++) {
-                    const int64_t pos = (int64_t)B * j - base;
-                    if (pos + cbits <= (int64_t)gamma) continue;
-                    uint32_t r[P], c[P];
-#pragma unroll
-                    for (int i = 0; i < P; i++) r[i] = res[(size_t)i * L + j];
-                    garner<P>(K, r, c);
-                    // high part c >> (gamma - pos) placed at ring bit 0
-                    const int cut = (int)((int64_t)gamma - pos);
-                    s += window_masked<P>(c, 32 * (int)u + cut, (int)cbits);
-                }
+            for (int64_t j = ja; j <= jb; j++) {
+                const int64_t pos = (int64_t)B * j - base;
+                if (pos + cbits <= (int64_t)gamma) continue;
+                const int64_t cut = (int64_t)gamma - pos;
+                s += coef_window<P>(coef + (size_t)j * P, me + cut, cbits);
             }
         }
     }
-    if (u < W) S[u] = s;
+    S[u] = s;
 }
 
 // ---------------------------------------------------------------- carry resolution

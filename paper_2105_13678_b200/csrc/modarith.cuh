@@ -13,12 +13,21 @@
 
 namespace pa {
 
-struct PrimeK {            // per-prime constants passed to kernels
+constexpr int kMaxPrimes = 16;   // NTT primes per product (CRT modulus <= 16 words)
+
+struct alignas(16) PrimeK {  // per-prime constants passed to kernels
     uint32_t p;            // prime, < 2^30
     uint32_t p2;           // 2p
     uint32_t pinv;         // p^{-1} mod 2^32   (Montgomery, R = 2^32)
     uint32_t r2;           // R^2 mod p         (to Montgomery form)
+    uint32_t pw[8];        // 2^(32 i) mod p, i < 8 (multiword limb reduction)
 };
+
+// REDC of t < 3 p 2^32: t 2^-32 mod p in [0, 4p)
+__device__ __forceinline__ uint32_t redc64(uint64_t t, uint32_t p, uint32_t pinv) {
+    const uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);
+    return hi - __umulhi(lo * pinv, p) + p;
+}
 
 // s in [0, 4p) -> [0, 2p)
 __device__ __forceinline__ uint32_t red2p(uint32_t s, uint32_t p2) { return min(s, s - p2); }

@@ -72,6 +72,7 @@ extern "C" int pa_last_error(char *buf, size_t len) {
 static constexpr int kMinLog2L = 10;
 static constexpr int kMaxLog2L = 23;
 static constexpr int kColMaxLog = 9;
+static constexpr int kMaxLimbBits = 256;
 
 static double log2_bound(uint64_t nterms, uint64_t overlap, uint32_t B) {
     // log2(nterms * overlap * (2^B - 1)^2)  (upper bound of a convolution coefficient)
@@ -82,10 +83,10 @@ static double log2_bound(uint64_t nterms, uint64_t overlap, uint32_t B) {
 // over `nterms` products; only coefficients below `need_coef` limbs... (all are needed:
 // the cyclic length must cover the full product so nothing wraps).
 static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int force_B, pa_stage_plan *out) {
-    static const uint32_t Bs[] = {16, 24, 32, 40, 48, 56};   // B <= 56: limb_redc needs v < p 2^32
+    // B <= 56: one 64-bit limb (limb_redc); larger B: multiword limbs (<= 8 words)
     double best = 1e300;
     pa_stage_plan bp{};
-    for (uint32_t B : Bs) {
+    for (uint32_t B = 16; B <= (uint32_t)kMaxLimbBits; B += 8) {
         if (force_B && (int)B != force_B) continue;
         const uint64_t wa = (abits + B - 1) / B, wb = (bbits + B - 1) / B;
         const uint64_t len = wa + wb - 1;
@@ -139,8 +140,8 @@ static int make_plan(const pa_params *prm, Plan *P) {
     if (p.n < 1) return set_err(PA_E_PARAM, "n must be >= 1");
     if (p.r < 16 || p.r % 16) return set_err(PA_E_PARAM, "r must be >= 16 and a multiple of 16 (got %llu)", (unsigned long long)p.r);
     if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
-    if (p.force_B && (p.force_B < 16 || p.force_B > 56 || p.force_B % 8))
-        return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, 56]");
+    if (p.force_B && (p.force_B < 16 || p.force_B > kMaxLimbBits || p.force_B % 8))
+        return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, %d]", kMaxLimbBits);
     uint64_t g = prm->gamma;
     if (g == 0) {
         for (uint64_t e : kMersenne) if (e > p.r) { g = e; break; }
@@ -173,7 +174,7 @@ struct StageDev {
     uint32_t *regtw[2] = {}, *regtwp[2] = {};
     uint32_t *rtw = nullptr;            // [P][stride]: col fwd, col inv, row fwd, row inv
     uint32_t rtw_stride = 0;
-    uint32_t rtw_off[4][kMaxRounds] = {};
+    uint32_t rtw_off[2][4][kMaxRounds] = {};   // [E_LOG - 4][col fwd, col inv, row fwd, row inv]
     uint32_t *ltw_lo[2] = {}, *ltw_hi[2] = {};
     uint32_t ltw_h = 0, ltw_lo_n = 0, ltw_hi_n = 0;
     uint32_t *tw4[2] = {};              // omega_L^(+-j1 k2) at k2 N1 + j1, [P][L]
@@ -203,9 +204,8 @@ struct DevAlloc {
 
 // Round twiddles of a sub-DFT of 2^S_LOG points with radix 2^5 rounds: for round rho,
 // table[k][t] = omega_{S_rho}^(t k), S_rho = S / G_rho.
-static void round_tables(uint32_t p, uint32_t wL, int lg, int slog, std::vector<uint32_t> &tab,
+static void round_tables(uint32_t p, uint32_t wL, int lg, int slog, int E_LOG, std::vector<uint32_t> &tab,
                          uint32_t off[kMaxRounds]) {
-    const int E_LOG = 5;
     const int Q = (slog + E_LOG - 1) / E_LOG;
     int glog = 0;
     for (int rho = 0; rho < kMaxRounds; rho++) off[rho] = 0;
@@ -263,6 +263,7 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cuda
         for (int it = 0; it < 5; it++) inv *= 2 - p * inv;
         pk[i].pinv = inv;
         pk[i].r2 = (uint32_t)powmod64(2, 64, p);
+        for (int w = 0; w < 8; w++) pk[i].pw[w] = (uint32_t)powmod64(2, 32ull * w, p);
         const uint32_t g = primitive_root(p);
         const uint32_t wf = (uint32_t)powmod64(g, (p - 1) >> lg, p);     // omega_L
         const uint32_t wi = inv_mod(wf, p);
@@ -284,10 +285,12 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cuda
             cur = 1;
             for (uint32_t e = 0; e < sd.ltw_hi_n; e++) { hi[dir].push_back(to_mont((uint32_t)cur, p)); cur = mulmod64(cur, step, p); }
         }
-        round_tables(p, wf, lg, clog, rt[i], sd.rtw_off[0]);
-        round_tables(p, wi, lg, clog, rt[i], sd.rtw_off[1]);
-        round_tables(p, wf, lg, rlog, rt[i], sd.rtw_off[2]);
-        round_tables(p, wi, lg, rlog, rt[i], sd.rtw_off[3]);
+        for (int el = 4; el <= 5; el++) {
+            round_tables(p, wf, lg, clog, el, rt[i], sd.rtw_off[el - 4][0]);
+            round_tables(p, wi, lg, clog, el, rt[i], sd.rtw_off[el - 4][1]);
+            round_tables(p, wf, lg, rlog, el, rt[i], sd.rtw_off[el - 4][2]);
+            round_tables(p, wi, lg, rlog, el, rt[i], sd.rtw_off[el - 4][3]);
+        }
     }
     sd.rtw_stride = (uint32_t)rt[0].size();
     std::vector<uint32_t> rtall;
@@ -313,37 +316,35 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cuda
                                       sd.lg, pl.n_row, sd.tw4[dir]);
         CUDA_TRY(cudaGetLastError());
     }
-    // CRT constants
+    // CRT constants (approximate-quotient CRT, carry.cuh crt_coeffs)
     CrtK &K = sd.crt;
     memset(&K, 0, sizeof K);
     K.P = P;
+    auto mul_words = [](std::vector<uint32_t> &x, uint32_t m) {   // x *= m (little-endian)
+        uint64_t carry = 0;
+        for (auto &w : x) { const uint64_t t = (uint64_t)w * m + carry; w = (uint32_t)t; carry = t >> 32; }
+        if (carry) x.push_back((uint32_t)carry);
+    };
+    std::vector<uint32_t> M{1};
+    for (uint32_t i = 0; i < P; i++) mul_words(M, pl.primes[i]);
+    if (M.size() > (size_t)kMaxPrimes) return set_err(PA_E_BOUND, "CRT modulus exceeds %d words", kMaxPrimes);
+    for (size_t w = 0; w < M.size(); w++) K.M[w] = M[w];
     for (uint32_t i = 0; i < P; i++) {
         const uint32_t p = pl.primes[i];
         K.p[i] = p;
         K.pinv[i] = pk[i].pinv;
-        uint64_t prodmod = 1;
-        for (uint32_t l = 0; l < i; l++) {
-            K.pmod[i][l] = to_mont(pl.primes[l] % p, p);
-            prodmod = mulmod64(prodmod, pl.primes[l] % p, p);
-        }
-        K.inv[i] = to_mont(i ? inv_mod((uint32_t)prodmod, p) : 1u, p);
-    }
-    std::vector<uint32_t> acc(kMaxPrimes, 0);
-    acc[0] = 1;
-    for (uint32_t l = 0; l <= P && l <= (uint32_t)kMaxPrimes; l++) {
-        for (int w = 0; w < kMaxPrimes; w++) K.prod[l][w] = acc[w];
-        if (l == P) break;
-        uint64_t carry = 0;
-        for (int w = 0; w < kMaxPrimes; w++) {
-            const uint64_t t = (uint64_t)acc[w] * pl.primes[l] + carry;
-            acc[w] = (uint32_t)t;
-            carry = t >> 32;
-        }
+        std::vector<uint32_t> Mi{1};
+        uint64_t mimod = 1;
+        for (uint32_t l = 0; l < P; l++)
+            if (l != i) { mul_words(Mi, pl.primes[l]); mimod = mulmod64(mimod, pl.primes[l] % p, p); }
+        for (size_t w = 0; w < Mi.size() && w < (size_t)kMaxPrimes; w++) K.MI[i][w] = Mi[w];
+        K.qinv[i] = to_mont(inv_mod((uint32_t)mimod, p), p);
+        K.G[i] = (uint64_t)(((unsigned __int128)1 << 64) / p);
     }
     return PA_OK;
 }
 
-static NttArgs ntt_args(const StageDev &sd, int dir, int pass /*0 col, 1 row*/) {
+static NttArgs ntt_args(const StageDev &sd, int dir, int pass /*0 col, 1 row*/, int elog = 5) {
     NttArgs a{};
     a.pk = sd.pk;
     a.regtw = sd.regtw[dir];
@@ -351,7 +352,7 @@ static NttArgs ntt_args(const StageDev &sd, int dir, int pass /*0 col, 1 row*/) 
     a.regtw_stride = 16;
     a.rtw = sd.rtw;
     a.rtw_stride = sd.rtw_stride;
-    for (int r = 0; r < kMaxRounds; r++) a.rtw_off[r] = sd.rtw_off[pass * 2 + dir][r];
+    for (int r = 0; r < kMaxRounds; r++) a.rtw_off[r] = sd.rtw_off[elog - 4][pass * 2 + dir][r];
     a.ltw_lo = sd.ltw_lo[dir];
     a.ltw_hi = sd.ltw_hi[dir];
     a.ltw_lo_stride = sd.ltw_lo_n;
@@ -449,12 +450,11 @@ static int launch_row(int slog, const RowArgs &A, cudaStream_t st) {
 
 template <int P, bool RING>
 static int launch_crt_t(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
-                        const uint32_t *addend, uint32_t n_addend, uint64_t *S, uint32_t W, cudaStream_t st) {
-    const uint32_t U = 256;
-    const uint32_t B = sd.pl.limb_bits;
-    const size_t smem = (size_t)((32 * U + 32 * P) / B + 3) * P * 4;
-    crt_colsum_tile<P, RING><<<(W + U - 1) / U, U, smem, st>>>(res, sd.L, ncoef, B, gamma, sd.crt, addend,
-                                                                n_addend, S, W);
+                        const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint64_t *S, uint32_t W,
+                        cudaStream_t st) {
+    crt_coeffs<P><<<(ncoef + 127) / 128, 128, 0, st>>>(res, sd.L, ncoef, sd.crt, coef);
+    CUDA_TRY(cudaGetLastError());
+    crt_colsum<P, RING><<<(W + 255) / 256, 256, 0, st>>>(coef, ncoef, sd.pl.limb_bits, gamma, addend, n_addend, S, W);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
@@ -491,16 +491,16 @@ static int launch_mac(int slog, const MacArgs &A, cudaStream_t st) {
 
 template <bool RING>
 static int launch_crt(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
-                      const uint32_t *addend, uint32_t n_addend, uint64_t *S, uint32_t W, cudaStream_t st) {
+                      const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint64_t *S, uint32_t W,
+                      cudaStream_t st) {
+#define PA_CRT_CASE(P) \
+    case P: return launch_crt_t<P, RING>(res, sd, ncoef, gamma, addend, n_addend, coef, S, W, st);
     switch (sd.pl.nprimes) {
-        case 2: return launch_crt_t<2, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
-        case 3: return launch_crt_t<3, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
-        case 4: return launch_crt_t<4, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
-        case 5: return launch_crt_t<5, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
-        case 6: return launch_crt_t<6, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
-        case 7: return launch_crt_t<7, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
-        case 8: return launch_crt_t<8, RING>(res, sd, ncoef, gamma, addend, n_addend, S, W, st);
+        PA_CRT_CASE(2) PA_CRT_CASE(3) PA_CRT_CASE(4) PA_CRT_CASE(5) PA_CRT_CASE(6) PA_CRT_CASE(7) PA_CRT_CASE(8)
+        PA_CRT_CASE(9) PA_CRT_CASE(10) PA_CRT_CASE(11) PA_CRT_CASE(12) PA_CRT_CASE(13) PA_CRT_CASE(14)
+        PA_CRT_CASE(15) PA_CRT_CASE(16)
     }
+#undef PA_CRT_CASE
     return set_err(PA_E_PARAM, "unsupported prime count %u", sd.pl.nprimes);
 }
 
@@ -523,6 +523,7 @@ struct pa_ctx {
     uint32_t *bhat = nullptr, *scratch_mh = nullptr, *acc_mh = nullptr;
     uint32_t *c_words = nullptr;
     uint64_t *S = nullptr;
+    uint32_t *coef = nullptr;                 // exact convolution coefficients [ncoef][P]
     uint32_t *y1 = nullptr, *Z = nullptr;
     uint32_t *cstate = nullptr;               // carry look-back: [kCarrySlots][1 + ntiles]
     uint32_t cstate_stride = 0;
@@ -598,6 +599,25 @@ static uint32_t mac_v_rt(int slog) {
     }
 }
 
+template <class Src>
+static int launch_pack(const Src &src, uint32_t B, uint32_t grid, const PrimeK *pk, uint32_t P, uint32_t nvec,
+                       uint32_t wxp, uint32_t *res, cudaStream_t st) {
+    const int nw = B <= 56 ? 0 : (int)((B + 31) / 32);
+    switch (nw) {
+        case 0: pack_residues<Src, 0><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 2: pack_residues<Src, 2><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 3: pack_residues<Src, 3><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 4: pack_residues<Src, 4><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 5: pack_residues<Src, 5><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 6: pack_residues<Src, 6><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 7: pack_residues<Src, 7><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 8: pack_residues<Src, 8><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        default: return set_err(PA_E_PARAM, "unsupported limb width %u", B);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
 // ---- pack -> forward column pass -> row pass with MAC -> inverse; residues in acc
 template <class Src>
 static int stage_transform(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec, uint32_t rows,
@@ -610,9 +630,8 @@ static int stage_transform(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nve
         ProfScope ps(c, tag_pack);
         const uint64_t total = (uint64_t)nvec * wxp;
         const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
-        pack_residues<Src><<<grid, 256, 0, c->stream>>>(src, sd.pk, P, nvec, wxp, c->res);
+        TRY(launch_pack(src, sd.pl.limb_bits, grid, sd.pk, P, nvec, wxp, c->res, c->stream));
         c->launches++;
-        CUDA_TRY(cudaGetLastError());
     }
     {
         ProfScope ps(c, tag_fwd1);
@@ -736,6 +755,7 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     TRY(c->da.alloc(&c->c_words, Wal32));
     const uint64_t Smax = std::max<uint64_t>(c->W_fold, c->W_Z);
     TRY(c->da.alloc(&c->S, Smax));
+    TRY(c->da.alloc(&c->coef, std::max<size_t>((size_t)Pm * Lm, (size_t)Ph * Lh)));
     TRY(c->da.alloc(&c->y1, c->W_fold));
     TRY(c->da.alloc(&c->Z, c->W_Z));
     c->cstate_stride = (uint32_t)(cdiv(Smax, kCarryTile) + 2);
@@ -889,9 +909,9 @@ static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
                         "mmh_pack", "mmh_fwd_col", "mmh_fwd_row_mac", "mmh_inverse"));
     {
         ProfScope ps(c, "mmh_crt");
-        TRY(launch_crt<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->S,
+        TRY(launch_crt<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->coef, c->S,
                              (uint32_t)c->W_ring, c->stream));
-        c->launches++;
+        c->launches += 2;
     }
     {
         ProfScope ps(c, "mmh_carry_fold");
@@ -913,8 +933,8 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     {
         ProfScope ps(c, "mh_crt");
         const uint64_t ncoef = std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1);
-        TRY(launch_crt<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->S, W, c->stream));
-        c->launches++;
+        TRY(launch_crt<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->coef, c->S, W, c->stream));
+        c->launches += 2;
     }
     {
         ProfScope ps(c, "mh_carry_extract");

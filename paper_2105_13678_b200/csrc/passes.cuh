@@ -61,6 +61,35 @@ __device__ __forceinline__ uint64_t key_limb(const KeySrc &s, uint32_t blk, uint
     return be >> (64 - 8 * nb);
 }
 
+// Multiword limb (B > 56 bits): w[i] = bits [32 i, 32 i + 32) of limb j, i < NW.
+// Word i is the big-endian value of the 4 key bytes ending 4 i bytes before the limb's
+// last byte; bytes before the limb (or the block) read as 0.
+template <int NW>
+__device__ __forceinline__ void key_limb_words(const KeySrc &s, uint32_t blk, uint32_t j, uint32_t (&w)[NW]) {
+    if (j >= s.wx) {
+#pragma unroll
+        for (int i = 0; i < NW; i++) w[i] = 0;
+        return;
+    }
+    const int64_t start = (int64_t)blk * s.blk_bytes;
+    const int64_t end = start + s.blk_bytes;
+    const int64_t hi = end - (int64_t)j * s.limb_bytes;
+    int64_t lo = hi - (int64_t)s.limb_bytes;
+    if (lo < start) lo = start;
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+        const int64_t pos = hi - 4 * (i + 1);               // first (most significant) byte
+        const int64_t wi = pos >> 2;                          // floor for negative too
+        const int sh = (int)(pos & 3) * 8;
+        const uint32_t a0 = key_word(s, wi), a1 = key_word(s, wi + 1);
+        uint32_t v = __byte_perm(__funnelshift_r(a0, a1, sh), 0, 0x0123);
+        const int64_t below = lo - pos;                       // leading bytes outside the limb
+        if (below >= 4) v = 0;
+        else if (below > 0) v &= 0xFFFFFFFFu >> (8 * below);
+        w[i] = v;
+    }
+}
+
 // Little-endian 32-bit word vectors (a_i, b, y): limb j = bits [B j, B j + B).
 struct WordSrc {
     const uint32_t *w;
@@ -82,6 +111,30 @@ __device__ __forceinline__ uint64_t word_limb(const WordSrc &s, uint32_t vec, ui
     return s.limb_bits >= 64 ? v : (v & ((1ull << s.limb_bits) - 1));
 }
 
+template <int NW>
+__device__ __forceinline__ void word_limb_words(const WordSrc &s, uint32_t vec, uint32_t j, uint32_t (&w)[NW]) {
+    if (j >= s.nlimbs) {
+#pragma unroll
+        for (int i = 0; i < NW; i++) w[i] = 0;
+        return;
+    }
+    const uint64_t bit = (uint64_t)j * s.limb_bits;
+    const uint32_t wi = (uint32_t)(bit >> 5);
+    const int sh = (int)(bit & 31);
+    const uint32_t *base = s.w + (size_t)vec * s.words;
+    uint32_t prev = wi < s.words ? __ldg(base + wi) : 0u;
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+        const uint32_t nx = wi + i + 1 < s.words ? __ldg(base + wi + i + 1) : 0u;
+        uint32_t v = __funnelshift_r(prev, nx, sh);
+        const int left = (int)s.limb_bits - 32 * i;          // limb bits from this word up
+        if (left <= 0) v = 0;
+        else if (left < 32) v &= (1u << left) - 1u;
+        w[i] = v;
+        prev = nx;
+    }
+}
+
 // Montgomery reduction of a limb value v < 2^56 (hi < 2^24 < p): v 2^-32 mod p in (0, 2p).
 // The factor 2^-32 is common to every element of a packed vector and is compensated in
 // the scale of the precomputed operand (pa_api.cu, setup_stage).
@@ -90,22 +143,51 @@ __device__ __forceinline__ uint32_t limb_redc(uint64_t v, uint32_t p, uint32_t p
     return hi - __umulhi(lo * pinv, p) + p;
 }
 
+// Multiword limb v = sum_i w_i 2^(32 i) -> v 2^-32 mod p in [0, 2p) (the same factor as
+// limb_redc): groups of <= 3 products w_i (2^(32 i) mod p) summed in 64 bits (< 3 p 2^32),
+// each group REDC-reduced and the groups added lazily.
+template <int NW>
+__device__ __forceinline__ uint32_t limb_words_redc(const uint32_t (&w)[NW], const PrimeK &k) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int g = 0; g < NW; g += 3) {
+        uint64_t t = 0;
+#pragma unroll
+        for (int i = g; i < g + 3 && i < NW; i++) t += (uint64_t)w[i] * k.pw[i];
+        s = red2p(s + red2p(redc64(t, k.p, k.pinv), k.p2), k.p2);
+    }
+    return s;
+}
+
 // S1 ("split the input bit sequence and map it to a prime field"): every
 // limb of every vector is extracted once and reduced modulo all P primes.
 // res layout: [vec][prime][wxp] with wxp = rows * N1 (zero beyond the vector's limbs).
-template <class Src>
+// NW = 0: limbs of <= 56 bits (one 64-bit value, limb_redc); else NW 32-bit words.
+template <class Src, int NW>
 __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeK *__restrict__ pk,
                                                      uint32_t P, uint32_t nvec, uint32_t wxp,
                                                      uint32_t *__restrict__ res) {
+    __shared__ PrimeK ks[kMaxPrimes];
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) ks[i] = pk[i];
+    __syncthreads();
     const uint64_t total = (uint64_t)nvec * wxp;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t iv = (uint32_t)(t / wxp), j = (uint32_t)(t % wxp);
-        const uint64_t v = src(iv, j);
         uint32_t *o = res + (size_t)iv * P * wxp + j;
-        for (uint32_t pi = 0; pi < P; pi++) {
-            const uint32_t p = pk[pi].p;
-            o[(size_t)pi * wxp] = v ? limb_redc(v, p, pk[pi].pinv) : 0u;
+        if constexpr (NW == 0) {
+            const uint64_t v = src(iv, j);
+            for (uint32_t pi = 0; pi < P; pi++) {
+                const uint32_t p = ks[pi].p;
+                o[(size_t)pi * wxp] = v ? limb_redc(v, p, ks[pi].pinv) : 0u;
+            }
+        } else {
+            uint32_t w[NW];
+            src.template words<NW>(iv, j, w);
+            uint32_t any = 0;
+#pragma unroll
+            for (int i = 0; i < NW; i++) any |= w[i];
+            for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = any ? limb_words_redc<NW>(w, ks[pi]) : 0u;
         }
     }
 }
@@ -113,10 +195,14 @@ __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeK
 struct KeyLimbs {
     KeySrc s;
     __device__ __forceinline__ uint64_t operator()(uint32_t iv, uint32_t j) const { return key_limb(s, iv, j); }
+    template <int NW>
+    __device__ __forceinline__ void words(uint32_t iv, uint32_t j, uint32_t (&w)[NW]) const { key_limb_words<NW>(s, iv, j, w); }
 };
 struct WordLimbs {
     WordSrc s;
     __device__ __forceinline__ uint64_t operator()(uint32_t iv, uint32_t j) const { return word_limb(s, iv, j); }
+    template <int NW>
+    __device__ __forceinline__ void words(uint32_t iv, uint32_t j, uint32_t (&w)[NW]) const { word_limb_words<NW>(s, iv, j, w); }
 };
 
 // ---------------------------------------------------------------- column pass
@@ -165,8 +251,8 @@ col_pass(const ColArgs A) {
             cx.p = pk.p; cx.p2 = pk.p2; cx.pinv = pk.pinv;
 #pragma unroll
             for (int j = 0; j < E / 2; j++) {
-                tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j);
-                twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j);
+                tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j * (32 / E));
+                twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j * (32 / E));
             }
             rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
         }
@@ -247,8 +333,8 @@ row_pass(const RowArgs A) {
         uint32_t tw[E / 2], twp[E / 2];
 #pragma unroll
         for (int j = 0; j < E / 2; j++) {
-            tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j);
-            twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j);
+            tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j * (32 / E));
+            twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j * (32 / E));
         }
         const uint32_t *rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
         uint32_t acc[E];
@@ -349,10 +435,14 @@ constexpr size_t mac_smem_bytes() {
 }
 __device__ __forceinline__ int swz32(int P) { return P ^ ((P >> 5) & 31); }
 
-// <= 128 registers per thread: 16 warps per SM (the register file bound)
-template <int S_LOG, int E_LOG>
-__global__ void __launch_bounds__(mac_v(S_LOG) * (1 << (S_LOG - E_LOG)),
-                                  (512 / (mac_v(S_LOG) * (1 << (S_LOG - E_LOG)))) < 8 ? (512 / (mac_v(S_LOG) * (1 << (S_LOG - E_LOG)))) : 8)
+// <= 4E registers per thread (the register file bounds the warps per SM)
+__host__ __device__ constexpr int mac_threads(int slog, int elog) { return mac_v(slog) * (1 << (slog - elog)); }
+__host__ __device__ constexpr int mac_minb(int slog, int elog) {
+    return (65536 / (mac_threads(slog, elog) * 4 * (1 << elog))) < 8 ? (65536 / (mac_threads(slog, elog) * 4 * (1 << elog)))
+                                                                        : 8;
+}
+template <int S_LOG, int E_LOG, int DBG = 0>
+__global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(S_LOG, E_LOG) < 1 ? 1 : mac_minb(S_LOG, E_LOG))
 row_mac(const MacArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int S = SP::S, E = SP::E;
@@ -422,15 +512,15 @@ row_mac(const MacArgs A) {
                 cx = Ctx32{pk.p, pk.p2, pk.pinv};
 #pragma unroll
                 for (int j = 0; j < E / 2; j++) {
-                    tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j);
-                    twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j);
+                    tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j * (32 / E));
+                    twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j * (32 / E));
                 }
                 rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
             }
 #pragma unroll
             for (int e = 0; e < E; e++) acc[e] = 0;
         }
-        const uint32_t k = (uint32_t)(it - it0);
+        const uint32_t k = (DBG == 2) ? 0u : (uint32_t)(it - it0);
         const int s = (int)(k & 1);
         mbar_wait(&bars[s], (k >> 1) & 1);
         uint32_t *xst = xs + s * SW;
@@ -442,9 +532,11 @@ row_mac(const MacArgs A) {
 #pragma unroll
                 for (int m = 0; m < R; m++) x[h * R + m] = xst[w * S + in_pos<S_LOG, E_LOG>(v, h, m)];
         }
-        if constexpr (SP::Q > 1) __syncthreads();        // natural-order reads done before in-place writes
-        round0_finish<S_LOG, E_LOG>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
-        rounds_rest<S_LOG, E_LOG, 1>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
+        if constexpr (DBG != 1) {
+            if constexpr (SP::Q > 1) __syncthreads();    // natural-order reads done before in-place writes
+            round0_finish<S_LOG, E_LOG>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
+            rounds_rest<S_LOG, E_LOG, 1>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
+        }
         mbar_wait(&bars[2], k & 1);
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
@@ -458,7 +550,7 @@ row_mac(const MacArgs A) {
                 }
         }
         __syncthreads();                                 // X stage s and A^ are free
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && DBG != 2) {
             if (it + 2 < it1) issue_x(it + 2, s);
             if (it + 1 < it1) issue_a(it + 1);
         }

@@ -72,11 +72,14 @@ def test_plan_configs(name):
 
 
 def test_plan_forced_limb_bits():
-    for Bl in (16, 24, 32, 40, 48, 56):
+    for Bl in (16, 24, 32, 40, 48, 56, 64, 96, 168, 200):
         info = P.plan(1 << 20, 1 << 16, 100_000, limb_bits=Bl)
         assert info["mmh"]["limb_bits"] == Bl and info["mh"]["limb_bits"] == Bl
     with pytest.raises(B.PAError):
-        P.plan(1 << 20, 1 << 16, 100_000, limb_bits=64)     # limb_redc needs B <= 56
+        P.plan(1 << 20, 1 << 16, 100_000, limb_bits=264)    # at most 8 words per limb
+    with pytest.raises(B.PAError) as e:
+        P.plan(1 << 20, 1 << 16, 100_000, limb_bits=256)    # would need > 16 primes
+    assert e.value.code == B.PA_E_BOUND
 
 
 def test_philox_matches_numpy():

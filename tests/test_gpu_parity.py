@@ -64,7 +64,7 @@ def test_parity_C2():
     assert gpu_hash(key, w.n, w.r, w.m, w.hash_seed) == oracle_seeded(key, w.n, w.r, w.m, w.hash_seed)
 
 
-@pytest.mark.parametrize("B", [16, 24, 32, 40, 48, 56])
+@pytest.mark.parametrize("B", [16, 24, 32, 40, 48, 56, 64, 72, 96, 128, 168, 200, 216])
 def test_limb_width_invariance(B):
     # reading A11: the limb width is internal and must not change the output
     n, r, m = 70_001, 2048, 9_999
