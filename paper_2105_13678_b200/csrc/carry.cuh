@@ -107,48 +107,52 @@ __device__ __forceinline__ uint32_t coef_window(const uint32_t *__restrict__ c, 
     return v;
 }
 
+// All bit positions here are < 2^31 (alpha, B L <= 2^31 for every accepted plan), so
+// the coefficient ranges use 32-bit unsigned division.
 template <int P, bool RING>
 __global__ void __launch_bounds__(256) crt_colsum(const uint32_t *__restrict__ coef, uint32_t ncoef, uint32_t B,
-                                                  uint64_t gamma, const uint32_t *__restrict__ addend,
+                                                  uint64_t gamma64, const uint32_t *__restrict__ addend,
                                                   uint32_t n_addend, uint64_t *__restrict__ S, uint32_t W) {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= W) return;
-    const int64_t cbits = 32 * P;
-    const int64_t me = 32 * (int64_t)u;
+    constexpr uint32_t cbits = 32 * P;
+    const uint32_t me = 32 * u;
+    const uint32_t gamma = (uint32_t)gamma64;
     uint64_t s = (!RING && addend && u < n_addend) ? addend[u] : 0ull;
-    const uint64_t span = RING ? gamma : (1ull << 62);
-    const uint64_t nchunks = RING ? ((uint64_t)B * ncoef + gamma - 1) / gamma : 1;
-    for (uint64_t t = 0; t < nchunks; t++) {
-        const int64_t base = (int64_t)(t * span);             // ring bit 0 of this chunk
-        const int64_t jc0 = (base + B - 1) / B;                // first j of the chunk
-        const int64_t jc1 = RING ? (int64_t)(((t + 1) * span + B - 1) / B) - 1 : (int64_t)ncoef - 1;
-        int64_t j0 = (me - cbits + base) / (int64_t)B;        // pieces [B j - base, + cbits) meeting me
-        int64_t j1 = (me + 31 + base) / (int64_t)B;
+    const uint32_t nchunks = RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
+    for (uint32_t t = 0; t < nchunks; t++) {
+        const uint32_t base = RING ? t * gamma : 0u;          // ring bit 0 of this chunk
+        const uint32_t jc0 = (base + B - 1) / B;               // first j of the chunk
+        uint32_t jc1 = ncoef - 1;
+        if (RING) jc1 = min(jc1, (uint32_t)(((uint64_t)(t + 1) * gamma + B - 1) / B) - 1);
+        // pieces [B j - base, B j - base + cbits) meeting [me, me + 32)
+        const uint32_t num0 = me + base;
+        uint32_t j0 = (num0 > cbits) ? (num0 - cbits) / B : 0u;
+        uint32_t j1 = (me + 31 + base) / B;
         if (j0 < jc0) j0 = jc0;
         if (j1 > jc1) j1 = jc1;
-        if (j1 > (int64_t)ncoef - 1) j1 = (int64_t)ncoef - 1;
-        for (int64_t j = j0; j <= j1; j++) {
+        for (uint32_t j = j0; j <= j1 && j1 != 0xFFFFFFFFu; j++) {
             const int64_t pos = (int64_t)B * j - base;
             int64_t len = cbits;
             if (RING && pos + len > (int64_t)gamma) len = (int64_t)gamma - pos;
-            s += coef_window<P>(coef + (size_t)j * P, me - pos, len);
+            s += coef_window<P>(coef + (size_t)j * P, (int64_t)me - pos, len);
         }
     }
     if (RING && me < cbits + 32) {
         // wrapped pieces: bits of a coefficient above the ring top land at ring bit 0
-        for (uint64_t t = 0; t < nchunks; t++) {
-            const int64_t base = (int64_t)(t * gamma);
+        for (uint32_t t = 0; t < nchunks; t++) {
+            const int64_t base = (int64_t)t * gamma;
             const int64_t top = base + (int64_t)gamma;
-            int64_t ja = (top - cbits) / (int64_t)B;
+            int64_t ja = (top - (int64_t)cbits) / (int64_t)B;
             const int64_t jc0 = (base + B - 1) / B;
             if (ja < jc0) ja = jc0;
             int64_t jb = (top - 1) / (int64_t)B;
             if (jb > (int64_t)ncoef - 1) jb = (int64_t)ncoef - 1;
             for (int64_t j = ja; j <= jb; j++) {
                 const int64_t pos = (int64_t)B * j - base;
-                if (pos + cbits <= (int64_t)gamma) continue;
+                if (pos + (int64_t)cbits <= (int64_t)gamma) continue;
                 const int64_t cut = (int64_t)gamma - pos;
-                s += coef_window<P>(coef + (size_t)j * P, me + cut, cbits);
+                s += coef_window<P>(coef + (size_t)j * P, (int64_t)me + cut, cbits);
             }
         }
     }
@@ -290,16 +294,16 @@ __global__ void __launch_bounds__(kCarryT) carry_mw(const Src src, uint32_t W, u
 // ---------------------------------------------------------------- Mersenne finish
 // y (Wtot words, y < 2^(32 Wtot)) -> y mod (2^gamma - 1), canonical in [0, p-1]
 // (reading A6), in place, by the fold x mod M_gamma = (x >> gamma) + (x mod 2^gamma)
-// repeated until nothing is left above bit gamma.  One CTA of
-// 1024 threads: the fold adds a short number (Wtot - floor(gamma/32) words) at bit 0,
-// whose carry ripples only through a run of all-ones words -- one chunk of 1024 words
-// almost always, more chunks only for such runs (correct either way).
+// repeated until nothing is left above bit gamma.  Run by one CTA (any
+// block size): the fold adds a short number (Wtot - floor(gamma/32) <= 64 words) at bit
+// 0, whose carry ripples only through a run of all-ones words -- one chunk of blockDim
+// words almost always, more chunks only for such runs (correct either way).
 constexpr int kFinT = 1024;
 
 __device__ __forceinline__ void fin_ripple(uint32_t *y, uint32_t Wtot, uint32_t from) {
     // add 1 at word `from`, rippling through all-ones words
     __shared__ uint32_t s_first;
-    for (uint32_t base = from; base < Wtot; base += kFinT) {
+    for (uint32_t base = from; base < Wtot; base += blockDim.x) {
         if (threadIdx.x == 0) s_first = 0xFFFFFFFFu;
         __syncthreads();
         const uint32_t u = base + threadIdx.x;
@@ -314,7 +318,7 @@ __device__ __forceinline__ void fin_ripple(uint32_t *y, uint32_t Wtot, uint32_t 
     }
 }
 
-__global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict__ y, uint32_t Wtot, uint64_t gamma) {
+__device__ void mersenne_finish_dev(uint32_t *y, uint32_t Wtot, uint64_t gamma) {
     __shared__ uint32_t T[64];
     __shared__ uint32_t s_nz, s_carry, s_bad;
     const uint32_t gw = (uint32_t)(gamma >> 5);
@@ -323,18 +327,18 @@ __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict_
     for (;;) {
         if (threadIdx.x == 0) s_nz = 0;
         __syncthreads();
-        if (threadIdx.x < nT) {
-            const uint32_t i = gw + threadIdx.x;
+        for (uint32_t t = threadIdx.x; t < nT; t += blockDim.x) {
+            const uint32_t i = gw + t;
             const uint32_t lo = y[i], hi = (i + 1 < Wtot) ? y[i + 1] : 0u;
-            const uint32_t t = gs ? __funnelshift_r(lo, hi, gs) : lo;
-            T[threadIdx.x] = t;
-            if (t) atomicOr(&s_nz, 1u);
+            const uint32_t v = gs ? __funnelshift_r(lo, hi, gs) : lo;
+            T[t] = v;
+            if (v) atomicOr(&s_nz, 1u);
         }
         __syncthreads();
         if (!s_nz) break;
-        if (threadIdx.x < nT) {                           // clear bits >= gamma
-            const uint32_t i = gw + threadIdx.x;
-            if (threadIdx.x == 0 && gs) y[i] &= (1u << gs) - 1u;
+        for (uint32_t t = threadIdx.x; t < nT; t += blockDim.x) {     // clear bits >= gamma
+            const uint32_t i = gw + t;
+            if (t == 0 && gs) y[i] &= (1u << gs) - 1u;
             else y[i] = 0u;
         }
         __syncthreads();
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict_
     }
     // canonical zero: y == 2^gamma - 1 -> 0
     const uint32_t Wg = (uint32_t)((gamma + 31) >> 5);
-    for (uint32_t base = 0; base < Wg; base += kFinT) {
+    for (uint32_t base = 0; base < Wg; base += blockDim.x) {
         if (threadIdx.x == 0) s_bad = 0;
         __syncthreads();
         const uint32_t u = base + threadIdx.x;
@@ -364,7 +368,242 @@ __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict_
         __syncthreads();
         if (s_bad) return;
     }
-    for (uint32_t u = threadIdx.x; u < Wg; u += kFinT) y[u] = 0u;
+    for (uint32_t u = threadIdx.x; u < Wg; u += blockDim.x) y[u] = 0u;
+}
+
+__global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict__ y, uint32_t Wtot, uint64_t gamma) {
+    mersenne_finish_dev(y, Wtot, gamma);
+}
+
+// ---------------------------------------------------------------- fused CRT + carries
+// S4/S5 (MMH) and S7 (MH) tail in one kernel.  A CTA (ticket order) owns kCarryTile
+// output words [u0, u1).  For each chunk of the ring it reconstructs, by CRT, the exact
+// coefficients whose pieces meet its words into shared memory, forms the 64-bit column
+// sums S_u of its words (RING: pieces cut at bit gamma, high parts land at bit 0 -- the
+// Mersenne fold of PAPER.md:130-132 per coefficient; LINEAR: plus the addend c), then
+// resolves the carries: digit d_u = lo32(S_u) + hi32(S_{u-1}) inside the tile, binary
+// generate/propagate scan over words u0+1.., and a small multi-bit carry between tiles:
+//   C_out = hi32(S_{u1-1}) + carry_out(c1),  c1 = [w_{u0} + C_in >= 2^32].
+// A tile whose carry-out does not depend on C_in (it generates, or some word does not
+// propagate) publishes C_out before waiting for its predecessor, so the chain is
+// almost never serial.  RING: the last CTA to finish runs the Mersenne finish.
+// state: [0] ticket, [1] done counter, [2 + t] tile t: bit 31 ready, bits 0..30 C_out.
+template <int P>
+__device__ __forceinline__ void crt_one(const uint32_t *__restrict__ res, uint32_t L, uint32_t j, const CrtK &K,
+                                        uint32_t *out, int stride) {
+    uint32_t y[P];
+    uint64_t slo = 1ull << 40, shi = 0;
+#pragma unroll
+    for (int i = 0; i < P; i++) {
+        const uint32_t r = res[(size_t)i * L + j];
+        y[i] = red1p(mul_mont(r, K.qinv[i], K.p[i], K.pinv[i]), K.p[i]);
+        const uint64_t q = (uint64_t)y[i] * K.G[i];
+        slo += q;
+        shi += (slo < q);
+    }
+    const uint32_t k = (uint32_t)shi;
+    uint64_t acc[P + 1];
+#pragma unroll
+    for (int w = 0; w <= P; w++) acc[w] = 0;
+#pragma unroll
+    for (int i = 0; i < P; i++)
+#pragma unroll
+        for (int w = 0; w < P; w++) {
+            const uint64_t t = mad_wide(y[i], K.MI[i][w], 0ull);
+            acc[w] += (uint32_t)t;
+            acc[w + 1] += t >> 32;
+        }
+    uint64_t carry = 0;
+    int64_t borrow = 0;
+#pragma unroll
+    for (int w = 0; w < P; w++) {
+        const uint64_t v = acc[w] + carry;
+        carry = v >> 32;
+        const uint64_t km = (uint64_t)k * K.M[w];
+        const int64_t d = (int64_t)(uint32_t)v - (int64_t)(uint32_t)km + borrow;
+        out[w * stride] = (uint32_t)d;
+        borrow = (d >> 32) - (int64_t)(km >> 32);
+    }
+}
+
+// bits [off, off + 32) of a coefficient held in shared memory (P words at stride 1)
+template <int P>
+__device__ __forceinline__ uint32_t coef_window_s(const uint32_t *c, int off, int len) {
+    if (off <= -32 || off >= len) return 0;
+    uint32_t v;
+    if (off < 0) {
+        v = c[0] << (-off);
+    } else {
+        const int wi = off >> 5, sh = off & 31;
+        const uint32_t lo = c[wi];
+        const uint32_t hi = (wi + 1 < P) ? c[wi + 1] : 0u;
+        v = __funnelshift_r(lo, hi, sh);
+    }
+    const int top = len - off;
+    if (top < 32) v &= (top <= 0) ? 0u : ((1u << top) - 1u);
+    return v;
+}
+
+template <int P>
+__host__ __device__ constexpr int crt_cstride() { return P | 1; }                 // odd stride: fewer bank conflicts
+
+template <int P, bool RING>
+__global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
+                                                     uint32_t B, uint32_t gamma, const CrtK K,
+                                                     const uint32_t *__restrict__ addend, uint32_t n_addend,
+                                                     uint32_t *__restrict__ out, uint32_t W, uint32_t cap,
+                                                     uint32_t *state, uint32_t Wfin) {
+    extern __shared__ uint32_t sc[];                          // [cap][P|1] coefficients
+    constexpr int CS = crt_cstride<P>();
+    constexpr uint32_t cbits = 32 * P;
+    __shared__ uint32_t s_tile, s_cin, s_c1, s_last;
+    __shared__ uint32_t s_hi[kCarryT];
+    if (threadIdx.x == 0) s_tile = atomicAdd(&state[0], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t u0 = tile * kCarryTile;
+    const uint32_t ub = u0 + threadIdx.x * kCarryV;            // this thread's first word
+    uint64_t S[kCarryV];
+#pragma unroll
+    for (int v = 0; v < kCarryV; v++) {
+        const uint32_t u = ub + v;
+        S[v] = (!RING && addend && u < n_addend) ? addend[u] : 0ull;
+    }
+    // ---- column sums, chunk by chunk
+    const uint32_t nchunks = RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
+    const uint32_t tb0 = 32 * u0, tb1 = 32 * min(u0 + kCarryTile, W);   // tile bits
+    for (uint32_t t = 0; t < nchunks; t++) {
+        const uint32_t base = RING ? t * gamma : 0u;
+        const uint32_t jc0 = (base + B - 1) / B;
+        uint32_t jc1 = ncoef - 1;
+        if (RING) jc1 = min(jc1, (uint32_t)(((uint64_t)(t + 1) * gamma + B - 1) / B) - 1);
+        uint32_t ja = (tb0 + base > cbits) ? (tb0 + base - cbits) / B : 0u;
+        uint32_t jb = (tb1 - 1 + base) / B;
+        if (ja < jc0) ja = jc0;
+        if (jb > jc1) jb = jc1;
+        if (jb < ja || jb == 0xFFFFFFFFu) continue;           // uniform
+        const uint32_t cnt = min(jb - ja + 1, cap);
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < cnt; q += blockDim.x) crt_one<P>(res, L, ja + q, K, sc + q * CS, 1);
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < kCarryV; v++) {
+            const uint32_t u = ub + v;
+            if (u >= W) continue;
+            const uint32_t me = 32 * u;
+            uint32_t j0 = (me + base > cbits) ? (me + base - cbits) / B : 0u;
+            uint32_t j1 = (me + 31 + base) / B;
+            if (j0 < ja) j0 = ja;
+            if (j1 > ja + cnt - 1) j1 = ja + cnt - 1;
+            for (uint32_t j = j0; j <= j1; j++) {
+                const int pos = (int)(B * j - base);
+                int len = (int)cbits;
+                if (RING && pos + len > (int)gamma) len = (int)gamma - pos;
+                S[v] += coef_window_s<P>(sc + (j - ja) * CS, (int)me - pos, len);
+            }
+        }
+    }
+    if (RING && tb0 < cbits + 32) {
+        // wrapped pieces: the bits of a coefficient above the ring top land at ring bit 0
+        uint32_t tmp[P];
+        for (uint32_t t = 0; t < nchunks; t++) {
+            const int64_t base = (int64_t)t * gamma;
+            const int64_t top = base + (int64_t)gamma;
+            int64_t jx = (top - (int64_t)cbits) / (int64_t)B;
+            const int64_t jc0 = (base + B - 1) / B;
+            if (jx < jc0) jx = jc0;
+            int64_t jy = (top - 1) / (int64_t)B;
+            if (jy > (int64_t)ncoef - 1) jy = (int64_t)ncoef - 1;
+            for (int64_t j = jx; j <= jy; j++) {
+                const int64_t pos = (int64_t)B * j - base;
+                if (pos + (int64_t)cbits <= (int64_t)gamma) continue;
+                const int cut = (int)((int64_t)gamma - pos);
+                bool need = false;
+#pragma unroll
+                for (int v = 0; v < kCarryV; v++) need |= (32 * (ub + v) < cbits + 32);
+                if (!need) continue;
+                crt_one<P>(res, L, (uint32_t)j, K, tmp, 1);
+#pragma unroll
+                for (int v = 0; v < kCarryV; v++) {
+                    const uint32_t me = 32 * (ub + v);
+                    if (ub + v < W && me < cbits + 32) S[v] += coef_window_s<P>(tmp, (int)me + cut, (int)cbits);
+                }
+            }
+        }
+    }
+    // ---- carries inside the tile (cin of word u0 handled separately, see above)
+    uint32_t w[kCarryV];
+    uint32_t gm = 0, pm = 0;
+    s_hi[threadIdx.x] = (uint32_t)(S[kCarryV - 1] >> 32);
+    __syncthreads();
+    uint32_t hprev = threadIdx.x ? s_hi[threadIdx.x - 1] : 0u;
+#pragma unroll
+    for (int v = 0; v < kCarryV; v++) {
+        const uint32_t u = ub + v;
+        const uint64_t t = (S[v] & 0xFFFFFFFFull) + hprev;
+        hprev = (uint32_t)(S[v] >> 32);
+        w[v] = (uint32_t)t;
+        const bool first = (threadIdx.x == 0 && v == 0);       // word u0: transparent in the scan
+        gm |= (uint32_t)(first ? 0u : (uint32_t)(t >> 32)) << v;
+        pm |= (uint32_t)(first || u >= W || w[v] == 0xFFFFFFFFu) << v;
+    }
+    uint32_t G = 0;
+#pragma unroll
+    for (int v = 0; v < kCarryV; v++) G = ((gm >> v) & 1u) | (((pm >> v) & 1u) & G);
+    const int Pall = (pm == (1u << kCarryV) - 1u);
+    const int allp = __syncthreads_and(Pall);
+    uint32_t bg;
+    (void)block_carries((int)G, Pall, 0, &bg);
+    const uint32_t hi_last = s_hi[kCarryT - 1];               // hi32 of the tile's last sum
+    volatile uint32_t *vs = state + 2;
+    if (threadIdx.x == 0) {
+        const bool indep = bg || !allp;
+        const uint32_t cout_indep = hi_last + bg;
+        if (indep) {
+            __threadfence();
+            vs[tile] = 0x80000000u | cout_indep;
+        }
+        uint32_t cin = 0;
+        if (tile > 0) {
+            uint32_t st;
+            while (!((st = vs[tile - 1]) & 0x80000000u)) { }
+            cin = st & 0x7FFFFFFFu;
+        }
+        const uint32_t c1 = (uint32_t)(((uint64_t)w[0] + cin) >> 32);     // thread 0 owns word u0
+        s_cin = cin;
+        s_c1 = c1;
+        if (!indep) {
+            __threadfence();
+            vs[tile] = 0x80000000u | (hi_last + (bg | ((uint32_t)allp & c1)));
+        }
+    }
+    __syncthreads();
+    const uint32_t cin = s_cin;
+    uint32_t c = block_carries((int)G, Pall, s_c1, nullptr);
+#pragma unroll
+    for (int v = 0; v < kCarryV; v++) {
+        const uint32_t u = ub + v;
+        const bool first = (threadIdx.x == 0 && v == 0);
+        if (first) {
+            if (u < W) out[u] = w[v] + cin;
+            continue;
+        }
+        if (u < W) out[u] = w[v] + c;
+        c = ((gm >> v) & 1u) | (((pm >> v) & 1u) & c);
+    }
+    if (RING) {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t ntiles = (W + kCarryTile - 1) / kCarryTile;
+            s_last = (atomicAdd(&state[1], 1u) == ntiles - 1);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            mersenne_finish_dev(out, Wfin, gamma);
+        }
+    }
 }
 
 // ---------------------------------------------------------------- MH output

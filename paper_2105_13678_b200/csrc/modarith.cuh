@@ -23,6 +23,13 @@ struct alignas(16) PrimeK {  // per-prime constants passed to kernels
     uint32_t pw[8];        // 2^(32 i) mod p, i < 8 (multiword limb reduction)
 };
 
+// a * b + c with a 32x32 -> 64-bit multiply (one IMAD.WIDE.U32)
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+    return r;
+}
+
 // REDC of t < 3 p 2^32: t 2^-32 mod p in [0, 4p)
 __device__ __forceinline__ uint32_t redc64(uint64_t t, uint32_t p, uint32_t pinv) {
     const uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);

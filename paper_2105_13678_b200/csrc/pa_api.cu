@@ -489,6 +489,41 @@ static int launch_mac(int slog, const MacArgs &A, cudaStream_t st) {
     return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
 }
 
+template <int P, bool RING>
+static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
+                              const uint32_t *addend, uint32_t n_addend, uint32_t *out, uint32_t W, uint32_t *state,
+                              uint32_t Wfin, cudaStream_t st) {
+    const uint32_t B = sd.pl.limb_bits;
+    const uint32_t cap = (32u * kCarryTile + 32u * P) / B + 3;
+    const size_t smem = (size_t)cap * crt_cstride<P>() * 4;
+    auto fn = crt_carry<P, RING>;
+    static size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
+    const uint32_t ntiles = (W + kCarryTile - 1) / kCarryTile;
+    fn<<<ntiles, kCarryT, smem, st>>>(res, sd.L, ncoef, B, (uint32_t)gamma, sd.crt, addend, n_addend, out, W, cap,
+                                      state, Wfin);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+template <bool RING>
+static int launch_crt_carry(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
+                            const uint32_t *addend, uint32_t n_addend, uint32_t *out, uint32_t W, uint32_t *state,
+                            uint32_t Wfin, cudaStream_t st) {
+#define PA_CC_CASE(P) \
+    case P: return launch_crt_carry_t<P, RING>(res, sd, ncoef, gamma, addend, n_addend, out, W, state, Wfin, st);
+    switch (sd.pl.nprimes) {
+        PA_CC_CASE(2) PA_CC_CASE(3) PA_CC_CASE(4) PA_CC_CASE(5) PA_CC_CASE(6) PA_CC_CASE(7) PA_CC_CASE(8)
+        PA_CC_CASE(9) PA_CC_CASE(10) PA_CC_CASE(11) PA_CC_CASE(12) PA_CC_CASE(13) PA_CC_CASE(14)
+        PA_CC_CASE(15) PA_CC_CASE(16)
+    }
+#undef PA_CC_CASE
+    return set_err(PA_E_PARAM, "unsupported prime count %u", sd.pl.nprimes);
+}
+
 template <bool RING>
 static int launch_crt(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
                       const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint64_t *S, uint32_t W,
@@ -584,6 +619,12 @@ static int run_carry(pa_ctx *c, const Src &src, uint32_t W, uint32_t *out) {
     return PA_OK;
 }
 
+// a zeroed look-back state slot ([ticket, done, tiles...]) for one fused launch
+static uint32_t *next_state(pa_ctx *c) {
+    if (c->cslot >= kCarrySlots) return nullptr;
+    return c->cstate + (size_t)(c->cslot++) * c->cstate_stride;
+}
+
 // y (W_fold words, resolved) -> y mod p, canonical (reading A6), in place
 static int mersenne_finish(pa_ctx *c, uint32_t *y) {
     mersenne_finish_k<<<1, kFinT, 0, c->stream>>>(y, (uint32_t)c->W_fold, c->pl.gamma);
@@ -597,6 +638,31 @@ static uint32_t mac_v_rt(int slog) {
         case 5: return mac_v(5); case 6: return mac_v(6); case 7: return mac_v(7); case 8: return mac_v(8);
         case 9: return mac_v(9); case 10: return mac_v(10); default: return 1;
     }
+}
+
+template <int NW>
+static void launch_pack_key(const KeySrc &s, uint32_t nvec, const PrimeK *pk, uint32_t P, uint32_t wxp, uint32_t *res,
+                            cudaStream_t st) {
+    const dim3 grid((wxp + kPackT - 1) / kPackT, nvec);
+    pack_key_residues<NW><<<grid, kPackT, 0, st>>>(s, pk, P, wxp, res);
+}
+
+static int launch_pack(const KeyLimbs &src, uint32_t B, uint32_t grid, const PrimeK *pk, uint32_t P, uint32_t nvec,
+                       uint32_t wxp, uint32_t *res, cudaStream_t st) {
+    const int nw = B <= 56 ? 0 : (int)((B + 31) / 32);
+    switch (nw) {
+        case 0: pack_residues<KeyLimbs, 0><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
+        case 2: launch_pack_key<2>(src.s, nvec, pk, P, wxp, res, st); break;
+        case 3: launch_pack_key<3>(src.s, nvec, pk, P, wxp, res, st); break;
+        case 4: launch_pack_key<4>(src.s, nvec, pk, P, wxp, res, st); break;
+        case 5: launch_pack_key<5>(src.s, nvec, pk, P, wxp, res, st); break;
+        case 6: launch_pack_key<6>(src.s, nvec, pk, P, wxp, res, st); break;
+        case 7: launch_pack_key<7>(src.s, nvec, pk, P, wxp, res, st); break;
+        case 8: launch_pack_key<8>(src.s, nvec, pk, P, wxp, res, st); break;
+        default: return set_err(PA_E_PARAM, "unsupported limb width %u", B);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
 }
 
 template <class Src>
@@ -908,15 +974,10 @@ static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
     TRY(stage_transform(c, c->smmh, KeyLimbs{ks}, c->nblk, c->rows_mmh, c->scratch, c->ahat, c->acc,
                         "mmh_pack", "mmh_fwd_col", "mmh_fwd_row_mac", "mmh_inverse"));
     {
-        ProfScope ps(c, "mmh_crt");
-        TRY(launch_crt<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->coef, c->S,
-                             (uint32_t)c->W_ring, c->stream));
-        c->launches += 2;
-    }
-    {
-        ProfScope ps(c, "mmh_carry_fold");
-        TRY(run_carry(c, SrcArr{c->S, (uint32_t)c->W_ring}, (uint32_t)c->W_fold, c->y1));
-        TRY(mersenne_finish(c, c->y1));
+        ProfScope ps(c, "mmh_crt_carry_fold");
+        TRY(launch_crt_carry<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->y1,
+                                   (uint32_t)c->W_fold, next_state(c), (uint32_t)c->W_fold, c->stream));
+        c->launches++;
     }
     *y_out = c->y1;
     return PA_OK;
@@ -931,14 +992,11 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
                         "mh_pack", "mh_fwd_col", "mh_fwd_row_mac", "mh_inverse"));
     const uint32_t W = (uint32_t)c->W_Z;
     {
-        ProfScope ps(c, "mh_crt");
+        ProfScope ps(c, "mh_crt_carry_extract");
         const uint64_t ncoef = std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1);
-        TRY(launch_crt<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->coef, c->S, W, c->stream));
-        c->launches += 2;
-    }
-    {
-        ProfScope ps(c, "mh_carry_extract");
-        TRY(run_carry(c, SrcArr{c->S, W}, W, c->Z));
+        TRY(launch_crt_carry<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->Z, W, next_state(c), 0,
+                                    c->stream));
+        c->launches++;
         const uint64_t nb = cdiv(p.m, 8), nw = cdiv(nb, 4);
         mh_extract<<<(uint32_t)cdiv(nw, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
         c->launches++;

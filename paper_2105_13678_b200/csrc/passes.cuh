@@ -153,7 +153,7 @@ __device__ __forceinline__ uint32_t limb_words_redc(const uint32_t (&w)[NW], con
     for (int g = 0; g < NW; g += 3) {
         uint64_t t = 0;
 #pragma unroll
-        for (int i = g; i < g + 3 && i < NW; i++) t += (uint64_t)w[i] * k.pw[i];
+        for (int i = g; i < g + 3 && i < NW; i++) t = mad_wide(w[i], k.pw[i], t);
         s = red2p(s + red2p(redc64(t, k.p, k.pinv), k.p2), k.p2);
     }
     return s;
@@ -190,6 +190,62 @@ __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeK
             for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = any ? limb_words_redc<NW>(w, ks[pi]) : 0u;
         }
     }
+}
+
+// S1 for key blocks with multiword limbs (B > 56): CTA (tile of 256 limbs, block iv).
+// The tile's key bytes are staged in shared memory with coalesced 32-bit loads; each
+// thread assembles its limb's NW words (big-endian bytes, readings A3/A4) from there and
+// reduces them modulo every prime.  res layout as pack_residues.
+constexpr int kPackT = 256;
+template <int NW>
+__global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeK *__restrict__ pk, uint32_t P,
+                                                          uint32_t wxp, uint32_t *__restrict__ res) {
+    constexpr int MAXW = (kPackT * 4 * NW) / 4 + 4;        // staged words (LB <= 4 NW bytes per limb)
+    __shared__ uint32_t sw[MAXW];
+    __shared__ PrimeK ks[kMaxPrimes];
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) ks[i] = pk[i];
+    const uint32_t iv = blockIdx.y;
+    const uint32_t jt0 = blockIdx.x * kPackT;
+    const int64_t start = (int64_t)iv * s.blk_bytes;
+    const int64_t end = start + s.blk_bytes;
+    const int64_t LB = s.limb_bytes;
+    const uint32_t jt1 = min(jt0 + kPackT, s.wx);           // limbs with data in this tile
+    int64_t tlo = end - LB * (int64_t)jt1 - 4;               // lowest byte any word may touch
+    if (tlo < start - 4) tlo = start - 4;
+    const int64_t gw0 = tlo >> 2;                           // floor
+    const int64_t thi = end - LB * (int64_t)jt0;
+    const int nw = (jt0 < jt1) ? (int)(((thi + 3) >> 2) - gw0 + 1) : 0;
+    for (int k = threadIdx.x; k < nw && k < MAXW; k += blockDim.x) sw[k] = key_word(s, gw0 + k);
+    __syncthreads();
+    const uint32_t j = jt0 + threadIdx.x;
+    if (j >= wxp) return;
+    uint32_t w[NW];
+    uint32_t any = 0;
+    if (j < s.wx) {
+        const int64_t hi = end - LB * (int64_t)j;
+        int64_t lo = hi - LB;
+        if (lo < start) lo = start;
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            const int64_t pos = hi - 4 * (i + 1);
+            const int64_t wi = (pos >> 2) - gw0;
+            const int sh = (int)(pos & 3) * 8;
+            const uint32_t a0 = (wi >= 0 && wi < nw) ? sw[wi] : 0u;
+            const uint32_t a1 = (wi + 1 >= 0 && wi + 1 < nw) ? sw[wi + 1] : 0u;
+            uint32_t v = __byte_perm(__funnelshift_r(a0, a1, sh), 0, 0x0123);
+            const int64_t below = lo - pos;
+            if (below >= 4) v = 0;
+            else if (below > 0) v &= 0xFFFFFFFFu >> (8 * below);
+            w[i] = v;
+            any |= v;
+        }
+    }
+    uint32_t *o = res + (size_t)iv * P * wxp + j;
+    if (!any) {
+        for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = 0u;
+        return;
+    }
+    for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = limb_words_redc<NW>(w, ks[pi]);
 }
 
 struct KeyLimbs {
