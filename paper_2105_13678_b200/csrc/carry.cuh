@@ -38,7 +38,7 @@ struct CrtK {
 //   k = floor(sum_i y_i / p_i) evaluated in 64-bit fixed point (q_i = y_i floor(2^64/p_i),
 //   error < P 2^-34 per unit) with a bias of 2^-24: exact because c/M <= 2^-0.5 keeps the
 //   fractional part away from 1.  All coefficients are independent (no Garner chain).
-// One thread per coefficient; coef[j][w], P words each.
+// One thread per coefficient; word-major layout coef[w][j] (coalesced), P words each.
 template <int P>
 __global__ void __launch_bounds__(128) crt_coeffs(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
                                                   const CrtK K, uint32_t *__restrict__ coef) {
@@ -62,14 +62,14 @@ __global__ void __launch_bounds__(128) crt_coeffs(const uint32_t *__restrict__ r
     for (int i = 0; i < P; i++)
 #pragma unroll
         for (int w = 0; w < P; w++) {
-            const uint64_t t = (uint64_t)y[i] * K.MI[i][w];
+            const uint64_t t = mad_wide(y[i], K.MI[i][w], 0ull);
             acc[w] += (uint32_t)t;
             acc[w + 1] += t >> 32;
         }
     // words of sum_i y_i M_i (P + 1 words) minus k M
     uint64_t carry = 0;
     int64_t borrow = 0;
-    uint32_t *out = coef + (size_t)j * P;
+    uint32_t *out = coef + j;
 #pragma unroll
     for (int w = 0; w < P; w++) {
         const uint64_t v = acc[w] + carry;
@@ -77,86 +77,9 @@ __global__ void __launch_bounds__(128) crt_coeffs(const uint32_t *__restrict__ r
         const uint64_t km = (uint64_t)k * K.M[w];
         // subtract low word of k M (its high part carries into the next word via `borrow`)
         const int64_t d = (int64_t)(uint32_t)v - (int64_t)(uint32_t)km + borrow;
-        out[w] = (uint32_t)d;
+        out[(size_t)w * ncoef] = (uint32_t)d;
         borrow = (d >> 32) - (int64_t)(km >> 32);       // arithmetic shift: -1 on underflow
     }
-}
-
-// Column sums of 32-bit output words u < W from exact coefficients coef[j] (P words):
-//   RING = true : coefficient j sits at ring bit (B j) mod gamma (MMH, S4+S5): pieces are
-//                 cut at bit gamma and their high part lands at ring bit 0 -- the fold
-//                 x mod M_gamma = floor(x / 2^gamma) + x mod 2^gamma
-//                 applied per coefficient before the carries;
-//   RING = false: coefficient j at bit B j, plus the addend words (MH, Eq. 4 b y + c).
-// S[u] = sum of the 32-bit windows of all pieces over [32u, 32u + 32), < 2^40.
-template <int P>
-__device__ __forceinline__ uint32_t coef_window(const uint32_t *__restrict__ c, int64_t off, int64_t len) {
-    // bits [off, off + 32) of the coefficient restricted to [0, len); off may be negative
-    if (off <= -32 || off >= len) return 0;
-    uint32_t v;
-    if (off < 0) {
-        v = __ldg(c) << (-off);
-    } else {
-        const int wi = (int)(off >> 5), sh = (int)(off & 31);
-        const uint32_t lo = __ldg(c + wi);
-        const uint32_t hi = (wi + 1 < P) ? __ldg(c + wi + 1) : 0u;
-        v = __funnelshift_r(lo, hi, sh);
-    }
-    const int64_t top = len - off;
-    if (top < 32) v &= (top <= 0) ? 0u : ((1u << top) - 1u);
-    return v;
-}
-
-// All bit positions here are < 2^31 (alpha, B L <= 2^31 for every accepted plan), so
-// the coefficient ranges use 32-bit unsigned division.
-template <int P, bool RING>
-__global__ void __launch_bounds__(256) crt_colsum(const uint32_t *__restrict__ coef, uint32_t ncoef, uint32_t B,
-                                                  uint64_t gamma64, const uint32_t *__restrict__ addend,
-                                                  uint32_t n_addend, uint64_t *__restrict__ S, uint32_t W) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= W) return;
-    constexpr uint32_t cbits = 32 * P;
-    const uint32_t me = 32 * u;
-    const uint32_t gamma = (uint32_t)gamma64;
-    uint64_t s = (!RING && addend && u < n_addend) ? addend[u] : 0ull;
-    const uint32_t nchunks = RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
-    for (uint32_t t = 0; t < nchunks; t++) {
-        const uint32_t base = RING ? t * gamma : 0u;          // ring bit 0 of this chunk
-        const uint32_t jc0 = (base + B - 1) / B;               // first j of the chunk
-        uint32_t jc1 = ncoef - 1;
-        if (RING) jc1 = min(jc1, (uint32_t)(((uint64_t)(t + 1) * gamma + B - 1) / B) - 1);
-        // pieces [B j - base, B j - base + cbits) meeting [me, me + 32)
-        const uint32_t num0 = me + base;
-        uint32_t j0 = (num0 > cbits) ? (num0 - cbits) / B : 0u;
-        uint32_t j1 = (me + 31 + base) / B;
-        if (j0 < jc0) j0 = jc0;
-        if (j1 > jc1) j1 = jc1;
-        for (uint32_t j = j0; j <= j1 && j1 != 0xFFFFFFFFu; j++) {
-            const int64_t pos = (int64_t)B * j - base;
-            int64_t len = cbits;
-            if (RING && pos + len > (int64_t)gamma) len = (int64_t)gamma - pos;
-            s += coef_window<P>(coef + (size_t)j * P, (int64_t)me - pos, len);
-        }
-    }
-    if (RING && me < cbits + 32) {
-        // wrapped pieces: bits of a coefficient above the ring top land at ring bit 0
-        for (uint32_t t = 0; t < nchunks; t++) {
-            const int64_t base = (int64_t)t * gamma;
-            const int64_t top = base + (int64_t)gamma;
-            int64_t ja = (top - (int64_t)cbits) / (int64_t)B;
-            const int64_t jc0 = (base + B - 1) / B;
-            if (ja < jc0) ja = jc0;
-            int64_t jb = (top - 1) / (int64_t)B;
-            if (jb > (int64_t)ncoef - 1) jb = (int64_t)ncoef - 1;
-            for (int64_t j = ja; j <= jb; j++) {
-                const int64_t pos = (int64_t)B * j - base;
-                if (pos + (int64_t)cbits <= (int64_t)gamma) continue;
-                const int64_t cut = (int64_t)gamma - pos;
-                s += coef_window<P>(coef + (size_t)j * P, (int64_t)me + cut, cbits);
-            }
-        }
-    }
-    S[u] = s;
 }
 
 // ---------------------------------------------------------------- carry resolution
@@ -376,9 +299,9 @@ __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict_
 }
 
 // ---------------------------------------------------------------- fused CRT + carries
-// S4/S5 (MMH) and S7 (MH) tail in one kernel.  A CTA (ticket order) owns kCarryTile
-// output words [u0, u1).  For each chunk of the ring it reconstructs, by CRT, the exact
-// coefficients whose pieces meet its words into shared memory, forms the 64-bit column
+// S4/S5 (MMH) and S7 (MH) tail after crt_coeffs.  A CTA (ticket order) owns kCarryTile
+// output words [u0, u1).  For each chunk of the ring it stages the exact coefficients
+// (from crt_coeffs) whose pieces meet its words in shared memory, forms the 64-bit column
 // sums S_u of its words (RING: pieces cut at bit gamma, high parts land at bit 0 -- the
 // Mersenne fold of PAPER.md:130-132 per coefficient; LINEAR: plus the addend c), then
 // resolves the carries: digit d_u = lo32(S_u) + hi32(S_{u-1}) inside the tile, binary
@@ -388,44 +311,6 @@ __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict_
 // propagate) publishes C_out before waiting for its predecessor, so the chain is
 // almost never serial.  RING: the last CTA to finish runs the Mersenne finish.
 // state: [0] ticket, [1] done counter, [2 + t] tile t: bit 31 ready, bits 0..30 C_out.
-template <int P>
-__device__ __forceinline__ void crt_one(const uint32_t *__restrict__ res, uint32_t L, uint32_t j, const CrtK &K,
-                                        uint32_t *out, int stride) {
-    uint32_t y[P];
-    uint64_t slo = 1ull << 40, shi = 0;
-#pragma unroll
-    for (int i = 0; i < P; i++) {
-        const uint32_t r = res[(size_t)i * L + j];
-        y[i] = red1p(mul_mont(r, K.qinv[i], K.p[i], K.pinv[i]), K.p[i]);
-        const uint64_t q = (uint64_t)y[i] * K.G[i];
-        slo += q;
-        shi += (slo < q);
-    }
-    const uint32_t k = (uint32_t)shi;
-    uint64_t acc[P + 1];
-#pragma unroll
-    for (int w = 0; w <= P; w++) acc[w] = 0;
-#pragma unroll
-    for (int i = 0; i < P; i++)
-#pragma unroll
-        for (int w = 0; w < P; w++) {
-            const uint64_t t = mad_wide(y[i], K.MI[i][w], 0ull);
-            acc[w] += (uint32_t)t;
-            acc[w + 1] += t >> 32;
-        }
-    uint64_t carry = 0;
-    int64_t borrow = 0;
-#pragma unroll
-    for (int w = 0; w < P; w++) {
-        const uint64_t v = acc[w] + carry;
-        carry = v >> 32;
-        const uint64_t km = (uint64_t)k * K.M[w];
-        const int64_t d = (int64_t)(uint32_t)v - (int64_t)(uint32_t)km + borrow;
-        out[w * stride] = (uint32_t)d;
-        borrow = (d >> 32) - (int64_t)(km >> 32);
-    }
-}
-
 // bits [off, off + 32) of a coefficient held in shared memory (P words at stride 1)
 template <int P>
 __device__ __forceinline__ uint32_t coef_window_s(const uint32_t *c, int off, int len) {
@@ -448,8 +333,8 @@ template <int P>
 __host__ __device__ constexpr int crt_cstride() { return P | 1; }                 // odd stride: fewer bank conflicts
 
 template <int P, bool RING>
-__global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
-                                                     uint32_t B, uint32_t gamma, const CrtK K,
+__global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict__ coefT, uint32_t L, uint32_t ncoef,
+                                                     uint32_t B, uint32_t gamma,
                                                      const uint32_t *__restrict__ addend, uint32_t n_addend,
                                                      uint32_t *__restrict__ out, uint32_t W, uint32_t cap,
                                                      uint32_t *state, uint32_t Wfin) {
@@ -484,7 +369,23 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
         if (jb < ja || jb == 0xFFFFFFFFu) continue;           // uniform
         const uint32_t cnt = min(jb - ja + 1, cap);
         __syncthreads();
-        for (uint32_t q = threadIdx.x; q < cnt; q += blockDim.x) crt_one<P>(res, L, ja + q, K, sc + q * CS, 1);
+        {
+            // stage cnt x P words; a thread issues 8 independent loads before its stores
+            const uint32_t tot = cnt * P;
+            for (uint32_t b0 = threadIdx.x; b0 < tot; b0 += 8 * blockDim.x) {
+                uint32_t v[8], dst[8];
+#pragma unroll
+                for (int q8 = 0; q8 < 8; q8++) {
+                    const uint32_t i = b0 + q8 * blockDim.x;
+                    const uint32_t w = i / cnt, q = i - w * cnt;
+                    dst[q8] = q * CS + w;
+                    v[q8] = (i < tot) ? __ldg(coefT + (size_t)w * ncoef + ja + q) : 0u;
+                }
+#pragma unroll
+                for (int q8 = 0; q8 < 8; q8++)
+                    if (b0 + q8 * blockDim.x < tot) sc[dst[q8]] = v[q8];
+            }
+        }
         __syncthreads();
 #pragma unroll
         for (int v = 0; v < kCarryV; v++) {
@@ -522,7 +423,8 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
 #pragma unroll
                 for (int v = 0; v < kCarryV; v++) need |= (32 * (ub + v) < cbits + 32);
                 if (!need) continue;
-                crt_one<P>(res, L, (uint32_t)j, K, tmp, 1);
+#pragma unroll
+                for (int w = 0; w < P; w++) tmp[w] = coefT[(size_t)w * ncoef + j];
 #pragma unroll
                 for (int v = 0; v < kCarryV; v++) {
                     const uint32_t me = 32 * (ub + v);

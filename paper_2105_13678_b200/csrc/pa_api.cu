@@ -3,14 +3,16 @@
 // stream-ordered orchestration of the sm_100a kernels of one hash.
 //
 // Hot path of one pa_hash (Algorithm 1), all on the ctx stream:
-//   S1+S2  col_pass<KEY>   pack key blocks into B-bit limbs, residues mod P primes,
-//                          first (column) NTT pass, four-step twiddle
-//   S2+S3  row_pass<MAC>   second NTT pass, multiply by the precomputed
-//                          transforms of a_i and accumulate over blocks
+//   S1     pack_key_residues  key blocks -> B-bit limbs -> residues mod P primes
+//   S2     col_pass<FWD>   first (column) NTT pass, four-step twiddle
+//   S2+S3  row_mac         second NTT pass, multiply by the precomputed transforms of
+//                          the a_i and accumulate over blocks (bulk-copy pipeline)
 //   S4     row_pass<INV>, col_pass<INV>   one inverse transform for all blocks
-//          crt_colsum + carry_{tiles,scan,apply}   exact Y = sum_i a_i x_i
-//   S5     fold_colsum + carry, fold_final x2, canonical zero  -> y = Y mod p
-//   S7     col_pass<WORDS>(y), row_pass<MAC>(B^), inverse, crt_colsum(+c), carry,
+//          crt_coeffs (exact coefficients) + crt_carry (column sums on the gamma-bit
+//          ring, carries with look-back)                  exact Y = sum_i a_i x_i
+//   S5     inside crt_carry: ring fold per coefficient, last CTA: residual fold and
+//          canonical zero                                 -> y = Y mod p
+//   S7     pack(y), col_pass, row_mac(B^), inverse, crt_coeffs + crt_carry (+c, linear),
 //          mh_extract -> out_bits = top m bits of (b y + c) mod 2^alpha
 #include <cuda_runtime.h>
 
@@ -448,17 +450,6 @@ static int launch_row(int slog, const RowArgs &A, cudaStream_t st) {
     return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
 }
 
-template <int P, bool RING>
-static int launch_crt_t(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
-                        const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint64_t *S, uint32_t W,
-                        cudaStream_t st) {
-    crt_coeffs<P><<<(ncoef + 127) / 128, 128, 0, st>>>(res, sd.L, ncoef, sd.crt, coef);
-    CUDA_TRY(cudaGetLastError());
-    crt_colsum<P, RING><<<(W + 255) / 256, 256, 0, st>>>(coef, ncoef, sd.pl.limb_bits, gamma, addend, n_addend, S, W);
-    CUDA_TRY(cudaGetLastError());
-    return PA_OK;
-}
-
 template <int S_LOG>
 static int launch_mac_t(const MacArgs &A, cudaStream_t st) {
     constexpr int E_LOG = 5;
@@ -491,11 +482,13 @@ static int launch_mac(int slog, const MacArgs &A, cudaStream_t st) {
 
 template <int P, bool RING>
 static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
-                              const uint32_t *addend, uint32_t n_addend, uint32_t *out, uint32_t W, uint32_t *state,
-                              uint32_t Wfin, cudaStream_t st) {
+                              const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint32_t *out, uint32_t W,
+                              uint32_t *state, uint32_t Wfin, cudaStream_t st) {
     const uint32_t B = sd.pl.limb_bits;
     const uint32_t cap = (32u * kCarryTile + 32u * P) / B + 3;
     const size_t smem = (size_t)cap * crt_cstride<P>() * 4;
+    crt_coeffs<P><<<(ncoef + 127) / 128, 128, 0, st>>>(res, sd.L, ncoef, sd.crt, coef);
+    CUDA_TRY(cudaGetLastError());
     auto fn = crt_carry<P, RING>;
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
@@ -503,7 +496,7 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
         smem_set = smem;
     }
     const uint32_t ntiles = (W + kCarryTile - 1) / kCarryTile;
-    fn<<<ntiles, kCarryT, smem, st>>>(res, sd.L, ncoef, B, (uint32_t)gamma, sd.crt, addend, n_addend, out, W, cap,
+    fn<<<ntiles, kCarryT, smem, st>>>(coef, sd.L, ncoef, B, (uint32_t)gamma, addend, n_addend, out, W, cap,
                                       state, Wfin);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
@@ -511,10 +504,10 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
 
 template <bool RING>
 static int launch_crt_carry(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
-                            const uint32_t *addend, uint32_t n_addend, uint32_t *out, uint32_t W, uint32_t *state,
-                            uint32_t Wfin, cudaStream_t st) {
+                            const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint32_t *out, uint32_t W,
+                            uint32_t *state, uint32_t Wfin, cudaStream_t st) {
 #define PA_CC_CASE(P) \
-    case P: return launch_crt_carry_t<P, RING>(res, sd, ncoef, gamma, addend, n_addend, out, W, state, Wfin, st);
+    case P: return launch_crt_carry_t<P, RING>(res, sd, ncoef, gamma, addend, n_addend, coef, out, W, state, Wfin, st);
     switch (sd.pl.nprimes) {
         PA_CC_CASE(2) PA_CC_CASE(3) PA_CC_CASE(4) PA_CC_CASE(5) PA_CC_CASE(6) PA_CC_CASE(7) PA_CC_CASE(8)
         PA_CC_CASE(9) PA_CC_CASE(10) PA_CC_CASE(11) PA_CC_CASE(12) PA_CC_CASE(13) PA_CC_CASE(14)
@@ -524,20 +517,6 @@ static int launch_crt_carry(const uint32_t *res, const StageDev &sd, uint32_t nc
     return set_err(PA_E_PARAM, "unsupported prime count %u", sd.pl.nprimes);
 }
 
-template <bool RING>
-static int launch_crt(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
-                      const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint64_t *S, uint32_t W,
-                      cudaStream_t st) {
-#define PA_CRT_CASE(P) \
-    case P: return launch_crt_t<P, RING>(res, sd, ncoef, gamma, addend, n_addend, coef, S, W, st);
-    switch (sd.pl.nprimes) {
-        PA_CRT_CASE(2) PA_CRT_CASE(3) PA_CRT_CASE(4) PA_CRT_CASE(5) PA_CRT_CASE(6) PA_CRT_CASE(7) PA_CRT_CASE(8)
-        PA_CRT_CASE(9) PA_CRT_CASE(10) PA_CRT_CASE(11) PA_CRT_CASE(12) PA_CRT_CASE(13) PA_CRT_CASE(14)
-        PA_CRT_CASE(15) PA_CRT_CASE(16)
-    }
-#undef PA_CRT_CASE
-    return set_err(PA_E_PARAM, "unsupported prime count %u", sd.pl.nprimes);
-}
 
 // ====================================================================== context
 struct ProfRec {
@@ -975,9 +954,9 @@ static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
                         "mmh_pack", "mmh_fwd_col", "mmh_fwd_row_mac", "mmh_inverse"));
     {
         ProfScope ps(c, "mmh_crt_carry_fold");
-        TRY(launch_crt_carry<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->y1,
+        TRY(launch_crt_carry<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->coef, c->y1,
                                    (uint32_t)c->W_fold, next_state(c), (uint32_t)c->W_fold, c->stream));
-        c->launches++;
+        c->launches += 2;
     }
     *y_out = c->y1;
     return PA_OK;
@@ -994,9 +973,9 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     {
         ProfScope ps(c, "mh_crt_carry_extract");
         const uint64_t ncoef = std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1);
-        TRY(launch_crt_carry<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->Z, W, next_state(c), 0,
-                                    c->stream));
-        c->launches++;
+        TRY(launch_crt_carry<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->coef, c->Z, W,
+                                    next_state(c), 0, c->stream));
+        c->launches += 2;
         const uint64_t nb = cdiv(p.m, 8), nw = cdiv(nb, 4);
         mh_extract<<<(uint32_t)cdiv(nw, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
         c->launches++;

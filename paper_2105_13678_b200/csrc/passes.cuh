@@ -200,7 +200,7 @@ constexpr int kPackT = 256;
 template <int NW>
 __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeK *__restrict__ pk, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
-    constexpr int MAXW = (kPackT * 4 * NW) / 4 + 4;        // staged words (LB <= 4 NW bytes per limb)
+    constexpr int MAXW = kPackT * NW + 4;                     // staged words (LB <= 4 NW bytes per limb)
     __shared__ uint32_t sw[MAXW];
     __shared__ PrimeK ks[kMaxPrimes];
     for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) ks[i] = pk[i];
@@ -208,32 +208,51 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     const uint32_t jt0 = blockIdx.x * kPackT;
     const int64_t start = (int64_t)iv * s.blk_bytes;
     const int64_t end = start + s.blk_bytes;
-    const int64_t LB = s.limb_bytes;
+    const int LB = (int)s.limb_bytes;
     const uint32_t jt1 = min(jt0 + kPackT, s.wx);           // limbs with data in this tile
-    int64_t tlo = end - LB * (int64_t)jt1 - 4;               // lowest byte any word may touch
+    int64_t tlo = end - (int64_t)LB * jt1 - 4;               // lowest byte any word may touch
     if (tlo < start - 4) tlo = start - 4;
-    const int64_t gw0 = tlo >> 2;                           // floor
-    const int64_t thi = end - LB * (int64_t)jt0;
+    const int64_t gw0 = tlo >> 2;                            // floor
+    const int64_t thi = end - (int64_t)LB * jt0;
     const int nw = (jt0 < jt1) ? (int)(((thi + 3) >> 2) - gw0 + 1) : 0;
-    for (int k = threadIdx.x; k < nw && k < MAXW; k += blockDim.x) sw[k] = key_word(s, gw0 + k);
+    // interior tiles: plain aligned word loads; tiles touching the key's ends: key_word
+    const bool interior = s.aligned && gw0 >= 0 && (gw0 + nw + 1) * 4 < (int64_t)s.nbytes;
+    const uint32_t *kw = reinterpret_cast<const uint32_t *>(s.key) + (interior ? gw0 : 0);
+    // all of a thread's loads are issued before its stores (no load->store serialisation)
+    constexpr int KU = (MAXW + kPackT - 1) / kPackT;
+    {
+        uint32_t v[KU];
+#pragma unroll
+        for (int u = 0; u < KU; u++) {
+            const int k = threadIdx.x + u * kPackT;
+            v[u] = (k < nw) ? (interior ? __ldg(kw + k) : key_word(s, gw0 + k)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < KU; u++) {
+            const int k = threadIdx.x + u * kPackT;
+            if (k < nw) sw[k] = v[u];
+        }
+    }
     __syncthreads();
     const uint32_t j = jt0 + threadIdx.x;
     if (j >= wxp) return;
     uint32_t w[NW];
     uint32_t any = 0;
     if (j < s.wx) {
-        const int64_t hi = end - LB * (int64_t)j;
-        int64_t lo = hi - LB;
-        if (lo < start) lo = start;
+        // byte offsets relative to the staged base 4 gw0 (all < 4 MAXW)
+        const int base = (int)(4 * gw0 - start);
+        const int hi = (int)(s.blk_bytes - (uint32_t)LB * j) - base;
+        int lo = hi - LB;
+        if (lo < -base) lo = -base;                           // block start
 #pragma unroll
         for (int i = 0; i < NW; i++) {
-            const int64_t pos = hi - 4 * (i + 1);
-            const int64_t wi = (pos >> 2) - gw0;
-            const int sh = (int)(pos & 3) * 8;
-            const uint32_t a0 = (wi >= 0 && wi < nw) ? sw[wi] : 0u;
-            const uint32_t a1 = (wi + 1 >= 0 && wi + 1 < nw) ? sw[wi + 1] : 0u;
+            const int pos = hi - 4 * (i + 1);
+            const int wi = pos >> 2;
+            const int sh = (pos & 3) * 8;
+            const uint32_t a0 = (wi >= 0) ? sw[wi] : 0u;
+            const uint32_t a1 = (wi + 1 >= 0) ? sw[wi + 1] : 0u;
             uint32_t v = __byte_perm(__funnelshift_r(a0, a1, sh), 0, 0x0123);
-            const int64_t below = lo - pos;
+            const int below = lo - pos;
             if (below >= 4) v = 0;
             else if (below > 0) v &= 0xFFFFFFFFu >> (8 * below);
             w[i] = v;
