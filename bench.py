@@ -235,6 +235,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--limb-bits", type=int, default=0, help="force the limb width B (0 = planner)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -265,7 +266,8 @@ def main():
     key_full = key_bytes(w.n, w.key_seed)
     lo, hi = key_slice_bytes(w.n, w.r, (b0, b1))
     key_dev = torch.from_numpy(key_full[lo:hi].copy()).to(dev)
-    ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None)
+    ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None,
+                    limb_bits=args.limb_bits)
     info = ctx.query()
     out = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)

@@ -330,10 +330,13 @@ __device__ __forceinline__ uint32_t coef_window_s(const uint32_t *c, int off, in
 }
 
 template <int P>
-__host__ __device__ constexpr int crt_cstride() { return P | 1; }                 // odd stride: fewer bank conflicts
+__host__ __device__ constexpr int crt_cstride() { return P | 1; }
+constexpr int kCCV = 4;                        // words per thread in crt_carry
+constexpr int kCCT = 256;                      // threads per tile
+constexpr int kCCTile = kCCV * kCCT;                 // odd stride: fewer bank conflicts
 
-template <int P, bool RING>
-__global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict__ coefT, uint32_t L, uint32_t ncoef,
+template <int P, bool RING, int DBG = 0>
+__global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ coefT, uint32_t L, uint32_t ncoef,
                                                      uint32_t B, uint32_t gamma,
                                                      const uint32_t *__restrict__ addend, uint32_t n_addend,
                                                      uint32_t *__restrict__ out, uint32_t W, uint32_t cap,
@@ -342,21 +345,21 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
     constexpr int CS = crt_cstride<P>();
     constexpr uint32_t cbits = 32 * P;
     __shared__ uint32_t s_tile, s_cin, s_c1, s_last;
-    __shared__ uint32_t s_hi[kCarryT];
+    __shared__ uint32_t s_hi[kCCT];
     if (threadIdx.x == 0) s_tile = atomicAdd(&state[0], 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
-    const uint32_t u0 = tile * kCarryTile;
-    const uint32_t ub = u0 + threadIdx.x * kCarryV;            // this thread's first word
-    uint64_t S[kCarryV];
+    const uint32_t u0 = tile * kCCTile;
+    const uint32_t ub = u0 + threadIdx.x * kCCV;            // this thread's first word
+    uint64_t S[kCCV];
 #pragma unroll
-    for (int v = 0; v < kCarryV; v++) {
+    for (int v = 0; v < kCCV; v++) {
         const uint32_t u = ub + v;
         S[v] = (!RING && addend && u < n_addend) ? addend[u] : 0ull;
     }
     // ---- column sums, chunk by chunk
-    const uint32_t nchunks = RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
-    const uint32_t tb0 = 32 * u0, tb1 = 32 * min(u0 + kCarryTile, W);   // tile bits
+    const uint32_t nchunks = (DBG & 8) ? 0u : RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
+    const uint32_t tb0 = 32 * u0, tb1 = 32 * min(u0 + kCCTile, W);   // tile bits
     for (uint32_t t = 0; t < nchunks; t++) {
         const uint32_t base = RING ? t * gamma : 0u;
         const uint32_t jc0 = (base + B - 1) / B;
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
         __syncthreads();
         {
             // stage cnt x P words; a thread issues 8 independent loads before its stores
-            const uint32_t tot = cnt * P;
+            const uint32_t tot = (DBG & 1) ? 0u : cnt * P;
             for (uint32_t b0 = threadIdx.x; b0 < tot; b0 += 8 * blockDim.x) {
                 uint32_t v[8], dst[8];
 #pragma unroll
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
         }
         __syncthreads();
 #pragma unroll
-        for (int v = 0; v < kCarryV; v++) {
+        for (int v = 0; v < kCCV; v++) {
             const uint32_t u = ub + v;
             if (u >= W) continue;
             const uint32_t me = 32 * u;
@@ -421,12 +424,12 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
                 const int cut = (int)((int64_t)gamma - pos);
                 bool need = false;
 #pragma unroll
-                for (int v = 0; v < kCarryV; v++) need |= (32 * (ub + v) < cbits + 32);
+                for (int v = 0; v < kCCV; v++) need |= (32 * (ub + v) < cbits + 32);
                 if (!need) continue;
 #pragma unroll
                 for (int w = 0; w < P; w++) tmp[w] = coefT[(size_t)w * ncoef + j];
 #pragma unroll
-                for (int v = 0; v < kCarryV; v++) {
+                for (int v = 0; v < kCCV; v++) {
                     const uint32_t me = 32 * (ub + v);
                     if (ub + v < W && me < cbits + 32) S[v] += coef_window_s<P>(tmp, (int)me + cut, (int)cbits);
                 }
@@ -434,13 +437,13 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
         }
     }
     // ---- carries inside the tile (cin of word u0 handled separately, see above)
-    uint32_t w[kCarryV];
+    uint32_t w[kCCV];
     uint32_t gm = 0, pm = 0;
-    s_hi[threadIdx.x] = (uint32_t)(S[kCarryV - 1] >> 32);
+    s_hi[threadIdx.x] = (uint32_t)(S[kCCV - 1] >> 32);
     __syncthreads();
     uint32_t hprev = threadIdx.x ? s_hi[threadIdx.x - 1] : 0u;
 #pragma unroll
-    for (int v = 0; v < kCarryV; v++) {
+    for (int v = 0; v < kCCV; v++) {
         const uint32_t u = ub + v;
         const uint64_t t = (S[v] & 0xFFFFFFFFull) + hprev;
         hprev = (uint32_t)(S[v] >> 32);
@@ -451,12 +454,12 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
     }
     uint32_t G = 0;
 #pragma unroll
-    for (int v = 0; v < kCarryV; v++) G = ((gm >> v) & 1u) | (((pm >> v) & 1u) & G);
-    const int Pall = (pm == (1u << kCarryV) - 1u);
+    for (int v = 0; v < kCCV; v++) G = ((gm >> v) & 1u) | (((pm >> v) & 1u) & G);
+    const int Pall = (pm == (1u << kCCV) - 1u);
     const int allp = __syncthreads_and(Pall);
     uint32_t bg;
     (void)block_carries((int)G, Pall, 0, &bg);
-    const uint32_t hi_last = s_hi[kCarryT - 1];               // hi32 of the tile's last sum
+    const uint32_t hi_last = s_hi[kCCT - 1];               // hi32 of the tile's last sum
     volatile uint32_t *vs = state + 2;
     if (threadIdx.x == 0) {
         const bool indep = bg || !allp;
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
             vs[tile] = 0x80000000u | cout_indep;
         }
         uint32_t cin = 0;
-        if (tile > 0) {
+        if (tile > 0 && !(DBG & 2)) {
             uint32_t st;
             while (!((st = vs[tile - 1]) & 0x80000000u)) { }
             cin = st & 0x7FFFFFFFu;
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
     const uint32_t cin = s_cin;
     uint32_t c = block_carries((int)G, Pall, s_c1, nullptr);
 #pragma unroll
-    for (int v = 0; v < kCarryV; v++) {
+    for (int v = 0; v < kCCV; v++) {
         const uint32_t u = ub + v;
         const bool first = (threadIdx.x == 0 && v == 0);
         if (first) {
@@ -493,11 +496,11 @@ __global__ void __launch_bounds__(kCarryT) crt_carry(const uint32_t *__restrict_
         if (u < W) out[u] = w[v] + c;
         c = ((gm >> v) & 1u) | (((pm >> v) & 1u) & c);
     }
-    if (RING) {
+    if (RING && !(DBG & 4)) {
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
-            const uint32_t ntiles = (W + kCarryTile - 1) / kCarryTile;
+            const uint32_t ntiles = (W + kCCTile - 1) / kCCTile;
             s_last = (atomicAdd(&state[1], 1u) == ntiles - 1);
         }
         __syncthreads();

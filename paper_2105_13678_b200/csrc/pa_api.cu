@@ -74,6 +74,7 @@ extern "C" int pa_last_error(char *buf, size_t len) {
 static constexpr int kMinLog2L = 10;
 static constexpr int kMaxLog2L = 23;
 static constexpr int kColMaxLog = 9;
+static constexpr int kMaxRowLog = 14;
 static constexpr int kMaxLimbBits = 256;
 
 static double log2_bound(uint64_t nterms, uint64_t overlap, uint32_t B) {
@@ -84,7 +85,10 @@ static double log2_bound(uint64_t nterms, uint64_t overlap, uint32_t B) {
 // Choose (B, P, L) for the product of an `abits`-bit and a `bbits`-bit operand, summed
 // over `nterms` products; only coefficients below `need_coef` limbs... (all are needed:
 // the cyclic length must cover the full product so nothing wraps).
-static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int force_B, pa_stage_plan *out) {
+// nvec: vectors transformed per hash (blocks for MMH, 1 for MH).  A single vector gets a
+// short column (many column groups, many row units) so the passes fill the GPU.
+static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int force_B, uint64_t nvec,
+                        pa_stage_plan *out) {
     // B <= 56: one 64-bit limb (limb_redc); larger B: multiword limbs (<= 8 words)
     double best = 1e300;
     pa_stage_plan bp{};
@@ -110,7 +114,8 @@ static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int for
             bp.limb_bits = B;
             bp.nprimes = P;
             bp.log2_len = (uint32_t)lg;
-            const int cl = std::min(kColMaxLog, lg / 2);
+            int cl = std::min(kColMaxLog, lg / 2);
+            if (nvec < 8) cl = std::max(std::min(cl, 7), lg - kMaxRowLog);
             bp.n_col = 1u << cl;
             bp.n_row = 1u << (lg - cl);
             for (uint32_t i = 0; i < P; i++) bp.primes[i] = ps[i];
@@ -159,9 +164,9 @@ static int make_plan(const pa_params *prm, Plan *P) {
     if (p.b0 == 0 && p.b1 == 0) p.b1 = p.k;
     if (p.b0 >= p.b1 || p.b1 > p.k) return set_err(PA_E_PARAM, "bad shard [%llu, %llu) of %llu blocks",
                                                   (unsigned long long)p.b0, (unsigned long long)p.b1, (unsigned long long)p.k);
-    if (plan_product(p.r, p.gamma, p.b1 - p.b0, p.force_B, &p.mmh) != PA_OK)
+    if (plan_product(p.r, p.gamma, p.b1 - p.b0, p.force_B, p.b1 - p.b0, &p.mmh) != PA_OK)
         return set_err(PA_E_BOUND, "no transform plan covers the MMH coefficient bound");
-    if (plan_product(p.gamma, p.alpha, 1, p.force_B, &p.mh) != PA_OK)
+    if (plan_product(p.gamma, p.alpha, 1, p.force_B, 1, &p.mh) != PA_OK)
         return set_err(PA_E_BOUND, "no transform plan covers the MH product");
     *P = p;
     return PA_OK;
@@ -485,7 +490,7 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
                               const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint32_t *out, uint32_t W,
                               uint32_t *state, uint32_t Wfin, cudaStream_t st) {
     const uint32_t B = sd.pl.limb_bits;
-    const uint32_t cap = (32u * kCarryTile + 32u * P) / B + 3;
+    const uint32_t cap = (32u * kCCTile + 32u * P) / B + 3;
     const size_t smem = (size_t)cap * crt_cstride<P>() * 4;
     crt_coeffs<P><<<(ncoef + 127) / 128, 128, 0, st>>>(res, sd.L, ncoef, sd.crt, coef);
     CUDA_TRY(cudaGetLastError());
@@ -495,8 +500,8 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
         CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         smem_set = smem;
     }
-    const uint32_t ntiles = (W + kCarryTile - 1) / kCarryTile;
-    fn<<<ntiles, kCarryT, smem, st>>>(coef, sd.L, ncoef, B, (uint32_t)gamma, addend, n_addend, out, W, cap,
+    const uint32_t ntiles = (W + kCCTile - 1) / kCCTile;
+    fn<<<ntiles, kCCT, smem, st>>>(coef, sd.L, ncoef, B, (uint32_t)gamma, addend, n_addend, out, W, cap,
                                       state, Wfin);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
@@ -803,7 +808,7 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     TRY(c->da.alloc(&c->coef, std::max<size_t>((size_t)Pm * Lm, (size_t)Ph * Lh)));
     TRY(c->da.alloc(&c->y1, c->W_fold));
     TRY(c->da.alloc(&c->Z, c->W_Z));
-    c->cstate_stride = (uint32_t)(cdiv(Smax, kCarryTile) + 2);
+    c->cstate_stride = (uint32_t)(cdiv(Smax, std::min(kCarryTile, kCCTile)) + 2);
     TRY(c->da.alloc(&c->cstate, (size_t)c->cstate_stride * kCarrySlots));
 
     // ---- hash keys (reading A7): a_i for the shard's blocks, b, c
