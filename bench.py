@@ -341,9 +341,21 @@ def main():
             bb.synchronize()
             t.append(a.elapsed_time(bb))
         e2e_ms = statistics.median(t)
+        # the PCIe floor: plain pinned copies of the same bytes (context for the e2e number)
+        kd = torch.empty_like(host_key, device=dev)
+        od = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
+        th2d, td2h = [], []
+        for _ in range(5):
+            a = torch.cuda.Event(enable_timing=True); bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream); kd.copy_(host_key, non_blocking=True); bb.record(stream); bb.synchronize()
+            th2d.append(a.elapsed_time(bb))
+            a.record(stream); host_out.copy_(od, non_blocking=True); bb.record(stream); bb.synchronize()
+            td2h.append(a.elapsed_time(bb))
         e2e = {"value": w.n / (e2e_ms * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": (w.n + 7) // 8, "d2h_bytes_per_step": (w.m + 7) // 8,
-               "api": "pa_hash_host (pinned host buffers, H2D + hash + D2H + sync)"}
+               "api": "pa_hash_host (pinned host buffers, H2D + hash + D2H + sync)",
+               "h2d_copy_ms": min(th2d), "d2h_copy_ms": min(td2h),
+               "h2d_gbs": (w.n + 7) // 8 / (min(th2d) * 1e-3) / 1e9}
 
     if rank != 0:
         if world > 1:

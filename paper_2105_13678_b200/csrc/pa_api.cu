@@ -548,6 +548,8 @@ struct pa_ctx {
     uint32_t cstate_stride = 0;
     int cslot = 0;
     uint8_t *key_dev = nullptr;               // staging for pa_hash_host
+    cudaStream_t copy_stream = nullptr;       // pa_hash_host H2D copies
+    cudaEvent_t copy_ev[9] = {};
     uint8_t *out_dev = nullptr;
     uint64_t Wg = 0, W_ring = 0, W_fold = 0, W_Z = 0, ncoef_mmh = 0;
     uint32_t launches = 0;            // launches of the current / last hash call
@@ -669,25 +671,26 @@ static int launch_pack(const Src &src, uint32_t B, uint32_t grid, const PrimeK *
 }
 
 // ---- pack -> forward column pass -> row pass with MAC -> inverse; residues in acc
+// ---- S1+S2 (first pass) of vectors [0, nvec) of src: pack -> residues -> forward
+// column pass into scratch.  `res` / `scratch` point at the first vector's slots.
 template <class Src>
-static int stage_transform(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec, uint32_t rows,
-                           uint32_t *scratch, const uint32_t *hat, uint32_t *acc,
-                           const char *tag_pack, const char *tag_fwd1, const char *tag_fwd2, const char *tag_inv) {
-    const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
+static int stage_pack_col(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec, uint32_t rows, uint32_t *res,
+                          uint32_t *scratch, const char *tag_pack, const char *tag_fwd1) {
+    const int clog = __builtin_ctz(sd.pl.n_col);
     const uint32_t P = sd.pl.nprimes;
     const uint32_t wxp = rows * sd.pl.n_row;
     {
         ProfScope ps(c, tag_pack);
         const uint64_t total = (uint64_t)nvec * wxp;
         const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
-        TRY(launch_pack(src, sd.pl.limb_bits, grid, sd.pk, P, nvec, wxp, c->res, c->stream));
+        TRY(launch_pack(src, sd.pl.limb_bits, grid, sd.pk, P, nvec, wxp, res, c->stream));
         c->launches++;
     }
     {
         ProfScope ps(c, tag_fwd1);
         ColArgs A{};
         A.nt = ntt_args(sd, 0, 0);
-        A.src = c->res;
+        A.src = res;
         A.rows = rows;
         A.tw4 = sd.tw4[0];
         A.dst = scratch;
@@ -696,45 +699,59 @@ static int stage_transform(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nve
         TRY(launch_col<COL_FWD>(clog, A, c->stream));
         c->launches++;
     }
-    if (!hat) return PA_OK;
-    {
-        ProfScope ps(c, tag_fwd2);
-        CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)P * sd.L * 4, c->stream));
-        MacArgs M{};
-        M.nt = ntt_args(sd, 0, 1);
-        M.src = scratch;
-        M.ahat = hat;
-        M.dst = acc;
-        M.nvec = nvec;
-        M.nunits = (sd.pl.n_col / mac_v_rt(rlog)) * P;
-        TRY(launch_mac(rlog, M, c->stream));
-        c->launches++;
-    }
-    {
-        ProfScope ps(c, tag_inv);
-        RowArgs R{};
-        R.nt = ntt_args(sd, 1, 1);
-        R.src = acc;
-        R.dst = acc;
-        R.tw4 = sd.tw4[1];
-        R.nvec = 1;
-        TRY(launch_row<ROW_INV>(rlog, R, c->stream));
-        ColArgs A{};
-        A.nt = ntt_args(sd, 1, 0);
-        A.src = acc;
-        A.dst = acc;
-        A.nvec = 1;
-        A.units = (sd.pl.n_row / 32) * P;
-        TRY(launch_col<COL_INV>(clog, A, c->stream));
-        c->launches += 2;
-    }
+    return PA_OK;
+}
+
+// ---- S2 (second pass) + S3 for vectors [0, nvec) (pointers at the first vector):
+// acc (+)= sum_i X_i (.) hat_i.  only: the single accumulation (balanced split, red.add
+// into zeroed acc); else first / later call of a multi-call accumulation (whole units per
+// CTA, store / modular read-modify-write, no atomics).
+static int stage_mac(pa_ctx *c, StageDev &sd, uint32_t nvec, const uint32_t *scratch, const uint32_t *hat,
+                     uint32_t *acc, bool first, const char *tag, bool only = true) {
+    const int rlog = __builtin_ctz(sd.pl.n_row);
+    const uint32_t P = sd.pl.nprimes;
+    ProfScope ps(c, tag);
+    if (only) CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)P * sd.L * 4, c->stream));
+    MacArgs M{};
+    M.mode = only ? 0u : (first ? 1u : 2u);
+    M.nt = ntt_args(sd, 0, 1);
+    M.src = scratch;
+    M.ahat = hat;
+    M.dst = acc;
+    M.nvec = nvec;
+    M.nunits = (sd.pl.n_col / mac_v_rt(rlog)) * P;
+    TRY(launch_mac(rlog, M, c->stream));
+    c->launches++;
+    return PA_OK;
+}
+
+// ---- S4: one inverse transform of acc (in place, natural order, canonical residues)
+static int stage_inverse(pa_ctx *c, StageDev &sd, uint32_t *acc, const char *tag) {
+    const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
+    const uint32_t P = sd.pl.nprimes;
+    ProfScope ps(c, tag);
+    RowArgs R{};
+    R.nt = ntt_args(sd, 1, 1);
+    R.src = acc;
+    R.dst = acc;
+    R.tw4 = sd.tw4[1];
+    R.nvec = 1;
+    TRY(launch_row<ROW_INV>(rlog, R, c->stream));
+    ColArgs A{};
+    A.nt = ntt_args(sd, 1, 0);
+    A.src = acc;
+    A.dst = acc;
+    A.nvec = 1;
+    A.units = (sd.pl.n_row / 32) * P;
+    TRY(launch_col<COL_INV>(clog, A, c->stream));
+    c->launches += 2;
     return PA_OK;
 }
 
 // ---- precompute transforms of word vectors (a_i or b) into hat (Montgomery, x 1/L)
 static int precompute_hat(pa_ctx *c, StageDev &sd, const WordSrc &ws, uint32_t nvec, uint32_t rows,
                           uint32_t *scratch, uint32_t *hat) {
-    TRY(stage_transform(c, sd, WordLimbs{ws}, nvec, rows, scratch, nullptr, nullptr, "pre_pack", "pre_col", "", ""));
+    TRY(stage_pack_col(c, sd, WordLimbs{ws}, nvec, rows, c->res, scratch, "pre_pack", "pre_col"));
     RowArgs R{};
     R.nt = ntt_args(sd, 0, 1);
     R.src = scratch;
@@ -916,6 +933,11 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->evpool) cudaEventDestroy(e);
     if (c->key_dev) cudaFree(c->key_dev);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        for (auto e : c->copy_ev) if (e) cudaEventDestroy(e);
+        cudaStreamDestroy(c->copy_stream);
+    }
     if (c->out_dev) cudaFree(c->out_dev);
     c->da.free_all();
     delete c;
@@ -941,22 +963,43 @@ extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
 }
 
 // ---- S1-S5 on this ctx's blocks -> canonical y in the returned buffer (Wg words)
-static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
+// key source of this ctx's blocks [v0, v1) (shard-relative), key_slice = the shard's bytes
+static KeySrc key_src(const pa_ctx *c, const uint8_t *key_slice, uint32_t v0, uint32_t v1) {
     const Plan &p = c->pl;
     const uint64_t total_bytes = cdiv(p.n, 8);
-    const uint64_t off = p.b0 * (p.r / 8);
-    const uint64_t nbytes = std::min<uint64_t>(total_bytes - std::min(off, total_bytes), (p.b1 - p.b0) * (p.r / 8));
+    const uint64_t R = p.r / 8;
+    const uint64_t off = (p.b0 + v0) * R;                       // global byte offset of block v0
+    const uint64_t nbytes = std::min<uint64_t>(total_bytes - std::min(off, total_bytes), (uint64_t)(v1 - v0) * R);
     KeySrc ks{};
-    ks.key = key_slice;
+    ks.key = key_slice + (uint64_t)v0 * R;
     ks.nbytes = nbytes;
     const bool has_last = (off + nbytes == total_bytes);      // bits >= n ignored
     ks.last_mask = (has_last && (p.n % 8)) ? ((0xFFu << (8 - p.n % 8)) & 0xFFu) : 0xFFu;
-    ks.blk_bytes = (uint32_t)(p.r / 8);
+    ks.blk_bytes = (uint32_t)R;
     ks.limb_bytes = p.mmh.limb_bits / 8;
     ks.wx = (uint32_t)cdiv(p.r, p.mmh.limb_bits);
-    ks.aligned = (((uintptr_t)key_slice) & 3) == 0;
-    TRY(stage_transform(c, c->smmh, KeyLimbs{ks}, c->nblk, c->rows_mmh, c->scratch, c->ahat, c->acc,
-                        "mmh_pack", "mmh_fwd_col", "mmh_fwd_row_mac", "mmh_inverse"));
+    ks.aligned = (((uintptr_t)ks.key) & 3) == 0;
+    return ks;
+}
+
+// ---- S1+S2 first pass for blocks [v0, v1) of the shard
+static int mmh_forward(pa_ctx *c, const uint8_t *key_slice, uint32_t v0, uint32_t v1) {
+    const uint32_t P = c->pl.mmh.nprimes;
+    const size_t wxp = (size_t)c->rows_mmh * c->pl.mmh.n_row;
+    return stage_pack_col(c, c->smmh, KeyLimbs{key_src(c, key_slice, v0, v1)}, v1 - v0, c->rows_mmh,
+                          c->res + (size_t)v0 * P * wxp, c->scratch + (size_t)v0 * P * c->smmh.L, "mmh_pack",
+                          "mmh_fwd_col");
+}
+
+static int mmh_mac(pa_ctx *c, uint32_t v0, uint32_t v1, bool first, bool only) {
+    const size_t off = (size_t)v0 * c->pl.mmh.nprimes * c->smmh.L;
+    return stage_mac(c, c->smmh, v1 - v0, c->scratch + off, c->ahat + off, c->acc, first, "mmh_fwd_row_mac", only);
+}
+
+// ---- S4+S5 after all blocks are accumulated -> canonical y
+static int mmh_tail(pa_ctx *c, uint32_t **y_out) {
+    const Plan &p = c->pl;
+    TRY(stage_inverse(c, c->smmh, c->acc, "mmh_inverse"));
     {
         ProfScope ps(c, "mmh_crt_carry_fold");
         TRY(launch_crt_carry<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->coef, c->y1,
@@ -967,13 +1010,21 @@ static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
     return PA_OK;
 }
 
+// ---- S1-S5 on this ctx's blocks -> canonical y in the returned buffer (Wg words)
+static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
+    TRY(mmh_forward(c, key_slice, 0, c->nblk));
+    TRY(mmh_mac(c, 0, c->nblk, true, true));
+    return mmh_tail(c, y_out);
+}
+
 // ---- S7 on canonical y -> out_bits
 static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     const Plan &p = c->pl;
     const uint32_t Bh = p.mh.limb_bits;
     WordSrc ws{y, (uint32_t)c->Wg, Bh, (uint32_t)cdiv(p.gamma, Bh)};
-    TRY(stage_transform(c, c->smh, WordLimbs{ws}, 1, c->rows_mh, c->scratch_mh, c->bhat, c->acc_mh,
-                        "mh_pack", "mh_fwd_col", "mh_fwd_row_mac", "mh_inverse"));
+    TRY(stage_pack_col(c, c->smh, WordLimbs{ws}, 1, c->rows_mh, c->res, c->scratch_mh, "mh_pack", "mh_fwd_col"));
+    TRY(stage_mac(c, c->smh, 1, c->scratch_mh, c->bhat, c->acc_mh, true, "mh_fwd_row_mac"));
+    TRY(stage_inverse(c, c->smh, c->acc_mh, "mh_inverse"));
     const uint32_t W = (uint32_t)c->W_Z;
     {
         ProfScope ps(c, "mh_crt_carry_extract");
@@ -1029,13 +1080,49 @@ extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8
     return rc;
 }
 
+// End-to-end hash from host buffers.  The key is copied in kCopyGroups block groups on a
+// copy stream; the pack, both forward passes and the multiply-accumulate of group g start
+// as soon as group g has landed (stream-ordered by events), so the PCIe transfer overlaps
+// the MMH transforms.
+static constexpr int kCopyGroups = 8;
+
 extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
     if (!c || !key_host || !out_host) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
     if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
     if (!c->out_dev) CUDA_TRY(cudaMalloc(&c->out_dev, mb));
-    CUDA_TRY(cudaMemcpyAsync(c->key_dev, key_host, nb, cudaMemcpyHostToDevice, c->stream));
-    TRY(pa_hash(c, c->key_dev, c->out_dev));
+    if (!c->copy_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
+    }
+    // the copies may overwrite key_dev only after earlier work on the ctx stream is done
+    CUDA_TRY(cudaEventRecord(c->copy_ev[kCopyGroups], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[kCopyGroups], 0));
+    const uint32_t nblk = c->nblk;
+    const int G = (int)std::min<uint32_t>(kCopyGroups, nblk);
+    const uint64_t R = c->pl.r / 8;
+    for (int g = 0; g < G; g++) {
+        const uint64_t lo = std::min<uint64_t>(nb, (uint64_t)(nblk * g / G) * R);
+        const uint64_t hi = std::min<uint64_t>(nb, (uint64_t)(nblk * (g + 1) / G) * R);
+        if (hi > lo) CUDA_TRY(cudaMemcpyAsync(c->key_dev + lo, key_host + lo, hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(cudaEventRecord(c->copy_ev[g], c->copy_stream));
+    }
+    c->launches = 0;
+    int rc = carry_reset(c);
+    bool first = true;
+    for (int g = 0; g < G && rc == PA_OK; g++) {
+        const uint32_t v0 = nblk * g / G, v1 = nblk * (g + 1) / G;
+        if (cudaStreamWaitEvent(c->stream, c->copy_ev[g], 0) != cudaSuccess) rc = set_err(PA_E_CUDA, "event wait failed");
+        if (rc == PA_OK && v1 > v0) rc = mmh_forward(c, c->key_dev, v0, v1);
+        if (rc == PA_OK && v1 > v0) rc = mmh_mac(c, v0, v1, first, G == 1);
+        first = false;
+    }
+    uint32_t *y = nullptr;
+    if (rc == PA_OK) rc = mmh_tail(c, &y);
+    if (rc == PA_OK) rc = run_mh(c, y, c->out_dev);
+    c->launches_total += c->launches;
+    TRY(rc);
     CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return PA_OK;

@@ -489,8 +489,9 @@ row_pass(const RowArgs A) {
 // the X stage, XOR-swizzled (bank-conflict free for every round pattern, checked by
 // scripts/dev/swizzle_sim.py), so a CTA needs only 3 V*S words of shared memory.
 // A unit's accumulators are added into dst with red.add (dst zeroed by the caller);
-// a unit split between two CTAs is thereby merged, values < 4p (the launcher keeps
-// gridDim.x <= nunits so no unit spans more than two CTAs).
+// a unit split between two CTAs is thereby merged.  Partials are canonical (< p) and
+// the launcher keeps gridDim.x <= nunits (no unit spans more than two CTAs), so up to two
+// launches may accumulate into the same dst: values < 4p.
 struct MacArgs {
     NttArgs nt;
     const uint32_t *src;      // [nvec][P][L] forward column-pass output
@@ -498,6 +499,9 @@ struct MacArgs {
     uint32_t *dst;            // [P][L] accumulators (zeroed), results in [0, 4p)
     uint32_t nvec;
     uint32_t nunits;          // (N2 / V) * P
+    uint32_t mode;            // 0: iterations split evenly, red.add into zeroed dst (< 4p)
+                              // 1: whole units per CTA, dst = sum (canonical)
+                              // 2: whole units per CTA, dst = (dst + sum) mod p (dst canonical)
 };
 
 // rows per CTA: V*S = 2048 words per operand and stage, and V <= S/2 <= N2 (planner)
@@ -534,8 +538,10 @@ row_mac(const MacArgs A) {
     const uint32_t P = a.nprimes;
     const uint32_t nvec = A.nvec;
     const uint64_t total = (uint64_t)A.nunits * nvec;
-    const uint64_t it0 = blockIdx.x * total / gridDim.x;
-    const uint64_t it1 = (blockIdx.x + 1) * total / gridDim.x;
+    const uint64_t it0 = A.mode ? (uint64_t)(blockIdx.x * (uint64_t)A.nunits / gridDim.x) * nvec
+                                : blockIdx.x * total / gridDim.x;
+    const uint64_t it1 = A.mode ? (uint64_t)((blockIdx.x + 1) * (uint64_t)A.nunits / gridDim.x) * nvec
+                                : (blockIdx.x + 1) * total / gridDim.x;
     auto sidx = [w](int pos) { return swz32(w * S + pos); };
     auto offset_of = [&](uint64_t it) -> size_t {
         const uint32_t unit = (uint32_t)(it / nvec), iv = (uint32_t)(it % nvec);
@@ -564,6 +570,12 @@ row_mac(const MacArgs A) {
     uint32_t tw[E / 2], twp[E / 2];
     uint32_t acc[E];
     Ctx32 cx{};
+    auto flush_one = [&](uint32_t *d, uint32_t v) {
+        v = red1p(v, cx.p);
+        if (A.mode == 0) atomicAdd(d, v);
+        else if (A.mode == 1) *d = v;
+        else *d = red1p(*d + v, cx.p);
+    };
     const uint32_t *rtw_p = nullptr;
     int64_t cur_unit = -1;
     uint32_t cur_pi = 0;
@@ -577,7 +589,7 @@ row_mac(const MacArgs A) {
 #pragma unroll
                 for (int h = 0; h < E / R; h++)
 #pragma unroll
-                    for (int mm = 0; mm < R; mm++) atomicAdd(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
+                    for (int mm = 0; mm < R; mm++) flush_one(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
             }
             cur_unit = unit;
             const uint32_t pi = unit % P;
@@ -637,7 +649,7 @@ row_mac(const MacArgs A) {
 #pragma unroll
         for (int h = 0; h < E / R; h++)
 #pragma unroll
-            for (int mm = 0; mm < R; mm++) atomicAdd(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
+            for (int mm = 0; mm < R; mm++) flush_one(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
     }
 }
 
