@@ -394,11 +394,11 @@ static int kinfo(F *fn, int threads, size_t smem, KInfo &ki) {
     return PA_OK;
 }
 
-template <int S_LOG, int MODE>
+template <int S_LOG, int N1_LOG, int MODE>
 static int launch_col_t(const ColArgs &A, cudaStream_t st) {
     constexpr int E_LOG = 5;
     static KInfo ki;
-    auto fn = col_pass<S_LOG, E_LOG, MODE>;
+    auto fn = col_pass<S_LOG, E_LOG, N1_LOG, MODE>;
     TRY(kinfo(fn, 32 * (1 << (S_LOG - E_LOG)), (size_t)(1 << S_LOG) * 32 * 4, ki));
     const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
@@ -406,16 +406,16 @@ static int launch_col_t(const ColArgs &A, cudaStream_t st) {
     return PA_OK;
 }
 
+// (column log, row log) pairs the planner produces (plan_product: MMH and single-vector rules)
 template <int MODE>
-static int launch_col(int slog, const ColArgs &A, cudaStream_t st) {
-    switch (slog) {
-        case 5: return launch_col_t<5, MODE>(A, st);
-        case 6: return launch_col_t<6, MODE>(A, st);
-        case 7: return launch_col_t<7, MODE>(A, st);
-        case 8: return launch_col_t<8, MODE>(A, st);
-        case 9: return launch_col_t<9, MODE>(A, st);
-    }
-    return set_err(PA_E_PARAM, "unsupported column length 2^%d", slog);
+static int launch_col(int slog, int n1log, const ColArgs &A, cudaStream_t st) {
+#define PA_COL(S, N) \
+    if (slog == S && n1log == N) return launch_col_t<S, N, MODE>(A, st);
+    PA_COL(5, 5) PA_COL(5, 6) PA_COL(6, 6) PA_COL(6, 7) PA_COL(7, 7) PA_COL(7, 8) PA_COL(7, 9) PA_COL(7, 10)
+    PA_COL(7, 11) PA_COL(7, 12) PA_COL(7, 13) PA_COL(7, 14) PA_COL(8, 8) PA_COL(8, 9) PA_COL(8, 14)
+    PA_COL(9, 9) PA_COL(9, 10) PA_COL(9, 11) PA_COL(9, 12) PA_COL(9, 13) PA_COL(9, 14)
+#undef PA_COL
+    return set_err(PA_E_PARAM, "unsupported column/row split 2^%d x 2^%d", slog, n1log);
 }
 
 constexpr int row_v(int slog) {
@@ -696,7 +696,7 @@ static int stage_pack_col(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec
         A.dst = scratch;
         A.nvec = nvec;
         A.units = (sd.pl.n_row / 32) * P * nvec;
-        TRY(launch_col<COL_FWD>(clog, A, c->stream));
+        TRY(launch_col<COL_FWD>(clog, __builtin_ctz(sd.pl.n_row), A, c->stream));
         c->launches++;
     }
     return PA_OK;
@@ -743,7 +743,7 @@ static int stage_inverse(pa_ctx *c, StageDev &sd, uint32_t *acc, const char *tag
     A.dst = acc;
     A.nvec = 1;
     A.units = (sd.pl.n_row / 32) * P;
-    TRY(launch_col<COL_INV>(clog, A, c->stream));
+    TRY(launch_col<COL_INV>(clog, rlog, A, c->stream));
     c->launches += 2;
     return PA_OK;
 }

@@ -293,20 +293,26 @@ struct ColArgs {
     uint32_t units;          // (N1/32) * P * nvec
 };
 
-// One CTA = 32 adjacent columns (one lane each) x S/E threads per column.
-template <int S_LOG, int E_LOG, int MODE>
+// One CTA = 32 adjacent columns (one lane each) x S/E threads per column.  The row
+// length N1 = 2^N1_LOG is a template parameter so every element address is a per-unit
+// base plus a compile-time offset (no per-element 64-bit index arithmetic).
+template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
 __global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)))
 col_pass(const ColArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int E = SP::E;
+    constexpr uint32_t N1 = 1u << N1_LOG;
+    constexpr uint32_t L = (1u << S_LOG) * N1;
     extern __shared__ uint32_t sm[];
     const int c = threadIdx.x & 31;
     const int v = threadIdx.x >> 5;
     const NttArgs &a = A.nt;
-    const uint32_t L = 1u << a.log2L;
     const uint32_t P = a.nprimes;
-    const uint32_t u0 = (uint32_t)(((uint64_t)blockIdx.x * A.units) / gridDim.x);
-    const uint32_t u1 = (uint32_t)(((uint64_t)(blockIdx.x + 1) * A.units) / gridDim.x);
+    const uint32_t nvec = A.nvec;
+    const uint32_t rows = A.rows;
+    const uint32_t units = A.units;
+    const uint32_t u0 = (uint32_t)(((uint64_t)blockIdx.x * units) / gridDim.x);
+    const uint32_t u1 = (uint32_t)(((uint64_t)(blockIdx.x + 1) * units) / gridDim.x);
     auto sidx = [c](int pos) { return pos * 32 + c; };
 
     uint32_t tw[E / 2], twp[E / 2];
@@ -315,8 +321,8 @@ col_pass(const ColArgs A) {
     const uint32_t *rtw_p = nullptr;
 
     for (uint32_t u = u0; u < u1; u++) {
-        const uint32_t iv = u % A.nvec;
-        const uint32_t pair = u / A.nvec;           // (cg, pi)
+        const uint32_t iv = u % nvec;
+        const uint32_t pair = u / nvec;             // (cg, pi)
         const uint32_t pi = pair % P;
         const uint32_t cg = pair / P;
         const uint32_t j1 = cg * 32 + c;
@@ -334,15 +340,18 @@ col_pass(const ColArgs A) {
         uint32_t x[E];
         {
             constexpr int R = 1 << SP::rlog(0);
-            const uint32_t *src = (MODE == COL_INV) ? A.src + (size_t)pi * L
-                                                    : A.src + ((size_t)iv * P + pi) * ((size_t)A.rows * a.n1);
+            const uint32_t *src = ((MODE == COL_INV) ? A.src + (size_t)pi * L
+                                                     : A.src + ((size_t)iv * P + pi) * ((size_t)rows * N1)) +
+                                  ((size_t)v << N1_LOG) + j1;
 #pragma unroll
             for (int h = 0; h < E / R; h++) {
 #pragma unroll
                 for (int m = 0; m < R; m++) {
-                    const uint32_t j2 = (uint32_t)in_pos<S_LOG, E_LOG>(v, h, m);
+                    constexpr int dummy = 0;
+                    (void)dummy;
+                    const int rel = SP::TPV * h + (SP::S / R) * m;          // in_pos - v
                     uint32_t val = 0;
-                    if (MODE == COL_INV || j2 < A.rows) val = src[(size_t)j2 * a.n1 + j1];
+                    if (MODE == COL_INV || (uint32_t)(v + rel) < rows) val = src[(size_t)rel << N1_LOG];
                     x[h * R + m] = val;
                 }
             }
@@ -352,15 +361,16 @@ col_pass(const ColArgs A) {
         rounds_rest<S_LOG, E_LOG, 1>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
-            uint32_t *dst = (MODE == COL_INV) ? A.dst + (size_t)pi * L
-                                              : A.dst + ((size_t)iv * P + pi) * L;
-            const uint32_t *tw4 = A.tw4 + (size_t)pi * L;
+            constexpr int G = 1 << SP::glog(SP::Q - 1);
+            const size_t vb = ((size_t)v << N1_LOG) + j1;
+            uint32_t *dst = ((MODE == COL_INV) ? A.dst + (size_t)pi * L : A.dst + ((size_t)iv * P + pi) * L) + vb;
+            const uint32_t *tw4 = A.tw4 + (size_t)pi * L + vb;
 #pragma unroll
             for (int h = 0; h < E / R; h++) {
 #pragma unroll
                 for (int mm = 0; mm < R; mm++) {
-                    const uint32_t k2 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
-                    const size_t o = (size_t)k2 * a.n1 + j1;
+                    const int rel = SP::TPV * h + G * bitrev<R>(mm);        // out_pos - v
+                    const size_t o = (size_t)rel << N1_LOG;
                     uint32_t val = x[h * R + mm];
                     if constexpr (MODE != COL_INV) val = mul_mont(val, __ldg(tw4 + o), cx.p, cx.pinv);
                     else val = red1p(val, cx.p);
