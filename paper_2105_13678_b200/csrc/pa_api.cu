@@ -461,9 +461,11 @@ static int launch_mac_t(const MacArgs &A, cudaStream_t st) {
     static KInfo ki;
     auto fn = row_mac<S_LOG, E_LOG>;
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
-    // grid <= nunits: every CTA runs >= nvec iterations, so a unit is split between at
-    // most two CTAs and the red.add merge of two partials in [0, 2p) stays < 4p < 2^32
-    const int grid = (int)std::min<uint64_t>(A.nunits, (uint64_t)ki.occ * g_num_sms);
+    // mode 0: grid <= 3 nunits, so every CTA runs >= nvec/3 iterations and a unit is split
+    // between at most four CTAs: four canonical partials (< p each) stay < 4p < 2^32.
+    // modes 1/2 (whole units per CTA): grid <= nunits.
+    const uint64_t cap = A.mode ? (uint64_t)A.nunits : 3ull * A.nunits;
+    const int grid = (int)std::min<uint64_t>(cap, (uint64_t)ki.occ * g_num_sms);
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;

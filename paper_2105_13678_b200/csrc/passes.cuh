@@ -297,7 +297,7 @@ struct ColArgs {
 // length N1 = 2^N1_LOG is a template parameter so every element address is a per-unit
 // base plus a compile-time offset (no per-element 64-bit index arithmetic).
 template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
-__global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)))
+__global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)), S_LOG <= 8 ? 3 : 1)
 col_pass(const ColArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int E = SP::E;
@@ -499,9 +499,8 @@ row_pass(const RowArgs A) {
 // the X stage, XOR-swizzled (bank-conflict free for every round pattern, checked by
 // scripts/dev/swizzle_sim.py), so a CTA needs only 3 V*S words of shared memory.
 // A unit's accumulators are added into dst with red.add (dst zeroed by the caller);
-// a unit split between two CTAs is thereby merged.  Partials are canonical (< p) and
-// the launcher keeps gridDim.x <= nunits (no unit spans more than two CTAs), so up to two
-// launches may accumulate into the same dst: values < 4p.
+// a unit split between CTAs is thereby merged.  Partials are canonical (< p) and the
+// launcher keeps gridDim.x <= 3 nunits (no unit spans more than four CTAs): values < 4p.
 struct MacArgs {
     NttArgs nt;
     const uint32_t *src;      // [nvec][P][L] forward column-pass output
