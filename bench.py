@@ -259,7 +259,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library then replays each hash as a CUDA graph
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
 
     k = w.k
     b0, b1 = shard_ranges(k, world)[rank]

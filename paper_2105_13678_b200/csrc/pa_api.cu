@@ -20,6 +20,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -551,6 +552,12 @@ struct pa_ctx {
     int cslot = 0;
     uint8_t *key_dev = nullptr;               // staging for pa_hash_host
     cudaStream_t copy_stream = nullptr;       // pa_hash_host H2D copies
+    cudaGraphExec_t graph_exec = nullptr;     // captured pa_hash (graphs_enabled)
+    const void *graph_key = nullptr, *graph_out = nullptr;
+    uint32_t graph_launches = 0;
+    cudaGraphExec_t hgraph_exec = nullptr;    // captured pa_hash_host
+    const void *hgraph_key = nullptr, *hgraph_out = nullptr;
+    uint32_t hgraph_launches = 0;
     cudaEvent_t copy_ev[9] = {};
     uint8_t *out_dev = nullptr;
     uint64_t Wg = 0, W_ring = 0, W_fold = 0, W_Z = 0, ncoef_mmh = 0;
@@ -934,6 +941,8 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     cudaStreamSynchronize(c->stream);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->evpool) cudaEventDestroy(e);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    if (c->hgraph_exec) cudaGraphExecDestroy(c->hgraph_exec);
     if (c->key_dev) cudaFree(c->key_dev);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
@@ -960,6 +969,8 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
 
 extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+    if (c->hgraph_exec) { cudaGraphExecDestroy(c->hgraph_exec); c->hgraph_exec = nullptr; }
     c->stream = (cudaStream_t)stream;
     return PA_OK;
 }
@@ -1042,16 +1053,49 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     return PA_OK;
 }
 
-extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
-    if (!c || !key_bits || !out_bits) return set_err(PA_E_PARAM, "NULL argument");
-    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
+static int hash_enqueue(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     c->launches = 0;
     TRY(carry_reset(c));
     uint32_t *y = nullptr;
-    int rc = run_mmh(c, key_bits, &y);
-    if (rc == PA_OK) rc = run_mh(c, y, out_bits);
+    TRY(run_mmh(c, key_bits, &y));
+    return run_mh(c, y, out_bits);
+}
+
+// On a non-default stream (and without stage profiling) the ~20 launches of one hash are
+// captured once into a CUDA graph per (key, out) pointer pair and replayed: no host
+// launch overhead, no inter-kernel launch gaps.  PA_NO_GRAPH=1 disables it.
+static bool graphs_enabled(const pa_ctx *c) {
+    static const bool off = getenv("PA_NO_GRAPH") && atoi(getenv("PA_NO_GRAPH"));
+    return !off && c->stream != nullptr && !c->prof;
+}
+
+extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
+    if (!c || !key_bits || !out_bits) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
+    if (!graphs_enabled(c)) {
+        const int rc = hash_enqueue(c, key_bits, out_bits);
+        c->launches_total += c->launches;
+        return rc;
+    }
+    if (!c->graph_exec || c->graph_key != key_bits || c->graph_out != out_bits) {
+        if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+        cudaGraph_t g = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = hash_enqueue(c, key_bits, out_bits);
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (rc != PA_OK) { if (g) cudaGraphDestroy(g); return rc; }
+        if (e != cudaSuccess) return set_err(PA_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        const cudaError_t e2 = cudaGraphInstantiate(&c->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e2 != cudaSuccess) { c->graph_exec = nullptr; return set_err(PA_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2)); }
+        c->graph_key = key_bits;
+        c->graph_out = out_bits;
+        c->graph_launches = c->launches;
+    }
+    CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream));
+    c->launches = c->graph_launches;
     c->launches_total += c->launches;
-    return rc;
+    return PA_OK;
 }
 
 extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
@@ -1088,16 +1132,8 @@ extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8
 // the MMH transforms.
 static constexpr int kCopyGroups = 8;
 
-extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
-    if (!c || !key_host || !out_host) return set_err(PA_E_PARAM, "NULL argument");
-    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
+static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
-    if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
-    if (!c->out_dev) CUDA_TRY(cudaMalloc(&c->out_dev, mb));
-    if (!c->copy_stream) {
-        CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-        for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
-    }
     // the copies may overwrite key_dev only after earlier work on the ctx stream is done
     CUDA_TRY(cudaEventRecord(c->copy_ev[kCopyGroups], c->stream));
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[kCopyGroups], 0));
@@ -1111,21 +1147,56 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
         CUDA_TRY(cudaEventRecord(c->copy_ev[g], c->copy_stream));
     }
     c->launches = 0;
-    int rc = carry_reset(c);
+    TRY(carry_reset(c));
     bool first = true;
-    for (int g = 0; g < G && rc == PA_OK; g++) {
+    for (int g = 0; g < G; g++) {
         const uint32_t v0 = nblk * g / G, v1 = nblk * (g + 1) / G;
-        if (cudaStreamWaitEvent(c->stream, c->copy_ev[g], 0) != cudaSuccess) rc = set_err(PA_E_CUDA, "event wait failed");
-        if (rc == PA_OK && v1 > v0) rc = mmh_forward(c, c->key_dev, v0, v1);
-        if (rc == PA_OK && v1 > v0) rc = mmh_mac(c, v0, v1, first, G == 1);
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_ev[g], 0));
+        if (v1 > v0) TRY(mmh_forward(c, c->key_dev, v0, v1));
+        if (v1 > v0) TRY(mmh_mac(c, v0, v1, first, G == 1));
         first = false;
     }
     uint32_t *y = nullptr;
-    if (rc == PA_OK) rc = mmh_tail(c, &y);
-    if (rc == PA_OK) rc = run_mh(c, y, c->out_dev);
-    c->launches_total += c->launches;
-    TRY(rc);
+    TRY(mmh_tail(c, &y));
+    TRY(run_mh(c, y, c->out_dev));
     CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
+    return PA_OK;
+}
+
+extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
+    if (!c || !key_host || !out_host) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
+    const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
+    if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
+    if (!c->out_dev) CUDA_TRY(cudaMalloc(&c->out_dev, mb));
+    if (!c->copy_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
+    }
+    if (!graphs_enabled(c)) {
+        const int rc = hash_host_enqueue(c, key_host, out_host);
+        c->launches_total += c->launches;
+        TRY(rc);
+    } else {
+        if (!c->hgraph_exec || c->hgraph_key != key_host || c->hgraph_out != out_host) {
+            if (c->hgraph_exec) { cudaGraphExecDestroy(c->hgraph_exec); c->hgraph_exec = nullptr; }
+            cudaGraph_t g = nullptr;
+            CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            const int rc = hash_host_enqueue(c, key_host, out_host);
+            const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+            if (rc != PA_OK) { if (g) cudaGraphDestroy(g); return rc; }
+            if (e != cudaSuccess) return set_err(PA_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+            const cudaError_t e2 = cudaGraphInstantiate(&c->hgraph_exec, g, 0);
+            cudaGraphDestroy(g);
+            if (e2 != cudaSuccess) { c->hgraph_exec = nullptr; return set_err(PA_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2)); }
+            c->hgraph_key = key_host;
+            c->hgraph_out = out_host;
+            c->hgraph_launches = c->launches;
+        }
+        CUDA_TRY(cudaGraphLaunch(c->hgraph_exec, c->stream));
+        c->launches = c->hgraph_launches;
+        c->launches_total += c->launches;
+    }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return PA_OK;
 }

@@ -191,6 +191,37 @@ def test_hash_host_and_determinism():
     assert o1 == o2 == o3 == oracle_seeded(key, n, r, m, 5)
 
 
+def test_graph_replay_on_stream():
+    # non-default stream: pa_hash is captured once as a CUDA graph and replayed; a replay
+    # must read the key buffer's current contents, a new buffer pair must re-capture
+    PAContext = _pa()
+    n, r, m, seed = 300_001, 4096, 20_000, 17
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = PAContext(n, r, m, seed=seed)
+        kd = torch.empty((n + 7) // 8, dtype=torch.uint8, device="cuda")
+        out = torch.empty((m + 7) // 8, dtype=torch.uint8, device="cuda")
+        for ks in (1, 2, 3):
+            key = key_bytes(n, ks)
+            kd.copy_(torch.from_numpy(key))
+            ctx.hash(kd, out)
+            s.synchronize()
+            assert bytes(out.cpu().numpy()) == oracle_seeded(key, n, r, m, seed)
+        kd2 = kd.clone()
+        out2 = ctx.hash(kd2)
+        s.synchronize()
+        assert bytes(out2.cpu().numpy()) == oracle_seeded(key_bytes(n, 3), n, r, m, seed)
+        # pa_hash_host (graph with H2D / D2H nodes) on the same pinned buffers
+        hk = torch.empty((n + 7) // 8, dtype=torch.uint8).pin_memory()
+        ho = torch.empty((m + 7) // 8, dtype=torch.uint8).pin_memory()
+        for ks in (4, 5):
+            key = key_bytes(n, ks)
+            hk.copy_(torch.from_numpy(key))
+            ctx.hash_host(hk, ho)
+            assert bytes(ho.numpy()) == oracle_seeded(key, n, r, m, seed)
+        ctx.close()
+
+
 def _golden():
     path = os.path.join(ROOT, "tests", "golden", "digests.json")
     return json.load(open(path)) if os.path.exists(path) else {}
