@@ -236,6 +236,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--limb-bits", type=int, default=0, help="force the limb width B (0 = planner)")
+    ap.add_argument("--only-device", action="store_true",
+                    help="timed device steps only (no per-stage pass, no e2e): for ncu launch lists")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -311,6 +313,13 @@ def main():
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_per_step = tot.item() / args.steps
 
+    if args.only_device:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": w.n / (ms_per_step * 1e-3) / 1e6, "unit": "Mbps",
+                              "ms_per_step": ms_per_step, "only_device": True}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     # ---- per-launch times: the same K steps again with CUDA events recorded on the
     # context stream around every launch (pa_ctx_set_profiling); e2e via the host API
     ctx.set_profiling(True)

@@ -49,11 +49,14 @@ def launches(path: str, tag: str) -> None:
 
 
 def full(rep: str, stage: str, tag: str) -> None:
+    """stage: one name, or comma-separated names of the report's launches in order."""
     recs = summarize(rep)
+    names = stage.split(",")
     lines = []
     traffic_path = os.path.join(PROF, "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    for rec in recs:
+    for i, rec in enumerate(recs):
+        stage = names[min(i, len(names) - 1)]
         lines.append(f"----- {os.path.basename(rep)} (stage {stage})")
         for k, v in rec.items():
             lines.append(f"  {k:80s} {v[:60]}")
@@ -66,8 +69,8 @@ def full(rep: str, stage: str, tag: str) -> None:
         traffic[stage] = {"kernel": rec.get("Kernel Name"), "dram_bytes_per_launch":
                           mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
                           "dram_read": mb("dram__bytes_read.sum"), "dram_write": mb("dram__bytes_write.sum"),
-                          "source": f"profiles/{tag}_{stage}.txt"}
-    open(os.path.join(PROF, f"{tag}_{stage}.txt"), "w").write("\n".join(lines) + "\n")
+                          "source": f"profiles/{tag}_{names[0] if len(names) == 1 else 'kernels'}.txt"}
+    open(os.path.join(PROF, f"{tag}_{names[0] if len(names) == 1 else 'kernels'}.txt"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
     print("\n".join(lines))
 
