@@ -517,9 +517,13 @@ struct MacArgs {
 __host__ __device__ constexpr int mac_v(int slog) {
     return (slog >= 11 ? 1 : (2048 >> slog)) < (1 << (slog - 1)) ? (slog >= 11 ? 1 : (2048 >> slog)) : (1 << (slog - 1));
 }
-template <int S_LOG>
+// exchange layout: a separate padded buffer (fewer instructions than the in-place XOR
+// swizzle, measured 118 vs 135 us for C4) whenever it fits; in place for 2^14-point rows
+__host__ __device__ constexpr int mac_pad(int slog) { return slog <= 13 ? 1 : 0; }
+template <int S_LOG, int PAD = mac_pad(S_LOG)>
 constexpr size_t mac_smem_bytes() {
-    return (size_t)3 * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8;
+    return (size_t)3 * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8 +
+           (PAD ? (size_t)mac_v(S_LOG) * ((1 << S_LOG) + (1 << S_LOG) / 32) * 4 : 0);
 }
 __device__ __forceinline__ int swz32(int P) { return P ^ ((P >> 5) & 31); }
 
@@ -529,7 +533,7 @@ __host__ __device__ constexpr int mac_minb(int slog, int elog) {
     return (65536 / (mac_threads(slog, elog) * 4 * (1 << elog))) < 8 ? (65536 / (mac_threads(slog, elog) * 4 * (1 << elog)))
                                                                         : 8;
 }
-template <int S_LOG, int E_LOG, int DBG = 0>
+template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG)>
 __global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(S_LOG, E_LOG) < 1 ? 1 : mac_minb(S_LOG, E_LOG))
 row_mac(const MacArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
@@ -540,6 +544,7 @@ row_mac(const MacArgs A) {
     uint32_t *xs = smem;                                 // [2][SW] X ring (exchange in place)
     uint32_t *as = smem + 2 * SW;                        // [SW]   A^
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 3 * SW);   // fullX[2], fullA
+    uint32_t *exb = smem + 3 * SW + 8;                   // PAD: [V][S + S/32] exchange
     const int w = threadIdx.x / SP::TPV;
     const int v = threadIdx.x % SP::TPV;
     const NttArgs &a = A.nt;
@@ -551,7 +556,10 @@ row_mac(const MacArgs A) {
                                 : blockIdx.x * total / gridDim.x;
     const uint64_t it1 = A.mode ? (uint64_t)((blockIdx.x + 1) * (uint64_t)A.nunits / gridDim.x) * nvec
                                 : (blockIdx.x + 1) * total / gridDim.x;
-    auto sidx = [w](int pos) { return swz32(w * S + pos); };
+    auto sidx = [w](int pos) {
+        if constexpr (PAD) return w * (S + S / 32) + pos + (pos >> 5);
+        else return swz32(w * S + pos);
+    };
     auto offset_of = [&](uint64_t it) -> size_t {
         const uint32_t unit = (uint32_t)(it / nvec), iv = (uint32_t)(it % nvec);
         const uint32_t pi = unit % P, rg = unit / P;
@@ -629,9 +637,10 @@ row_mac(const MacArgs A) {
                 for (int m = 0; m < R; m++) x[h * R + m] = xst[w * S + in_pos<S_LOG, E_LOG>(v, h, m)];
         }
         if constexpr (DBG != 1) {
-            if constexpr (SP::Q > 1) __syncthreads();    // natural-order reads done before in-place writes
-            round0_finish<S_LOG, E_LOG>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
-            rounds_rest<S_LOG, E_LOG, 1>(x, xst, sidx, v, tw, twp, rtw_p, a, cx);
+            uint32_t *exch = PAD ? exb : xst;
+            if constexpr (SP::Q > 1 && !PAD) __syncthreads();   // natural-order reads before in-place writes
+            round0_finish<S_LOG, E_LOG>(x, exch, sidx, v, tw, twp, rtw_p, a, cx);
+            rounds_rest<S_LOG, E_LOG, 1>(x, exch, sidx, v, tw, twp, rtw_p, a, cx);
         }
         mbar_wait(&bars[2], k & 1);
         {

@@ -1,18 +1,18 @@
 // dev check + timing: row_mac variants vs old row_pass<ROW_MAC> on a real context's buffers
 #include "../../paper_2105_13678_b200/csrc/pa_api.cu"
 #include <cstdlib>
-template <int S_LOG, int E_LOG, int DBG = 0>
+template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG)>
 static float run_variant(const StageDev &sd, pa_ctx *c, uint32_t *out, int reps) {
     const uint32_t P = sd.pl.nprimes;
     MacArgs M{}; M.nt = ntt_args(sd, 0, 1, E_LOG); M.src = c->scratch; M.ahat = c->ahat; M.dst = out; M.nvec = c->nblk;
     M.nunits = (sd.pl.n_col / mac_v(S_LOG)) * P;
-    auto fn = row_mac<S_LOG, E_LOG, DBG>;
+    auto fn = row_mac<S_LOG, E_LOG, DBG, PAD>;
     const int thr = mac_threads(S_LOG, E_LOG);
-    const size_t sm = mac_smem_bytes<S_LOG>();
+    const size_t sm = mac_smem_bytes<S_LOG, PAD>();
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, thr, sm);
-    const int grid = std::min<int>(M.nunits, occ * 148);
+    const int grid = std::min<int>(3 * M.nunits, occ * 148);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     float best = 1e9;
     for (int i = 0; i < reps; i++) {
@@ -24,7 +24,7 @@ static float run_variant(const StageDev &sd, pa_ctx *c, uint32_t *out, int reps)
         float ms; cudaEventElapsedTime(&ms, a, b);
         best = std::min(best, ms);
     }
-    printf("  row_mac<%d,%d,dbg%d>: threads %d occ %d grid %d  best %.1f us\n", S_LOG, E_LOG, DBG, thr, occ, grid, best * 1e3);
+    printf("  row_mac<%d,%d,dbg%d,pad%d>: threads %d occ %d grid %d  best %.1f us\n", S_LOG, E_LOG, DBG, PAD, thr, occ, grid, best * 1e3);
     return best;
 }
 int main(int argc, char **argv) {
@@ -66,6 +66,9 @@ int main(int argc, char **argv) {
         run_variant<10, 4>(sd, c, o2, reps); check("E16");
     } else if (rlog == 9) {
         run_variant<9, 5>(sd, c, o2, reps); check("E32");
+        run_variant<9, 5, 0, 0>(sd, c, o2, reps); check("E32 swizzle");
+        run_variant<9, 5, 1>(sd, c, o2, reps);
+        run_variant<9, 5, 2>(sd, c, o2, reps);
         run_variant<9, 4>(sd, c, o2, reps); check("E16");
     } else if (rlog == 5) {
         run_variant<5, 5>(sd, c, o2, reps); check("E32");
