@@ -426,7 +426,8 @@ constexpr int row_v(int slog) {
 template <int S_LOG, int MODE>
 static int launch_row_t(const RowArgs &A0, cudaStream_t st) {
     constexpr int E_LOG = 5;
-    constexpr int V = row_v(S_LOG);
+    // the inverse transforms a single vector: small CTAs (V S = 2048 words) give enough units
+    constexpr int V = MODE == ROW_INV ? mac_v(S_LOG) : row_v(S_LOG);
     static KInfo ki;
     auto fn = row_pass<S_LOG, E_LOG, V, MODE>;
     constexpr int S = 1 << S_LOG;
