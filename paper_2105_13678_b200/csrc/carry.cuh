@@ -55,17 +55,26 @@ __global__ void __launch_bounds__(128) crt_coeffs(const uint32_t *__restrict__ r
         shi += (slo < q);
     }
     const uint32_t k = (uint32_t)shi;
+    // sum_i y_i (M/p_i): products < 2^62, so four of them are summed in one 64-bit
+    // accumulator per word (one mad.wide each) before being split into 32-bit columns
     uint64_t acc[P + 1];
 #pragma unroll
     for (int w = 0; w <= P; w++) acc[w] = 0;
 #pragma unroll
-    for (int i = 0; i < P; i++)
+    for (int g = 0; g < P; g += 4) {
+        uint64_t t[P];
+#pragma unroll
+        for (int w = 0; w < P; w++) t[w] = 0;
+#pragma unroll
+        for (int i = g; i < g + 4 && i < P; i++)
+#pragma unroll
+            for (int w = 0; w < P; w++) t[w] = mad_wide(y[i], K.MI[i][w], t[w]);
 #pragma unroll
         for (int w = 0; w < P; w++) {
-            const uint64_t t = mad_wide(y[i], K.MI[i][w], 0ull);
-            acc[w] += (uint32_t)t;
-            acc[w + 1] += t >> 32;
+            acc[w] += (uint32_t)t[w];
+            acc[w + 1] += t[w] >> 32;
         }
+    }
     // words of sum_i y_i M_i (P + 1 words) minus k M
     uint64_t carry = 0;
     int64_t borrow = 0;
@@ -341,25 +350,42 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
                                                      const uint32_t *__restrict__ addend, uint32_t n_addend,
                                                      uint32_t *__restrict__ out, uint32_t W, uint32_t cap,
                                                      uint32_t *state, uint32_t Wfin) {
-    extern __shared__ uint32_t sc[];                          // [cap][P|1] coefficients
-    constexpr int CS = crt_cstride<P>();
+    (void)cap;
+    // column sums of the tile's words, scatter form: a thread owns whole coefficients
+    // (P words loaded from coefT, coalesced) and adds their P + 1 bit-shifted words into
+    // the tile's 64-bit sums in shared memory (shared-memory atomics: <= ceil(32(P+1)/B)+1
+    // contributions per word)
+    __shared__ unsigned long long s_sum[kCCTile];
     constexpr uint32_t cbits = 32 * P;
     __shared__ uint32_t s_tile, s_cin, s_c1, s_last;
     __shared__ uint32_t s_hi[kCCT];
     if (threadIdx.x == 0) s_tile = atomicAdd(&state[0], 1u);
+    for (uint32_t i = threadIdx.x; i < kCCTile; i += blockDim.x) s_sum[i] = 0ull;
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t u0 = tile * kCCTile;
     const uint32_t ub = u0 + threadIdx.x * kCCV;            // this thread's first word
-    uint64_t S[kCCV];
-#pragma unroll
-    for (int v = 0; v < kCCV; v++) {
-        const uint32_t u = ub + v;
-        S[v] = (!RING && addend && u < n_addend) ? addend[u] : 0ull;
-    }
-    // ---- column sums, chunk by chunk
     const uint32_t nchunks = (DBG & 8) ? 0u : RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
     const uint32_t tb0 = 32 * u0, tb1 = 32 * min(u0 + kCCTile, W);   // tile bits
+    // adds bits [0, len) of coefficient c, placed at tile-relative bit d, into s_sum
+    auto scatter = [&](const uint32_t (&c)[P], int64_t d, int64_t len) {
+        uint32_t m[P];
+#pragma unroll
+        for (int w = 0; w < P; w++) {
+            const int64_t top = len - 32 * w;                  // bits of word w inside [0, len)
+            m[w] = top >= 32 ? c[w] : (top <= 0 ? 0u : (c[w] & ((1u << top) - 1u)));
+        }
+        const int64_t wq = d >> 5;                            // floor
+        const int s = (int)(d & 31);
+#pragma unroll
+        for (int i = 0; i <= P; i++) {
+            const int64_t wi = wq + i;
+            if (wi < 0 || wi >= (int64_t)kCCTile) continue;
+            const uint32_t lo = (i > 0) ? m[i - 1] : 0u, hi = (i < P) ? m[i] : 0u;
+            const uint32_t val = s ? __funnelshift_l(lo, hi, s) : hi;
+            if (val) atomicAdd(&s_sum[wi], (unsigned long long)val);
+        }
+    };
     for (uint32_t t = 0; t < nchunks; t++) {
         const uint32_t base = RING ? t * gamma : 0u;
         const uint32_t jc0 = (base + B - 1) / B;
@@ -370,46 +396,18 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
         if (ja < jc0) ja = jc0;
         if (jb > jc1) jb = jc1;
         if (jb < ja || jb == 0xFFFFFFFFu) continue;           // uniform
-        const uint32_t cnt = min(jb - ja + 1, cap);
-        __syncthreads();
-        {
-            // stage cnt x P words; a thread issues 8 independent loads before its stores
-            const uint32_t tot = (DBG & 1) ? 0u : cnt * P;
-            for (uint32_t b0 = threadIdx.x; b0 < tot; b0 += 8 * blockDim.x) {
-                uint32_t v[8], dst[8];
+        for (uint32_t j = ja + threadIdx.x; j <= jb; j += blockDim.x) {
+            uint32_t c[P];
 #pragma unroll
-                for (int q8 = 0; q8 < 8; q8++) {
-                    const uint32_t i = b0 + q8 * blockDim.x;
-                    const uint32_t w = i / cnt, q = i - w * cnt;
-                    dst[q8] = q * CS + w;
-                    v[q8] = (i < tot) ? __ldg(coefT + (size_t)w * ncoef + ja + q) : 0u;
-                }
-#pragma unroll
-                for (int q8 = 0; q8 < 8; q8++)
-                    if (b0 + q8 * blockDim.x < tot) sc[dst[q8]] = v[q8];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int v = 0; v < kCCV; v++) {
-            const uint32_t u = ub + v;
-            if (u >= W) continue;
-            const uint32_t me = 32 * u;
-            uint32_t j0 = (me + base > cbits) ? (me + base - cbits) / B : 0u;
-            uint32_t j1 = (me + 31 + base) / B;
-            if (j0 < ja) j0 = ja;
-            if (j1 > ja + cnt - 1) j1 = ja + cnt - 1;
-            for (uint32_t j = j0; j <= j1; j++) {
-                const int pos = (int)(B * j - base);
-                int len = (int)cbits;
-                if (RING && pos + len > (int)gamma) len = (int)gamma - pos;
-                S[v] += coef_window_s<P>(sc + (j - ja) * CS, (int)me - pos, len);
-            }
+            for (int w = 0; w < P; w++) c[w] = (DBG & 1) ? 0u : __ldg(coefT + (size_t)w * ncoef + j);
+            const int64_t pos = (int64_t)B * j - base;        // ring / linear bit of the piece
+            int64_t len = cbits;
+            if (RING && pos + len > (int64_t)gamma) len = (int64_t)gamma - pos;
+            scatter(c, pos - (int64_t)tb0, len);
         }
     }
-    if (RING && tb0 < cbits + 32) {
+    if (RING && tb0 < cbits + 32 && !(DBG & 8)) {
         // wrapped pieces: the bits of a coefficient above the ring top land at ring bit 0
-        uint32_t tmp[P];
         for (uint32_t t = 0; t < nchunks; t++) {
             const int64_t base = (int64_t)t * gamma;
             const int64_t top = base + (int64_t)gamma;
@@ -418,23 +416,32 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
             if (jx < jc0) jx = jc0;
             int64_t jy = (top - 1) / (int64_t)B;
             if (jy > (int64_t)ncoef - 1) jy = (int64_t)ncoef - 1;
-            for (int64_t j = jx; j <= jy; j++) {
+            for (int64_t j = jx + threadIdx.x; j <= jy; j += blockDim.x) {
                 const int64_t pos = (int64_t)B * j - base;
                 if (pos + (int64_t)cbits <= (int64_t)gamma) continue;
                 const int cut = (int)((int64_t)gamma - pos);
-                bool need = false;
+                uint32_t c[P], h[P];
 #pragma unroll
-                for (int v = 0; v < kCCV; v++) need |= (32 * (ub + v) < cbits + 32);
-                if (!need) continue;
+                for (int w = 0; w < P; w++) c[w] = coefT[(size_t)w * ncoef + j];
+                // h = c >> cut (the part above the ring top), placed at ring bit 0
+                const int cw = cut >> 5, cs = cut & 31;
 #pragma unroll
-                for (int w = 0; w < P; w++) tmp[w] = coefT[(size_t)w * ncoef + j];
+                for (int w = 0; w < P; w++) {
+                    uint32_t lo = 0, hi = 0;
 #pragma unroll
-                for (int v = 0; v < kCCV; v++) {
-                    const uint32_t me = 32 * (ub + v);
-                    if (ub + v < W && me < cbits + 32) S[v] += coef_window_s<P>(tmp, (int)me + cut, (int)cbits);
+                    for (int q = 0; q < P; q++) { if (q == w + cw) lo = c[q]; if (q == w + cw + 1) hi = c[q]; }
+                    h[w] = cs ? __funnelshift_r(lo, hi, cs) : lo;
                 }
+                scatter(h, -(int64_t)tb0, cbits);
             }
         }
+    }
+    __syncthreads();
+    uint64_t S[kCCV];
+#pragma unroll
+    for (int v = 0; v < kCCV; v++) {
+        const uint32_t u = ub + v;
+        S[v] = s_sum[threadIdx.x * kCCV + v] + ((!RING && addend && u < n_addend) ? addend[u] : 0ull);
     }
     // ---- carries inside the tile (cin of word u0 handled separately, see above)
     uint32_t w[kCCV];

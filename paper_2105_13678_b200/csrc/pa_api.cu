@@ -495,7 +495,7 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
                               uint32_t *state, uint32_t Wfin, cudaStream_t st) {
     const uint32_t B = sd.pl.limb_bits;
     const uint32_t cap = (32u * kCCTile + 32u * P) / B + 3;
-    const size_t smem = (size_t)cap * crt_cstride<P>() * 4;
+    const size_t smem = 0;
     crt_coeffs<P><<<(ncoef + 127) / 128, 128, 0, st>>>(res, sd.L, ncoef, sd.crt, coef);
     CUDA_TRY(cudaGetLastError());
     auto fn = crt_carry<P, RING>;
