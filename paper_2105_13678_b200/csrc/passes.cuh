@@ -520,9 +520,9 @@ __host__ __device__ constexpr int mac_v(int slog) {
 // exchange layout: a separate padded buffer (fewer instructions than the in-place XOR
 // swizzle, measured 118 vs 135 us for C4) whenever it fits; in place for 2^14-point rows
 __host__ __device__ constexpr int mac_pad(int slog) { return slog <= 13 ? 1 : 0; }
-template <int S_LOG, int PAD = mac_pad(S_LOG)>
+template <int S_LOG, int PAD = mac_pad(S_LOG), int NSX = 2>
 constexpr size_t mac_smem_bytes() {
-    return (size_t)3 * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8 +
+    return (size_t)(NSX + 1) * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8 +
            (PAD ? (size_t)mac_v(S_LOG) * ((1 << S_LOG) + (1 << S_LOG) / 32) * 4 : 0);
 }
 __device__ __forceinline__ int swz32(int P) { return P ^ ((P >> 5) & 31); }
@@ -533,7 +533,7 @@ __host__ __device__ constexpr int mac_minb(int slog, int elog) {
     return (65536 / (mac_threads(slog, elog) * 4 * (1 << elog))) < 8 ? (65536 / (mac_threads(slog, elog) * 4 * (1 << elog)))
                                                                         : 8;
 }
-template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG)>
+template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = 2>
 __global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(S_LOG, E_LOG) < 1 ? 1 : mac_minb(S_LOG, E_LOG))
 row_mac(const MacArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
@@ -542,9 +542,9 @@ row_mac(const MacArgs A) {
     constexpr uint32_t SW = V * S;                       // words per operand per stage
     extern __shared__ __align__(128) uint32_t smem[];
     uint32_t *xs = smem;                                 // [2][SW] X ring (exchange in place)
-    uint32_t *as = smem + 2 * SW;                        // [SW]   A^
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 3 * SW);   // fullX[2], fullA
-    uint32_t *exb = smem + 3 * SW + 8;                   // PAD: [V][S + S/32] exchange
+    uint32_t *as = smem + NSX * SW;                      // [SW]   A^
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (NSX + 1) * SW);   // fullX[NSX], fullA
+    uint32_t *exb = smem + (NSX + 1) * SW + 8;           // PAD: [V][S + S/32] exchange
     const int w = threadIdx.x / SP::TPV;
     const int v = threadIdx.x % SP::TPV;
     const NttArgs &a = A.nt;
@@ -570,16 +570,16 @@ row_mac(const MacArgs A) {
         bulk_g2s(xs + s * SW, A.src + offset_of(it), SW * 4, &bars[s]);
     };
     auto issue_a = [&](uint64_t it) {
-        mbar_arrive_expect_tx(&bars[2], SW * 4);
-        bulk_g2s(as, A.ahat + offset_of(it), SW * 4, &bars[2]);
+        mbar_arrive_expect_tx(&bars[NSX], SW * 4);
+        bulk_g2s(as, A.ahat + offset_of(it), SW * 4, &bars[NSX]);
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 3; s++) mbar_init(&bars[s], 1);
+        for (int s = 0; s <= NSX; s++) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 2; s++)
+        for (int s = 0; s < NSX; s++)
             if (it0 + s < it1) issue_x(it0 + s, s);
         if (it0 < it1) issue_a(it0);
     }
@@ -625,8 +625,8 @@ row_mac(const MacArgs A) {
             for (int e = 0; e < E; e++) acc[e] = 0;
         }
         const uint32_t k = (DBG == 2) ? 0u : (uint32_t)(it - it0);
-        const int s = (int)(k & 1);
-        mbar_wait(&bars[s], (k >> 1) & 1);
+        const int s = (int)(k % NSX);
+        mbar_wait(&bars[s], (k / NSX) & 1);
         uint32_t *xst = xs + s * SW;
         uint32_t x[E];
         {
@@ -642,7 +642,7 @@ row_mac(const MacArgs A) {
             round0_finish<S_LOG, E_LOG>(x, exch, sidx, v, tw, twp, rtw_p, a, cx);
             rounds_rest<S_LOG, E_LOG, 1>(x, exch, sidx, v, tw, twp, rtw_p, a, cx);
         }
-        mbar_wait(&bars[2], k & 1);
+        mbar_wait(&bars[NSX], k & 1);
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
             const uint32_t *arow = as + w * S;
@@ -656,7 +656,7 @@ row_mac(const MacArgs A) {
         }
         __syncthreads();                                 // X stage s and A^ are free
         if (threadIdx.x == 0 && DBG != 2) {
-            if (it + 2 < it1) issue_x(it + 2, s);
+            if (it + NSX < it1) issue_x(it + NSX, s);
             if (it + 1 < it1) issue_a(it + 1);
         }
     }
