@@ -236,6 +236,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--limb-bits", type=int, default=0, help="force the limb width B (0 = planner)")
+    ap.add_argument("--batch", type=int, default=8, help="keys per pa_hash_batch in the stream-mode line")
     ap.add_argument("--only-device", action="store_true",
                     help="timed device steps only (no per-stage pass, no e2e): for ncu launch lists")
     args = ap.parse_args()
@@ -333,6 +334,31 @@ def main():
     nsteps_prof = args.steps
     stages = {kname: (v[0], v[1]) for kname, v in stages.items()}
 
+    # ---- stream mode (pa_hash_batch, NEXT-3): a batch of independent keys, MH / tail of one
+    # key overlapping the MMH of the next; reported beside the single-key `value`
+    stream_mode = None
+    if world == 1 and args.batch > 1:
+        keys_b = [key_dev] + [torch.empty_like(key_dev).copy_(key_dev.roll(j)) for j in range(1, args.batch)]
+        outs_b = [torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev) for _ in range(args.batch)]
+        for _ in range(2):
+            ctx.hash_batch(keys_b, outs_b)
+        torch.cuda.synchronize()
+        tb = []
+        for _ in range(max(3, args.steps // 5)):
+            if not args.no_flush:
+                flush.fill_(1)
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.hash_batch(keys_b, outs_b)
+            bb.record(stream)
+            bb.synchronize()
+            tb.append(a.elapsed_time(bb))
+        ms_b = statistics.median(tb)
+        stream_mode = {"keys_per_batch": args.batch, "value": args.batch * w.n / (ms_b * 1e-3) / 1e6, "unit": "Mbps",
+                       "ms_per_batch": ms_b, "ms_per_key": ms_b / args.batch,
+                       "api": "pa_hash_batch (device buffers; two buffer sets / streams, graph replay)"}
+
     e2e = None
     if world == 1:
         host_key = torch.from_numpy(key_full).pin_memory()
@@ -390,6 +416,7 @@ def main():
         "roofline": roof,
         "stages_ms_per_step": {kk: v[0] / nsteps_prof for kk, v in sorted(stages.items())},
         "e2e": e2e,
+        "stream": stream_mode,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample(w, 2)

@@ -125,6 +125,15 @@ int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out);
  * Asynchronous on the context stream. */
 int pa_hash(pa_ctx *ctx, const uint8_t *key_bits, uint8_t *out_bits);
 
+/* Stream mode: hash `count` independent keys with this
+ * context's hash function.  keys[j] / outs[j]: HOST arrays of DEVICE pointers, each as in
+ * pa_hash.  Keys alternate between two buffer sets and streams (forked from and joined
+ * back into the context stream), so one key's latency-bound MH / tail kernels overlap the
+ * next key's MMH transforms.  The first call allocates the second buffer set (about the
+ * per-hash scratch of pa_ctx_query's device_bytes minus the precomputed transforms).
+ * Asynchronous on the context stream; outputs are identical to count pa_hash calls. */
+int pa_hash_batch(pa_ctx *ctx, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count);
+
 /* End-to-end variant with HOST buffers: copies the key host->device, hashes,
  * copies the output device->host and synchronizes the stream before returning.
  * Pinned host memory gives full PCIe bandwidth; the copy is split in chunks that

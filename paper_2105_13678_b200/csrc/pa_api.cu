@@ -533,6 +533,15 @@ struct ProfRec {
     cudaEvent_t a, b;
 };
 
+// Per-hash working buffers (everything a hash writes).  A context has one active set;
+// pa_hash_batch adds a second set + stream and alternates keys between them.
+struct HashBufs {
+    uint32_t *res = nullptr, *scratch = nullptr, *acc = nullptr, *scratch_mh = nullptr, *acc_mh = nullptr;
+    uint64_t *S = nullptr;
+    uint32_t *coef = nullptr, *y1 = nullptr, *Z = nullptr, *cstate = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
 struct pa_ctx {
     Plan pl{};
     int device = 0;
@@ -568,8 +577,31 @@ struct pa_ctx {
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> evpool;
     std::map<std::string, std::pair<double, uint32_t>> acc_ms;
+    // pa_hash_batch: second buffer set (own stream), fork/join events, captured batch graph
+    bool alt_ready = false;
+    HashBufs alt;
+    size_t res_words = 0;
+    cudaEvent_t bev[2] = {};
+    cudaGraphExec_t bgraph_exec = nullptr;
+    std::vector<const void *> bgraph_ptrs;
+    uint32_t bgraph_launches = 0;
 };
 static constexpr int kCarrySlots = 8;
+
+// exchange the active per-hash buffers (and stream) with the alternate set
+static void swap_bufs(pa_ctx *c) {
+    std::swap(c->res, c->alt.res);
+    std::swap(c->scratch, c->alt.scratch);
+    std::swap(c->acc, c->alt.acc);
+    std::swap(c->scratch_mh, c->alt.scratch_mh);
+    std::swap(c->acc_mh, c->alt.acc_mh);
+    std::swap(c->S, c->alt.S);
+    std::swap(c->coef, c->alt.coef);
+    std::swap(c->y1, c->alt.y1);
+    std::swap(c->Z, c->alt.Z);
+    std::swap(c->cstate, c->alt.cstate);
+    std::swap(c->stream, c->alt.stream);
+}
 
 static cudaEvent_t ev_get(pa_ctx *c) {
     if (!c->evpool.empty()) { cudaEvent_t e = c->evpool.back(); c->evpool.pop_back(); return e; }
@@ -822,6 +854,7 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     const uint64_t res_words = std::max<uint64_t>(
         (uint64_t)c->nblk * Pm * std::max(rows_x, rows_a) * p.mmh.n_row,
         (uint64_t)Ph * std::max(rows_y, rows_b) * p.mh.n_row);
+    c->res_words = res_words;
     TRY(c->da.alloc(&c->res, res_words));
     TRY(c->da.alloc(&c->ahat, (size_t)c->nblk * Pm * Lm));
     TRY(c->da.alloc(&c->scratch, (size_t)c->nblk * Pm * Lm));
@@ -944,6 +977,12 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     for (auto e : c->evpool) cudaEventDestroy(e);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->hgraph_exec) cudaGraphExecDestroy(c->hgraph_exec);
+    if (c->bgraph_exec) cudaGraphExecDestroy(c->bgraph_exec);
+    if (c->alt_ready) {
+        cudaStreamSynchronize(c->alt.stream);
+        cudaStreamDestroy(c->alt.stream);
+        for (auto e : c->bev) cudaEventDestroy(e);
+    }
     if (c->key_dev) cudaFree(c->key_dev);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
@@ -972,6 +1011,7 @@ extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
     if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
     if (c->hgraph_exec) { cudaGraphExecDestroy(c->hgraph_exec); c->hgraph_exec = nullptr; }
+    if (c->bgraph_exec) { cudaGraphExecDestroy(c->bgraph_exec); c->bgraph_exec = nullptr; }
     c->stream = (cudaStream_t)stream;
     return PA_OK;
 }
@@ -1125,6 +1165,84 @@ extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8
     if (rc == PA_OK) rc = run_mh(c, c->y1, out_bits);
     c->launches_total += c->launches;
     return rc;
+}
+
+// ---- stream mode: `count` independent keys, hashed with the same
+// function, alternately on two buffer sets / streams so that one key's latency-bound
+// MH and tail kernels overlap the next key's MMH transforms.
+static int alloc_alt(pa_ctx *c) {
+    if (c->alt_ready) return PA_OK;
+    const Plan &p = c->pl;
+    const size_t Pm = p.mmh.nprimes, Lm = c->smmh.L, Ph = p.mh.nprimes, Lh = c->smh.L;
+    HashBufs &b = c->alt;
+    TRY(c->da.alloc(&b.res, c->res_words));
+    TRY(c->da.alloc(&b.scratch, (size_t)c->nblk * Pm * Lm));
+    TRY(c->da.alloc(&b.acc, Pm * Lm));
+    TRY(c->da.alloc(&b.scratch_mh, Ph * Lh));
+    TRY(c->da.alloc(&b.acc_mh, Ph * Lh));
+    TRY(c->da.alloc(&b.S, std::max<uint64_t>(c->W_fold, c->W_Z)));
+    TRY(c->da.alloc(&b.coef, std::max(Pm * Lm, Ph * Lh)));
+    TRY(c->da.alloc(&b.y1, c->W_fold));
+    TRY(c->da.alloc(&b.Z, c->W_Z));
+    TRY(c->da.alloc(&b.cstate, (size_t)c->cstate_stride * kCarrySlots));
+    CUDA_TRY(cudaStreamCreateWithFlags(&b.stream, cudaStreamNonBlocking));
+    for (auto &e : c->bev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->alt_ready = true;
+    return PA_OK;
+}
+
+static int batch_enqueue(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
+    // fork: the alternate stream starts after the work already on the ctx stream
+    CUDA_TRY(cudaEventRecord(c->bev[0], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->alt.stream, c->bev[0], 0));
+    uint32_t total = 0;
+    for (uint32_t j = 0; j < count; j++) {
+        if (j & 1) swap_bufs(c);
+        const int rc = hash_enqueue(c, keys[j], outs[j]);
+        total += c->launches;
+        if (j & 1) swap_bufs(c);
+        TRY(rc);
+    }
+    // join
+    CUDA_TRY(cudaEventRecord(c->bev[1], c->alt.stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->bev[1], 0));
+    c->launches = total;
+    return PA_OK;
+}
+
+extern "C" int pa_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
+    if (!c || (count && (!keys || !outs))) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
+    for (uint32_t j = 0; j < count; j++)
+        if (!keys[j] || !outs[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
+    if (count == 0) return PA_OK;
+    if (count == 1) return pa_hash(c, keys[0], outs[0]);
+    TRY(alloc_alt(c));
+    if (!graphs_enabled(c)) {
+        const int rc = batch_enqueue(c, keys, outs, count);
+        c->launches_total += c->launches;
+        return rc;
+    }
+    std::vector<const void *> ptrs;
+    for (uint32_t j = 0; j < count; j++) { ptrs.push_back(keys[j]); ptrs.push_back(outs[j]); }
+    if (!c->bgraph_exec || ptrs != c->bgraph_ptrs) {
+        if (c->bgraph_exec) { cudaGraphExecDestroy(c->bgraph_exec); c->bgraph_exec = nullptr; }
+        cudaGraph_t g = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = batch_enqueue(c, keys, outs, count);
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (rc != PA_OK) { if (g) cudaGraphDestroy(g); return rc; }
+        if (e != cudaSuccess) return set_err(PA_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        const cudaError_t e2 = cudaGraphInstantiate(&c->bgraph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e2 != cudaSuccess) { c->bgraph_exec = nullptr; return set_err(PA_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2)); }
+        c->bgraph_ptrs = ptrs;
+        c->bgraph_launches = c->launches;
+    }
+    CUDA_TRY(cudaGraphLaunch(c->bgraph_exec, c->stream));
+    c->launches = c->bgraph_launches;
+    c->launches_total += c->launches;
+    return PA_OK;
 }
 
 // End-to-end hash from host buffers.  The key is copied in kCopyGroups block groups on a

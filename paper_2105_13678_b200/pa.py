@@ -130,6 +130,19 @@ class PAContext:
         B.check(B.pa_hash(self._h, ctypes.c_void_p(key.data_ptr()), ctypes.c_void_p(out.data_ptr())))
         return out
 
+    def hash_batch(self, keys, outs=None):
+        """pa_hash_batch: a list of CUDA uint8 key tensors -> list of outputs (stream mode)."""
+        torch = self._torch
+        keys = [self._dev_u8(k, self.nbytes_in) for k in keys]
+        if outs is None:
+            outs = [torch.empty(self.nbytes_out, dtype=torch.uint8, device=k.device) for k in keys]
+        if len(outs) != len(keys):
+            raise ValueError("keys and outs differ in length")
+        kp = (ctypes.c_void_p * len(keys))(*[k.data_ptr() for k in keys])
+        op = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        B.check(B.pa_hash_batch(self._h, kp, op, len(keys)))
+        return outs
+
     def hash_host(self, key_host, out_host=None):
         """pa_hash_host: host buffers (numpy uint8 / pinned torch CPU tensor), synchronous."""
         torch = self._torch

@@ -4,4 +4,4 @@ mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-python -c "import json;d=json.load(open('gpurun_out/bench.json'));print(d['ms_per_step'], d['value'], d['e2e'], d['clocks']);print(json.dumps(d['stages_ms_per_step'],indent=0))"
+python -c "import json;d=json.load(open('gpurun_out/bench.json'));print(d['ms_per_step'], d['value'], d['e2e'], d['clocks']); print('stream', d.get('stream'));print(json.dumps(d['stages_ms_per_step'],indent=0))"

@@ -222,6 +222,27 @@ def test_graph_replay_on_stream():
         ctx.close()
 
 
+@pytest.mark.parametrize("on_stream", [False, True])
+def test_hash_batch_stream_mode(on_stream):
+    # pa_hash_batch (NEXT-3): alternating buffer sets / streams give the same bytes as
+    # one pa_hash per key; on a non-default stream the whole batch is a replayed graph
+    PAContext = _pa()
+    n, r, m, seed = 500_001, 4096, 30_000, 23
+    s = torch.cuda.Stream() if on_stream else torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        ctx = PAContext(n, r, m, seed=seed)
+        keys = [key_bytes(n, 100 + j) for j in range(5)]
+        kd = [torch.from_numpy(k).cuda() for k in keys]
+        for rep in range(2):
+            outs = ctx.hash_batch(kd)
+            s.synchronize()
+            for k, o in zip(keys, outs):
+                assert bytes(o.cpu().numpy()) == oracle_seeded(k, n, r, m, seed)
+            kd = kd[::-1]
+            keys = keys[::-1]
+        ctx.close()
+
+
 def _golden():
     path = os.path.join(ROOT, "tests", "golden", "digests.json")
     return json.load(open(path)) if os.path.exists(path) else {}
