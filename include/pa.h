@@ -103,8 +103,16 @@ typedef struct {
     const uint32_t *b_words;
     const uint32_t *c_words;
     void *stream;            /* cudaStream_t, NULL = legacy default stream */
-    int32_t limb_bits;       /* 0 = planner's choice, else force B (multiple of 8, 16..64) */
+    int32_t limb_bits;       /* 0 = planner's choice, else force B (multiple of 8, 16..256) */
     int32_t strict;          /* nonzero: reject m >= gamma ("gamma > beta") */
+    /* Paper mode (Algorithm 1 exactly): when
+     * nonzero, the key is split into paper_k blocks of gamma bits (r is ignored; gamma must
+     * be given), window t = key bits [t gamma, (t+1) gamma); a window equal to 2^gamma - 1
+     * is cast away and the next consumed (reading A10); alpha = gamma
+     * and m < gamma are required.  Needs n >= paper_k * gamma; fewer than
+     * paper_k usable windows -> PA_E_INSUFFICIENT_INPUT (pa_ctx_status / pa_hash_host).
+     * Not available for shard contexts. */
+    uint64_t paper_k;
 } pa_params;
 
 /* Create a context on the current CUDA device.  `p` is the Mersenne EXPONENT
@@ -148,6 +156,11 @@ int pa_mmh_partial(pa_ctx *ctx, const uint8_t *key_slice, uint32_t *y_out);
 /* Stages S6-S7: y = sum_{g<G} y_parts[g] mod p (each part ceil(gamma/32) words,
  * DEVICE, contiguous), then MH into out_bits (DEVICE, ceil(m/8) bytes). */
 int pa_mh_merge(pa_ctx *ctx, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits);
+
+/* Synchronizes the context stream and returns the device-side status of the last hash:
+ * PA_OK, or PA_E_INSUFFICIENT_INPUT (paper mode: fewer than paper_k usable windows; the
+ * output is then undefined). */
+int pa_ctx_status(pa_ctx *ctx);
 
 /* Free everything the context owns; NULL is a no-op. */
 void pa_ctx_destroy(pa_ctx *ctx);

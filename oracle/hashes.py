@@ -153,3 +153,44 @@ def pa_hash_seeded(key, n: int, r: int, m: int, seed: int, gamma: int | None = N
     pp = plan_params(n, r, m, gamma)
     a, b, c = expand_hash_keys(seed, pp["k"], pp["gamma"], pp["alpha"])
     return pa_hash(key, n, r, m, pp["gamma"], a, b, c)
+
+
+# ------------------------------------------ Algorithm 1 in the paper's shape, byte keys
+def paper_blocks(key, n: int, gamma: int, k: int):
+    """bits_to_field_blocks on an n-bit
+    MSB-first byte key, with Python-int slicing instead of a bit list: windows are the
+    successive gamma-bit windows at bit offsets t*gamma; a window equal to 2^gamma - 1 is
+    cast away and the next one consumed (reading A10).  Returns (blocks, windows used).
+    Raises ValueError (SPEC.md:74 InsufficientInput) if fewer than k windows qualify."""
+    kb = bytes(np.asarray(key, dtype=np.uint8)) if not isinstance(key, bytes) else key
+    nbytes = (n + 7) // 8
+    if len(kb) < nbytes:
+        raise ValueError("key shorter than ceil(n/8) bytes")
+    full = int.from_bytes(kb[:nbytes], "big") >> (8 * nbytes - n)      # the n-bit integer
+    allones = (1 << gamma) - 1
+    blocks, t = [], 0
+    while len(blocks) < k:
+        if (t + 1) * gamma > n:
+            raise ValueError(f"insufficient input: filled {len(blocks)} of {k} blocks")
+        v = (full >> (n - (t + 1) * gamma)) & allones
+        t += 1
+        if v == allones:
+            continue
+        blocks.append(v)
+    return blocks, t
+
+
+def pa_hash_paper(key, n: int, gamma: int, k: int, m: int, a: Sequence[int], b: int, c: int) -> bytes:
+    """Algorithm 1 exactly as the paper shapes it: k gamma-bit blocks
+    with the reload rule, alpha = gamma, beta = m < gamma; output MSB-first."""
+    if m >= gamma:
+        raise ValueError("Algorithm 1 requires gamma > beta (PAPER.md:143)")
+    x, _ = paper_blocks(key, n, gamma, k)
+    y = mmh_eval(a, x, gamma)
+    return mh_output(y, b, c, gamma, m)
+
+
+def pa_hash_paper_seeded(key, n: int, gamma: int, k: int, m: int, seed: int) -> bytes:
+    """pa_hash_paper with hash keys from ``seed`` (reading A7; alpha = gamma)."""
+    a, b, c = expand_hash_keys(seed, k, gamma, gamma)
+    return pa_hash_paper(key, n, gamma, k, m, a, b, c)

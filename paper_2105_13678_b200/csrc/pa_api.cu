@@ -131,6 +131,7 @@ static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int for
 
 struct Plan {
     uint64_t n, r, m, gamma, alpha, k, b0, b1, seed;
+    uint64_t paper_k;        // paper mode (gamma-bit blocks, reload rule) when nonzero
     int strict, force_B;
     pa_stage_plan mmh, mh;
 };
@@ -145,12 +146,32 @@ static int make_plan(const pa_params *prm, Plan *P) {
     Plan p{};
     p.n = prm->n; p.r = prm->r; p.m = prm->m; p.seed = prm->seed;
     p.strict = prm->strict; p.force_B = prm->limb_bits;
+    p.paper_k = prm->paper_k;
     if (p.n < 1) return set_err(PA_E_PARAM, "n must be >= 1");
-    if (p.r < 16 || p.r % 16) return set_err(PA_E_PARAM, "r must be >= 16 and a multiple of 16 (got %llu)", (unsigned long long)p.r);
     if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
     if (p.force_B && (p.force_B < 16 || p.force_B > kMaxLimbBits || p.force_B % 8))
         return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, %d]", kMaxLimbBits);
     uint64_t g = prm->gamma;
+    if (p.paper_k) {
+        // paper mode: Algorithm 1 as written, gamma-bit blocks
+        if (!g) return set_err(PA_E_PARAM, "paper mode needs an explicit gamma (p = 2^gamma - 1)");
+        if (!is_mersenne(g)) return set_err(PA_E_PARAM, "gamma=%llu is not a known Mersenne exponent (SPEC.md:33)", (unsigned long long)g);
+        if (p.m >= g) return set_err(PA_E_PARAM, "paper mode: m must be < gamma (PAPER.md:143)");
+        if (p.paper_k > p.n / g) return set_err(PA_E_PARAM, "paper mode: n must be >= paper_k * gamma (n = gamma k, PAPER.md:282)");
+        if (prm->block_begin || prm->block_end) return set_err(PA_E_PARAM, "paper mode is not available for shard contexts");
+        p.gamma = g;
+        p.r = g;
+        p.alpha = g;
+        p.k = p.paper_k;
+        p.b0 = 0; p.b1 = p.k;
+        if (plan_product(g, g, p.k, p.force_B, p.k, &p.mmh) != PA_OK)
+            return set_err(PA_E_BOUND, "no transform plan covers the MMH coefficient bound");
+        if (plan_product(g, g, 1, p.force_B, 1, &p.mh) != PA_OK)
+            return set_err(PA_E_BOUND, "no transform plan covers the MH product");
+        *P = p;
+        return PA_OK;
+    }
+    if (p.r < 16 || p.r % 16) return set_err(PA_E_PARAM, "r must be >= 16 and a multiple of 16 (got %llu)", (unsigned long long)p.r);
     if (g == 0) {
         for (uint64_t e : kMersenne) if (e > p.r) { g = e; break; }
         if (g == 0) return set_err(PA_E_PARAM, "no known Mersenne exponent > r");
@@ -560,6 +581,10 @@ struct pa_ctx {
     uint32_t *cstate = nullptr;               // carry look-back: [kCarrySlots][1 + ntiles]
     uint32_t cstate_stride = 0;
     int cslot = 0;
+    uint64_t *offs = nullptr;                 // paper mode: bit offset of each block's window
+    uint32_t *wflags = nullptr;               // paper mode: window has a zero bit, [T]
+    uint32_t *status = nullptr;               // device status of the last hash (paper mode)
+    uint32_t T = 0;                           // paper mode: windows in the key
     uint8_t *key_dev = nullptr;               // staging for pa_hash_host
     cudaStream_t copy_stream = nullptr;       // pa_hash_host H2D copies
     cudaGraphExec_t graph_exec = nullptr;     // captured pa_hash (graphs_enabled)
@@ -870,6 +895,13 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     TRY(c->da.alloc(&c->Z, c->W_Z));
     c->cstate_stride = (uint32_t)(cdiv(Smax, std::min(kCarryTile, kCCTile)) + 2);
     TRY(c->da.alloc(&c->cstate, (size_t)c->cstate_stride * kCarrySlots));
+    TRY(c->da.alloc(&c->status, 4));
+    CUDA_TRY(cudaMemsetAsync(c->status, 0, 4, c->stream));
+    if (p.paper_k) {
+        c->T = (uint32_t)(p.n / p.gamma);
+        TRY(c->da.alloc(&c->offs, p.k));
+        TRY(c->da.alloc(&c->wflags, c->T));
+    }
 
     // ---- hash keys (reading A7): a_i for the shard's blocks, b, c
     std::vector<uint32_t> aw((size_t)c->nblk * Wa32), bw, cw, tmp;
@@ -994,6 +1026,16 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     delete c;
 }
 
+extern "C" int pa_ctx_status(pa_ctx *c) {
+    if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    uint32_t st = 0;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(&st, c->status, 4, cudaMemcpyDeviceToHost));
+    if (st) return set_err(PA_E_INSUFFICIENT_INPUT, "paper mode: fewer than %llu windows of the key differ from 2^gamma - 1 (SPEC.md:74)",
+                           (unsigned long long)c->pl.k);
+    return PA_OK;
+}
+
 extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
     if (!c || !info) return set_err(PA_E_PARAM, "NULL argument");
     memset(info, 0, sizeof *info);
@@ -1036,10 +1078,67 @@ static KeySrc key_src(const pa_ctx *c, const uint8_t *key_slice, uint32_t v0, ui
     return ks;
 }
 
+template <int NW>
+static void launch_pack_bits(const KeySrc &s, const uint64_t *offs, uint32_t gamma, uint32_t B, uint32_t wx,
+                             uint32_t nvec, const PrimeK *pk, uint32_t P, uint32_t wxp, uint32_t *res, cudaStream_t st) {
+    const dim3 grid((wxp + kPackT - 1) / kPackT, nvec);
+    pack_bits_residues<NW><<<grid, kPackT, 0, st>>>(s, offs, gamma, B, wx, pk, P, wxp, res);
+}
+
+// ---- paper mode S1: windows with a zero bit -> block offsets (reload rule), pack
+static int paper_pack(pa_ctx *c, const uint8_t *key) {
+    const Plan &p = c->pl;
+    KeySrc ks{};
+    ks.key = key;
+    ks.nbytes = cdiv(p.n, 8);
+    ks.last_mask = (p.n % 8) ? ((0xFFu << (8 - p.n % 8)) & 0xFFu) : 0xFFu;
+    ks.aligned = (((uintptr_t)key) & 3) == 0;
+    {
+        ProfScope ps(c, "mmh_reload_windows");
+        CUDA_TRY(cudaMemsetAsync(c->wflags, 0, (size_t)c->T * 4, c->stream));
+        const uint64_t nchunk = cdiv(cdiv((uint64_t)c->T * p.gamma, 8), 16);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(nchunk, 256), (uint64_t)g_num_sms * 16);
+        window_flags<<<std::max(1u, grid), 256, 0, c->stream>>>(ks, (uint32_t)p.gamma, c->T, c->wflags);
+        window_resolve<<<1, 32, 0, c->stream>>>(c->wflags, c->T, (uint32_t)p.k, (uint32_t)p.gamma, c->offs, c->status);
+        c->launches += 2;
+        CUDA_TRY(cudaGetLastError());
+    }
+    ProfScope ps(c, "mmh_pack");
+    const uint32_t B = p.mmh.limb_bits, P = p.mmh.nprimes;
+    const uint32_t wx = (uint32_t)cdiv(p.gamma, B);
+    const uint32_t wxp = c->rows_mmh * p.mmh.n_row;
+    const int nw = (int)cdiv(B, 32);
+    switch (nw) {
+#define PA_PB(N) case N: launch_pack_bits<N>(ks, c->offs, (uint32_t)p.gamma, B, wx, c->nblk, c->smmh.pk, P, wxp, c->res, c->stream); break;
+        PA_PB(1) PA_PB(2) PA_PB(3) PA_PB(4) PA_PB(5) PA_PB(6) PA_PB(7) PA_PB(8)
+#undef PA_PB
+        default: return set_err(PA_E_PARAM, "unsupported limb width %u", B);
+    }
+    c->launches++;
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
 // ---- S1+S2 first pass for blocks [v0, v1) of the shard
 static int mmh_forward(pa_ctx *c, const uint8_t *key_slice, uint32_t v0, uint32_t v1) {
     const uint32_t P = c->pl.mmh.nprimes;
     const size_t wxp = (size_t)c->rows_mmh * c->pl.mmh.n_row;
+    if (c->pl.paper_k) {
+        if (v0 != 0 || v1 != c->nblk) return set_err(PA_E_STATE, "paper mode hashes all blocks at once");
+        TRY(paper_pack(c, key_slice));
+        ProfScope ps(c, "mmh_fwd_col");
+        ColArgs A{};
+        A.nt = ntt_args(c->smmh, 0, 0);
+        A.src = c->res;
+        A.rows = c->rows_mmh;
+        A.tw4 = c->smmh.tw4[0];
+        A.dst = c->scratch;
+        A.nvec = c->nblk;
+        A.units = (c->pl.mmh.n_row / 32) * P * c->nblk;
+        TRY(launch_col<COL_FWD>(__builtin_ctz(c->pl.mmh.n_col), __builtin_ctz(c->pl.mmh.n_row), A, c->stream));
+        c->launches++;
+        return PA_OK;
+    }
     return stage_pack_col(c, c->smmh, KeyLimbs{key_src(c, key_slice, v0, v1)}, v1 - v0, c->rows_mmh,
                           c->res + (size_t)v0 * P * wxp, c->scratch + (size_t)v0 * P * c->smmh.L, "mmh_pack",
                           "mmh_fwd_col");
@@ -1257,11 +1356,12 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     CUDA_TRY(cudaEventRecord(c->copy_ev[kCopyGroups], c->stream));
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[kCopyGroups], 0));
     const uint32_t nblk = c->nblk;
-    const int G = (int)std::min<uint32_t>(kCopyGroups, nblk);
+    // paper mode: the reload rule needs the whole key before any block offset is known
+    const int G = c->pl.paper_k ? 1 : (int)std::min<uint32_t>(kCopyGroups, nblk);
     const uint64_t R = c->pl.r / 8;
     for (int g = 0; g < G; g++) {
-        const uint64_t lo = std::min<uint64_t>(nb, (uint64_t)(nblk * g / G) * R);
-        const uint64_t hi = std::min<uint64_t>(nb, (uint64_t)(nblk * (g + 1) / G) * R);
+        const uint64_t lo = G == 1 ? 0 : std::min<uint64_t>(nb, (uint64_t)(nblk * g / G) * R);
+        const uint64_t hi = G == 1 ? nb : std::min<uint64_t>(nb, (uint64_t)(nblk * (g + 1) / G) * R);
         if (hi > lo) CUDA_TRY(cudaMemcpyAsync(c->key_dev + lo, key_host + lo, hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
         CUDA_TRY(cudaEventRecord(c->copy_ev[g], c->copy_stream));
     }
@@ -1317,6 +1417,7 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
         c->launches_total += c->launches;
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->pl.paper_k) return pa_ctx_status(c);
     return PA_OK;
 }
 

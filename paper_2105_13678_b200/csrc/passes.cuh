@@ -267,6 +267,128 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = limb_words_redc<NW>(w, ks[pi]);
 }
 
+// ---------------------------------------------------------------- paper mode (NEXT-1)
+// Algorithm 1 as written: gamma-bit windows t = key bits
+// [t gamma, (t+1) gamma) (MSB-first); a window equal to 2^gamma - 1 is cast
+// away and the next one consumed (reading A10).  Windows stay at
+// multiples of gamma, so the reload rule is: block i = the i-th window with a zero bit.
+
+// flags[t] = 1 if window t (t < T) contains a zero bit (flags zeroed by the caller).
+__global__ void __launch_bounds__(256) window_flags(const KeySrc s, uint32_t gamma, uint32_t T, uint32_t *flags) {
+    const uint64_t nbits = (uint64_t)T * gamma;
+    const uint64_t nbytes = (nbits + 7) >> 3;
+    const uint64_t nchunk = (nbytes + 15) >> 4;                // 16 bytes per thread
+    for (uint64_t ch = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ch < nchunk;
+         ch += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t last = 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint64_t wb = ch * 16 + 4 * q;                 // first byte of this word
+            if (wb >= nbytes) break;
+            const uint32_t word = key_word(s, (int64_t)(wb >> 2));
+#pragma unroll
+            for (int bb = 0; bb < 4; bb++) {
+                const uint64_t b = wb + bb;
+                if (b >= nbytes) break;
+                uint32_t z = ~(word >> (8 * bb)) & 0xFFu;          // zero bits, bit 7 = position 8b
+                const uint64_t p0 = 8 * b;
+                if (p0 + 8 > nbits) z &= (0xFF00u >> (nbits - p0)) & 0xFFu;   // positions >= nbits
+                if (!z) continue;
+                const uint32_t t0 = (uint32_t)(p0 / gamma), t1 = (uint32_t)((p0 + 7) / gamma);
+                if (t0 == t1) {
+                    if (t0 != last) { flags[t0] = 1u; last = t0; }
+                } else {
+                    for (int i = 0; i < 8; i++)
+                        if ((z >> (7 - i)) & 1u) {
+                            const uint32_t t = (uint32_t)((p0 + i) / gamma);
+                            if (t != last && t < T) { flags[t] = 1u; last = t; }
+                        }
+                }
+            }
+        }
+    }
+}
+
+// offs[i] = bit offset of block i (the i-th window with a zero bit); status 1 if fewer
+// than k windows qualify (SPEC.md:74 InsufficientInput), else 0.  One thread.
+__global__ void window_resolve(const uint32_t *flags, uint32_t T, uint32_t k, uint32_t gamma, uint64_t *offs,
+                               uint32_t *status) {
+    if (threadIdx.x || blockIdx.x) return;
+    uint32_t i = 0;
+    for (uint32_t t = 0; t < T && i < k; t++)
+        if (flags[t]) offs[i++] = (uint64_t)t * gamma;
+    *status = (i < k) ? 1u : 0u;
+    for (; i < k; i++) offs[i] = 0;                            // output undefined; reads stay in bounds
+}
+
+// S1 in paper mode: block iv = the gamma-bit window at key bit offs[iv]; limb j, word w =
+// integer bits [B j + 32 w, + 32) = the 32 key bits starting at
+// q = offs[iv] + gamma - (B j + 32 w) - 32 (MSB-first), bits before the window read 0.
+template <int NW>
+__global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, const uint64_t *__restrict__ offs,
+                                                           uint32_t gamma, uint32_t B, uint32_t wx,
+                                                           const PrimeK *__restrict__ pk, uint32_t P, uint32_t wxp,
+                                                           uint32_t *__restrict__ res) {
+    constexpr int MAXW = kPackT * NW + 8;
+    __shared__ uint32_t sw[MAXW];
+    __shared__ PrimeK ks[kMaxPrimes];
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) ks[i] = pk[i];
+    const uint32_t iv = blockIdx.y;
+    const uint32_t jt0 = blockIdx.x * kPackT;
+    const int64_t off = (int64_t)offs[iv];
+    const uint32_t jt1 = min(jt0 + kPackT, wx);
+    // key bits of the tile: [off + gamma - B jt1, off + gamma - B jt0), clipped at off
+    int64_t blo = off + (int64_t)gamma - (int64_t)B * jt1 - 32;
+    if (blo < off - 32) blo = off - 32;
+    const int64_t bhi = off + (int64_t)gamma - (int64_t)B * jt0;
+    const int64_t gw0 = (blo >> 3) >> 2;                      // first staged word (floor)
+    const int nw = (jt0 < jt1) ? (int)((((bhi + 7) >> 3) + 3) / 4 - gw0 + 2) : 0;
+    constexpr int KU = (MAXW + kPackT - 1) / kPackT;
+    {
+        uint32_t v[KU];
+#pragma unroll
+        for (int u = 0; u < KU; u++) {
+            const int k = threadIdx.x + u * kPackT;
+            v[u] = (k < nw && k < MAXW) ? key_word(s, gw0 + k) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < KU; u++) {
+            const int k = threadIdx.x + u * kPackT;
+            if (k < nw && k < MAXW) sw[k] = v[u];
+        }
+    }
+    __syncthreads();
+    const uint32_t j = jt0 + threadIdx.x;
+    if (j >= wxp) return;
+    uint32_t w[NW];
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+        const int64_t ib = (int64_t)B * j + 32 * i;            // integer bit of the word's LSB
+        uint32_t v = 0;
+        if (j < wx && ib < (int64_t)gamma) {
+            const int64_t q = off + (int64_t)gamma - ib - 32;  // key bit of the word's MSB
+            const int64_t rb = (q >> 3) - 4 * gw0;             // staged byte (q >= off - 32 >= 4 gw0 * 8 - ...)
+            const int sh = (int)(q & 7);
+            const int wi = (int)(rb >> 2), bb = (int)(rb & 3);
+            const uint32_t a0 = (wi >= 0) ? sw[wi] : 0u, a1 = sw[wi + 1], a2 = sw[wi + 2];
+            const uint32_t lo = __funnelshift_r(a0, a1, 8 * bb), hi = __funnelshift_r(a1, a2, 8 * bb);
+            const uint64_t be = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+            v = (uint32_t)(be >> (32 - sh));
+            const int64_t valid = (int64_t)gamma - ib;          // bits of this word inside the window
+            if (valid < 32) v &= (1u << valid) - 1u;
+        }
+        w[i] = v;
+        any |= v;
+    }
+    uint32_t *o = res + (size_t)iv * P * wxp + j;
+    if (!any) {
+        for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = 0u;
+        return;
+    }
+    for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = limb_words_redc<NW>(w, ks[pi]);
+}
+
 struct KeyLimbs {
     KeySrc s;
     __device__ __forceinline__ uint64_t operator()(uint32_t iv, uint32_t j) const { return key_limb(s, iv, j); }

@@ -19,9 +19,10 @@ def _words(v: int, bits: int) -> np.ndarray:
 
 
 def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
-            stream=None, limb_bits=0, strict=False, keep=None) -> B.pa_params:
+            stream=None, limb_bits=0, strict=False, keep=None, paper_k=0) -> B.pa_params:
     prm = B.pa_params()
     prm.n, prm.r, prm.m, prm.gamma, prm.seed = n, r, m, gamma, seed & (2**64 - 1)
+    prm.paper_k = paper_k
     if block_range is not None:
         prm.block_begin, prm.block_end = block_range
     prm.limb_bits = limb_bits
@@ -29,7 +30,7 @@ def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
     prm.stream = stream
     keep = [] if keep is None else keep
     if a is not None or b is not None or c is not None:
-        info = plan(n, r, m, gamma, block_range=block_range, limb_bits=limb_bits)
+        info = plan(n, r, m, gamma, block_range=block_range, limb_bits=limb_bits, paper_k=paper_k)
         g, alpha = info["gamma"], info["alpha"]
         if a is not None:
             aw = np.concatenate([_words(v, g) for v in a]).astype("<u4")
@@ -47,9 +48,9 @@ def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
 
 
 def plan(n: int, r: int, m: int, gamma: int = 0, block_range=None, limb_bits: int = 0,
-         strict: bool = False) -> dict:
+         strict: bool = False, paper_k: int = 0) -> dict:
     """Validate parameters and return the transform plan (host only, no GPU)."""
-    prm = _params(n, r, m, gamma, 0, block_range, limb_bits=limb_bits, strict=strict)
+    prm = _params(n, r, m, gamma, 0, block_range, limb_bits=limb_bits, strict=strict, paper_k=paper_k)
     info = B.pa_info()
     B.check(B.pa_plan(ctypes.byref(prm), ctypes.byref(info)))
     return info.as_dict()
@@ -66,7 +67,7 @@ class PAContext:
 
     def __init__(self, n: int, r: int, m: int, gamma: int = 0, seed: int = 0, *,
                  block_range=None, a=None, b=None, c=None, stream=None, limb_bits: int = 0,
-                 strict: bool = False):
+                 strict: bool = False, paper_k: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise B.PAError(B.PA_E_CUDA, "no CUDA device: the library has no CPU path")
@@ -75,7 +76,7 @@ class PAContext:
         self.stream = st
         keep: list = []
         prm = _params(n, r, m, gamma, seed, block_range, a, b, c, ctypes.c_void_p(st.cuda_stream),
-                      limb_bits, strict, keep)
+                      limb_bits, strict, keep, paper_k)
         h = ctypes.c_void_p()
         B.check(B.pa_ctx_create_ex(ctypes.byref(prm), ctypes.byref(h)))
         self._h = h
@@ -88,6 +89,11 @@ class PAContext:
         self.y_words = (self.gamma + 31) // 32
 
     # ------------------------------------------------------------------ queries
+    def status(self) -> None:
+        """pa_ctx_status: raises PAError(PA_E_INSUFFICIENT_INPUT) if the last hash (paper
+        mode) found fewer than paper_k usable windows."""
+        B.check(B.pa_ctx_status(self._h))
+
     def query(self) -> dict:
         info = B.pa_info()
         B.check(B.pa_ctx_query(self._h, ctypes.byref(info)))

@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import hashes, seeds  # noqa: E402
-from synth import CONFIGS, key_bytes  # noqa: E402
+from synth import CONFIGS, PAPER_CONFIGS, key_bytes  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "digests.json")
 
@@ -39,7 +39,40 @@ def _partial(args):
     return hashes.reduce_mersenne(acc, pp["gamma"])
 
 
+def _paper_partial(args):
+    name, lo, hi = args
+    w = PAPER_CONFIGS[name]
+    key = key_bytes(w.n, w.key_seed)
+    x, _ = hashes.paper_blocks(key, w.n, w.gamma, w.k)
+    acc = 0
+    for i in range(lo, hi):
+        acc += seeds.expand_a(w.hash_seed, i, w.gamma) * x[i]
+    return hashes.reduce_mersenne(acc, w.gamma)
+
+
+def golden_paper(name: str, procs: int) -> dict:
+    """Paper mode (NEXT-1): Algorithm 1 with gamma-bit blocks, reload, alpha = gamma."""
+    w = PAPER_CONFIGS[name]
+    t0 = time.time()
+    G = min(procs, w.k)
+    cuts = [(name, w.k * g // G, w.k * (g + 1) // G) for g in range(G)]
+    with Pool(procs) as pool:
+        ys = pool.map(_paper_partial, cuts)
+    y = hashes.merge_residues(ys, w.gamma)
+    b, c = seeds.expand_b(w.hash_seed, w.gamma), seeds.expand_c(w.hash_seed, w.gamma)
+    out = hashes.mh_output(y, b, c, w.gamma, w.m)
+    return {"config": name, "mode": "paper (gamma-bit blocks, reload rule, alpha = gamma)", "n": w.n,
+            "gamma": w.gamma, "alpha": w.gamma, "k": w.k, "m": w.m, "key_seed": w.key_seed,
+            "hash_seed": w.hash_seed,
+            "y_sha256": hashlib.sha256(y.to_bytes((w.gamma + 7) // 8, "little")).hexdigest(),
+            "out_sha256": hashlib.sha256(out).hexdigest(), "out_head": out[:16].hex(),
+            "oracle": "oracle.hashes.paper_blocks + CPython int products, fold reduction",
+            "seconds": round(time.time() - t0, 1)}
+
+
 def golden(name: str, procs: int) -> dict:
+    if name in PAPER_CONFIGS:
+        return golden_paper(name, procs)
     w = CONFIGS[name]
     pp = hashes.plan_params(w.n, w.r, w.m)
     k = pp["k"]

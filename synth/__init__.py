@@ -13,4 +13,4 @@ no transforms).  It only produces:
 Both the oracle (``oracle/``) and the CUDA product path consume these bytes;
 neither imports the other.
 """
-from .workloads import CONFIGS, Workload, get_workload, key_bytes, special_key  # noqa: F401
+from .workloads import CONFIGS, PAPER_CONFIGS, PaperWorkload, Workload, get_workload, key_bytes, special_key  # noqa: F401

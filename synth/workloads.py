@@ -52,6 +52,33 @@ CONFIGS: dict[str, Workload] = {
 }
 
 
+# the paper's own shape (Algorithm 1 with gamma-bit blocks, reload
+# rule, m < gamma): the CV-QKD case of Table 3 (k = 10) with the gamma SPEC
+# derives for the 2.6e8-bit block: n = gamma k = 259,649,510, compression
+# ratio 0.0972 -> m = round(0.0972 n) = 25,237,932 < gamma.
+@dataclass(frozen=True)
+class PaperWorkload:
+    name: str
+    n: int          # key bits (= gamma k, no spare windows)
+    gamma: int      # Mersenne exponent, blocks are gamma bits
+    k: int          # blocks
+    m: int          # output bits (< gamma)
+    cfg_no: int
+
+    @property
+    def key_seed(self) -> int:
+        return 0x6B6579 + self.cfg_no
+
+    @property
+    def hash_seed(self) -> int:
+        return 0x5EED0000 + self.cfg_no
+
+
+PAPER_CONFIGS: dict[str, PaperWorkload] = {
+    "P1": PaperWorkload("P1", 259_649_510, 25_964_951, 10, 25_237_932, 11),
+}
+
+
 def get_workload(name: str) -> Workload:
     return CONFIGS[name]
 

@@ -136,3 +136,20 @@ def test_ctx_create_without_gpu_fails_loudly():
     with pytest.raises(B.PAError):
         P.PAContext(1 << 12, 256, 100)
     assert not B.pa_ctx_create(1 << 12, 256, 100, 0, 1)
+
+
+def test_plan_paper_mode():
+    # NEXT-1: Algorithm 1 in the paper's shape (gamma-bit blocks, alpha = gamma)
+    info = P.plan(259_649_510, 0, 25_237_932, 25_964_951, paper_k=10)
+    assert info["gamma"] == info["alpha"] == 25_964_951 and info["k"] == 10
+    for s in (info["mmh"], info["mh"]):
+        assert s["bound_log2"] < s["modulus_log2"]
+    bad = [dict(n=1000, r=0, m=10, gamma=0, paper_k=3),            # gamma required
+           dict(n=1000, r=0, m=107, gamma=107, paper_k=3),         # m < gamma
+           dict(n=300, r=0, m=10, gamma=107, paper_k=3),           # n >= k gamma
+           dict(n=1000, r=0, m=10, gamma=100, paper_k=3)]          # not a Mersenne exponent
+    for kw in bad:
+        with pytest.raises(B.PAError):
+            P.plan(kw["n"], kw["r"], kw["m"], kw["gamma"], paper_k=kw["paper_k"])
+    with pytest.raises(B.PAError):
+        P.plan(1000, 0, 10, 107, block_range=(0, 1), paper_k=3)    # no shards

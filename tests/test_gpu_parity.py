@@ -243,21 +243,79 @@ def test_hash_batch_stream_mode(on_stream):
         ctx.close()
 
 
+def _paper_key(n, gamma, seed, allones=(), trailing_ones=False):
+    """Random n-bit key with the given gamma-bit windows set to all ones."""
+    key = bytearray(key_bytes(n, seed))
+    full = int.from_bytes(bytes(key), "big") >> (8 * len(key) - n)
+    ones = (1 << gamma) - 1
+    for t in allones:
+        full |= ones << (n - (t + 1) * gamma)
+    if trailing_ones:
+        full |= (1 << (n % gamma)) - 1 if n % gamma else 0
+    nb = (n + 7) // 8
+    return np.frombuffer((full << (8 * nb - n)).to_bytes(nb, "big"), np.uint8).copy()
+
+
+@pytest.mark.parametrize("gamma,k,extra,allones", [
+    (521, 3, 0, ()), (607, 10, 1, (4,)), (1279, 4, 3, (0, 1, 5)), (4423, 6, 2, (6,)),
+    (19937, 3, 1, (0,)), (9689, 10, 0, ())])
+def test_paper_mode_parity(gamma, k, extra, allones):
+    # NEXT-1: gamma-bit blocks, reload rule (PAPER.md:130,147-148), alpha = gamma, m < gamma
+    PAContext = _pa()
+    n = (k + extra) * gamma + 5
+    m = gamma - 3
+    key = _paper_key(n, gamma, gamma + k, allones)
+    seed = 77 + gamma
+    ctx = PAContext(n, 0, m, gamma, seed=seed, paper_k=k)
+    out = ctx.hash(torch.from_numpy(key).cuda())
+    ctx.status()
+    got = bytes(out.cpu().numpy())
+    want = hashes.pa_hash_paper_seeded(key, n, gamma, k, m, seed)
+    assert got == want
+    assert bytes(ctx.hash_host(key)) == want
+    ctx.close()
+
+
+def test_paper_mode_insufficient_input():
+    PAContext = _pa()
+    gamma, k = 607, 4
+    n = 5 * gamma
+    key = _paper_key(n, gamma, 3, allones=(0, 2))                    # only 3 usable windows
+    ctx = PAContext(n, 0, 100, gamma, seed=1, paper_k=k)
+    ctx.hash(torch.from_numpy(key).cuda())
+    with pytest.raises(Exception) as e:
+        ctx.status()
+    assert "INSUFFICIENT" in str(e.value)
+    with pytest.raises(Exception):
+        ctx.hash_host(key)
+    key = _paper_key(n, gamma, 3, allones=(0,))                       # 4 usable windows: fine
+    out = ctx.hash(torch.from_numpy(key).cuda())
+    ctx.status()
+    assert bytes(out.cpu().numpy()) == hashes.pa_hash_paper_seeded(key, n, gamma, k, 100, 1)
+    ctx.close()
+
+
 def _golden():
     path = os.path.join(ROOT, "tests", "golden", "digests.json")
     return json.load(open(path)) if os.path.exists(path) else {}
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5a", "C5b", "C5c"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5a", "C5b", "C5c", "P1"])
 def test_full_size_golden(name):
+    from synth import PAPER_CONFIGS
     db = _golden()
     if name not in db:
         pytest.skip(f"no golden digest for {name}")
     rec = db[name]
-    w = CONFIGS[name]
     PAContext = _pa()
-    key = key_bytes(w.n, w.key_seed)
-    ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed)
+    if name in PAPER_CONFIGS:
+        w = PAPER_CONFIGS[name]
+        key = key_bytes(w.n, w.key_seed)
+        ctx = PAContext(w.n, 0, w.m, w.gamma, seed=w.hash_seed, paper_k=w.k)
+    else:
+        w = CONFIGS[name]
+        key = key_bytes(w.n, w.key_seed)
+        ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed)
     out = ctx.hash(torch.from_numpy(key).cuda())
     torch.cuda.synchronize()
     got = bytes(out.cpu().numpy())

@@ -249,3 +249,38 @@ def test_special_keys_oracles_agree(kind):
     assert schoolbook.pa_hash(key, n, r, m, pp["gamma"], a, b, c, nthreads=2) == py
     if kind == "zero":
         assert py == hashes.pack_output(c >> (pp["alpha"] - m), m)
+
+
+def test_paper_blocks_match_bit_list_version():
+    # the byte-key fast path of Algorithm 1's split + reload equals bits_to_field_blocks
+    import random
+    rng = random.Random(7)
+    for gamma in (5, 7, 13, 17):
+        k = 4
+        for trial in range(30):
+            nb = rng.randrange(k * gamma // 8 + 2, k * gamma // 8 + 12)
+            kb = bytearray(rng.getrandbits(8) for _ in range(nb))
+            # plant all-ones windows to exercise the reload rule
+            n = 8 * nb - rng.randrange(0, 8)
+            bits = [(kb[i >> 3] >> (7 - (i & 7))) & 1 for i in range(n)]
+            for t in range(n // gamma):
+                if rng.random() < 0.3:
+                    for q in range(t * gamma, (t + 1) * gamma):
+                        bits[q] = 1
+            kb = bytearray((n + 7) // 8)
+            for i, bit in enumerate(bits):
+                kb[i >> 3] |= bit << (7 - (i & 7))
+            try:
+                want, used, _ = hashes.bits_to_field_blocks(bits, gamma, k)
+            except ValueError:
+                with pytest.raises(ValueError):
+                    hashes.paper_blocks(bytes(kb), n, gamma, k)
+                continue
+            got, t_used = hashes.paper_blocks(bytes(kb), n, gamma, k)
+            assert got == want and t_used * gamma == used
+
+
+def test_pa_hash_paper_spec_example():
+    # gamma=3, k=2, m=2, a=(3,5), b=3, c=1, bits 010 110 -> 10
+    key = bytes([0b01011000])
+    assert hashes.pa_hash_paper(key, 6, 3, 2, 2, [3, 5], 3, 1) == bytes([0b10000000])
