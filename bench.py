@@ -186,11 +186,15 @@ def cpu_oracle_sample(w, nblocks: int = 2) -> dict:
     """Time the CPU oracle (oracle/, as it stands) on a bounded sample of the workload:
     the MMH products + fold of the first `nblocks` blocks."""
     from oracle import hashes, seeds
-    from synth import key_bytes
-    pp = hashes.plan_params(w.n, w.r, w.m)
+    from synth import PAPER_CONFIGS, key_bytes
     key = key_bytes(w.n, w.key_seed)
+    if w.name in PAPER_CONFIGS:            # Algorithm 1 as written: gamma-bit blocks, reload
+        pp = {"gamma": w.gamma}
+        x = hashes.paper_blocks(key, w.n, w.gamma, w.k)[0][:nblocks]
+    else:
+        pp = hashes.plan_params(w.n, w.r, w.m)
+        x = hashes.key_blocks(key, w.n, w.r)[:nblocks]
     a = [seeds.expand_a(w.hash_seed, i, pp["gamma"]) for i in range(nblocks)]
-    x = hashes.key_blocks(key, w.n, w.r)[:nblocks]
     t0 = time.perf_counter()
     hashes.mmh_eval(a, x, pp["gamma"])
     dt = time.perf_counter() - t0
@@ -242,8 +246,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
-    from synth import CONFIGS, key_bytes
-    w = CONFIGS[args.config]
+    from synth import CONFIGS, PAPER_CONFIGS, key_bytes
+    paper = args.config in PAPER_CONFIGS
+    w = PAPER_CONFIGS[args.config] if paper else CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, w)
         return
@@ -267,12 +272,17 @@ def main():
     torch.cuda.set_stream(stream)
 
     k = w.k
+    if paper and world > 1:
+        raise SystemExit("paper-mode configs (reload rule over the whole key) run on one GPU")
     b0, b1 = shard_ranges(k, world)[rank]
     key_full = key_bytes(w.n, w.key_seed)
-    lo, hi = key_slice_bytes(w.n, w.r, (b0, b1))
+    lo, hi = (0, w.nbytes) if paper else key_slice_bytes(w.n, w.r, (b0, b1))
     key_dev = torch.from_numpy(key_full[lo:hi].copy()).to(dev)
-    ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None,
-                    limb_bits=args.limb_bits)
+    if paper:
+        ctx = PAContext(w.n, 0, w.m, w.gamma, seed=w.hash_seed, limb_bits=args.limb_bits, paper_k=w.k)
+    else:
+        ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None,
+                        limb_bits=args.limb_bits)
     info = ctx.query()
     out = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -405,7 +415,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (i.i.d. Bernoulli(0.5) key bits from Philox4x64-10; hash keys from seed)",
-        "config": {"workload": w.name, "n": w.n, "r": w.r, "m": w.m, "k": k, "gamma": info["gamma"],
+        "config": {"workload": w.name, "mode": "paper (gamma-bit blocks, reload)" if paper else "r-bit blocks",
+                   "n": w.n, "r": w.r, "m": w.m, "k": k, "gamma": info["gamma"],
                    "alpha": info["alpha"],
                    "mmh_plan": {kk: info["mmh"][kk] for kk in ("limb_bits", "nprimes", "log2_len", "n_col", "n_row")},
                    "mh_plan": {kk: info["mh"][kk] for kk in ("limb_bits", "nprimes", "log2_len", "n_col", "n_row")},

@@ -1095,10 +1095,7 @@ static int paper_pack(pa_ctx *c, const uint8_t *key) {
     ks.aligned = (((uintptr_t)key) & 3) == 0;
     {
         ProfScope ps(c, "mmh_reload_windows");
-        CUDA_TRY(cudaMemsetAsync(c->wflags, 0, (size_t)c->T * 4, c->stream));
-        const uint64_t nchunk = cdiv(cdiv((uint64_t)c->T * p.gamma, 8), 16);
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(nchunk, 256), (uint64_t)g_num_sms * 16);
-        window_flags<<<std::max(1u, grid), 256, 0, c->stream>>>(ks, (uint32_t)p.gamma, c->T, c->wflags);
+        window_flags<<<c->T, 256, 0, c->stream>>>(ks, (uint32_t)p.gamma, c->T, c->wflags);
         window_resolve<<<1, 32, 0, c->stream>>>(c->wflags, c->T, (uint32_t)p.k, (uint32_t)p.gamma, c->offs, c->status);
         c->launches += 2;
         CUDA_TRY(cudaGetLastError());

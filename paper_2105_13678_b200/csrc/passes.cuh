@@ -273,40 +273,30 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
 // away and the next one consumed (reading A10).  Windows stay at
 // multiples of gamma, so the reload rule is: block i = the i-th window with a zero bit.
 
-// flags[t] = 1 if window t (t < T) contains a zero bit (flags zeroed by the caller).
+// flags[t] = 1 if window t contains a zero bit.  CTA t scans window t in chunks of
+// blockDim words and stops at the first chunk holding a zero bit: for keys of i.i.d.
+// bits that is the first chunk, so the check reads ~1 KB per window; an all-ones window
+// (the reload case) is scanned completely (correct, proportionally slower).
 __global__ void __launch_bounds__(256) window_flags(const KeySrc s, uint32_t gamma, uint32_t T, uint32_t *flags) {
-    const uint64_t nbits = (uint64_t)T * gamma;
-    const uint64_t nbytes = (nbits + 7) >> 3;
-    const uint64_t nchunk = (nbytes + 15) >> 4;                // 16 bytes per thread
-    for (uint64_t ch = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; ch < nchunk;
-         ch += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t last = 0xFFFFFFFFu;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const uint64_t wb = ch * 16 + 4 * q;                 // first byte of this word
-            if (wb >= nbytes) break;
-            const uint32_t word = key_word(s, (int64_t)(wb >> 2));
-#pragma unroll
-            for (int bb = 0; bb < 4; bb++) {
-                const uint64_t b = wb + bb;
-                if (b >= nbytes) break;
-                uint32_t z = ~(word >> (8 * bb)) & 0xFFu;          // zero bits, bit 7 = position 8b
-                const uint64_t p0 = 8 * b;
-                if (p0 + 8 > nbits) z &= (0xFF00u >> (nbits - p0)) & 0xFFu;   // positions >= nbits
-                if (!z) continue;
-                const uint32_t t0 = (uint32_t)(p0 / gamma), t1 = (uint32_t)((p0 + 7) / gamma);
-                if (t0 == t1) {
-                    if (t0 != last) { flags[t0] = 1u; last = t0; }
-                } else {
-                    for (int i = 0; i < 8; i++)
-                        if ((z >> (7 - i)) & 1u) {
-                            const uint32_t t = (uint32_t)((p0 + i) / gamma);
-                            if (t != last && t < T) { flags[t] = 1u; last = t; }
-                        }
-                }
-            }
+    const uint32_t t = blockIdx.x;
+    if (t >= T) return;
+    const uint64_t lo = (uint64_t)t * gamma, hi = lo + gamma;  // window bits [lo, hi)
+    const uint64_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
+    for (uint64_t base = w0; base < w1; base += blockDim.x) {
+        const uint64_t wi = base + threadIdx.x;
+        uint32_t z = 0;
+        if (wi < w1) {
+            z = ~__byte_perm(key_word(s, (int64_t)wi), 0, 0x0123);     // bit 31 = position 32 wi
+            const uint64_t p0 = 32 * wi;
+            if (p0 < lo) z &= 0xFFFFFFFFu >> (lo - p0);                 // positions before the window
+            if (p0 + 32 > hi) z &= 0xFFFFFFFFu << (p0 + 32 - hi);       // positions after it
+        }
+        if (__syncthreads_or(z != 0)) {
+            if (threadIdx.x == 0) flags[t] = 1u;
+            return;
         }
     }
+    if (threadIdx.x == 0) flags[t] = 0u;
 }
 
 // offs[i] = bit offset of block i (the i-th window with a zero bit); status 1 if fewer
@@ -375,7 +365,8 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
             const uint32_t lo = __funnelshift_r(a0, a1, 8 * bb), hi = __funnelshift_r(a1, a2, 8 * bb);
             const uint64_t be = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
             v = (uint32_t)(be >> (32 - sh));
-            const int64_t valid = (int64_t)gamma - ib;          // bits of this word inside the window
+            int64_t valid = (int64_t)gamma - ib;                // bits of this word inside the window
+            if (valid > (int64_t)B - 32 * i) valid = (int64_t)B - 32 * i;   // ... and inside the limb
             if (valid < 32) v &= (1u << valid) - 1u;
         }
         w[i] = v;

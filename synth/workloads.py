@@ -73,6 +73,14 @@ class PaperWorkload:
     def hash_seed(self) -> int:
         return 0x5EED0000 + self.cfg_no
 
+    @property
+    def r(self) -> int:          # block bits (= gamma in the paper's shape)
+        return self.gamma
+
+    @property
+    def nbytes(self) -> int:
+        return (self.n + 7) // 8
+
 
 PAPER_CONFIGS: dict[str, PaperWorkload] = {
     "P1": PaperWorkload("P1", 259_649_510, 25_964_951, 10, 25_237_932, 11),
