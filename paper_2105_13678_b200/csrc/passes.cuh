@@ -410,7 +410,7 @@ struct ColArgs {
 // length N1 = 2^N1_LOG is a template parameter so every element address is a per-unit
 // base plus a compile-time offset (no per-element 64-bit index arithmetic).
 template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
-__global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)), S_LOG <= 8 ? 3 : 1)
+__global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)), S_LOG == 8 ? 4 : (S_LOG < 8 ? 3 : 1))
 col_pass(const ColArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int E = SP::E;
