@@ -633,9 +633,9 @@ __host__ __device__ constexpr int mac_v(int slog) {
 // exchange layout: a separate padded buffer (fewer instructions than the in-place XOR
 // swizzle, measured 118 vs 135 us for C4) whenever it fits; in place for 2^14-point rows
 __host__ __device__ constexpr int mac_pad(int slog) { return slog <= 13 ? 1 : 0; }
-template <int S_LOG, int PAD = mac_pad(S_LOG), int NSX = 2>
+template <int S_LOG, int PAD = mac_pad(S_LOG), int NSX = 2, int AIN = 0>
 constexpr size_t mac_smem_bytes() {
-    return (size_t)(NSX + 1) * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8 +
+    return (size_t)(NSX + (AIN ? 0 : 1)) * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8 +
            (PAD ? (size_t)mac_v(S_LOG) * ((1 << S_LOG) + (1 << S_LOG) / 32) * 4 : 0);
 }
 __device__ __forceinline__ int swz32(int P) { return P ^ ((P >> 5) & 31); }
@@ -646,7 +646,7 @@ __host__ __device__ constexpr int mac_minb(int slog, int elog) {
     return (65536 / (mac_threads(slog, elog) * 4 * (1 << elog))) < 8 ? (65536 / (mac_threads(slog, elog) * 4 * (1 << elog)))
                                                                         : 8;
 }
-template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = 2>
+template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = 2, int AIN = 0>
 __global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(S_LOG, E_LOG) < 1 ? 1 : mac_minb(S_LOG, E_LOG))
 row_mac(const MacArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
@@ -655,9 +655,13 @@ row_mac(const MacArgs A) {
     constexpr uint32_t SW = V * S;                       // words per operand per stage
     extern __shared__ __align__(128) uint32_t smem[];
     uint32_t *xs = smem;                                 // [2][SW] X ring (exchange in place)
-    uint32_t *as = smem + NSX * SW;                      // [SW]   A^
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (NSX + 1) * SW);   // fullX[NSX], fullA
-    uint32_t *exb = smem + (NSX + 1) * SW + 8;           // PAD: [V][S + S/32] exchange
+    // AIN: A^ rows are copied into the X stage once its natural-order reads are done
+    // (the exchange is in the separate padded buffer), saving a third stage of smem
+    static_assert(!AIN || PAD, "AIN needs the separate exchange buffer");
+    constexpr int NST = NSX + (AIN ? 0 : 1);
+    uint32_t *as = smem + NSX * SW;                      // [SW]   A^ (unless AIN)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NST * SW);   // fullX[NSX], fullA
+    uint32_t *exb = smem + NST * SW + 8;                 // PAD: [V][S + S/32] exchange
     const int w = threadIdx.x / SP::TPV;
     const int v = threadIdx.x % SP::TPV;
     const NttArgs &a = A.nt;
@@ -682,9 +686,9 @@ row_mac(const MacArgs A) {
         mbar_arrive_expect_tx(&bars[s], SW * 4);
         bulk_g2s(xs + s * SW, A.src + offset_of(it), SW * 4, &bars[s]);
     };
-    auto issue_a = [&](uint64_t it) {
+    auto issue_a = [&](uint64_t it, uint32_t *dst) {
         mbar_arrive_expect_tx(&bars[NSX], SW * 4);
-        bulk_g2s(as, A.ahat + offset_of(it), SW * 4, &bars[NSX]);
+        bulk_g2s(dst, A.ahat + offset_of(it), SW * 4, &bars[NSX]);
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s <= NSX; s++) mbar_init(&bars[s], 1);
@@ -694,7 +698,7 @@ row_mac(const MacArgs A) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSX; s++)
             if (it0 + s < it1) issue_x(it0 + s, s);
-        if (it0 < it1) issue_a(it0);
+        if (!AIN && it0 < it1) issue_a(it0, as);
     }
 
     uint32_t tw[E / 2], twp[E / 2];
@@ -749,6 +753,10 @@ row_mac(const MacArgs A) {
 #pragma unroll
                 for (int m = 0; m < R; m++) x[h * R + m] = xst[w * S + in_pos<S_LOG, E_LOG>(v, h, m)];
         }
+        if constexpr (AIN) {
+            __syncthreads();                             // X stage s read: A^(it) may land there
+            if (threadIdx.x == 0) issue_a(it, xst);
+        }
         if constexpr (DBG != 1) {
             uint32_t *exch = PAD ? exb : xst;
             if constexpr (SP::Q > 1 && !PAD) __syncthreads();   // natural-order reads before in-place writes
@@ -758,7 +766,7 @@ row_mac(const MacArgs A) {
         mbar_wait(&bars[NSX], k & 1);
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
-            const uint32_t *arow = as + w * S;
+            const uint32_t *arow = (AIN ? xst : as) + w * S;
 #pragma unroll
             for (int h = 0; h < E / R; h++)
 #pragma unroll
@@ -770,7 +778,7 @@ row_mac(const MacArgs A) {
         __syncthreads();                                 // X stage s and A^ are free
         if (threadIdx.x == 0 && DBG != 2) {
             if (it + NSX < it1) issue_x(it + NSX, s);
-            if (it + 1 < it1) issue_a(it + 1);
+            if (!AIN && it + 1 < it1) issue_a(it + 1, as);
         }
     }
     if (cur_unit >= 0) {
