@@ -51,6 +51,24 @@ CASES = [
 ]
 
 
+EDGE = [
+    (1, 16, 1),                # one key bit, one block, one output bit
+    (15, 16, 7),               # a single partial block; pad bits of the last byte random
+    (16, 16, 40),              # m > gamma = 17: alpha = m (reading A1)
+    (17, 16, 17),              # second block holds one bit
+    (4096, 4096, 4423 - 1),    # n = r exactly, m = gamma - 1
+    (8191, 64, 13),            # gamma = 89: tiny ring, many blocks
+    (1 << 16, 1 << 16, 3),     # one block, three output bits
+]
+
+
+@pytest.mark.parametrize("n,r,m", EDGE)
+def test_parity_edge_sizes(n, r, m):
+    key = key_bytes(n, n * 31 + r)
+    seed = n + 5
+    assert gpu_hash(key, n, r, m, seed) == oracle_seeded(key, n, r, m, seed)
+
+
 @pytest.mark.parametrize("n,r,m", CASES)
 def test_parity_seeded(n, r, m):
     key = key_bytes(n, n ^ 0xABC)
