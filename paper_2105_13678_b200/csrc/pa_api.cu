@@ -1173,7 +1173,7 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     const uint32_t Bh = p.mh.limb_bits;
     WordSrc ws{y, (uint32_t)c->Wg, Bh, (uint32_t)cdiv(p.gamma, Bh)};
     TRY(stage_pack_col(c, c->smh, WordLimbs{ws}, 1, c->rows_mh, c->res, c->scratch_mh, "mh_pack", "mh_fwd_col"));
-    TRY(stage_mac(c, c->smh, 1, c->scratch_mh, c->bhat, c->acc_mh, true, "mh_fwd_row_mac"));
+    TRY(stage_mac(c, c->smh, 1, c->scratch_mh, c->bhat, c->acc_mh, true, "mh_fwd_row_mac", false));
     TRY(stage_inverse(c, c->smh, c->acc_mh, "mh_inverse"));
     const uint32_t W = (uint32_t)c->W_Z;
     {
