@@ -148,6 +148,12 @@ int pa_hash_batch(pa_ctx *ctx, const uint8_t *const *keys, uint8_t *const *outs,
  * overlap the first pass of the transform. */
 int pa_hash_host(pa_ctx *ctx, const uint8_t *key_host, uint8_t *out_host);
 
+/* End-to-end stream mode: `count` keys in HOST memory (keys_host[j]: ceil(n/8) bytes,
+ * outs_host[j]: ceil(m/8) bytes; pinned memory for full PCIe bandwidth).  Key j's H2D
+ * overlaps the hash of key j-1 (two device staging buffers, the two buffer sets of
+ * pa_hash_batch).  Synchronous.  Not available in paper mode or for shards. */
+int pa_hash_host_batch(pa_ctx *ctx, const uint8_t *const *keys_host, uint8_t *const *outs_host, uint32_t count);
+
 /* Stages S1-S5 on this context's blocks: y_part = sum_{i in shard} a_i x_i mod p,
  * canonical, as ceil(gamma/32) little-endian 32-bit words at DEVICE pointer y_out.
  * key_slice: DEVICE pointer to the shard's key bytes (see pa_hash). Asynchronous. */

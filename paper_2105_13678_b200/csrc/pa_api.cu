@@ -595,6 +595,8 @@ struct pa_ctx {
     uint32_t hgraph_launches = 0;
     cudaEvent_t copy_ev[9] = {};
     uint8_t *out_dev = nullptr;
+    uint8_t *key_dev2 = nullptr, *out_dev2 = nullptr;   // pa_hash_host_batch second staging set
+    cudaEvent_t hb_copy[2] = {}, hb_done[2] = {};
     uint64_t Wg = 0, W_ring = 0, W_fold = 0, W_Z = 0, ncoef_mmh = 0;
     uint32_t launches = 0;            // launches of the current / last hash call
     uint32_t launches_total = 0;      // since creation
@@ -1022,6 +1024,10 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
         cudaStreamDestroy(c->copy_stream);
     }
     if (c->out_dev) cudaFree(c->out_dev);
+    if (c->key_dev2) cudaFree(c->key_dev2);
+    if (c->out_dev2) cudaFree(c->out_dev2);
+    for (auto e : c->hb_copy) if (e) cudaEventDestroy(e);
+    for (auto e : c->hb_done) if (e) cudaEventDestroy(e);
     c->da.free_all();
     delete c;
 }
@@ -1415,6 +1421,66 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->pl.paper_k) return pa_ctx_status(c);
+    return PA_OK;
+}
+
+// ---- end-to-end stream mode: host-resident keys.  Key j's H2D (copy stream, into staging
+// buffer j % 2) overlaps the hash of key j - 1 (buffer set / stream (j - 1) % 2); the copy
+// of key j waits for the hash of key j - 2 (same staging buffer) to finish; the output of
+// key j is copied back on its hash stream.  Synchronous: returns after the last D2H.
+extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, uint8_t *const *outs_host,
+                                  uint32_t count) {
+    if (!c || (count && (!keys_host || !outs_host))) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
+    if (c->pl.paper_k) return set_err(PA_E_STATE, "paper mode: use pa_hash_host per key");
+    for (uint32_t j = 0; j < count; j++)
+        if (!keys_host[j] || !outs_host[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
+    if (count == 0) return PA_OK;
+    const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
+    if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
+    if (!c->out_dev) CUDA_TRY(cudaMalloc(&c->out_dev, mb));
+    if (!c->key_dev2) CUDA_TRY(cudaMalloc(&c->key_dev2, nb));
+    if (!c->out_dev2) CUDA_TRY(cudaMalloc(&c->out_dev2, mb));
+    if (!c->copy_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
+    }
+    if (!c->hb_copy[0])
+        for (int s = 0; s < 2; s++) {
+            CUDA_TRY(cudaEventCreateWithFlags(&c->hb_copy[s], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->hb_done[s], cudaEventDisableTiming));
+        }
+    TRY(alloc_alt(c));
+    uint8_t *kbuf[2] = {c->key_dev, c->key_dev2}, *obuf[2] = {c->out_dev, c->out_dev2};
+    // fork: both hash streams and the copy stream start after prior ctx-stream work
+    CUDA_TRY(cudaEventRecord(c->bev[0], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->alt.stream, c->bev[0], 0));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->bev[0], 0));
+    uint32_t total = 0;
+    int rc = PA_OK;
+    for (uint32_t j = 0; j < count && rc == PA_OK; j++) {
+        const int s = (int)(j & 1);
+        if (j >= 2 && cudaStreamWaitEvent(c->copy_stream, c->hb_done[s], 0) != cudaSuccess) rc = set_err(PA_E_CUDA, "event wait failed");
+        if (rc == PA_OK && cudaMemcpyAsync(kbuf[s], keys_host[j], nb, cudaMemcpyHostToDevice, c->copy_stream) != cudaSuccess)
+            rc = set_err(PA_E_CUDA, "H2D copy failed");
+        if (rc == PA_OK && cudaEventRecord(c->hb_copy[s], c->copy_stream) != cudaSuccess) rc = set_err(PA_E_CUDA, "event record failed");
+        if (rc != PA_OK) break;
+        if (s) swap_bufs(c);
+        if (cudaStreamWaitEvent(c->stream, c->hb_copy[s], 0) != cudaSuccess) rc = set_err(PA_E_CUDA, "event wait failed");
+        if (rc == PA_OK) rc = hash_enqueue(c, kbuf[s], obuf[s]);
+        total += c->launches;
+        if (rc == PA_OK && cudaMemcpyAsync(outs_host[j], obuf[s], mb, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+            rc = set_err(PA_E_CUDA, "D2H copy failed");
+        if (rc == PA_OK && cudaEventRecord(c->hb_done[s], c->stream) != cudaSuccess) rc = set_err(PA_E_CUDA, "event record failed");
+        if (s) swap_bufs(c);
+    }
+    // join
+    CUDA_TRY(cudaEventRecord(c->bev[1], c->alt.stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->bev[1], 0));
+    c->launches = total;
+    c->launches_total += total;
+    TRY(rc);
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
     return PA_OK;
 }
 

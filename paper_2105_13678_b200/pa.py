@@ -149,6 +149,21 @@ class PAContext:
         B.check(B.pa_hash_batch(self._h, kp, op, len(keys)))
         return outs
 
+    def hash_host_batch(self, keys_host, outs_host=None):
+        """pa_hash_host_batch: host keys (numpy uint8 / pinned torch CPU tensors) -> host
+        outputs, H2D of key j overlapping the hash of key j-1.  Synchronous."""
+        torch = self._torch
+
+        def ptr(x):
+            return x.data_ptr() if isinstance(x, torch.Tensor) else np.ascontiguousarray(x).ctypes.data
+        keys_host = [k if isinstance(k, torch.Tensor) else np.ascontiguousarray(k, dtype=np.uint8) for k in keys_host]
+        if outs_host is None:
+            outs_host = [np.zeros(self.nbytes_out, dtype=np.uint8) for _ in keys_host]
+        kp = (ctypes.c_void_p * len(keys_host))(*[ptr(k) for k in keys_host])
+        op = (ctypes.c_void_p * len(outs_host))(*[ptr(o) for o in outs_host])
+        B.check(B.pa_hash_host_batch(self._h, kp, op, len(keys_host)))
+        return outs_host
+
     def hash_host(self, key_host, out_host=None):
         """pa_hash_host: host buffers (numpy uint8 / pinned torch CPU tensor), synchronous."""
         torch = self._torch

@@ -313,6 +313,22 @@ def test_paper_mode_insufficient_input():
     ctx.close()
 
 
+def test_hash_host_batch():
+    # end-to-end stream mode: host keys, H2D of key j overlapping the hash of key j-1
+    PAContext = _pa()
+    n, r, m, seed = 700_001, 8192, 40_000, 31
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = PAContext(n, r, m, seed=seed)
+        keys = [key_bytes(n, 200 + j) for j in range(5)]
+        pinned = [torch.from_numpy(k).pin_memory() for k in keys]
+        for hk in (keys, pinned):
+            outs = ctx.hash_host_batch(hk)
+            for k, o in zip(keys, outs):
+                assert bytes(np.asarray(o)) == oracle_seeded(k, n, r, m, seed)
+        ctx.close()
+
+
 def _golden():
     path = os.path.join(ROOT, "tests", "golden", "digests.json")
     return json.load(open(path)) if os.path.exists(path) else {}
