@@ -239,25 +239,38 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     uint32_t w[NW];
     uint32_t any = 0;
     if (j < s.wx) {
-        // byte offsets relative to the staged base 4 gw0 (all < 4 MAXW)
+        // byte offsets relative to the staged base 4 gw0 (all < 4 MAXW).  Word i of the limb
+        // is the big-endian value of the 4 bytes ending 4 i bytes before the limb's end, so
+        // all words share the byte shift (hi & 3) and walk down the staged words by one.
         const int base = (int)(4 * gw0 - start);
         const int hi = (int)(s.blk_bytes - (uint32_t)LB * j) - base;
-        int lo = hi - LB;
-        if (lo < -base) lo = -base;                           // block start
+        const int sh = (hi & 3) * 8;
+        const int wtop = (hi >> 2) - 1;                       // staged word holding byte hi - 4
+        uint32_t nxt = sw[wtop + 1];
 #pragma unroll
         for (int i = 0; i < NW; i++) {
-            const int pos = hi - 4 * (i + 1);
-            const int wi = pos >> 2;
-            const int sh = (pos & 3) * 8;
-            const uint32_t a0 = (wi >= 0) ? sw[wi] : 0u;
-            const uint32_t a1 = (wi + 1 >= 0) ? sw[wi + 1] : 0u;
-            uint32_t v = __byte_perm(__funnelshift_r(a0, a1, sh), 0, 0x0123);
-            const int below = lo - pos;
-            if (below >= 4) v = 0;
-            else if (below > 0) v &= 0xFFFFFFFFu >> (8 * below);
-            w[i] = v;
-            any |= v;
+            const uint32_t cur = sw[max(wtop - i, 0)];
+            w[i] = __byte_perm(__funnelshift_r(cur, nxt, sh), 0, 0x0123);
+            nxt = cur;
         }
+        // the block's top limb is shorter than B: clear the bytes before the block start
+        int lo = hi - LB;
+        if (lo < -base) {
+            lo = -base;
+#pragma unroll
+            for (int i = 0; i < NW; i++) {
+                const int below = lo - (hi - 4 * (i + 1));
+                if (below >= 4) w[i] = 0;
+                else if (below > 0) w[i] &= 0xFFFFFFFFu >> (8 * below);
+            }
+        }
+        // a limb narrower than its NW words (B % 32): mask the top word
+        if (LB < 4 * NW) {
+            const int topbytes = LB - 4 * (NW - 1);
+            w[NW - 1] &= 0xFFFFFFFFu >> (8 * (4 - topbytes));
+        }
+#pragma unroll
+        for (int i = 0; i < NW; i++) any |= w[i];
     }
     uint32_t *o = res + (size_t)iv * P * wxp + j;
     if (!any) {
