@@ -255,6 +255,8 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--limb-bits", type=int, default=0, help="force the limb width B (0 = planner)")
     ap.add_argument("--batch", type=int, default=8, help="keys per pa_hash_batch in the stream-mode line")
+    ap.add_argument("--no-comparators", dest="comparators", action="store_false",
+                    help="skip the MH-only PA comparator measurement")
     ap.add_argument("--only-device", action="store_true",
                     help="timed device steps only (no per-stage pass, no e2e): for ncu launch lists")
     args = ap.parse_args()
@@ -383,6 +385,35 @@ def main():
                        "ms_per_batch": ms_b, "ms_per_key": ms_b / args.batch,
                        "api": "pa_hash_batch (device buffers; two buffer sets / streams, graph replay)"}
 
+    # ---- comparator (NEXT-4; Table 1 / Fig. 3): MH-only PA on the same key and (n, m),
+    # top m bits of (b x + c) mod 2^n over the whole key, same kernels and timing rules
+    comparators = None
+    if world == 1 and not paper and args.comparators:
+        cctx = PAContext(w.n, 0, w.m, 0, seed=w.hash_seed, mh_only=True)
+        cout = torch.empty(cctx.nbytes_out, dtype=torch.uint8, device=dev)
+        for _ in range(args.warmup):
+            cctx.hash(key_dev, cout)
+        torch.cuda.synchronize()
+        tc = []
+        for _ in range(max(3, args.steps // 5)):
+            if not args.no_flush:
+                flush.fill_(1)
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cctx.hash(key_dev, cout)
+            bb.record(stream)
+            bb.synchronize()
+            tc.append(a.elapsed_time(bb))
+        msc = statistics.median(tc)
+        ci = cctx.query()
+        comparators = {"mh_only_pa": {
+            "value": w.n / (msc * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": msc,
+            "plan": {kk: ci["mh"][kk] for kk in ("limb_bits", "nprimes", "log2_len")},
+            "what": "modular-arithmetic-hashing-only PA (PAPER.md:66, SPEC.md:305-313): top m bits of "
+                    "(b x + c) mod 2^n, one n x n-bit product, same NTT/CRT kernels"}}
+        cctx.close()
+
     e2e = None
     if world == 1:
         host_key = torch.from_numpy(key_full).pin_memory()
@@ -463,6 +494,7 @@ def main():
         "stages_ms_per_step": {kk: v[0] / nsteps_prof for kk, v in sorted(stages.items())},
         "e2e": e2e,
         "stream": stream_mode,
+        "comparators": comparators,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample(w)

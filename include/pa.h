@@ -113,6 +113,12 @@ typedef struct {
      * paper_k usable windows -> PA_E_INSUFFICIENT_INPUT (pa_ctx_status / pa_hash_host).
      * Not available for shard contexts. */
     uint64_t paper_k;
+    /* Comparator (Table 1 "Modular Arithmetic Hashing PA",
+     * SPEC.md:305-313): when nonzero the context computes MH-only PA instead of MMH-MH:
+     * out = top m bits of (b x + c) mod 2^n, x = the n-bit key integer (MSB-first),
+     * b odd and c drawn with alpha = n (reading A7).  r, gamma, shards and paper_k must be 0;
+     * m <= n.  pa_hash / pa_hash_host only. */
+    uint64_t mh_only;
 } pa_params;
 
 /* Create a context on the current CUDA device.  `p` is the Mersenne EXPONENT

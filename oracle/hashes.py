@@ -194,3 +194,22 @@ def pa_hash_paper_seeded(key, n: int, gamma: int, k: int, m: int, seed: int) -> 
     """pa_hash_paper with hash keys from ``seed`` (reading A7; alpha = gamma)."""
     a, b, c = expand_hash_keys(seed, k, gamma, gamma)
     return pa_hash_paper(key, n, gamma, k, m, a, b, c)
+
+
+# ------------------------------------------------- comparator: MH-only PA (NEXT-4)
+def mh_only_pa(key, n: int, m: int, b: int, c: int) -> bytes:
+    """Modular-arithmetic-hashing-only PA (Table 1): the n
+    input bits read MSB-first as an integer x; output = top m bits of (b x + c) mod 2^n,
+    i.e. Eq. 4 with alpha = n, beta = m.  Emitted MSB-first (reading A5)."""
+    if m > n:
+        raise ValueError("m > n (SPEC.md:309)")
+    kb = bytes(np.asarray(key, dtype=np.uint8)) if not isinstance(key, bytes) else key
+    nbytes = (n + 7) // 8
+    x = int.from_bytes(kb[:nbytes], "big") >> (8 * nbytes - n)
+    return mh_output(x, b, c, n, m)
+
+
+def mh_only_pa_seeded(key, n: int, m: int, seed: int) -> bytes:
+    """mh_only_pa with b, c from ``seed`` (reading A7 streams, alpha = n)."""
+    from .seeds import expand_b, expand_c
+    return mh_only_pa(key, n, m, expand_b(seed, n), expand_c(seed, n))

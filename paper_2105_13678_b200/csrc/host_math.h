@@ -65,7 +65,7 @@ inline uint32_t primitive_root(uint32_t p) {
 inline int two_adic(uint32_t p) { int v = 0; uint32_t q = p - 1; while (!(q & 1)) { q >>= 1; v++; } return v; }
 
 // NTT primes p < 2^30 (so 4p < 2^32 for lazy butterflies), p = c 2^v + 1 with
-// v >= 20, in decreasing order.  Any subset whose 2-adic valuations cover log2 L
+// v >= 20, in decreasing order (the planner takes the largest usable ones first).  Any subset whose 2-adic valuations cover log2 L
 // can serve a transform of length L.
 static const uint32_t kPrimes[] = {
     1053818881u, 1051721729u, 1045430273u, 1012924417u, 1007681537u, 1004535809u,
@@ -73,6 +73,10 @@ static const uint32_t kPrimes[] = {
     957349889u, 950009857u, 943718401u, 940572673u, 938475521u, 935329793u,
     925892609u, 924844033u, 919601153u, 918552577u, 913309697u, 907018241u,
     899678209u, 897581057u, 883949569u, 880803841u,
+    // smaller primes with 2-adicity >= 22, for transforms of length 2^22 / 2^23
+    // (the MH-only comparator over a whole 2.6e8-bit key)
+    754974721u, 683671553u, 666894337u, 645922817u, 595591169u, 469762049u, 415236097u,
+    377487361u,
 };
 
 // Mersenne exponents.

@@ -132,6 +132,7 @@ static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int for
 struct Plan {
     uint64_t n, r, m, gamma, alpha, k, b0, b1, seed;
     uint64_t paper_k;        // paper mode (gamma-bit blocks, reload rule) when nonzero
+    uint64_t mh_only;        // comparator: MH-only PA over the whole n-bit key
     int strict, force_B;
     pa_stage_plan mmh, mh;
 };
@@ -147,11 +148,28 @@ static int make_plan(const pa_params *prm, Plan *P) {
     p.n = prm->n; p.r = prm->r; p.m = prm->m; p.seed = prm->seed;
     p.strict = prm->strict; p.force_B = prm->limb_bits;
     p.paper_k = prm->paper_k;
+    p.mh_only = prm->mh_only;
     if (p.n < 1) return set_err(PA_E_PARAM, "n must be >= 1");
     if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
     if (p.force_B && (p.force_B < 16 || p.force_B > kMaxLimbBits || p.force_B % 8))
         return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, %d]", kMaxLimbBits);
     uint64_t g = prm->gamma;
+    if (p.mh_only) {
+        // comparator: z = top m bits of (b x + c) mod 2^n
+        if (prm->gamma || prm->r || p.paper_k || prm->block_begin || prm->block_end)
+            return set_err(PA_E_PARAM, "MH-only PA takes no gamma, r, paper_k or shard");
+        if (p.m > p.n) return set_err(PA_E_PARAM, "MH-only PA: m must be <= n (SPEC.md:309)");
+        if (p.n > (1ull << 31)) return set_err(PA_E_PARAM, "MH-only PA: n <= 2^31");
+        p.gamma = p.n;                  // width of the MH operand y (= x)
+        p.alpha = p.n;
+        p.r = p.n;
+        p.k = 0;
+        p.b0 = p.b1 = 0;
+        if (plan_product(p.n, p.n, 1, p.force_B, 1, &p.mh) != PA_OK)
+            return set_err(PA_E_BOUND, "no transform plan covers the MH-only product");
+        *P = p;
+        return PA_OK;
+    }
     if (p.paper_k) {
         // paper mode: Algorithm 1 as written, gamma-bit blocks
         if (!g) return set_err(PA_E_PARAM, "paper mode needs an explicit gamma (p = 2^gamma - 1)");
@@ -859,21 +877,21 @@ static uint32_t rows_for(uint64_t limbs, uint32_t n1, uint32_t n2) {
 
 static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     Plan &p = c->pl;
-    TRY(setup_stage(c->da, p.mmh, c->smmh, c->stream));
+    if (!p.mh_only) TRY(setup_stage(c->da, p.mmh, c->smmh, c->stream));   // MH-only: no MMH stage
     TRY(setup_stage(c->da, p.mh, c->smh, c->stream));
     c->nblk = (uint32_t)(p.b1 - p.b0);
     const uint32_t Lm = c->smmh.L, Pm = p.mmh.nprimes;
     const uint32_t Lh = c->smh.L, Ph = p.mh.nprimes;
     const uint32_t Bm = p.mmh.limb_bits, Bh = p.mh.limb_bits;
-    const uint64_t wx = cdiv(p.r, Bm), wa = cdiv(p.gamma, Bm);
-    c->ncoef_mmh = wx + wa - 1;
+    const uint64_t wx = Bm ? cdiv(p.r, Bm) : 0, wa = Bm ? cdiv(p.gamma, Bm) : 0;
+    c->ncoef_mmh = Bm ? wx + wa - 1 : 0;
     c->Wg = cdiv(p.gamma, 32);
     c->W_ring = c->Wg + Pm + 2;              // wrapped pieces of tiny rings may pass the top
     c->W_fold = c->W_ring + 2;               // 64-bit column sums carry into 2 more words
     c->W_Z = cdiv(p.alpha, 32);
     const uint64_t Wa32 = cdiv(p.gamma, 32), Wal32 = cdiv(p.alpha, 32);
-    const uint32_t rows_x = rows_for(wx, p.mmh.n_row, p.mmh.n_col);
-    const uint32_t rows_a = rows_for(wa, p.mmh.n_row, p.mmh.n_col);
+    const uint32_t rows_x = Bm ? rows_for(wx, p.mmh.n_row, p.mmh.n_col) : 0;
+    const uint32_t rows_a = Bm ? rows_for(wa, p.mmh.n_row, p.mmh.n_col) : 0;
     c->rows_mmh = rows_x;
     const uint32_t rows_y = rows_for(cdiv(p.gamma, Bh), p.mh.n_row, p.mh.n_col);
     const uint32_t rows_b = rows_for(cdiv(p.alpha, Bh), p.mh.n_row, p.mh.n_col);
@@ -893,7 +911,7 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     const uint64_t Smax = std::max<uint64_t>(c->W_fold, c->W_Z);
     TRY(c->da.alloc(&c->S, Smax));
     TRY(c->da.alloc(&c->coef, std::max<size_t>((size_t)Pm * Lm, (size_t)Ph * Lh)));
-    TRY(c->da.alloc(&c->y1, c->W_fold));
+    TRY(c->da.alloc(&c->y1, std::max<uint64_t>(c->W_fold, c->Wg)));
     TRY(c->da.alloc(&c->Z, c->W_Z));
     c->cstate_stride = (uint32_t)(cdiv(Smax, std::min(kCarryTile, kCCTile)) + 2);
     TRY(c->da.alloc(&c->cstate, (size_t)c->cstate_stride * kCarrySlots));
@@ -943,7 +961,7 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     CUDA_TRY(cudaMemcpyAsync(b_dev, bw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->c_words, cw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
     WordSrc wsa{a_dev, (uint32_t)Wa32, Bm, (uint32_t)wa};
-    int rc = precompute_hat(c, c->smmh, wsa, c->nblk, rows_a, c->scratch, c->ahat);
+    int rc = p.mh_only ? PA_OK : precompute_hat(c, c->smmh, wsa, c->nblk, rows_a, c->scratch, c->ahat);
     WordSrc wsb{b_dev, (uint32_t)Wal32, Bh, (uint32_t)cdiv(p.alpha, Bh)};
     if (rc == PA_OK) rc = precompute_hat(c, c->smh, wsb, 1, rows_b, c->scratch_mh, c->bhat);
     cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -1199,6 +1217,21 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
 static int hash_enqueue(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     c->launches = 0;
     TRY(carry_reset(c));
+    if (c->pl.mh_only) {
+        // comparator: y := x, the n-bit key integer, then the MH stage with alpha = n
+        KeySrc ks{};
+        ks.key = key_bits;
+        ks.nbytes = cdiv(c->pl.n, 8);
+        ks.last_mask = (c->pl.n % 8) ? ((0xFFu << (8 - c->pl.n % 8)) & 0xFFu) : 0xFFu;
+        ks.aligned = (((uintptr_t)key_bits) & 3) == 0;
+        {
+            ProfScope ps(c, "mh_only_key_words");
+            key_to_words<<<(uint32_t)cdiv(c->Wg, 256), 256, 0, c->stream>>>(ks, c->pl.n, (uint32_t)c->Wg, c->y1);
+            c->launches++;
+            CUDA_TRY(cudaGetLastError());
+        }
+        return run_mh(c, c->y1, out_bits);
+    }
     uint32_t *y = nullptr;
     TRY(run_mmh(c, key_bits, &y));
     return run_mh(c, y, out_bits);
@@ -1314,6 +1347,7 @@ static int batch_enqueue(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *
 
 extern "C" int pa_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
     if (!c || (count && (!keys || !outs))) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.mh_only) return set_err(PA_E_STATE, "MH-only comparator: use pa_hash");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     for (uint32_t j = 0; j < count; j++)
         if (!keys[j] || !outs[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
@@ -1359,14 +1393,22 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     CUDA_TRY(cudaEventRecord(c->copy_ev[kCopyGroups], c->stream));
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[kCopyGroups], 0));
     const uint32_t nblk = c->nblk;
-    // paper mode: the reload rule needs the whole key before any block offset is known
-    const int G = c->pl.paper_k ? 1 : (int)std::min<uint32_t>(kCopyGroups, nblk);
+    // paper mode: the reload rule needs the whole key before any block offset is known;
+    // MH-only: one product over the whole key
+    const bool whole = c->pl.paper_k || c->pl.mh_only;
+    const int G = whole ? 1 : (int)std::min<uint32_t>(kCopyGroups, nblk);
     const uint64_t R = c->pl.r / 8;
     for (int g = 0; g < G; g++) {
         const uint64_t lo = G == 1 ? 0 : std::min<uint64_t>(nb, (uint64_t)(nblk * g / G) * R);
         const uint64_t hi = G == 1 ? nb : std::min<uint64_t>(nb, (uint64_t)(nblk * (g + 1) / G) * R);
         if (hi > lo) CUDA_TRY(cudaMemcpyAsync(c->key_dev + lo, key_host + lo, hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
         CUDA_TRY(cudaEventRecord(c->copy_ev[g], c->copy_stream));
+    }
+    if (whole) {
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_ev[0], 0));
+        TRY(hash_enqueue(c, c->key_dev, c->out_dev));
+        CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
+        return PA_OK;
     }
     c->launches = 0;
     TRY(carry_reset(c));
@@ -1432,7 +1474,7 @@ extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, ui
                                   uint32_t count) {
     if (!c || (count && (!keys_host || !outs_host))) return set_err(PA_E_PARAM, "NULL argument");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
-    if (c->pl.paper_k) return set_err(PA_E_STATE, "paper mode: use pa_hash_host per key");
+    if (c->pl.paper_k || c->pl.mh_only) return set_err(PA_E_STATE, "paper mode / MH-only: use pa_hash_host per key");
     for (uint32_t j = 0; j < count; j++)
         if (!keys_host[j] || !outs_host[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
     if (count == 0) return PA_OK;

@@ -393,6 +393,24 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
     for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = limb_words_redc<NW>(w, ks[pi]);
 }
 
+// MH-only comparator: out[u] = bits [32 u, 32 u + 32) of x, the integer of key bits
+// [0, n) read MSB-first, i.e. key bits [n - 32 u - 32, n - 32 u).
+__global__ void key_to_words(const KeySrc s, uint64_t n, uint32_t W, uint32_t *__restrict__ out) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= W) return;
+    const int64_t q = (int64_t)n - 32 * ((int64_t)u + 1);      // key bit of the word's MSB
+    const int64_t bq = q >> 3;                                  // floor (q may be negative)
+    const int sh = (int)(q & 7);
+    const int64_t wi = bq >> 2;
+    const int bb = (int)(bq & 3);
+    const uint32_t a0 = key_word(s, wi), a1 = key_word(s, wi + 1), a2 = key_word(s, wi + 2);
+    const uint32_t lo = __funnelshift_r(a0, a1, 8 * bb), hi = __funnelshift_r(a1, a2, 8 * bb);
+    const uint64_t be = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+    uint32_t v = (uint32_t)(be >> (32 - sh));
+    if (q < 0) v &= 0xFFFFFFFFu >> (-q);                        // positions before bit 0 of the key
+    out[u] = v;
+}
+
 struct KeyLimbs {
     KeySrc s;
     __device__ __forceinline__ uint64_t operator()(uint32_t iv, uint32_t j) const { return key_limb(s, iv, j); }

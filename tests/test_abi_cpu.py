@@ -153,3 +153,16 @@ def test_plan_paper_mode():
             P.plan(kw["n"], kw["r"], kw["m"], kw["gamma"], paper_k=kw["paper_k"])
     with pytest.raises(B.PAError):
         P.plan(1000, 0, 10, 107, block_range=(0, 1), paper_k=3)    # no shards
+
+
+def test_plan_mh_only():
+    info = P.plan(260_000_000, 0, 26_000_000, 0, mh_only=True)
+    assert info["alpha"] == 260_000_000 and info["mh"]["bound_log2"] < info["mh"]["modulus_log2"]
+    for kw in (dict(gamma=89), dict(r=64), dict(paper_k=3), dict(block_range=(0, 1))):
+        args = dict(n=1000, r=0, m=10, gamma=0)
+        args.update({k: v for k, v in kw.items() if k in ("gamma", "r")})
+        with pytest.raises(B.PAError):
+            P.plan(args["n"], args["r"], args["m"], args["gamma"], mh_only=True,
+                   paper_k=kw.get("paper_k", 0), block_range=kw.get("block_range"))
+    with pytest.raises(B.PAError):
+        P.plan(100, 0, 101, 0, mh_only=True)                      # m > n

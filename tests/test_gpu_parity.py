@@ -329,6 +329,20 @@ def test_hash_host_batch():
         ctx.close()
 
 
+@pytest.mark.parametrize("n,m", [(1, 1), (100, 37), (4096, 4096), (70_001, 7_000), (1_000_003, 100_000)])
+def test_mh_only_comparator(n, m):
+    # NEXT-4 comparator: MH-only PA = top m bits of (b x + c) mod 2^n
+    PAContext = _pa()
+    key = key_bytes(n, n + 3)
+    ctx = PAContext(n, 0, m, 0, seed=n, mh_only=True)
+    out = ctx.hash(torch.from_numpy(key).cuda())
+    torch.cuda.synchronize()
+    want = hashes.mh_only_pa_seeded(key, n, m, n)
+    assert bytes(out.cpu().numpy()) == want
+    assert bytes(ctx.hash_host(key)) == want
+    ctx.close()
+
+
 def _golden():
     path = os.path.join(ROOT, "tests", "golden", "digests.json")
     return json.load(open(path)) if os.path.exists(path) else {}

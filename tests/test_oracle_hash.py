@@ -284,3 +284,21 @@ def test_pa_hash_paper_spec_example():
     # gamma=3, k=2, m=2, a=(3,5), b=3, c=1, bits 010 110 -> 10
     key = bytes([0b01011000])
     assert hashes.pa_hash_paper(key, 6, 3, 2, 2, [3, 5], 3, 1) == bytes([0b10000000])
+
+
+def test_mh_only_pa_spec_example():
+    # n=4, m=2, b=5, c=3, x=0111 (7) -> (38 mod 16) = 6 -> 01
+    assert hashes.mh_only_pa(bytes([0b01110000]), 4, 2, 5, 3) == bytes([0b01000000])
+    # b=1, c=0, m=n -> identity
+    assert hashes.mh_only_pa(bytes([0xA5, 0x3C]), 16, 16, 1, 0) == bytes([0xA5, 0x3C])
+
+
+def test_mh_only_equals_mh_eval_exhaustive():
+    # mh_only_pa(n, m) == mh_eval with alpha = n, beta = m, exhaustive at n <= 8
+    n, m = 6, 3
+    for x in range(1 << n):
+        for b in range(1, 1 << n, 2):
+            for c in (0, 5, 63):
+                key = bytes([x << 2])
+                got = hashes.mh_only_pa(key, n, m, b, c)
+                assert got == bytes([hashes.mh_eval(b, c, x, n, m) << 5])
