@@ -385,6 +385,36 @@ def main():
                        "ms_per_batch": ms_b, "ms_per_key": ms_b / args.batch,
                        "api": "pa_hash_batch (device buffers; two buffer sets / streams, graph replay)"}
 
+    # ---- fresh hash keys per job (NEXT-2): pa_ctx_rekey (device Philox expansion + transforms
+    # of the a_i and b) before every hash -- the "cold" throughput of a new function per job
+    fresh = None
+    if world == 1:
+        for j in range(2):
+            ctx.rekey(w.hash_seed + 1 + j)
+            ctx.hash(key_dev, out)
+        torch.cuda.synchronize()
+        tf, tr = [], []
+        for j in range(max(3, args.steps // 5)):
+            if not args.no_flush:
+                flush.fill_(1)
+            a = torch.cuda.Event(enable_timing=True)
+            mid = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.rekey(w.hash_seed + 100 + j)
+            mid.record(stream)
+            ctx.hash(key_dev, out)
+            bb.record(stream)
+            bb.synchronize()
+            tf.append(a.elapsed_time(bb))
+            tr.append(a.elapsed_time(mid))
+        ctx.rekey(w.hash_seed)                                   # restore the benchmarked function
+        torch.cuda.synchronize()
+        msf = statistics.median(tf)
+        fresh = {"value": w.n / (msf * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": msf,
+                 "rekey_ms": statistics.median(tr),
+                 "api": "pa_ctx_rekey (device Philox4x64-10 expansion of a_i, b, c + their transforms) then pa_hash"}
+
     # ---- comparator (NEXT-4; Table 1 / Fig. 3): MH-only PA on the same key and (n, m),
     # top m bits of (b x + c) mod 2^n over the whole key, same kernels and timing rules
     comparators = None
@@ -495,6 +525,7 @@ def main():
         "e2e": e2e,
         "stream": stream_mode,
         "comparators": comparators,
+        "fresh_keys": fresh,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample(w)

@@ -169,6 +169,12 @@ int pa_mmh_partial(pa_ctx *ctx, const uint8_t *key_slice, uint32_t *y_out);
  * DEVICE, contiguous), then MH into out_bits (DEVICE, ceil(m/8) bytes). */
 int pa_mh_merge(pa_ctx *ctx, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits);
 
+/* Fresh hash keys per job: re-draw a_i, b, c from `seed` on the
+ * GPU (reading A7; bit-identical to pa_expand_a / pa_expand_bc and to a context created
+ * with this seed) and recompute the transforms of the a_i and b.  Asynchronous on the
+ * context stream: hashes enqueued after it use the new function. */
+int pa_ctx_rekey(pa_ctx *ctx, uint64_t seed);
+
 /* Synchronizes the context stream and returns the device-side status of the last hash:
  * PA_OK, or PA_E_INSUFFICIENT_INPUT (paper mode: fewer than paper_k usable windows; the
  * output is then undefined). */

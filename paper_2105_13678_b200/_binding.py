@@ -77,6 +77,7 @@ pa_mmh_partial = _sig("pa_mmh_partial", i32, vp, vp, vp)
 pa_mh_merge = _sig("pa_mh_merge", i32, vp, vp, u32, vp)
 pa_ctx_destroy = _sig("pa_ctx_destroy", None, vp)
 pa_ctx_status = _sig("pa_ctx_status", i32, vp)
+pa_ctx_rekey = _sig("pa_ctx_rekey", i32, vp, u64)
 pa_ctx_query = _sig("pa_ctx_query", i32, vp, ctypes.POINTER(pa_info))
 pa_ctx_set_stream = _sig("pa_ctx_set_stream", i32, vp, vp)
 pa_ctx_set_profiling = _sig("pa_ctx_set_profiling", i32, vp, i32)
@@ -89,7 +90,7 @@ pa_expand_bc = _sig("pa_expand_bc", i32, u64, u64, vp, vp)
 pa_last_error = _sig("pa_last_error", i32, ctypes.c_char_p, ctypes.c_size_t)
 
 EXPORTED = ["pa_ctx_create", "pa_ctx_create_ex", "pa_hash", "pa_hash_host", "pa_hash_batch", "pa_hash_host_batch", "pa_mmh_partial", "pa_mh_merge",
-            "pa_ctx_destroy", "pa_ctx_status", "pa_ctx_query", "pa_ctx_set_stream", "pa_ctx_set_profiling",
+            "pa_ctx_destroy", "pa_ctx_status", "pa_ctx_rekey", "pa_ctx_query", "pa_ctx_set_stream", "pa_ctx_set_profiling",
             "pa_ctx_stage_times", "pa_plan", "pa_philox4x64_10", "pa_expand_a", "pa_expand_bc",
             "pa_last_error"]
 

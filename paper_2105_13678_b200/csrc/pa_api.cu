@@ -32,6 +32,7 @@
 #include "modarith.cuh"
 #include "ntt.cuh"
 #include "passes.cuh"
+#include "rekey.cuh"
 
 using namespace pa;
 
@@ -599,6 +600,8 @@ struct pa_ctx {
     uint32_t *cstate = nullptr;               // carry look-back: [kCarrySlots][1 + ntiles]
     uint32_t cstate_stride = 0;
     int cslot = 0;
+    uint32_t *a_words_dev = nullptr, *b_words_dev = nullptr;   // pa_ctx_rekey expansions
+    uint32_t *rekey_ok = nullptr;             // per vector: first draw accepted
     uint64_t *offs = nullptr;                 // paper mode: bit offset of each block's window
     uint32_t *wflags = nullptr;               // paper mode: window has a zero bit, [T]
     uint32_t *status = nullptr;               // device status of the last hash (paper mode)
@@ -1048,6 +1051,60 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     for (auto e : c->hb_done) if (e) cudaEventDestroy(e);
     c->da.free_all();
     delete c;
+}
+
+// ---- fresh hash keys per job (NEXT-2): expand a_i, b, c from `seed` on the GPU (reading
+// A7, bit-identical to pa_expand_a / pa_expand_bc) and recompute the transforms of the a_i
+// and of b.  Asynchronous on the context stream; later hashes use the new function.
+extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
+    if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    const Plan &p = c->pl;
+    const uint32_t Wa32 = (uint32_t)cdiv(p.gamma, 32), Wal32 = (uint32_t)cdiv(p.alpha, 32);
+    if (!c->a_words_dev) {
+        TRY(c->da.alloc(&c->a_words_dev, std::max<size_t>((size_t)c->nblk * Wa32, 1)));
+        TRY(c->da.alloc(&c->b_words_dev, Wal32));
+        TRY(c->da.alloc(&c->rekey_ok, (size_t)c->nblk + 2));
+    }
+    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+    const uint32_t launches0 = c->launches;
+    c->launches = 0;
+    {
+        ProfScope ps(c, "rekey_expand");
+        const uint32_t grid = (uint32_t)g_num_sms * 4;
+        if (c->nblk) {
+            CUDA_TRY(cudaMemsetAsync(c->rekey_ok, 0, (size_t)c->nblk * 4, c->stream));
+            expand_keys_first<<<grid, 256, 0, c->stream>>>(seed, p.b0, p.gamma, Wa32, c->nblk, 0, c->a_words_dev,
+                                                           c->rekey_ok);
+            expand_keys_dev<<<c->nblk, 256, 0, c->stream>>>(seed, p.b0, p.gamma, Wa32, 1, 0, c->a_words_dev, c->rekey_ok);
+        }
+        CUDA_TRY(cudaMemsetAsync(c->rekey_ok + c->nblk, 0, 8, c->stream));
+        expand_keys_first<<<grid, 256, 0, c->stream>>>(seed, kStreamB, p.alpha, Wal32, 1, 1, c->b_words_dev,
+                                                       c->rekey_ok + c->nblk);
+        expand_keys_first<<<grid, 256, 0, c->stream>>>(seed, kStreamC, p.alpha, Wal32, 1, 0, c->c_words,
+                                                       c->rekey_ok + c->nblk + 1);
+        c->launches += c->nblk ? 4 : 2;
+        CUDA_TRY(cudaGetLastError());
+    }
+    c->pl.seed = seed;
+    int rc = PA_OK;
+    {
+        ProfScope ps(c, "rekey_transforms");
+        if (c->nblk) {
+            const uint32_t Bm = p.mmh.limb_bits;
+            WordSrc wsa{c->a_words_dev, Wa32, Bm, (uint32_t)cdiv(p.gamma, Bm)};
+            rc = precompute_hat(c, c->smmh, wsa, c->nblk, rows_for(cdiv(p.gamma, Bm), p.mmh.n_row, p.mmh.n_col),
+                                c->scratch, c->ahat);
+        }
+        const uint32_t Bh = p.mh.limb_bits;
+        WordSrc wsb{c->b_words_dev, Wal32, Bh, (uint32_t)cdiv(p.alpha, Bh)};
+        if (rc == PA_OK)
+            rc = precompute_hat(c, c->smh, wsb, 1, rows_for(cdiv(p.alpha, Bh), p.mh.n_row, p.mh.n_col), c->scratch_mh,
+                                c->bhat);
+        c->launches += 5 + (c->nblk ? 3 : 0);
+    }
+    c->launches_total += c->launches;
+    c->launches = launches0;
+    return rc;
 }
 
 extern "C" int pa_ctx_status(pa_ctx *c) {

@@ -91,6 +91,10 @@ class PAContext:
         self.y_words = (self.gamma + 31) // 32
 
     # ------------------------------------------------------------------ queries
+    def rekey(self, seed: int) -> None:
+        """pa_ctx_rekey: fresh hash keys from ``seed`` expanded and transformed on the GPU."""
+        B.check(B.pa_ctx_rekey(self._h, seed & (2**64 - 1)))
+
     def status(self) -> None:
         """pa_ctx_status: raises PAError(PA_E_INSUFFICIENT_INPUT) if the last hash (paper
         mode) found fewer than paper_k usable windows."""

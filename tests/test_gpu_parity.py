@@ -343,6 +343,37 @@ def test_mh_only_comparator(n, m):
     ctx.close()
 
 
+def test_rekey_fresh_keys_on_gpu():
+    # NEXT-2: a_i, b, c re-drawn on the GPU (reading A7) give the same function as a context
+    # created with that seed; seed 32048 makes block 0's first gamma=17 draw all ones, so
+    # the device rejection/redraw path is exercised
+    PAContext = _pa()
+    for (n, r, m, s1, s2) in [(300_001, 4096, 20_000, 5, 77), (1_000, 16, 10, 9, 32048)]:
+        key = key_bytes(n, s1 + s2)
+        ctx = PAContext(n, r, m, seed=s1)
+        kd = torch.from_numpy(key).cuda()
+        assert bytes(ctx.hash(kd).cpu().numpy()) == oracle_seeded(key, n, r, m, s1)
+        ctx.rekey(s2)
+        got = bytes(ctx.hash(kd).cpu().numpy())
+        torch.cuda.synchronize()
+        assert got == oracle_seeded(key, n, r, m, s2)
+        ctx.close()
+    # paper mode and the MH-only comparator re-key too
+    g_, k_ = 607, 4
+    pn = 5 * g_
+    pkey = key_bytes(pn, 4)
+    pctx = PAContext(pn, 0, 100, g_, seed=1, paper_k=k_)
+    pctx.rekey(2)
+    assert bytes(pctx.hash(torch.from_numpy(pkey).cuda()).cpu().numpy()) == \
+        hashes.pa_hash_paper_seeded(pkey, pn, g_, k_, 100, 2)
+    pctx.close()
+    mctx = PAContext(5000, 0, 300, 0, seed=1, mh_only=True)
+    mkey = key_bytes(5000, 8)
+    mctx.rekey(3)
+    assert bytes(mctx.hash(torch.from_numpy(mkey).cuda()).cpu().numpy()) == hashes.mh_only_pa_seeded(mkey, 5000, 300, 3)
+    mctx.close()
+
+
 def _golden():
     path = os.path.join(ROOT, "tests", "golden", "digests.json")
     return json.load(open(path)) if os.path.exists(path) else {}
