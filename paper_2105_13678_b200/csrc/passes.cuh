@@ -772,7 +772,7 @@ row_mac(const MacArgs A) {
 #pragma unroll
             for (int e = 0; e < E; e++) acc[e] = 0;
         }
-        const uint32_t k = (DBG == 2) ? 0u : (uint32_t)(it - it0);
+        const uint32_t k = (DBG == 2 || DBG == 3) ? 0u : (uint32_t)(it - it0);
         const int s = (int)(k % NSX);
         mbar_wait(&bars[s], (k / NSX) & 1);
         uint32_t *xst = xs + s * SW;
@@ -803,11 +803,12 @@ row_mac(const MacArgs A) {
 #pragma unroll
                 for (int mm = 0; mm < R; mm++) {
                     const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
-                    acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], arow[k1], cx.p, cx.pinv), cx.p2);
+                    if constexpr (DBG == 3) acc[h * R + mm] += x[h * R + mm];
+                    else acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], arow[k1], cx.p, cx.pinv), cx.p2);
                 }
         }
         __syncthreads();                                 // X stage s and A^ are free
-        if (threadIdx.x == 0 && DBG != 2) {
+        if (threadIdx.x == 0 && DBG != 2 && DBG != 3) {
             if (it + NSX < it1) issue_x(it + NSX, s);
             if (!AIN && it + 1 < it1) issue_a(it + 1, as);
         }
