@@ -259,6 +259,12 @@ def main():
                     help="skip the MH-only PA comparator measurement")
     ap.add_argument("--only-device", action="store_true",
                     help="timed device steps only (no per-stage pass, no e2e): for ncu launch lists")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo only to validate the multi-rank path)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (validation of the N>1 host path on a 1-GPU box; not a bench)")
+    ap.add_argument("--verify", action="store_true",
+                    help="N>1: rank 0 checks the sharded hash against a whole-key single-GPU context")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -279,10 +285,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         args.gpus = world
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     # a dedicated (non-default) stream: the library then replays each hash as a CUDA graph
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
@@ -312,6 +323,19 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    verified = None
+    if world > 1 and args.verify:
+        res = distributed_hash(ctx, key_dev)
+        torch.cuda.synchronize()
+        if rank == 0:
+            whole = PAContext(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits)
+            ref = torch.empty(whole.nbytes_out, dtype=torch.uint8, device=dev)
+            whole.hash(torch.from_numpy(key_full).to(dev), ref)
+            torch.cuda.synchronize()
+            verified = bool(torch.equal(res, ref))
+            whole.close()
+            if not verified:
+                raise SystemExit("sharded hash differs from the whole-key hash")
     launches0 = ctx.query()["launches_total"]
     if world > 1:
         dist.barrier()
@@ -527,6 +551,10 @@ def main():
         "comparators": comparators,
         "fresh_keys": fresh,
     }
+    if verified is not None:
+        line["verified_vs_whole_key"] = verified
+    if world > 1 and (args.same_device or args.dist_backend != "nccl"):
+        line["validation_only"] = f"{world} ranks, backend {args.dist_backend}, same_device={args.same_device}"
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample(w)
     print(json.dumps(line), flush=True)
