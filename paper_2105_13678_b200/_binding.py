@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_pa.so")
+# PA_DEV_LIB: an in-tree A/B build of the same sources (scripts/build_variant.sh), development only
+LIB_PATH = os.environ.get("PA_DEV_LIB") or os.path.join(_HERE, "_pa.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "

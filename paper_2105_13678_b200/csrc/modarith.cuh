@@ -23,6 +23,12 @@ struct alignas(16) PrimeK {  // per-prime constants passed to kernels
     uint32_t pw[8];        // 2^(32 i) mod p, i < 8 (multiword limb reduction)
 };
 
+// All primes of a stage by value: passed as a kernel parameter, so the per-prime constants
+// are constant-bank operands of the multiply instructions (no shared/global loads)
+struct PrimeSet {
+    PrimeK k[kMaxPrimes];
+};
+
 // a * b + c with a 32x32 -> 64-bit multiply (one IMAD.WIDE.U32)
 __device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
     uint64_t r;

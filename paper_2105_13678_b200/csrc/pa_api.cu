@@ -218,6 +218,7 @@ struct StageDev {
     pa_stage_plan pl{};
     uint32_t L = 0, lg = 0;
     PrimeK *pk = nullptr;
+    PrimeSet pks{};                     // host copy, passed by value to the pack kernels
     uint32_t *scale = nullptr;
     uint32_t *regtw[2] = {}, *regtwp[2] = {};
     uint32_t *rtw = nullptr;            // [P][stride]: col fwd, col inv, row fwd, row inv
@@ -348,6 +349,7 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cuda
     TRY(da.alloc(&sd.scale, P));
     TRY(da.alloc(&sd.rtw, rtall.size()));
     CUDA_TRY(cudaMemcpy(sd.pk, pk.data(), P * sizeof(PrimeK), cudaMemcpyHostToDevice));
+    for (uint32_t i = 0; i < P; i++) sd.pks.k[i] = pk[i];
     CUDA_TRY(cudaMemcpy(sd.scale, scale.data(), P * 4, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(sd.rtw, rtall.data(), rtall.size() * 4, cudaMemcpyHostToDevice));
     for (int dir = 0; dir < 2; dir++) {
@@ -717,13 +719,13 @@ static uint32_t mac_v_rt(int slog) {
 }
 
 template <int NW>
-static void launch_pack_key(const KeySrc &s, uint32_t nvec, const PrimeK *pk, uint32_t P, uint32_t wxp, uint32_t *res,
+static void launch_pack_key(const KeySrc &s, uint32_t nvec, const PrimeSet &pk, uint32_t P, uint32_t wxp, uint32_t *res,
                             cudaStream_t st) {
     const dim3 grid((wxp + kPackT - 1) / kPackT, nvec);
     pack_key_residues<NW><<<grid, kPackT, 0, st>>>(s, pk, P, wxp, res);
 }
 
-static int launch_pack(const KeyLimbs &src, uint32_t B, uint32_t grid, const PrimeK *pk, uint32_t P, uint32_t nvec,
+static int launch_pack(const KeyLimbs &src, uint32_t B, uint32_t grid, const PrimeSet &pk, uint32_t P, uint32_t nvec,
                        uint32_t wxp, uint32_t *res, cudaStream_t st) {
     const int nw = B <= 56 ? 0 : (int)((B + 31) / 32);
     switch (nw) {
@@ -742,7 +744,7 @@ static int launch_pack(const KeyLimbs &src, uint32_t B, uint32_t grid, const Pri
 }
 
 template <class Src>
-static int launch_pack(const Src &src, uint32_t B, uint32_t grid, const PrimeK *pk, uint32_t P, uint32_t nvec,
+static int launch_pack(const Src &src, uint32_t B, uint32_t grid, const PrimeSet &pk, uint32_t P, uint32_t nvec,
                        uint32_t wxp, uint32_t *res, cudaStream_t st) {
     const int nw = B <= 56 ? 0 : (int)((B + 31) / 32);
     switch (nw) {
@@ -773,7 +775,7 @@ static int stage_pack_col(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec
         ProfScope ps(c, tag_pack);
         const uint64_t total = (uint64_t)nvec * wxp;
         const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
-        TRY(launch_pack(src, sd.pl.limb_bits, grid, sd.pk, P, nvec, wxp, res, c->stream));
+        TRY(launch_pack(src, sd.pl.limb_bits, grid, sd.pks, P, nvec, wxp, res, c->stream));
         c->launches++;
     }
     {
@@ -1161,7 +1163,7 @@ static KeySrc key_src(const pa_ctx *c, const uint8_t *key_slice, uint32_t v0, ui
 
 template <int NW>
 static void launch_pack_bits(const KeySrc &s, const uint64_t *offs, uint32_t gamma, uint32_t B, uint32_t wx,
-                             uint32_t nvec, const PrimeK *pk, uint32_t P, uint32_t wxp, uint32_t *res, cudaStream_t st) {
+                             uint32_t nvec, const PrimeSet &pk, uint32_t P, uint32_t wxp, uint32_t *res, cudaStream_t st) {
     const dim3 grid((wxp + kPackT - 1) / kPackT, nvec);
     pack_bits_residues<NW><<<grid, kPackT, 0, st>>>(s, offs, gamma, B, wx, pk, P, wxp, res);
 }
@@ -1187,7 +1189,7 @@ static int paper_pack(pa_ctx *c, const uint8_t *key) {
     const uint32_t wxp = c->rows_mmh * p.mmh.n_row;
     const int nw = (int)cdiv(B, 32);
     switch (nw) {
-#define PA_PB(N) case N: launch_pack_bits<N>(ks, c->offs, (uint32_t)p.gamma, B, wx, c->nblk, c->smmh.pk, P, wxp, c->res, c->stream); break;
+#define PA_PB(N) case N: launch_pack_bits<N>(ks, c->offs, (uint32_t)p.gamma, B, wx, c->nblk, c->smmh.pks, P, wxp, c->res, c->stream); break;
         PA_PB(1) PA_PB(2) PA_PB(3) PA_PB(4) PA_PB(5) PA_PB(6) PA_PB(7) PA_PB(8)
 #undef PA_PB
         default: return set_err(PA_E_PARAM, "unsupported limb width %u", B);

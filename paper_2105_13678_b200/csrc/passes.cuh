@@ -159,17 +159,30 @@ __device__ __forceinline__ uint32_t limb_words_redc(const uint32_t (&w)[NW], con
     return s;
 }
 
+// The residues of one multiword limb modulo all P primes, stored P x wxp apart from o.
+template <int NW>
+__device__ __forceinline__ void store_residues(uint32_t *o, uint32_t wxp, uint32_t P, uint32_t any,
+                                               const uint32_t (&w)[NW], const PrimeSet &ks) {
+    if (any) {
+#pragma unroll
+        for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
+            if (pi >= P) break;
+            *o = limb_words_redc<NW>(w, ks.k[pi]);
+            o += wxp;
+        }
+    } else {
+        for (uint32_t pi = 0; pi < P; pi++, o += wxp) *o = 0u;
+    }
+}
+
 // S1 ("split the input bit sequence and map it to a prime field"): every
 // limb of every vector is extracted once and reduced modulo all P primes.
 // res layout: [vec][prime][wxp] with wxp = rows * N1 (zero beyond the vector's limbs).
 // NW = 0: limbs of <= 56 bits (one 64-bit value, limb_redc); else NW 32-bit words.
 template <class Src, int NW>
-__global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeK *__restrict__ pk,
+__global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeSet ks,
                                                      uint32_t P, uint32_t nvec, uint32_t wxp,
                                                      uint32_t *__restrict__ res) {
-    __shared__ PrimeK ks[kMaxPrimes];
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) ks[i] = pk[i];
-    __syncthreads();
     const uint64_t total = (uint64_t)nvec * wxp;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
@@ -177,17 +190,16 @@ __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeK
         uint32_t *o = res + (size_t)iv * P * wxp + j;
         if constexpr (NW == 0) {
             const uint64_t v = src(iv, j);
-            for (uint32_t pi = 0; pi < P; pi++) {
-                const uint32_t p = ks[pi].p;
-                o[(size_t)pi * wxp] = v ? limb_redc(v, p, ks[pi].pinv) : 0u;
-            }
+#pragma unroll
+            for (uint32_t pi = 0; pi < kMaxPrimes; pi++)
+                if (pi < P) o[(size_t)pi * wxp] = v ? limb_redc(v, ks.k[pi].p, ks.k[pi].pinv) : 0u;
         } else {
             uint32_t w[NW];
             src.template words<NW>(iv, j, w);
             uint32_t any = 0;
 #pragma unroll
             for (int i = 0; i < NW; i++) any |= w[i];
-            for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = any ? limb_words_redc<NW>(w, ks[pi]) : 0u;
+            store_residues<NW>(o, wxp, P, any, w, ks);
         }
     }
 }
@@ -198,12 +210,10 @@ __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeK
 // reduces them modulo every prime.  res layout as pack_residues.
 constexpr int kPackT = 256;
 template <int NW>
-__global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeK *__restrict__ pk, uint32_t P,
+__global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
     constexpr int MAXW = kPackT * NW + 4;                     // staged words (LB <= 4 NW bytes per limb)
     __shared__ uint32_t sw[MAXW];
-    __shared__ PrimeK ks[kMaxPrimes];
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) ks[i] = pk[i];
     const uint32_t iv = blockIdx.y;
     const uint32_t jt0 = blockIdx.x * kPackT;
     const int64_t start = (int64_t)iv * s.blk_bytes;
@@ -220,18 +230,23 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     const uint32_t *kw = reinterpret_cast<const uint32_t *>(s.key) + (interior ? gw0 : 0);
     // all of a thread's loads are issued before its stores (no load->store serialisation)
     constexpr int KU = (MAXW + kPackT - 1) / kPackT;
-    {
-        uint32_t v[KU];
+    uint32_t v[KU];
+    if (interior) {
 #pragma unroll
         for (int u = 0; u < KU; u++) {
             const int k = threadIdx.x + u * kPackT;
-            v[u] = (k < nw) ? (interior ? __ldg(kw + k) : key_word(s, gw0 + k)) : 0u;
+            v[u] = (k < nw) ? __ldg(kw + k) : 0u;
         }
-#pragma unroll
+    } else {
         for (int u = 0; u < KU; u++) {
             const int k = threadIdx.x + u * kPackT;
-            if (k < nw) sw[k] = v[u];
+            v[u] = (k < nw) ? key_word(s, gw0 + k) : 0u;
         }
+    }
+#pragma unroll
+    for (int u = 0; u < KU; u++) {
+        const int k = threadIdx.x + u * kPackT;
+        if (k < nw) sw[k] = v[u];
     }
     __syncthreads();
     const uint32_t j = jt0 + threadIdx.x;
@@ -272,12 +287,7 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
 #pragma unroll
         for (int i = 0; i < NW; i++) any |= w[i];
     }
-    uint32_t *o = res + (size_t)iv * P * wxp + j;
-    if (!any) {
-        for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = 0u;
-        return;
-    }
-    for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = limb_words_redc<NW>(w, ks[pi]);
+    store_residues<NW>(res + (size_t)iv * P * wxp + j, wxp, P, any, w, ks);
 }
 
 // ---------------------------------------------------------------- paper mode (NEXT-1)
@@ -330,12 +340,10 @@ __global__ void window_resolve(const uint32_t *flags, uint32_t T, uint32_t k, ui
 template <int NW>
 __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, const uint64_t *__restrict__ offs,
                                                            uint32_t gamma, uint32_t B, uint32_t wx,
-                                                           const PrimeK *__restrict__ pk, uint32_t P, uint32_t wxp,
+                                                           const PrimeSet ks, uint32_t P, uint32_t wxp,
                                                            uint32_t *__restrict__ res) {
     constexpr int MAXW = kPackT * NW + 8;
     __shared__ uint32_t sw[MAXW];
-    __shared__ PrimeK ks[kMaxPrimes];
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) ks[i] = pk[i];
     const uint32_t iv = blockIdx.y;
     const uint32_t jt0 = blockIdx.x * kPackT;
     const int64_t off = (int64_t)offs[iv];
@@ -385,12 +393,7 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
         w[i] = v;
         any |= v;
     }
-    uint32_t *o = res + (size_t)iv * P * wxp + j;
-    if (!any) {
-        for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = 0u;
-        return;
-    }
-    for (uint32_t pi = 0; pi < P; pi++) o[(size_t)pi * wxp] = limb_words_redc<NW>(w, ks[pi]);
+    store_residues<NW>(res + (size_t)iv * P * wxp + j, wxp, P, any, w, ks);
 }
 
 // MH-only comparator: out[u] = bits [32 u, 32 u + 32) of x, the integer of key bits
@@ -441,7 +444,10 @@ struct ColArgs {
 // length N1 = 2^N1_LOG is a template parameter so every element address is a per-unit
 // base plus a compile-time offset (no per-element 64-bit index arithmetic).
 template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
-__global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)), S_LOG == 8 ? 4 : (S_LOG < 8 ? 3 : 1))
+#ifndef PA_COL8_MINB
+#define PA_COL8_MINB 4
+#endif
+__global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)), S_LOG == 8 ? PA_COL8_MINB : (S_LOG < 8 ? 3 : 1))
 col_pass(const ColArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int E = SP::E;
@@ -671,14 +677,15 @@ constexpr size_t mac_smem_bytes() {
 }
 __device__ __forceinline__ int swz32(int P) { return P ^ ((P >> 5) & 31); }
 
-// <= 4E registers per thread (the register file bounds the warps per SM)
 __host__ __device__ constexpr int mac_threads(int slog, int elog) { return mac_v(slog) * (1 << (slog - elog)); }
-__host__ __device__ constexpr int mac_minb(int slog, int elog) {
-    return (65536 / (mac_threads(slog, elog) * 4 * (1 << elog))) < 8 ? (65536 / (mac_threads(slog, elog) * 4 * (1 << elog)))
-                                                                        : 8;
+// CTAs per SM as shared memory admits them (227 KB usable, 1 KB reserved per CTA); the
+// register budget per thread follows from it (65536 / (minb * threads), e.g. 6 CTAs of 64
+// threads -> 167 registers: measured 124 -> 118 us for the C4 row_mac against a 128 cap)
+__host__ __device__ constexpr int mac_minb(size_t smem_bytes) {
+    return (int)(232448 / (smem_bytes + 1024)) < 1 ? 1 : ((int)(232448 / (smem_bytes + 1024)) > 8 ? 8 : (int)(232448 / (smem_bytes + 1024)));
 }
 template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = 2, int AIN = 0>
-__global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(S_LOG, E_LOG) < 1 ? 1 : mac_minb(S_LOG, E_LOG))
+__global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(mac_smem_bytes<S_LOG, PAD, NSX, AIN>()))
 row_mac(const MacArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int S = SP::S, E = SP::E;
