@@ -212,6 +212,25 @@ int pa_philox4x64_10(uint64_t key0, uint64_t key1, uint64_t nwords, uint64_t *ou
 int pa_expand_a(uint64_t seed, uint64_t i, uint64_t gamma, uint32_t *out);
 int pa_expand_bc(uint64_t seed, uint64_t alpha, uint32_t *b_out, uint32_t *c_out);
 
+/* Parameter derivation of the paper's shape.
+ *
+ * pa_derive_security_coefficient: s = ceil(2 log2(1/epsilon) - 2), at least 1 -- the
+ *   smallest s with 2^(-s/2-1) <= epsilon, inverting the composition bound of PAPER.md:185-188
+ *   ("secure under composition").  0 < epsilon < 1, else PA_E_PARAM.
+ * pa_select_block_count: k = floor(1/ratio) for the compression ratio 0 < ratio < 1
+ *   ("k <= 1/r"; Table 3: 0.2957 -> 3, 0.0972 -> 10), else PA_E_PARAM.
+ * pa_select_gamma: the largest Mersenne exponent (SPEC.md:33 table) with k gamma <= target_n
+ *   ("n is equal to gamma x k"); when even k * 3 > target_n, the smallest
+ *   exponent with *exceeds = 1.  target_n >= 1 and k >= 1, else PA_E_PARAM.
+ * pa_derive_paper_params: the composition SPEC.md:185-191, 465: k from ratio, gamma from
+ *   (target_n, k), n = k gamma, s from epsilon, m = n - t - s.  PA_E_PARAM when m <= 0 or
+ *   m + s > gamma (the invariant "m + s <= gamma").  Outputs may be NULL. */
+int pa_derive_security_coefficient(double epsilon, uint64_t *s);
+int pa_select_block_count(double ratio, uint64_t *k);
+int pa_select_gamma(uint64_t target_n, uint64_t k, uint64_t *gamma, int *exceeds);
+int pa_derive_paper_params(uint64_t target_n, double ratio, uint64_t t, double epsilon, uint64_t *gamma,
+                           uint64_t *k, uint64_t *n, uint64_t *s, uint64_t *m);
+
 /* Code of the last failure on this thread; copies its message into buf. */
 int pa_last_error(char *buf, size_t len);
 

@@ -4,4 +4,5 @@ The package is a thin Python layer over the C-ABI library ``_pa.so`` (include/pa
 hand-written sm_100a CUDA kernels do every step of the hash; PyTorch provides device
 memory, streams and ``torch.distributed`` process groups.  There is no CPU fallback.
 """
-from .pa import PAContext, plan, shard_ranges  # noqa: F401
+from .pa import (PAContext, derive_paper_params, derive_security_coefficient, plan,  # noqa: F401
+                 select_block_count, select_gamma, shard_ranges)

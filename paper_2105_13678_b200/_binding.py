@@ -89,11 +89,17 @@ pa_philox4x64_10 = _sig("pa_philox4x64_10", i32, u64, u64, u64, vp)
 pa_expand_a = _sig("pa_expand_a", i32, u64, u64, u64, vp)
 pa_expand_bc = _sig("pa_expand_bc", i32, u64, u64, vp, vp)
 pa_last_error = _sig("pa_last_error", i32, ctypes.c_char_p, ctypes.c_size_t)
+pa_derive_security_coefficient = _sig("pa_derive_security_coefficient", i32, ctypes.c_double, ctypes.POINTER(u64))
+pa_select_block_count = _sig("pa_select_block_count", i32, ctypes.c_double, ctypes.POINTER(u64))
+pa_select_gamma = _sig("pa_select_gamma", i32, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(i32))
+pa_derive_paper_params = _sig("pa_derive_paper_params", i32, u64, ctypes.c_double, u64, ctypes.c_double,
+                              *([ctypes.POINTER(u64)] * 5))
 
 EXPORTED = ["pa_ctx_create", "pa_ctx_create_ex", "pa_hash", "pa_hash_host", "pa_hash_batch", "pa_hash_host_batch", "pa_mmh_partial", "pa_mh_merge",
             "pa_ctx_destroy", "pa_ctx_status", "pa_ctx_rekey", "pa_ctx_query", "pa_ctx_set_stream", "pa_ctx_set_profiling",
             "pa_ctx_stage_times", "pa_plan", "pa_philox4x64_10", "pa_expand_a", "pa_expand_bc",
-            "pa_last_error"]
+            "pa_last_error", "pa_derive_security_coefficient", "pa_select_block_count", "pa_select_gamma",
+            "pa_derive_paper_params"]
 
 
 class PAError(RuntimeError):

@@ -799,11 +799,11 @@ static int stage_pack_col(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec
 // into zeroed acc); else first / later call of a multi-call accumulation (whole units per
 // CTA, store / modular read-modify-write, no atomics).
 static int stage_mac(pa_ctx *c, StageDev &sd, uint32_t nvec, const uint32_t *scratch, const uint32_t *hat,
-                     uint32_t *acc, bool first, const char *tag, bool only = true) {
+                     uint32_t *acc, bool first, const char *tag, bool only = true, bool zero = true) {
     const int rlog = __builtin_ctz(sd.pl.n_row);
     const uint32_t P = sd.pl.nprimes;
     ProfScope ps(c, tag);
-    if (only) CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)P * sd.L * 4, c->stream));
+    if (only && zero) CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)P * sd.L * 4, c->stream));
     MacArgs M{};
     M.mode = only ? 0u : (first ? 1u : 2u);
     M.nt = ntt_args(sd, 0, 1);
@@ -1224,9 +1224,10 @@ static int mmh_forward(pa_ctx *c, const uint8_t *key_slice, uint32_t v0, uint32_
                           "mmh_fwd_col");
 }
 
-static int mmh_mac(pa_ctx *c, uint32_t v0, uint32_t v1, bool first, bool only) {
+static int mmh_mac(pa_ctx *c, uint32_t v0, uint32_t v1, bool first, bool only, bool zero = true) {
     const size_t off = (size_t)v0 * c->pl.mmh.nprimes * c->smmh.L;
-    return stage_mac(c, c->smmh, v1 - v0, c->scratch + off, c->ahat + off, c->acc, first, "mmh_fwd_row_mac", only);
+    return stage_mac(c, c->smmh, v1 - v0, c->scratch + off, c->ahat + off, c->acc, first, "mmh_fwd_row_mac", only,
+                     zero);
 }
 
 // ---- S4+S5 after all blocks are accumulated -> canonical y
@@ -1245,8 +1246,10 @@ static int mmh_tail(pa_ctx *c, uint32_t **y_out) {
 
 // ---- S1-S5 on this ctx's blocks -> canonical y in the returned buffer (Wg words)
 static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
+    // accumulators zeroed first: the chain pack -> col -> row_mac is back-to-back kernels
+    CUDA_TRY(cudaMemsetAsync(c->acc, 0, (size_t)c->pl.mmh.nprimes * c->smmh.L * 4, c->stream));
     TRY(mmh_forward(c, key_slice, 0, c->nblk));
-    TRY(mmh_mac(c, 0, c->nblk, true, true));
+    TRY(mmh_mac(c, 0, c->nblk, true, true, false));
     return mmh_tail(c, y_out);
 }
 
@@ -1628,6 +1631,51 @@ extern "C" int pa_expand_a(uint64_t seed, uint64_t i, uint64_t gamma, uint32_t *
     std::vector<uint32_t> w;
     TRY(expand_words(seed, i, gamma, w, true));
     memcpy(out, w.data(), w.size() * 4);
+    return PA_OK;
+}
+
+extern "C" int pa_derive_security_coefficient(double epsilon, uint64_t *s) {
+    if (!(epsilon > 0.0 && epsilon < 1.0) || !s) return set_err(PA_E_PARAM, "epsilon must be in (0, 1)");
+    // smallest integer s >= 1 with 2^(-s/2 - 1) <= epsilon, i.e. s >= 2 log2(1/epsilon) - 2;
+    // the 1e-9 slack keeps exact powers (epsilon = 2^-j) from rounding up
+    const double x = 2.0 * std::log2(1.0 / epsilon) - 2.0;
+    const double c = std::ceil(x - 1e-9);
+    *s = c < 1.0 ? 1 : (uint64_t)c;
+    return PA_OK;
+}
+
+extern "C" int pa_select_block_count(double ratio, uint64_t *k) {
+    if (!(ratio > 0.0 && ratio < 1.0) || !k) return set_err(PA_E_PARAM, "compression ratio must be in (0, 1)");
+    *k = (uint64_t)std::floor(1.0 / ratio + 1e-12);
+    return PA_OK;
+}
+
+extern "C" int pa_select_gamma(uint64_t target_n, uint64_t k, uint64_t *gamma, int *exceeds) {
+    if (!target_n || !k || !gamma) return set_err(PA_E_PARAM, "target_n and k must be >= 1");
+    uint64_t best = 0;
+    for (uint64_t e : kMersenne)
+        if (e <= target_n / k) best = e;
+    if (exceeds) *exceeds = best ? 0 : 1;
+    *gamma = best ? best : kMersenne[0];
+    return PA_OK;
+}
+
+extern "C" int pa_derive_paper_params(uint64_t target_n, double ratio, uint64_t t, double epsilon, uint64_t *gamma,
+                                      uint64_t *k, uint64_t *n, uint64_t *s, uint64_t *m) {
+    uint64_t kk = 0, g = 0, ss = 0;
+    int ex = 0;
+    TRY(pa_select_block_count(ratio, &kk));
+    TRY(pa_select_gamma(target_n, kk, &g, &ex));
+    TRY(pa_derive_security_coefficient(epsilon, &ss));
+    const uint64_t nn = kk * g;
+    if (t + ss >= nn) return set_err(PA_E_PARAM, "m = n - t - s must be > 0");
+    const uint64_t mm = nn - t - ss;
+    if (mm + ss > g) return set_err(PA_E_PARAM, "m + s must be <= gamma (SPEC.md:187)");
+    if (gamma) *gamma = g;
+    if (k) *k = kk;
+    if (n) *n = nn;
+    if (s) *s = ss;
+    if (m) *m = mm;
     return PA_OK;
 }
 

@@ -58,6 +58,36 @@ def plan(n: int, r: int, m: int, gamma: int = 0, block_range=None, limb_bits: in
     return info.as_dict()
 
 
+# ---- parameter derivation of the paper's shape (NEXT-1; include/pa.h)
+def derive_security_coefficient(epsilon: float) -> int:
+    """pa_derive_security_coefficient: s = ceil(2 log2(1/epsilon) - 2), at least 1."""
+    s = ctypes.c_uint64()
+    B.check(B.pa_derive_security_coefficient(float(epsilon), ctypes.byref(s)))
+    return s.value
+
+
+def select_block_count(ratio: float) -> int:
+    """pa_select_block_count: k = floor(1/ratio) (PAPER.md:282-285)."""
+    k = ctypes.c_uint64()
+    B.check(B.pa_select_block_count(float(ratio), ctypes.byref(k)))
+    return k.value
+
+
+def select_gamma(target_n: int, k: int) -> tuple[int, bool]:
+    """pa_select_gamma: (largest Mersenne exponent with k gamma <= target_n, exceeds flag)."""
+    g, ex = ctypes.c_uint64(), ctypes.c_int32()
+    B.check(B.pa_select_gamma(int(target_n), int(k), ctypes.byref(g), ctypes.byref(ex)))
+    return g.value, bool(ex.value)
+
+
+def derive_paper_params(target_n: int, ratio: float, t: int, epsilon: float) -> dict:
+    """pa_derive_paper_params: {gamma, k, n, s, m} with m = n - t - s and m + s <= gamma."""
+    v = [ctypes.c_uint64() for _ in range(5)]
+    B.check(B.pa_derive_paper_params(int(target_n), float(ratio), int(t), float(epsilon),
+                                     *[ctypes.byref(x) for x in v]))
+    return dict(zip(("gamma", "k", "n", "s", "m"), (x.value for x in v)))
+
+
 def shard_ranges(k: int, G: int) -> list[tuple[int, int]]:
     """Rank g owns blocks [floor(k g / G), floor(k (g+1) / G))."""
     return [(k * g // G, k * (g + 1) // G) for g in range(G)]
