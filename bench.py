@@ -275,10 +275,11 @@ def main():
         run_reference(args, w)
         return
 
+    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2105_13678_b200 import PAContext
-    from paper_2105_13678_b200.pa import distributed_hash, key_slice_bytes, shard_ranges
+    from paper_2105_13678_b200.pa import distributed_hash, key_slice_bytes, shard_ranges, stream_hash
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -371,6 +372,50 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+    # ---- N>1 stream mode (NEXT-3): G independent keys per step, the MH root rotating
+    # (key j merged on rank j mod G), so MH no longer serialises on rank 0
+    mr_stream = None
+    if world > 1:
+        def roll_slice(j):
+            kb = np.roll(key_full, 977 * j)
+            if w.n % 8:
+                kb[-1] &= (0xFF << (8 - w.n % 8)) & 0xFF
+            return kb
+        keys_j = [torch.from_numpy(roll_slice(j)[lo:hi].copy()).to(dev) for j in range(world)]
+        for _ in range(2):
+            outs_j = stream_hash(ctx, keys_j)
+        torch.cuda.synchronize()
+        if args.verify:
+            ok = torch.ones(1, dtype=torch.int32, device=dev)
+            for j, o in outs_j.items():
+                whole = PAContext(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits)
+                ref = torch.empty(whole.nbytes_out, dtype=torch.uint8, device=dev)
+                whole.hash(torch.from_numpy(roll_slice(j)).to(dev), ref)
+                torch.cuda.synchronize()
+                ok &= int(torch.equal(o, ref))
+                whole.close()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if not ok.item():
+                raise SystemExit("rotating-root stream hash differs from the whole-key hash")
+            verified = True if verified is None else verified
+        dist.barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        bb = torch.cuda.Event(enable_timing=True)
+        nst = max(3, args.steps // 5)
+        a.record(stream)
+        for _ in range(nst):
+            stream_hash(ctx, keys_j)
+        bb.record(stream)
+        torch.cuda.synchronize()
+        ts = torch.tensor([a.elapsed_time(bb) / nst], dtype=torch.float64, device=dev)
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        ms_s = ts.item()
+        mr_stream = {"keys_per_step": world, "value": world * w.n / (ms_s * 1e-3) / 1e6, "unit": "Mbps",
+                     "ms_per_step": ms_s, "ms_per_key": ms_s / world,
+                     "api": "stream_hash: pa_mmh_partial per shard, async gather to rank j mod G, pa_mh_merge there",
+                     "l2": "not flushed between keys (back-to-back stream)"}
+
     # ---- per-launch times: the same K steps again with CUDA events recorded on the
     # context stream around every launch (pa_ctx_set_profiling); e2e via the host API
     ctx.set_profiling(True)
@@ -547,7 +592,7 @@ def main():
         "roofline": roof,
         "stages_ms_per_step": {kk: v[0] / nsteps_prof for kk, v in sorted(stages.items())},
         "e2e": e2e,
-        "stream": stream_mode,
+        "stream": stream_mode if world == 1 else mr_stream,
         "comparators": comparators,
         "fresh_keys": fresh,
     }

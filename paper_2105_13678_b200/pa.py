@@ -288,3 +288,35 @@ def distributed_hash(ctx: PAContext, key_slice, group=None, root: int = 0):
     """Multi-GPU hash with a shard context: pa_mmh_partial on every rank, NCCL all-gather
     of the residues, pa_mh_merge on `root` (S6-S7)."""
     return shard_gather_merge(ctx.mmh_partial, ctx.mh_merge, key_slice, group, root)
+
+
+def stream_gather_merge(partial_fn, merge_fn, key_slices, group=None):
+    """NEXT-3: a stream of independent keys with the MH root rotating.
+    Key j: every rank computes its shard residue y_g = partial_fn(key_slices[j]); the residues
+    are gathered to rank j mod G (asynchronously, so the gather of key j overlaps the partial
+    of key j+1), which runs merge_fn(parts) (sum mod p + MH).  Every rank thus does one
+    G-th of each key's MMH and one MH in G: the MH term no longer serialises on one root.
+    Returns {j: output} for the keys this rank is root of."""
+    import torch
+    import torch.distributed as dist
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    pending = []
+    for j, ks in enumerate(key_slices):
+        y = partial_fn(ks).contiguous()
+        root = j % G
+        parts = torch.empty((G, y.numel()), dtype=y.dtype, device=y.device) if me == root else None
+        work = dist.gather(y, list(parts.unbind(0)) if parts is not None else None, dst=root, group=group,
+                           async_op=True)
+        pending.append((j, root, y, parts, work))
+    outs = {}
+    for j, root, y, parts, work in pending:
+        work.wait()
+        if me == root:
+            outs[j] = merge_fn(parts)
+    return outs
+
+
+def stream_hash(ctx: PAContext, key_slices, group=None):
+    """Rotating-root stream hash with a shard context (pa_mmh_partial / pa_mh_merge)."""
+    return stream_gather_merge(ctx.mmh_partial, ctx.mh_merge, key_slices, group)

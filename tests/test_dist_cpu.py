@@ -84,3 +84,49 @@ def test_gloo_two_ranks_equals_single(n, r, m):
     assert res[1] is None                       # output exists on the root only
     want = hashes.pa_hash_seeded(key_bytes(n, 0x77), n, r, m, seed)
     assert res[0] == want
+
+
+def _stream_worker(rank, world, port, n, r, m, seed, nkeys, q):
+    """NEXT-3 rotating-root stream: key j's residues are gathered to rank j mod G."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_13678_b200.pa import key_slice_bytes, shard_ranges, stream_gather_merge
+        pp = hashes.plan_params(n, r, m)
+        k, gamma, alpha = pp["k"], pp["gamma"], pp["alpha"]
+        b0, b1 = shard_ranges(k, world)[rank]
+        lo, hi = key_slice_bytes(n, r, (b0, b1))
+        slices = [key_bytes(n, 0x100 + j)[lo:hi] for j in range(nkeys)]
+        a_shard = {i: seeds.expand_a(seed, i, gamma) for i in range(b0, b1)}
+
+        def partial(ks):
+            nbits = min(n - b0 * r, (b1 - b0) * r)
+            xs = hashes.key_blocks(np.asarray(ks), nbits, r)
+            return _words_tensor(hashes.mmh_eval([a_shard[b0 + j] for j in range(len(xs))], xs, gamma), gamma)
+
+        def merge(parts):
+            y = hashes.merge_residues([_int(p) for p in parts], gamma)
+            return hashes.mh_output(y, seeds.expand_b(seed, alpha), seeds.expand_c(seed, alpha), alpha, m)
+
+        q.put((rank, stream_gather_merge(partial, merge, slices)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_rotating_root_stream():
+    world, seed, nkeys = 2, 4321, 3
+    n, r, m = 50_000, 2048, 3_000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stream_worker, args=(i, world, port, n, r, m, seed, nkeys, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sorted(res[0]) == [0, 2] and sorted(res[1]) == [1]      # roots rotate: j mod G
+    for rank, outs in res.items():
+        for j, out in outs.items():
+            assert out == hashes.pa_hash_seeded(key_bytes(n, 0x100 + j), n, r, m, seed), (rank, j)

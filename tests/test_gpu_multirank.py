@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_two_rank_bench_matches_whole_key(config):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + int(config[1])),
-           "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
+           "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3", "--dist-backend", "gloo",
            "--same-device", "--verify", "--config", config, "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
@@ -27,3 +27,5 @@ def test_two_rank_bench_matches_whole_key(config):
     assert line["n_gpus"] == 2
     assert line["verified_vs_whole_key"] is True
     assert line["value"] > 0 and line["gpu_launches"] > 0
+    # NEXT-3 rotating-root stream mode ran and was verified against whole-key hashes too
+    assert line["stream"]["keys_per_step"] == 2 and line["stream"]["value"] > 0
