@@ -16,6 +16,8 @@ Contents
                       (gamma-bit blocks with reload) and in the r-bit-block shape
                       the B200 library computes (readings A1-A10 of DESIGN.md).
 ``oracle.seeds``      hash-key expansion a_i, b, c from a 64-bit seed (reading A7).
+``oracle.toeplitz``   Toeplitz-hashing PA over GF(2), the NEXT-4 comparator,
+                      readings A14 (index convention) and A15 (seeded diagonal).
 ``oracle.params``     NEXT-1 parameter derivation (security coefficient, block count,
                       gamma selection), exact rational scans.
 ``oracle.security``   brute-force universality / composition checks
