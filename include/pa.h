@@ -119,6 +119,16 @@ typedef struct {
      * b odd and c drawn with alpha = n (reading A7).  r, gamma, shards and paper_k must be 0;
      * m <= n.  pa_hash / pa_hash_host only. */
     uint64_t mh_only;
+    /* Comparator (Table 1 "Toeplitz Hashing PA"):
+     * when nonzero the context computes Toeplitz-hashing PA over GF(2):
+     * out bit j = XOR_{i<n} d[m-1-j+i] x_i (reading A14), x_i = key bit i (MSB-first), the
+     * n + m - 1 diagonal bits d drawn from `seed` (reading A15).  Exact integer NTT
+     * convolution mod one 30-bit prime, r x r block split (r = min(2^22, 2^ceil(log2 max(n,
+     * m))), at least 512; limb_bits != 0 forces r = 2^limb_bits, 9..22).  r, gamma, shards,
+     * paper_k, mh_only must be 0; n below the prime
+     * (n < 2^29).  pa_query reports r, k = ceil(n/r) input blocks, alpha = ceil(m/r) output
+     * blocks and the transform in `mmh`.  pa_hash / pa_hash_host only. */
+    uint64_t toeplitz;
 } pa_params;
 
 /* Create a context on the current CUDA device.  `p` is the Mersenne EXPONENT

@@ -66,3 +66,11 @@ def toeplitz_pa_matrix(key, n: int, m: int, d: int) -> bytes:
 
 def toeplitz_pa_seeded(key, n: int, m: int, seed: int) -> bytes:
     return toeplitz_pa(key, n, m, expand_diagonal(seed, n + m - 1))
+
+
+def toeplitz_bits(key, n: int, m: int, d: int, js) -> list[int]:
+    """Output bits j in js only (the same definition, one row at a time): for sampled
+    parity at sizes where the whole output is out of the oracle's reach."""
+    X = _key_int_lsb_first(key, n)
+    mask = (1 << n) - 1
+    return [(((d >> (m - 1 - j)) & mask & X).bit_count()) & 1 for j in js]

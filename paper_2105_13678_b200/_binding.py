@@ -58,7 +58,8 @@ class pa_params(ctypes.Structure):
     _fields_ = [("n", u64), ("r", u64), ("m", u64), ("gamma", u64), ("seed", u64),
                 ("block_begin", u64), ("block_end", u64),
                 ("a_words", vp), ("b_words", vp), ("c_words", vp),
-                ("stream", vp), ("limb_bits", i32), ("strict", i32), ("paper_k", u64), ("mh_only", u64)]
+                ("stream", vp), ("limb_bits", i32), ("strict", i32), ("paper_k", u64), ("mh_only", u64),
+                ("toeplitz", u64)]
 
 
 def _sig(name, res, *args):

@@ -33,6 +33,7 @@
 #include "ntt.cuh"
 #include "passes.cuh"
 #include "rekey.cuh"
+#include "toeplitz.cuh"
 
 using namespace pa;
 
@@ -76,6 +77,7 @@ extern "C" int pa_last_error(char *buf, size_t len) {
 static constexpr int kMinLog2L = 10;
 static constexpr int kMaxLog2L = 23;
 static constexpr int kColMaxLog = 9;
+static uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 static constexpr int kMaxRowLog = 14;
 static constexpr int kMaxLimbBits = 256;
 
@@ -134,6 +136,8 @@ struct Plan {
     uint64_t n, r, m, gamma, alpha, k, b0, b1, seed;
     uint64_t paper_k;        // paper mode (gamma-bit blocks, reload rule) when nonzero
     uint64_t mh_only;        // comparator: MH-only PA over the whole n-bit key
+    uint64_t toeplitz;       // comparator: Toeplitz-hashing PA (tz_nb input, tz_no output blocks of r bits)
+    uint64_t tz_nb, tz_no;
     int strict, force_B;
     pa_stage_plan mmh, mh;
 };
@@ -150,8 +154,48 @@ static int make_plan(const pa_params *prm, Plan *P) {
     p.strict = prm->strict; p.force_B = prm->limb_bits;
     p.paper_k = prm->paper_k;
     p.mh_only = prm->mh_only;
+    p.toeplitz = prm->toeplitz;
     if (p.n < 1) return set_err(PA_E_PARAM, "n must be >= 1");
     if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
+    if (p.toeplitz) {
+        // comparator: Toeplitz-hashing PA, r x r blocks, one prime
+        if (prm->gamma || prm->r || p.paper_k || p.mh_only || prm->block_begin || prm->block_end)
+            return set_err(PA_E_PARAM, "Toeplitz PA takes no gamma, r, paper_k, mh_only or shard");
+        if (p.n >= (1ull << 29) || p.m >= (1ull << 31))
+            return set_err(PA_E_PARAM, "Toeplitz PA: n < 2^29 (counts below the prime), m < 2^31");
+        const uint64_t big = std::max(p.n, p.m);
+        int lr = 9;
+        while (lr < 22 && (1ull << lr) < big) lr++;
+        if (prm->limb_bits) {               // forced block size r = 2^limb_bits (tests, tuning)
+            if (prm->limb_bits < 9 || prm->limb_bits > 22) return set_err(PA_E_PARAM, "Toeplitz: limb_bits = log2 r in [9, 22]");
+            lr = prm->limb_bits;
+        }
+        const int lg = lr + 1;
+        p.r = 1ull << lr;
+        p.tz_nb = cdiv(p.n, p.r);
+        p.tz_no = cdiv(p.m, p.r);
+        if (p.tz_no > (uint64_t)kTzMaxOut) return set_err(PA_E_PARAM, "Toeplitz PA: m <= %d * 2^22", kTzMaxOut);
+        p.k = p.tz_nb;
+        p.alpha = p.tz_no;
+        p.gamma = 0;
+        p.b0 = 0; p.b1 = p.k;
+        uint32_t prime = 0;
+        for (uint32_t q : kPrimes) if (two_adic(q) >= lg && q > p.n) { prime = q; break; }
+        if (!prime) return set_err(PA_E_BOUND, "no NTT prime for Toeplitz length 2^%d", lg);
+        pa_stage_plan &sp = p.mmh;
+        sp = pa_stage_plan{};
+        sp.limb_bits = 1;
+        sp.nprimes = 1;
+        sp.log2_len = (uint32_t)lg;
+        const int cl = std::min(kColMaxLog, lg / 2);
+        sp.n_col = 1u << cl;
+        sp.n_row = 1u << (lg - cl);
+        sp.primes[0] = prime;
+        sp.bound_log2 = std::log2((double)p.n);
+        sp.modulus_log2 = std::log2((double)prime);
+        *P = p;
+        return PA_OK;
+    }
     if (p.force_B && (p.force_B < 16 || p.force_B > kMaxLimbBits || p.force_B % 8))
         return set_err(PA_E_PARAM, "limb_bits must be a multiple of 8 in [16, %d]", kMaxLimbBits);
     uint64_t g = prm->gamma;
@@ -476,7 +520,8 @@ static int launch_row_t(const RowArgs &A0, cudaStream_t st) {
     TRY(kinfo(fn, V * (S >> E_LOG), (size_t)V * (S + S / 32) * 4, ki));
     RowArgs A = A0;
     A.units = (A.nt.n2 / V) * A.nt.nprimes;
-    const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
+    const uint64_t work = MODE == ROW_STORE ? (uint64_t)A.units * A.nvec : A.units;
+    const int grid = (int)std::min<uint64_t>(work, (uint64_t)ki.occ * g_num_sms);
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
@@ -608,6 +653,7 @@ struct pa_ctx {
     uint32_t *wflags = nullptr;               // paper mode: window has a zero bit, [T]
     uint32_t *status = nullptr;               // device status of the last hash (paper mode)
     uint32_t T = 0;                           // paper mode: windows in the key
+    uint32_t *tz_scale = nullptr;             // Toeplitz: [R, L^-1 R^2] (ROW_STORE scales of x and e')
     uint8_t *key_dev = nullptr;               // staging for pa_hash_host
     cudaStream_t copy_stream = nullptr;       // pa_hash_host H2D copies
     cudaGraphExec_t graph_exec = nullptr;     // captured pa_hash (graphs_enabled)
@@ -676,7 +722,6 @@ struct ProfScope {
     }
 };
 
-static uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 // zero all look-back state slots used by one hash (one memset)
 static int carry_reset(pa_ctx *c) {
@@ -875,13 +920,133 @@ static int expand_words(uint64_t key0, uint64_t key1, uint64_t bits, std::vector
 }
 
 static const uint64_t kStreamB = 1ull << 63, kStreamC = (1ull << 63) + 1;
+static const uint64_t kStreamT = (1ull << 63) + 2;       // Toeplitz diagonal (reading A15)
+
+// ====================================================================== Toeplitz comparator
+// (NEXT-4; toeplitz.cuh).  Forward transform of nvec bit vectors (one prime): column pass
+// from the packed coefficients, then the row pass in place with the output scale.
+static int tz_forward(pa_ctx *c, const uint32_t *res, uint32_t nvec, uint32_t rows, uint32_t *dst,
+                      const uint32_t *scale, const char *tag_col, const char *tag_row) {
+    StageDev &sd = c->smmh;
+    const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
+    {
+        ProfScope ps(c, tag_col);
+        ColArgs A{};
+        A.nt = ntt_args(sd, 0, 0);
+        A.src = res;
+        A.rows = rows;
+        A.tw4 = sd.tw4[0];
+        A.dst = dst;
+        A.nvec = nvec;
+        A.units = (sd.pl.n_row / 32) * nvec;
+        TRY(launch_col<COL_FWD>(clog, rlog, A, c->stream));
+        c->launches++;
+    }
+    {
+        ProfScope ps(c, tag_row);
+        RowArgs R{};
+        R.nt = ntt_args(sd, 0, 1);
+        R.src = dst;
+        R.dst = dst;
+        R.scale = scale;
+        R.nvec = nvec;
+        TRY(launch_row<ROW_STORE>(rlog, R, c->stream));
+        c->launches++;
+    }
+    return PA_OK;
+}
+
+static int toeplitz_alloc_and_precompute(pa_ctx *c) {
+    const Plan &p = c->pl;
+    TRY(setup_stage(c->da, p.mmh, c->smmh, c->stream));
+    const StageDev &sd = c->smmh;
+    const uint32_t L = sd.L, lr = sd.lg - 1, nb = (uint32_t)p.tz_nb, no = (uint32_t)p.tz_no;
+    const uint32_t ne = nb + no - 1;
+    c->nblk = nb;
+    TRY(c->da.alloc(&c->res, std::max<size_t>((size_t)nb << lr, (size_t)ne * L)));
+    TRY(c->da.alloc(&c->scratch, (size_t)nb * L));             // X^ (in place after the column pass)
+    TRY(c->da.alloc(&c->ahat, (size_t)ne * L));                // E'^ = T(e') L^-1 R
+    TRY(c->da.alloc(&c->acc, (size_t)no * L));
+    TRY(c->da.alloc(&c->tz_scale, 2));
+    TRY(c->da.alloc(&c->status, 4));
+    const uint32_t q = p.mmh.primes[0];
+    const uint32_t sc[2] = {(uint32_t)powmod64(2, 32, q),
+                            (uint32_t)mulmod64(inv_mod(L % q, q), powmod64(2, 64, q), q)};
+    CUDA_TRY(cudaMemcpyAsync(c->tz_scale, sc, sizeof sc, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->status, 0, 4, c->stream));
+    // diagonal d: n + m - 1 bits of stream (seed, 2^63 + 2), LSB-first words (reading A15)
+    const uint64_t nd = p.n + p.m - 1;
+    std::vector<uint32_t> dw;
+    TRY(expand_words(p.seed, kStreamT, nd, dw, false));
+    uint32_t *dw_dev = nullptr;
+    CUDA_TRY(cudaMalloc(&dw_dev, dw.size() * 4));
+    CUDA_TRY(cudaMemcpyAsync(dw_dev, dw.data(), dw.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    const uint64_t tot = (uint64_t)ne * L;
+    toeplitz_pack_diag<<<(uint32_t)std::min<uint64_t>(cdiv(tot, 256), (uint64_t)g_num_sms * 16), 256, 0,
+                         c->stream>>>(dw_dev, nd, p.m, lr, no, ne, c->res);
+    int rc = cudaGetLastError() == cudaSuccess ? PA_OK : set_err(PA_E_CUDA, "toeplitz_pack_diag launch failed");
+    if (rc == PA_OK) rc = tz_forward(c, c->res, ne, sd.pl.n_col, c->ahat, c->tz_scale + 1, "pre_col", "pre_row");
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(dw_dev);
+    if (rc != PA_OK) return rc;
+    if (e != cudaSuccess) return set_err(PA_E_CUDA, "Toeplitz precompute failed: %s", cudaGetErrorString(e));
+    return PA_OK;
+}
+
+template <int O>
+static void launch_tz_mac(const pa_ctx *c, uint32_t grid) {
+    const StageDev &sd = c->smmh;
+    toeplitz_mac<O><<<grid, 256, 0, c->stream>>>(c->scratch, c->ahat, (uint32_t)c->pl.tz_nb, sd.L, sd.pl.primes[0],
+                                                 sd.pks.k[0].pinv, c->acc);
+}
+
+static int run_toeplitz(pa_ctx *c, const uint8_t *key, uint8_t *out_bits) {
+    const Plan &p = c->pl;
+    StageDev &sd = c->smmh;
+    const uint32_t L = sd.L, lr = sd.lg - 1, nb = (uint32_t)p.tz_nb, no = (uint32_t)p.tz_no;
+    {
+        ProfScope ps(c, "tz_pack");
+        const uint64_t tot = (uint64_t)nb << lr;
+        toeplitz_pack_bits<<<(uint32_t)std::min<uint64_t>(cdiv(tot, 256), (uint64_t)g_num_sms * 16), 256, 0,
+                             c->stream>>>(key, p.n, tot, c->res);
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+    }
+    TRY(tz_forward(c, c->res, nb, sd.pl.n_col / 2, c->scratch, c->tz_scale, "tz_fwd_col", "tz_fwd_row"));
+    {
+        ProfScope ps(c, "tz_mac");
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(L, 256), (uint64_t)g_num_sms * 8);
+        switch (no) {
+#define PA_TZ(O) case O: launch_tz_mac<O>(c, grid); break;
+            PA_TZ(1) PA_TZ(2) PA_TZ(3) PA_TZ(4) PA_TZ(5) PA_TZ(6) PA_TZ(7) PA_TZ(8)
+            PA_TZ(9) PA_TZ(10) PA_TZ(11) PA_TZ(12) PA_TZ(13) PA_TZ(14) PA_TZ(15) PA_TZ(16)
+#undef PA_TZ
+            default: return set_err(PA_E_PARAM, "Toeplitz: %u output blocks", no);
+        }
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+    }
+    for (uint32_t o = 0; o < no; o++) TRY(stage_inverse(c, sd, c->acc + (size_t)o * L, "tz_inverse"));
+    {
+        ProfScope ps(c, "tz_extract");
+        const uint64_t nbytes = cdiv(p.m, 8), nwarp = cdiv(p.m, 32);
+        toeplitz_extract<<<(uint32_t)std::min<uint64_t>(cdiv(nwarp, 8), (uint64_t)g_num_sms * 16), 256, 0,
+                           c->stream>>>(c->acc, lr, L, p.m, out_bits, nbytes);
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+    }
+    return PA_OK;
+}
 
 static uint32_t rows_for(uint64_t limbs, uint32_t n1, uint32_t n2) {
     return (uint32_t)std::min<uint64_t>(n2, cdiv(limbs, n1));
 }
 
+static int toeplitz_alloc_and_precompute(pa_ctx *c);
+
 static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     Plan &p = c->pl;
+    if (p.toeplitz) return toeplitz_alloc_and_precompute(c);
     if (!p.mh_only) TRY(setup_stage(c->da, p.mmh, c->smmh, c->stream));   // MH-only: no MMH stage
     TRY(setup_stage(c->da, p.mh, c->smh, c->stream));
     c->nblk = (uint32_t)(p.b1 - p.b0);
@@ -1060,6 +1225,7 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
 // and of b.  Asynchronous on the context stream; later hashes use the new function.
 extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "rekey is for MMH-MH contexts");
     const Plan &p = c->pl;
     const uint32_t Wa32 = (uint32_t)cdiv(p.gamma, 32), Wal32 = (uint32_t)cdiv(p.alpha, 32);
     if (!c->a_words_dev) {
@@ -1278,6 +1444,7 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
 
 static int hash_enqueue(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     c->launches = 0;
+    if (c->pl.toeplitz) return run_toeplitz(c, key_bits, out_bits);
     TRY(carry_reset(c));
     if (c->pl.mh_only) {
         // comparator: y := x, the n-bit key integer, then the MH stage with alpha = n
@@ -1338,6 +1505,7 @@ extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
 
 extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
     if (!c || !key_slice || !y_out) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     c->launches = 0;
     TRY(carry_reset(c));
     uint32_t *y = nullptr;
@@ -1351,6 +1519,7 @@ extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_o
 extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits) {
     if (!c || !y_parts || !out_bits || G == 0) return set_err(PA_E_PARAM, "bad argument");
     if (G > (1u << 24)) return set_err(PA_E_PARAM, "too many parts");
+    if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     c->launches = 0;
     TRY(carry_reset(c));
     int rc;
@@ -1409,7 +1578,7 @@ static int batch_enqueue(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *
 
 extern "C" int pa_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
     if (!c || (count && (!keys || !outs))) return set_err(PA_E_PARAM, "NULL argument");
-    if (c->pl.mh_only) return set_err(PA_E_STATE, "MH-only comparator: use pa_hash");
+    if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     for (uint32_t j = 0; j < count; j++)
         if (!keys[j] || !outs[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
@@ -1457,7 +1626,7 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     const uint32_t nblk = c->nblk;
     // paper mode: the reload rule needs the whole key before any block offset is known;
     // MH-only: one product over the whole key
-    const bool whole = c->pl.paper_k || c->pl.mh_only;
+    const bool whole = c->pl.paper_k || c->pl.mh_only || c->pl.toeplitz;
     const int G = whole ? 1 : (int)std::min<uint32_t>(kCopyGroups, nblk);
     const uint64_t R = c->pl.r / 8;
     for (int g = 0; g < G; g++) {
@@ -1536,7 +1705,8 @@ extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, ui
                                   uint32_t count) {
     if (!c || (count && (!keys_host || !outs_host))) return set_err(PA_E_PARAM, "NULL argument");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
-    if (c->pl.paper_k || c->pl.mh_only) return set_err(PA_E_STATE, "paper mode / MH-only: use pa_hash_host per key");
+    if (c->pl.paper_k || c->pl.mh_only || c->pl.toeplitz)
+        return set_err(PA_E_STATE, "paper mode / comparators: use pa_hash_host per key");
     for (uint32_t j = 0; j < count; j++)
         if (!keys_host[j] || !outs_host[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
     if (count == 0) return PA_OK;

@@ -559,7 +559,11 @@ row_pass(const RowArgs A) {
     const uint32_t P = a.nprimes;
     auto sidx = [w](int pos) { return w * RS + pos + (pos >> 5); };
 
-    for (uint32_t u = blockIdx.x; u < A.units; u += gridDim.x) {
+    // ROW_STORE: the vectors are independent, so (unit, vector) pairs are spread over the
+    // grid (iv = uu / units); MAC accumulates over all vectors inside a unit
+    const uint32_t nflat = (MODE == ROW_STORE) ? A.units * A.nvec : A.units;
+    for (uint32_t uu = blockIdx.x; uu < nflat; uu += gridDim.x) {
+        const uint32_t u = (MODE == ROW_STORE) ? uu % A.units : uu;
         const uint32_t pi = u % P;
         const uint32_t rg = u / P;
         const uint32_t k2 = rg * V + w;                  // row index
@@ -575,8 +579,9 @@ row_pass(const RowArgs A) {
         uint32_t acc[E];
 #pragma unroll
         for (int e = 0; e < E; e++) acc[e] = 0;
-        const uint32_t nv = (MODE == ROW_INV) ? 1u : A.nvec;
-        for (uint32_t iv = 0; iv < nv; iv++) {
+        const uint32_t iv0 = (MODE == ROW_STORE) ? uu / A.units : 0u;
+        const uint32_t nv = (MODE == ROW_INV) ? 1u : ((MODE == ROW_STORE) ? iv0 + 1 : A.nvec);
+        for (uint32_t iv = iv0; iv < nv; iv++) {
             const size_t vbase = (MODE == ROW_INV) ? (size_t)pi * L : ((size_t)iv * P + pi) * L;
             const uint32_t *src = A.src + vbase + (size_t)k2 * S;
             uint32_t x[E];

@@ -1,0 +1,101 @@
+// Toeplitz-hashing PA, the comparator of Table 1 / Fig. 3 (SURVEY.md
+// §8(f) NEXT-4): output_j = XOR_i d[m-1-j+i] x_i over GF(2) (reading A14).
+//
+// Exact integer convolution, no floating point: every key bit and every
+// diagonal bit is one coefficient, so each needed convolution coefficient is a count <= n
+// below the single NTT prime, and its parity is the output bit.  The m x n matrix is cut
+// into r x r Toeplitz blocks (the Table 1 split): block (o, b) only depends on
+// delta = b - o, so with e'_delta the reversed diagonal window of that block,
+//   y_o = sum_b e'_(b-o) (*) x_b,   output bit o r + j' = coefficient r - 1 + j' of y_o,
+// and a cyclic length L = 2r keeps the needed coefficients free of wrap-around.  The sum
+// over b is taken in the transform domain (toeplitz_mac), one inverse per output block.
+#pragma once
+#include <cstdint>
+#include "modarith.cuh"
+
+namespace pa {
+
+// x_b[j] = key bit b r + j (MSB-first within bytes, reading A4), 0 beyond n; out [nb][r]
+// (the natural order the forward column pass reads, r = rows * N1).
+__global__ void __launch_bounds__(256) toeplitz_pack_bits(const uint8_t *__restrict__ key, uint64_t n,
+                                                          uint64_t total, uint32_t *__restrict__ out) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        if (t < n) v = (__ldg(key + (t >> 3)) >> (7 - (t & 7))) & 1u;
+        out[t] = v;
+    }
+}
+
+// Reversed diagonal windows: out[dp][s] = d[m + (dp - (O-1)) r + r - 2 - s] for s <= 2r - 2,
+// 0 for s = 2r - 1 and for indices outside [0, n + m - 1).  d is LSB-first in 32-bit words
+// (reading A15).  out [ne][L], L = 2r.
+__global__ void __launch_bounds__(256) toeplitz_pack_diag(const uint32_t *__restrict__ dw, uint64_t nd, uint64_t m,
+                                                          uint32_t log2r, uint32_t O, uint32_t ne,
+                                                          uint32_t *__restrict__ out) {
+    const uint64_t r = 1ull << log2r, L = 2 * r;
+    const uint64_t total = (uint64_t)ne * L;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t dp = t >> (log2r + 1), s = t & (L - 1);
+        uint32_t v = 0;
+        if (s + 1 < L) {
+            const int64_t idx = (int64_t)m + ((int64_t)dp - (int64_t)(O - 1)) * (int64_t)r + (int64_t)r - 2 - (int64_t)s;
+            if (idx >= 0 && (uint64_t)idx < nd) v = (__ldg(dw + (idx >> 5)) >> (idx & 31)) & 1u;
+        }
+        out[t] = v;
+    }
+}
+
+// acc[o][e] = sum_b Xh[b][e] * Eh[b - o + O - 1][e] mod p for o < O (canonical), i.e. the
+// transform-domain sum over input blocks of every output block.  Eh holds T(e') L^-1 R
+// (Montgomery), Xh plain transforms, so mul_mont leaves T(x) T(e') / L.  For a fixed e the
+// E index window b .. b + O - 1 slides by one per input block: O registers, one new load.
+constexpr int kTzMaxOut = 16;
+template <int O>
+__global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__ Xh, const uint32_t *__restrict__ Eh,
+                                                    uint32_t nb, uint32_t L, uint32_t p, uint32_t pinv,
+                                                    uint32_t *__restrict__ acc) {
+    const uint32_t p2 = 2 * p;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < L; e += gridDim.x * blockDim.x) {
+        uint32_t a[O], w[O];
+#pragma unroll
+        for (int o = 0; o < O; o++) {
+            a[o] = 0;
+            w[o] = __ldg(Eh + (size_t)(O - 1 - o) * L + e);        // w[o] = E[b + O - 1 - o] at b = 0
+        }
+        for (uint32_t b = 0; b < nb; b++) {
+            const uint32_t x = __ldg(Xh + (size_t)b * L + e);
+#pragma unroll
+            for (int o = 0; o < O; o++) a[o] = red2p(a[o] + mul_mont(x, w[o], p, pinv), p2);
+            if (b + 1 < nb) {
+#pragma unroll
+                for (int o = O - 1; o > 0; o--) w[o] = w[o - 1];
+                w[0] = __ldg(Eh + (size_t)(b + O) * L + e);
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < O; o++) acc[(size_t)o * L + e] = red1p(a[o], p);
+    }
+}
+
+// Output bit j < m = parity of coefficient r - 1 + (j mod r) of block j / r (canonical
+// residues = exact counts < p).  One warp per 32 output bits: ballot, emitted MSB-first.
+__global__ void __launch_bounds__(256) toeplitz_extract(const uint32_t *__restrict__ acc, uint32_t log2r, uint32_t L,
+                                                        uint64_t m, uint8_t *__restrict__ out, uint64_t nbytes) {
+    const uint64_t r = 1ull << log2r;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t wq = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wq * 32 < m; wq += nwarps) {
+        const uint64_t j = wq * 32 + lane;
+        uint32_t bit = 0;
+        if (j < m) bit = __ldg(acc + (j >> log2r) * L + (r - 1) + (j & (r - 1))) & 1u;
+        const uint32_t mask = __brev(__ballot_sync(0xFFFFFFFFu, bit));   // bit 31 = output bit 32 wq
+        if (lane < 4) {
+            const uint64_t q = wq * 4 + lane;
+            if (q < nbytes) out[q] = (uint8_t)(mask >> (24 - 8 * lane));
+        }
+    }
+}
+
+}  // namespace pa

@@ -19,11 +19,13 @@ def _words(v: int, bits: int) -> np.ndarray:
 
 
 def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
-            stream=None, limb_bits=0, strict=False, keep=None, paper_k=0, mh_only=False) -> B.pa_params:
+            stream=None, limb_bits=0, strict=False, keep=None, paper_k=0, mh_only=False,
+            toeplitz=False) -> B.pa_params:
     prm = B.pa_params()
     prm.n, prm.r, prm.m, prm.gamma, prm.seed = n, r, m, gamma, seed & (2**64 - 1)
     prm.paper_k = paper_k
     prm.mh_only = 1 if mh_only else 0
+    prm.toeplitz = 1 if toeplitz else 0
     if block_range is not None:
         prm.block_begin, prm.block_end = block_range
     prm.limb_bits = limb_bits
@@ -49,10 +51,10 @@ def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
 
 
 def plan(n: int, r: int, m: int, gamma: int = 0, block_range=None, limb_bits: int = 0,
-         strict: bool = False, paper_k: int = 0, mh_only: bool = False) -> dict:
+         strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False) -> dict:
     """Validate parameters and return the transform plan (host only, no GPU)."""
     prm = _params(n, r, m, gamma, 0, block_range, limb_bits=limb_bits, strict=strict, paper_k=paper_k,
-                  mh_only=mh_only)
+                  mh_only=mh_only, toeplitz=toeplitz)
     info = B.pa_info()
     B.check(B.pa_plan(ctypes.byref(prm), ctypes.byref(info)))
     return info.as_dict()
@@ -99,7 +101,7 @@ class PAContext:
 
     def __init__(self, n: int, r: int, m: int, gamma: int = 0, seed: int = 0, *,
                  block_range=None, a=None, b=None, c=None, stream=None, limb_bits: int = 0,
-                 strict: bool = False, paper_k: int = 0, mh_only: bool = False):
+                 strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise B.PAError(B.PA_E_CUDA, "no CUDA device: the library has no CPU path")
@@ -108,7 +110,7 @@ class PAContext:
         self.stream = st
         keep: list = []
         prm = _params(n, r, m, gamma, seed, block_range, a, b, c, ctypes.c_void_p(st.cuda_stream),
-                      limb_bits, strict, keep, paper_k, mh_only)
+                      limb_bits, strict, keep, paper_k, mh_only, toeplitz)
         h = ctypes.c_void_p()
         B.check(B.pa_ctx_create_ex(ctypes.byref(prm), ctypes.byref(h)))
         self._h = h

@@ -166,3 +166,23 @@ def test_plan_mh_only():
                    paper_k=kw.get("paper_k", 0), block_range=kw.get("block_range"))
     with pytest.raises(B.PAError):
         P.plan(100, 0, 101, 0, mh_only=True)                      # m > n
+
+
+def test_toeplitz_plan():
+    """NEXT-4 Toeplitz comparator plan: one prime above n, L = 2r, r x r block counts."""
+    info = P.plan(260_000_000, 0, 26_000_000, toeplitz=True)
+    assert info["r"] == 1 << 22 and info["k"] == 62 and info["alpha"] == 7
+    t = info["mmh"]
+    assert t["nprimes"] == 1 and t["log2_len"] == 23 and t["primes"][0] > 260_000_000
+    assert t["n_col"] * t["n_row"] == 1 << 23
+    small = P.plan(100, 0, 37, toeplitz=True)
+    assert small["r"] == 512 and small["k"] == 1 and small["alpha"] == 1
+    forced = P.plan(5000, 0, 1500, toeplitz=True, limb_bits=9)
+    assert forced["k"] == 10 and forced["alpha"] == 3
+    for kw in (dict(n=1 << 29, m=10), dict(n=100, m=17 << 22)):
+        with pytest.raises(B.PAError):
+            P.plan(kw["n"], 0, kw["m"], toeplitz=True)
+    with pytest.raises(B.PAError):
+        P.plan(100, 16, 10, toeplitz=True)            # r is chosen by the planner
+    with pytest.raises(B.PAError):
+        P.plan(100, 0, 10, toeplitz=True, limb_bits=8)
