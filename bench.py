@@ -512,6 +512,32 @@ def main():
             "what": "modular-arithmetic-hashing-only PA (PAPER.md:66, SPEC.md:305-313): top m bits of "
                     "(b x + c) mod 2^n, one n x n-bit product, same NTT/CRT kernels"}}
         cctx.close()
+        # Toeplitz-hashing PA (Table 1's other comparator) on the same key and m
+        tctx = PAContext(w.n, 0, w.m, 0, seed=w.hash_seed, toeplitz=True)
+        tout = torch.empty(tctx.nbytes_out, dtype=torch.uint8, device=dev)
+        for _ in range(args.warmup):
+            tctx.hash(key_dev, tout)
+        torch.cuda.synchronize()
+        tt = []
+        for _ in range(max(3, args.steps // 10)):
+            if not args.no_flush:
+                flush.fill_(1)
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            tctx.hash(key_dev, tout)
+            bb.record(stream)
+            bb.synchronize()
+            tt.append(a.elapsed_time(bb))
+        mst = statistics.median(tt)
+        ti = tctx.query()
+        comparators["toeplitz_pa"] = {
+            "value": w.n / (mst * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": mst,
+            "plan": {"r": ti["r"], "input_blocks": ti["k"], "output_blocks": ti["alpha"],
+                     "log2_len": ti["mmh"]["log2_len"], "prime": ti["mmh"]["primes"][0]},
+            "what": "Toeplitz-hashing PA over GF(2) (Table 1, PAPER.md:57-71; SPEC.md:287-304): exact "
+                    "single-prime NTT convolution of bit coefficients, r x r block split, parity of counts"}
+        tctx.close()
 
     e2e = None
     if world == 1:

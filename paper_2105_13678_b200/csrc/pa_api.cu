@@ -1225,7 +1225,7 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
 // and of b.  Asynchronous on the context stream; later hashes use the new function.
 extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
-    if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "rekey is for MMH-MH contexts");
+    if (c->pl.toeplitz) return set_err(PA_E_STATE, "rekey: not for the Toeplitz comparator");
     const Plan &p = c->pl;
     const uint32_t Wa32 = (uint32_t)cdiv(p.gamma, 32), Wal32 = (uint32_t)cdiv(p.alpha, 32);
     if (!c->a_words_dev) {
