@@ -63,7 +63,9 @@ __host__ __device__ constexpr int bitrev(int q) {
 
 // In-register DIF DFT of radix R = 2^RLOG on x[0..R): natural order in, X[bitrev(q)]
 // in x[q] out.  tw[j] = omega_E^j, twp[j] its Shoup companion (j < E/2).
-template <int RLOG, int E>
+// ZH: the upper half x[R/2..R) is known to be zero (a column whose non-zero rows all lie in
+// the first half): the first stage is then (a, a w), no sums or differences.
+template <int RLOG, int E, bool ZH = false>
 __device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const uint32_t *twp,
                                         uint32_t p, uint32_t p2) {
     constexpr int R = 1 << RLOG;
@@ -73,7 +75,10 @@ __device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const u
         for (int s = 0; s < R; s += 2 * h) {
 #pragma unroll
             for (int i = 0; i < h; i++) {
-                if (i == 0) {
+                if (ZH && h == R / 2) {
+                    const int j = i * (E / (2 * h));
+                    x[s + i + h] = (i == 0) ? x[s + i] : mul_shoup(x[s + i], tw[j], twp[j], p);
+                } else if (i == 0) {
                     bfly_dif1(x[s], x[s + h], p2);
                 } else {
                     const int j = i * (E / (2 * h));
@@ -142,7 +147,7 @@ __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SId
 }
 
 // Round 0 post-processing: DFT of the loaded groups, twiddle, store to shared memory.
-template <int S_LOG, int E_LOG, class SIdx>
+template <int S_LOG, int E_LOG, bool ZH = false, class SIdx>
 __device__ __forceinline__ void round0_finish(uint32_t *x, uint32_t *sm, const SIdx &sidx, int v,
                                               const uint32_t *tw, const uint32_t *twp,
                                               const uint32_t *rtw_p, const NttArgs &a,
@@ -154,7 +159,7 @@ __device__ __forceinline__ void round0_finish(uint32_t *x, uint32_t *sm, const S
     constexpr int T = S / R;
     constexpr int NG = E / R;
 #pragma unroll
-    for (int h = 0; h < NG; h++) dft_reg<RL, E>(x + h * R, tw, twp, c.p, c.p2);
+    for (int h = 0; h < NG; h++) dft_reg<RL, E, ZH>(x + h * R, tw, twp, c.p, c.p2);
     if constexpr (SP::Q > 1) {
 #pragma unroll
         for (int h = 0; h < NG; h++) {

@@ -1430,7 +1430,9 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     const uint32_t W = (uint32_t)c->W_Z;
     {
         ProfScope ps(c, "mh_crt_carry_extract");
-        const uint64_t ncoef = std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1);
+        // only (b y + c) mod 2^alpha is needed: coefficients j with j B >= alpha cannot reach it
+        const uint64_t ncoef = std::min<uint64_t>(std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1),
+                                                  cdiv(p.alpha, Bh));
         TRY(launch_crt_carry<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->coef, c->Z, W,
                                     next_state(c), 0, c->stream));
         c->launches += 2;

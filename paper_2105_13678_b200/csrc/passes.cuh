@@ -507,7 +507,12 @@ col_pass(const ColArgs A) {
             }
         }
         __syncthreads();    // previous unit's last-round smem reads are done
-        round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+        // round 0's first stage pairs rows q and q + S/2: with all non-zero rows in the
+        // first half (the zero-padded upper half of every packed vector) it is (a, a w)
+        if (MODE == COL_FWD && 2 * rows <= (1u << S_LOG))
+            round0_finish<S_LOG, E_LOG, true>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+        else
+            round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         rounds_rest<S_LOG, E_LOG, 1>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
