@@ -320,6 +320,15 @@ __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict_
 // propagate) publishes C_out before waiting for its predecessor, so the chain is
 // almost never serial.  RING: the last CTA to finish runs the Mersenne finish.
 // state: [0] ticket, [1] done counter, [2 + t] tile t: bit 31 ready, bits 0..30 C_out.
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // bits [off, off + 32) of a coefficient held in shared memory (P words at stride 1)
 template <int P>
 __device__ __forceinline__ uint32_t coef_window_s(const uint32_t *c, int off, int len) {
@@ -467,27 +476,23 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     uint32_t bg;
     (void)block_carries((int)G, Pall, 0, &bg);
     const uint32_t hi_last = s_hi[kCCT - 1];               // hi32 of the tile's last sum
-    volatile uint32_t *vs = state + 2;
+    // the look-back flags carry their whole payload (ready bit + C_out), so relaxed gpu-scope
+    // accesses suffice: no fence orders other data behind them
+    uint32_t *vs = state + 2;
     if (threadIdx.x == 0) {
         const bool indep = bg || !allp;
         const uint32_t cout_indep = hi_last + bg;
-        if (indep) {
-            __threadfence();
-            vs[tile] = 0x80000000u | cout_indep;
-        }
+        if (indep) st_relaxed_gpu(vs + tile, 0x80000000u | cout_indep);
         uint32_t cin = 0;
         if (tile > 0 && !(DBG & 2)) {
             uint32_t st;
-            while (!((st = vs[tile - 1]) & 0x80000000u)) { }
+            while (!((st = ld_relaxed_gpu(vs + tile - 1)) & 0x80000000u)) { }
             cin = st & 0x7FFFFFFFu;
         }
         const uint32_t c1 = (uint32_t)(((uint64_t)w[0] + cin) >> 32);     // thread 0 owns word u0
         s_cin = cin;
         s_c1 = c1;
-        if (!indep) {
-            __threadfence();
-            vs[tile] = 0x80000000u | (hi_last + (bg | ((uint32_t)allp & c1)));
-        }
+        if (!indep) st_relaxed_gpu(vs + tile, 0x80000000u | (hi_last + (bg | ((uint32_t)allp & c1))));
     }
     __syncthreads();
     const uint32_t cin = s_cin;
@@ -504,9 +509,11 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
         c = ((gm >> v) & 1u) | (((pm >> v) & 1u) & c);
     }
     if (RING && !(DBG & 4)) {
-        __threadfence();
+        // the CTA barrier orders every thread's output stores before thread 0's fence, which
+        // (cumulatively) publishes them before the done-counter increment
         __syncthreads();
         if (threadIdx.x == 0) {
+            __threadfence();
             const uint32_t ntiles = (W + kCCTile - 1) / kCCTile;
             s_last = (atomicAdd(&state[1], 1u) == ntiles - 1);
         }
