@@ -349,7 +349,10 @@ __device__ __forceinline__ uint32_t coef_window_s(const uint32_t *c, int off, in
 
 template <int P>
 __host__ __device__ constexpr int crt_cstride() { return P | 1; }
-constexpr int kCCV = 4;                        // words per thread in crt_carry
+#ifndef PA_CCV
+#define PA_CCV 4
+#endif
+constexpr int kCCV = PA_CCV;                   // words per thread in crt_carry
 constexpr int kCCT = 256;                      // threads per tile
 constexpr int kCCTile = kCCV * kCCT;                 // odd stride: fewer bank conflicts
 
