@@ -76,7 +76,7 @@ extern "C" int pa_last_error(char *buf, size_t len) {
 // ====================================================================== planning
 static constexpr int kMinLog2L = 10;
 static constexpr int kMaxLog2L = 23;
-static constexpr int kColMaxLog = 9;
+static constexpr int kColMaxLog = 8;      // column pass length cap (2^9 only when the row would exceed 2^14)
 static uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 static constexpr int kMaxRowLog = 14;
 static constexpr int kMaxLimbBits = 256;
@@ -118,10 +118,10 @@ static int plan_product(uint64_t abits, uint64_t bbits, uint64_t nterms, int for
             bp.limb_bits = B;
             bp.nprimes = P;
             bp.log2_len = (uint32_t)lg;
-            int cl = std::min(kColMaxLog, lg / 2);
-            // single-vector stages (MH): 2^8-point columns (C4 MH 2^8 x 2^10: 353.7 vs 359.5 us
-            // for 2^7 x 2^11, 360 for 2^9 x 2^9)
-            if (nvec < 8) cl = std::max(std::min(cl, 8), lg - kMaxRowLog);
+            // 2^8-point columns at most unless the row would exceed 2^14: the 512-thread
+            // 2^9 column pass runs one CTA per SM (C5c 2.34 -> 2.18 ms, P1 412 -> 399 us at 2^8);
+            // single-vector stages (MH) likewise (C4 MH 2^8 x 2^10 353.7 us, 2^7 x 2^11 359.5 us)
+            const int cl = std::max(std::min(kColMaxLog, lg / 2), lg - kMaxRowLog);
             bp.n_col = 1u << cl;
             bp.n_row = 1u << (lg - cl);
             for (uint32_t i = 0; i < P; i++) bp.primes[i] = ps[i];
@@ -189,7 +189,7 @@ static int make_plan(const pa_params *prm, Plan *P) {
         sp.limb_bits = 1;
         sp.nprimes = 1;
         sp.log2_len = (uint32_t)lg;
-        const int cl = std::min(kColMaxLog, lg / 2);
+        const int cl = std::max(std::min(kColMaxLog, lg / 2), lg - kMaxRowLog);
         sp.n_col = 1u << cl;
         sp.n_row = 1u << (lg - cl);
         sp.primes[0] = prime;
@@ -500,9 +500,8 @@ template <int MODE>
 static int launch_col(int slog, int n1log, const ColArgs &A, cudaStream_t st) {
 #define PA_COL(S, N) \
     if (slog == S && n1log == N) return launch_col_t<S, N, MODE>(A, st);
-    PA_COL(5, 5) PA_COL(5, 6) PA_COL(6, 6) PA_COL(6, 7) PA_COL(7, 7) PA_COL(7, 8) PA_COL(7, 9) PA_COL(7, 10)
-    PA_COL(7, 11) PA_COL(7, 12) PA_COL(7, 13) PA_COL(7, 14) PA_COL(8, 8) PA_COL(8, 9) PA_COL(8, 10) PA_COL(8, 11) PA_COL(8, 12) PA_COL(8, 13) PA_COL(8, 14)
-    PA_COL(9, 9) PA_COL(9, 10) PA_COL(9, 11) PA_COL(9, 12) PA_COL(9, 13) PA_COL(9, 14)
+    PA_COL(5, 5) PA_COL(5, 6) PA_COL(6, 6) PA_COL(6, 7) PA_COL(7, 7) PA_COL(7, 8) PA_COL(8, 8) PA_COL(8, 9)
+    PA_COL(8, 10) PA_COL(8, 11) PA_COL(8, 12) PA_COL(8, 13) PA_COL(8, 14) PA_COL(9, 14)
 #undef PA_COL
     return set_err(PA_E_PARAM, "unsupported column/row split 2^%d x 2^%d", slog, n1log);
 }
