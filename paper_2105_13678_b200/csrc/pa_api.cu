@@ -549,34 +549,70 @@ static int launch_row(int slog, const RowArgs &A, cudaStream_t st) {
     return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
 }
 
+// Grid of the row MAC.  Mode 0 splits the (unit, vector) iterations evenly: a unit then
+// spans at most ceil(grid / nunits) + 1 consecutive CTAs, and CTA b adds its canonical
+// partials (< p) into slot b mod nslot, so a slot sees at most four partials of a unit
+// (< 4p < 2^32).  nslot = 1 while grid <= 3 nunits; few units and many vectors (C5a: 88
+// units of 2048 vectors) take up to kMacSlots slots to keep every SM busy.  Modes 1/2
+// (whole units per CTA): grid <= nunits, one slot.
+static constexpr uint32_t kMacSlots = 4;
 template <int S_LOG>
-static int launch_mac_t(const MacArgs &A, cudaStream_t st) {
+static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, uint32_t *nslot) {
     constexpr int E_LOG = 5;
     static KInfo ki;
     auto fn = row_mac<S_LOG, E_LOG>;
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
-    // mode 0: grid <= 3 nunits, so every CTA runs >= nvec/3 iterations and a unit is split
-    // between at most four CTAs: four canonical partials (< p each) stay < 4p < 2^32.
-    // modes 1/2 (whole units per CTA): grid <= nunits.
-    const uint64_t cap = A.mode ? (uint64_t)A.nunits : 3ull * A.nunits;
-    const int grid = (int)std::min<uint64_t>(cap, (uint64_t)ki.occ * g_num_sms);
+    const uint64_t full = (uint64_t)ki.occ * g_num_sms;
+    *nslot = 1;
+    if (mode) {
+        *grid = (int)std::min<uint64_t>(nunits, full);
+        return PA_OK;
+    }
+    // one slot: grid <= 3 nunits, every CTA runs >= nvec/3 iterations, a unit touches <= 4 CTAs
+    uint64_t g = std::min<uint64_t>(full, 3ull * nunits);
+    const uint64_t T = (uint64_t)nunits * nvec;
+    if (g < full && nvec >= 8) {
+        uint64_t gs = std::min<uint64_t>(full, T);
+        for (;;) {
+            const uint64_t q = T / gs;                       // fewest iterations a CTA runs
+            const uint64_t span = cdiv(nvec, q) + 1;         // most CTAs a unit touches
+            const uint64_t ns = cdiv(span, 4);
+            if (ns <= kMacSlots) {
+                if (ns > 1) { g = gs; *nslot = (uint32_t)ns; }
+                break;
+            }
+            gs = gs * 3 / 4;
+        }
+    }
+    *grid = (int)g;
+    return PA_OK;
+}
+
+template <int S_LOG>
+static int launch_mac_t(const MacArgs &A, int grid, cudaStream_t st) {
+    constexpr int E_LOG = 5;
+    static KInfo ki;
+    auto fn = row_mac<S_LOG, E_LOG>;
+    TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
 
-static int launch_mac(int slog, const MacArgs &A, cudaStream_t st) {
+static int mac_grid(int slog, uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, uint32_t *nslot) {
     switch (slog) {
-        case 5: return launch_mac_t<5>(A, st);
-        case 6: return launch_mac_t<6>(A, st);
-        case 7: return launch_mac_t<7>(A, st);
-        case 8: return launch_mac_t<8>(A, st);
-        case 9: return launch_mac_t<9>(A, st);
-        case 10: return launch_mac_t<10>(A, st);
-        case 11: return launch_mac_t<11>(A, st);
-        case 12: return launch_mac_t<12>(A, st);
-        case 13: return launch_mac_t<13>(A, st);
-        case 14: return launch_mac_t<14>(A, st);
+#define PA_MG(S) case S: return mac_grid_t<S>(nunits, nvec, mode, grid, nslot);
+        PA_MG(5) PA_MG(6) PA_MG(7) PA_MG(8) PA_MG(9) PA_MG(10) PA_MG(11) PA_MG(12) PA_MG(13) PA_MG(14)
+#undef PA_MG
+    }
+    return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
+}
+
+static int launch_mac(int slog, const MacArgs &A, int grid, cudaStream_t st) {
+    switch (slog) {
+#define PA_LM(S) case S: return launch_mac_t<S>(A, grid, st);
+        PA_LM(5) PA_LM(6) PA_LM(7) PA_LM(8) PA_LM(9) PA_LM(10) PA_LM(11) PA_LM(12) PA_LM(13) PA_LM(14)
+#undef PA_LM
     }
     return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
 }
@@ -672,6 +708,7 @@ struct pa_ctx {
     uint8_t *key_dev2 = nullptr, *out_dev2 = nullptr;   // pa_hash_host_batch second staging set
     cudaEvent_t hb_copy[2] = {}, hb_done[2] = {};
     uint64_t Wg = 0, W_ring = 0, W_fold = 0, W_Z = 0, ncoef_mmh = 0;
+    uint32_t mac_slots = 1;           // accumulator slots of the last MMH row MAC (mac_grid)
     uint32_t launches = 0;            // launches of the current / last hash call
     uint32_t launches_total = 0;      // since creation
     bool prof = false;
@@ -853,7 +890,6 @@ static int stage_mac(pa_ctx *c, StageDev &sd, uint32_t nvec, const uint32_t *scr
     const int rlog = __builtin_ctz(sd.pl.n_row);
     const uint32_t P = sd.pl.nprimes;
     ProfScope ps(c, tag);
-    if (only && zero) CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)P * sd.L * 4, c->stream));
     MacArgs M{};
     M.mode = only ? 0u : (first ? 1u : 2u);
     M.nt = ntt_args(sd, 0, 1);
@@ -862,19 +898,26 @@ static int stage_mac(pa_ctx *c, StageDev &sd, uint32_t nvec, const uint32_t *scr
     M.dst = acc;
     M.nvec = nvec;
     M.nunits = (sd.pl.n_col / mac_v_rt(rlog)) * P;
-    TRY(launch_mac(rlog, M, c->stream));
+    int grid = 0;
+    TRY(mac_grid(rlog, M.nunits, nvec, M.mode, &grid, &M.nslot));
+    M.slot_stride = P * sd.L;
+    if (only && zero) CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M.nslot * P * sd.L * 4, c->stream));
+    if (&sd == &c->smmh) c->mac_slots = M.nslot;
+    TRY(launch_mac(rlog, M, grid, c->stream));
     c->launches++;
     return PA_OK;
 }
 
 // ---- S4: one inverse transform of acc (in place, natural order, canonical residues)
-static int stage_inverse(pa_ctx *c, StageDev &sd, uint32_t *acc, const char *tag) {
+static int stage_inverse(pa_ctx *c, StageDev &sd, uint32_t *acc, const char *tag, uint32_t nslot = 1) {
     const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
     const uint32_t P = sd.pl.nprimes;
     ProfScope ps(c, tag);
     RowArgs R{};
     R.nt = ntt_args(sd, 1, 1);
     R.src = acc;
+    R.nsrc = nslot;
+    R.src_stride = P * sd.L;
     R.dst = acc;
     R.tw4 = sd.tw4[1];
     R.nvec = 1;
@@ -1078,7 +1121,7 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     TRY(c->da.alloc(&c->res, res_words));
     TRY(c->da.alloc(&c->ahat, (size_t)c->nblk * Pm * Lm));
     TRY(c->da.alloc(&c->scratch, (size_t)c->nblk * Pm * Lm));
-    TRY(c->da.alloc(&c->acc, (size_t)Pm * Lm));
+    TRY(c->da.alloc(&c->acc, (size_t)kMacSlots * Pm * Lm));     // row MAC slots (mac_grid)
     TRY(c->da.alloc(&c->bhat, (size_t)Ph * Lh));
     TRY(c->da.alloc(&c->scratch_mh, (size_t)Ph * Lh));
     TRY(c->da.alloc(&c->acc_mh, (size_t)Ph * Lh));
@@ -1404,7 +1447,7 @@ static int mmh_mac(pa_ctx *c, uint32_t v0, uint32_t v1, bool first, bool only, b
 // ---- S4+S5 after all blocks are accumulated -> canonical y
 static int mmh_tail(pa_ctx *c, uint32_t **y_out) {
     const Plan &p = c->pl;
-    TRY(stage_inverse(c, c->smmh, c->acc, "mmh_inverse"));
+    TRY(stage_inverse(c, c->smmh, c->acc, "mmh_inverse", c->mac_slots));
     {
         ProfScope ps(c, "mmh_crt_carry_fold");
         TRY(launch_crt_carry<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->coef, c->y1,
@@ -1418,7 +1461,14 @@ static int mmh_tail(pa_ctx *c, uint32_t **y_out) {
 // ---- S1-S5 on this ctx's blocks -> canonical y in the returned buffer (Wg words)
 static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
     // accumulators zeroed first: the chain pack -> col -> row_mac is back-to-back kernels
-    CUDA_TRY(cudaMemsetAsync(c->acc, 0, (size_t)c->pl.mmh.nprimes * c->smmh.L * 4, c->stream));
+    {
+        const uint32_t P = c->pl.mmh.nprimes;
+        const int rlog = __builtin_ctz(c->pl.mmh.n_row);
+        int grid = 0;
+        uint32_t nslot = 1;
+        TRY(mac_grid(rlog, (c->pl.mmh.n_col / mac_v_rt(rlog)) * P, c->nblk, 0, &grid, &nslot));
+        CUDA_TRY(cudaMemsetAsync(c->acc, 0, (size_t)nslot * P * c->smmh.L * 4, c->stream));
+    }
     TRY(mmh_forward(c, key_slice, 0, c->nblk));
     TRY(mmh_mac(c, 0, c->nblk, true, true, false));
     return mmh_tail(c, y_out);
@@ -1550,7 +1600,7 @@ static int alloc_alt(pa_ctx *c) {
     HashBufs &b = c->alt;
     TRY(c->da.alloc(&b.res, c->res_words));
     TRY(c->da.alloc(&b.scratch, (size_t)c->nblk * Pm * Lm));
-    TRY(c->da.alloc(&b.acc, Pm * Lm));
+    TRY(c->da.alloc(&b.acc, (size_t)kMacSlots * Pm * Lm));
     TRY(c->da.alloc(&b.scratch_mh, Ph * Lh));
     TRY(c->da.alloc(&b.acc_mh, Ph * Lh));
     TRY(c->da.alloc(&b.S, std::max<uint64_t>(c->W_fold, c->W_Z)));

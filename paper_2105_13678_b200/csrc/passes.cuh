@@ -546,6 +546,8 @@ struct RowArgs {
     const uint32_t *ahat;     // MAC: [nvec][P][L] (Montgomery form, times 1/L)
     const uint32_t *scale;    // STORE: [P] Montgomery constant multiplied into outputs
     const uint32_t *tw4;      // INV: omega_L^(-j1 k2) table [P][L] (Montgomery, canonical)
+    uint32_t nsrc;            // INV: the input is the sum of nsrc slots src + s * src_stride (each < 4p)
+    uint32_t src_stride;
     uint32_t nvec;
     uint32_t units;           // (N2 / V) * P
 };
@@ -600,6 +602,18 @@ row_pass(const RowArgs A) {
                         // ROW_INV input: accumulators merged with red.add, in [0, 4p)
                         x[h * R + m] = (MODE == ROW_INV) ? red2p(t, cx.p2) : t;
                     }
+            }
+            if constexpr (MODE == ROW_INV) {
+                // the row MAC's further accumulator slots (each < 4p), one batch of loads each
+                for (uint32_t q = 1; q < A.nsrc; q++) {
+                    constexpr int R = 1 << SP::rlog(0);
+                    const uint32_t *sq = src + (size_t)q * A.src_stride;
+#pragma unroll
+                    for (int h = 0; h < E / R; h++)
+#pragma unroll
+                        for (int m = 0; m < R; m++)
+                            x[h * R + m] = red2p(x[h * R + m] + red2p(sq[in_pos<S_LOG, E_LOG>(v, h, m)], cx.p2), cx.p2);
+                }
             }
             __syncthreads();
             round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
@@ -671,6 +685,8 @@ struct MacArgs {
     uint32_t mode;            // 0: iterations split evenly, red.add into zeroed dst (< 4p)
                               // 1: whole units per CTA, dst = sum (canonical)
                               // 2: whole units per CTA, dst = (dst + sum) mod p (dst canonical)
+    uint32_t nslot;           // mode 0: CTA b adds into slot b mod nslot (dst + slot * slot_stride),
+    uint32_t slot_stride;     // so that no slot receives more than four partials of a unit
 };
 
 // rows per CTA: V*S = 2048 words per operand and stage, and V <= S/2 <= N2 (planner)
@@ -752,6 +768,7 @@ row_mac(const MacArgs A) {
     uint32_t tw[E / 2], twp[E / 2];
     uint32_t acc[E];
     Ctx32 cx{};
+    uint32_t *const dslot = A.dst + (size_t)(blockIdx.x % A.nslot) * A.slot_stride;   // mode 0 slot
     auto flush_one = [&](uint32_t *d, uint32_t v) {
         v = red1p(v, cx.p);
         if (A.mode == 0) atomicAdd(d, v);
@@ -767,7 +784,7 @@ row_mac(const MacArgs A) {
             if (cur_unit >= 0) {
                 constexpr int R = 1 << SP::rlog(SP::Q - 1);
                 const uint32_t fpi = (uint32_t)cur_unit % P, frg = (uint32_t)cur_unit / P;
-                uint32_t *dst = A.dst + (size_t)fpi * L + (size_t)(frg * V + w) * S;
+                uint32_t *dst = dslot + (size_t)fpi * L + (size_t)(frg * V + w) * S;
 #pragma unroll
                 for (int h = 0; h < E / R; h++)
 #pragma unroll
@@ -833,7 +850,7 @@ row_mac(const MacArgs A) {
     if (cur_unit >= 0) {
         constexpr int R = 1 << SP::rlog(SP::Q - 1);
         const uint32_t fpi = (uint32_t)cur_unit % P, frg = (uint32_t)cur_unit / P;
-        uint32_t *dst = A.dst + (size_t)fpi * L + (size_t)(frg * V + w) * S;
+        uint32_t *dst = dslot + (size_t)fpi * L + (size_t)(frg * V + w) * S;
 #pragma unroll
         for (int h = 0; h < E / R; h++)
 #pragma unroll
