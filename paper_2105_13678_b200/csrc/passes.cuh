@@ -373,25 +373,34 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
     if (j >= wxp) return;
     uint32_t w[NW];
     uint32_t any = 0;
+    if (j < wx) {
+        // word i of the limb = window bits [B j + 32 i, +32) = the 32 key bits whose MSB is key
+        // bit q_i = off + gamma - B j - 32 (i + 1): every word shares q_0's byte and bit shift
+        // and sits one staged word lower than the previous one
+        const int64_t q0 = off + (int64_t)gamma - (int64_t)B * j - 32;
+        const int64_t rb0 = (q0 >> 3) - 4 * gw0;               // staged byte of word 0
+        const int sh = (int)(q0 & 7), bb = (int)(rb0 & 3);
+        const int wi0 = (int)(rb0 >> 2);
+        const int rem = (int)((int64_t)gamma - (int64_t)B * j); // window bits from the limb up
+        uint32_t a1 = sw[wi0 + 1], a2 = sw[wi0 + 2];
 #pragma unroll
-    for (int i = 0; i < NW; i++) {
-        const int64_t ib = (int64_t)B * j + 32 * i;            // integer bit of the word's LSB
-        uint32_t v = 0;
-        if (j < wx && ib < (int64_t)gamma) {
-            const int64_t q = off + (int64_t)gamma - ib - 32;  // key bit of the word's MSB
-            const int64_t rb = (q >> 3) - 4 * gw0;             // staged byte (q >= off - 32 >= 4 gw0 * 8 - ...)
-            const int sh = (int)(q & 7);
-            const int wi = (int)(rb >> 2), bb = (int)(rb & 3);
-            const uint32_t a0 = (wi >= 0) ? sw[wi] : 0u, a1 = sw[wi + 1], a2 = sw[wi + 2];
+        for (int i = 0; i < NW; i++) {
+            const int wi = wi0 - i;
+            const uint32_t a0 = (wi >= 0) ? sw[wi] : 0u;
             const uint32_t lo = __funnelshift_r(a0, a1, 8 * bb), hi = __funnelshift_r(a1, a2, 8 * bb);
             const uint64_t be = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
-            v = (uint32_t)(be >> (32 - sh));
-            int64_t valid = (int64_t)gamma - ib;                // bits of this word inside the window
-            if (valid > (int64_t)B - 32 * i) valid = (int64_t)B - 32 * i;   // ... and inside the limb
-            if (valid < 32) v &= (1u << valid) - 1u;
+            uint32_t v = (uint32_t)(be >> (32 - sh));
+            const int valid = min(rem - 32 * i, (int)B - 32 * i);   // bits inside window and limb
+            if (valid <= 0) v = 0u;
+            else if (valid < 32) v &= (1u << valid) - 1u;
+            w[i] = v;
+            any |= v;
+            a2 = a1;
+            a1 = a0;
         }
-        w[i] = v;
-        any |= v;
+    } else {
+#pragma unroll
+        for (int i = 0; i < NW; i++) w[i] = 0u;
     }
     store_residues<NW>(res + (size_t)iv * P * wxp + j, wxp, P, any, w, ks);
 }
