@@ -547,6 +547,10 @@ __global__ void mh_extract(const uint32_t *__restrict__ Z, uint64_t nwz, uint64_
     const int64_t valid = (int64_t)m - 32 * (int64_t)q;              // output bits present here
     if (valid < 32) v &= valid <= 0 ? 0u : ~((1u << (32 - valid)) - 1u);
     const uint32_t be = __byte_perm(v, 0, 0x0123);
+    if (4 * q + 4 <= nbytes && !(reinterpret_cast<uintptr_t>(out) & 3)) {
+        reinterpret_cast<uint32_t *>(out)[q] = be;                 // coalesced word store
+        return;
+    }
 #pragma unroll
     for (int b = 0; b < 4; b++)
         if (4 * q + b < nbytes) out[4 * q + b] = (uint8_t)(be >> (8 * b));

@@ -401,3 +401,22 @@ def test_full_size_golden(name):
     ctx.close()
     assert got[:16].hex() == rec["out_head"]
     assert hashlib.sha256(got).hexdigest() == rec["out_sha256"]
+
+
+@pytest.mark.gpu
+def test_unaligned_key_and_output_pointers():
+    """The C ABI takes plain device pointers: keys and outputs at odd byte offsets give the
+    same bits (byte stores / byte loads on the unaligned paths)."""
+    PAContext = _pa()
+    n, r, m = 300_001, 4096, 40_003
+    key = key_bytes(n, 31)
+    ctx = PAContext(n, r, m, seed=5)
+    want = oracle_seeded(key, n, r, m, 5)
+    kb = torch.zeros(len(key) + 3, dtype=torch.uint8, device="cuda")
+    kb[1:1 + len(key)] = torch.from_numpy(key).cuda()
+    ob = torch.zeros(ctx.nbytes_out + 3, dtype=torch.uint8, device="cuda")
+    ctx.hash(kb[1:1 + len(key)], ob[3:3 + ctx.nbytes_out])
+    torch.cuda.synchronize()
+    assert bytes(ob[3:3 + ctx.nbytes_out].cpu().numpy()) == want
+    assert int(ob[:3].sum()) == 0
+    ctx.close()
