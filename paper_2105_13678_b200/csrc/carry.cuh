@@ -367,19 +367,22 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     // (P words loaded from coefT, coalesced) and adds their P + 1 bit-shifted words into
     // the tile's 64-bit sums in shared memory (shared-memory atomics: <= ceil(32(P+1)/B)+1
     // contributions per word)
-    __shared__ unsigned long long s_sum[kCCTile];
+    // 64-bit column sums as two 32-bit words: a native 32-bit shared atomicAdd on the low
+    // word (its old value reveals the carry) instead of a 64-bit add, which sm_100a only has
+    // as a compare-and-swap loop
+    __shared__ uint32_t s_clo[kCCTile], s_chi[kCCTile];
     constexpr uint32_t cbits = 32 * P;
     __shared__ uint32_t s_tile, s_cin, s_c1, s_last;
     __shared__ uint32_t s_hi[kCCT];
     if (threadIdx.x == 0) s_tile = atomicAdd(&state[0], 1u);
-    for (uint32_t i = threadIdx.x; i < kCCTile; i += blockDim.x) s_sum[i] = 0ull;
+    for (uint32_t i = threadIdx.x; i < kCCTile; i += blockDim.x) s_clo[i] = s_chi[i] = 0u;
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t u0 = tile * kCCTile;
     const uint32_t ub = u0 + threadIdx.x * kCCV;            // this thread's first word
     const uint32_t nchunks = (DBG & 8) ? 0u : RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
     const uint32_t tb0 = 32 * u0, tb1 = 32 * min(u0 + kCCTile, W);   // tile bits
-    // adds bits [0, len) of coefficient c, placed at tile-relative bit d, into s_sum
+    // adds bits [0, len) of coefficient c, placed at tile-relative bit d, into the sums
     auto scatter = [&](const uint32_t (&c)[P], int64_t d, int64_t len) {
         uint32_t m[P];
 #pragma unroll
@@ -395,7 +398,10 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
             if (wi < 0 || wi >= (int64_t)kCCTile) continue;
             const uint32_t lo = (i > 0) ? m[i - 1] : 0u, hi = (i < P) ? m[i] : 0u;
             const uint32_t val = s ? __funnelshift_l(lo, hi, s) : hi;
-            if (val) atomicAdd(&s_sum[wi], (unsigned long long)val);
+            if (val) {
+                const uint32_t old = atomicAdd(&s_clo[wi], val);
+                if (old + val < old) atomicAdd(&s_chi[wi], 1u);
+            }
         }
     };
     for (uint32_t t = 0; t < nchunks; t++) {
@@ -453,7 +459,8 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
 #pragma unroll
     for (int v = 0; v < kCCV; v++) {
         const uint32_t u = ub + v;
-        S[v] = s_sum[threadIdx.x * kCCV + v] + ((!RING && addend && u < n_addend) ? addend[u] : 0ull);
+        const uint32_t iw = threadIdx.x * kCCV + v;
+        S[v] = (((uint64_t)s_chi[iw] << 32) | s_clo[iw]) + ((!RING && addend && u < n_addend) ? addend[u] : 0ull);
     }
     // ---- carries inside the tile (cin of word u0 handled separately, see above)
     uint32_t w[kCCV];
