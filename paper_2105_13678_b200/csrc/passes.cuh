@@ -750,29 +750,44 @@ row_mac(const MacArgs A) {
         if constexpr (PAD) return w * (S + S / 32) + pos + (pos >> 5);
         else return swz32(w * S + pos);
     };
-    auto offset_of = [&](uint64_t it) -> size_t {
-        const uint32_t unit = (uint32_t)(it / nvec), iv = (uint32_t)(it % nvec);
-        const uint32_t pi = unit % P, rg = unit / P;
-        return ((size_t)iv * P + pi) * L + (size_t)rg * SW;
+    // iteration it = (unit, iv), unit = (rg, pi): cursors stepped incrementally (the loop
+    // does no integer division; one set of divisions per cursor at the start)
+    struct Cur {
+        uint32_t iv, pi, rg;
     };
-    auto issue_x = [&](uint64_t it, int s) {
+    auto cur_at = [&](uint64_t it) -> Cur {
+        const uint32_t unit = (uint32_t)(it / nvec);
+        return Cur{(uint32_t)(it - (uint64_t)unit * nvec), unit % P, unit / P};
+    };
+    auto step = [&](Cur &c) {
+        if (++c.iv == nvec) {
+            c.iv = 0;
+            if (++c.pi == P) { c.pi = 0; c.rg++; }
+        }
+    };
+    auto offset_of = [&](const Cur &c) -> size_t { return ((size_t)c.iv * P + c.pi) * L + (size_t)c.rg * SW; };
+    auto issue_x = [&](const Cur &c, int s) {
         mbar_arrive_expect_tx(&bars[s], SW * 4);
-        bulk_g2s(xs + s * SW, A.src + offset_of(it), SW * 4, &bars[s]);
+        bulk_g2s(xs + s * SW, A.src + offset_of(c), SW * 4, &bars[s]);
     };
-    auto issue_a = [&](uint64_t it, uint32_t *dst) {
+    auto issue_a = [&](const Cur &c, uint32_t *dst) {
         mbar_arrive_expect_tx(&bars[NSX], SW * 4);
-        bulk_g2s(dst, A.ahat + offset_of(it), SW * 4, &bars[NSX]);
+        bulk_g2s(dst, A.ahat + offset_of(c), SW * 4, &bars[NSX]);
     };
+    Cur cc = cur_at(it0);                                // iteration it
+    Cur cn = cc;                                         // next X to issue (it + NSX)
+    Cur ca = cc;                                         // next A^ to issue (it + 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s <= NSX; s++) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NSX; s++)
-            if (it0 + s < it1) issue_x(it0 + s, s);
-        if (!AIN && it0 < it1) issue_a(it0, as);
+    for (int s = 0; s < NSX; s++) {
+        if (threadIdx.x == 0 && it0 + s < it1) issue_x(cn, s);
+        step(cn);
     }
+    if (threadIdx.x == 0 && !AIN && it0 < it1) issue_a(ca, as);
+    step(ca);
 
     uint32_t tw[E / 2], twp[E / 2];
     uint32_t acc[E];
@@ -785,22 +800,22 @@ row_mac(const MacArgs A) {
         else *d = red1p(*d + v, cx.p);
     };
     const uint32_t *rtw_p = nullptr;
-    int64_t cur_unit = -1;
+    bool have_unit = false;
+    uint32_t fpi = 0, frg = 0;                           // unit being accumulated
     uint32_t cur_pi = 0;
-    for (uint64_t it = it0; it < it1; it++) {
-        const uint32_t unit = (uint32_t)(it / nvec);
-        if ((int64_t)unit != cur_unit) {
-            if (cur_unit >= 0) {
+    for (uint64_t it = it0; it < it1; it++, step(cc)) {
+        if (!have_unit || cc.iv == 0) {
+            if (have_unit) {
                 constexpr int R = 1 << SP::rlog(SP::Q - 1);
-                const uint32_t fpi = (uint32_t)cur_unit % P, frg = (uint32_t)cur_unit / P;
                 uint32_t *dst = dslot + (size_t)fpi * L + (size_t)(frg * V + w) * S;
 #pragma unroll
                 for (int h = 0; h < E / R; h++)
 #pragma unroll
                     for (int mm = 0; mm < R; mm++) flush_one(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
             }
-            cur_unit = unit;
-            const uint32_t pi = unit % P;
+            fpi = cc.pi;
+            frg = cc.rg;
+            const uint32_t pi = cc.pi;
             if (rtw_p == nullptr || pi != cur_pi) {
                 cur_pi = pi;
                 const PrimeK pk = a.pk[pi];
@@ -812,6 +827,7 @@ row_mac(const MacArgs A) {
                 }
                 rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
             }
+            have_unit = true;
 #pragma unroll
             for (int e = 0; e < E; e++) acc[e] = 0;
         }
@@ -829,7 +845,7 @@ row_mac(const MacArgs A) {
         }
         if constexpr (AIN) {
             __syncthreads();                             // X stage s read: A^(it) may land there
-            if (threadIdx.x == 0) issue_a(it, xst);
+            if (threadIdx.x == 0) issue_a(cc, xst);
         }
         if constexpr (DBG != 1) {
             uint32_t *exch = PAD ? exb : xst;
@@ -852,13 +868,14 @@ row_mac(const MacArgs A) {
         }
         __syncthreads();                                 // X stage s and A^ are free
         if (threadIdx.x == 0 && DBG != 2 && DBG != 3) {
-            if (it + NSX < it1) issue_x(it + NSX, s);
-            if (!AIN && it + 1 < it1) issue_a(it + 1, as);
+            if (it + NSX < it1) issue_x(cn, s);
+            if (!AIN && it + 1 < it1) issue_a(ca, as);
         }
+        step(cn);
+        step(ca);
     }
-    if (cur_unit >= 0) {
+    if (have_unit) {
         constexpr int R = 1 << SP::rlog(SP::Q - 1);
-        const uint32_t fpi = (uint32_t)cur_unit % P, frg = (uint32_t)cur_unit / P;
         uint32_t *dst = dslot + (size_t)fpi * L + (size_t)(frg * V + w) * S;
 #pragma unroll
         for (int h = 0; h < E / R; h++)
