@@ -479,11 +479,19 @@ col_pass(const ColArgs A) {
     Ctx32 cx{};
     const uint32_t *rtw_p = nullptr;
 
+    // unit u = ((cg P + pi) nvec + iv): stepped incrementally, no division in the loop
+    uint32_t iv = 0, pi = 0, cg = 0;
+    if (u0 < u1) {
+        const uint32_t pair0 = u0 / nvec;
+        iv = u0 - pair0 * nvec;
+        pi = pair0 % P;
+        cg = pair0 / P;
+    }
     for (uint32_t u = u0; u < u1; u++) {
-        const uint32_t iv = u % nvec;
-        const uint32_t pair = u / nvec;             // (cg, pi)
-        const uint32_t pi = pair % P;
-        const uint32_t cg = pair / P;
+        if (u != u0 && ++iv == nvec) {
+            iv = 0;
+            if (++pi == P) { pi = 0; cg++; }
+        }
         const uint32_t j1 = cg * 32 + c;
         if ((int)pi != cur_pi) {
             cur_pi = (int)pi;
