@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeS
     const uint64_t total = (uint64_t)nvec * wxp;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t iv = (uint32_t)(t / wxp), j = (uint32_t)(t % wxp);
+        // 32-bit quotient whenever the index fits (a 64-bit division is a software call)
+        const uint32_t iv = (t >> 32) ? (uint32_t)(t / wxp) : (uint32_t)t / wxp;
+        const uint32_t j = (uint32_t)(t - (uint64_t)iv * wxp);
         uint32_t *o = res + (size_t)iv * P * wxp + j;
         if constexpr (NW == 0) {
             const uint64_t v = src(iv, j);
