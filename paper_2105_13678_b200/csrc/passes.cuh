@@ -214,14 +214,17 @@ constexpr int kPackT = 256;
 template <int NW>
 __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
-    constexpr int MAXW = kPackT * NW + 4;                     // staged words (LB <= 4 NW bytes per limb)
+    // a tile is 2 kPackT limbs, two per thread (limbs t and t + kPackT): the per-prime
+    // constants, loop and addressing are shared by both limbs' reductions
+    constexpr int TL = 2 * kPackT;
+    constexpr int MAXW = TL * NW + 4;                         // staged words (LB <= 4 NW bytes per limb)
     __shared__ uint32_t sw[MAXW];
     const uint32_t iv = blockIdx.y;
-    const uint32_t jt0 = blockIdx.x * kPackT;
+    const uint32_t jt0 = blockIdx.x * TL;
     const int64_t start = (int64_t)iv * s.blk_bytes;
     const int64_t end = start + s.blk_bytes;
     const int LB = (int)s.limb_bytes;
-    const uint32_t jt1 = min(jt0 + kPackT, s.wx);           // limbs with data in this tile
+    const uint32_t jt1 = min(jt0 + TL, s.wx);               // limbs with data in this tile
     int64_t tlo = end - (int64_t)LB * jt1 - 4;               // lowest byte any word may touch
     if (tlo < start - 4) tlo = start - 4;
     const int64_t gw0 = tlo >> 2;                            // floor
@@ -251,14 +254,17 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
         if (k < nw) sw[k] = v[u];
     }
     __syncthreads();
-    const uint32_t j = jt0 + threadIdx.x;
-    if (j >= wxp) return;
-    uint32_t w[NW];
-    uint32_t any = 0;
-    if (j < s.wx) {
-        // byte offsets relative to the staged base 4 gw0 (all < 4 MAXW).  Word i of the limb
-        // is the big-endian value of the 4 bytes ending 4 i bytes before the limb's end, so
-        // all words share the byte shift (hi & 3) and walk down the staged words by one.
+    // limb j's NW words (big-endian bytes, readings A3/A4).  Byte offsets relative to the
+    // staged base 4 gw0 (all < 4 MAXW).  Word i of the limb is the big-endian value of the
+    // 4 bytes ending 4 i bytes before the limb's end, so all words share the byte shift
+    // (hi & 3) and walk down the staged words by one.
+    auto extract = [&](uint32_t j, uint32_t (&w)[NW]) -> uint32_t {
+        uint32_t any = 0;
+        if (j >= s.wx) {
+#pragma unroll
+            for (int i = 0; i < NW; i++) w[i] = 0u;
+            return 0u;
+        }
         const int base = (int)(4 * gw0 - start);
         const int hi = (int)(s.blk_bytes - (uint32_t)LB * j) - base;
         const int sh = (hi & 3) * 8;
@@ -288,8 +294,31 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
         }
 #pragma unroll
         for (int i = 0; i < NW; i++) any |= w[i];
+        return any;
+    };
+    const uint32_t ja = jt0 + threadIdx.x, jb = ja + kPackT;
+    if (ja >= wxp) return;
+    uint32_t wa[NW], wb[NW];
+    const uint32_t anya = extract(ja, wa), anyb = extract(jb, wb);
+    const bool okb = jb < wxp;
+    uint32_t *oa = res + (size_t)iv * P * wxp + ja;
+    if (!(anya | anyb)) {
+        for (uint32_t pi = 0; pi < P; pi++, oa += wxp) {
+            *oa = 0u;
+            if (okb) oa[kPackT] = 0u;
+        }
+        return;
     }
-    store_residues<NW>(res + (size_t)iv * P * wxp + j, wxp, P, any, w, ks);
+    // a zero limb reduces to p (== 0 mod p, inside the [0, 2p) range the column pass takes)
+#pragma unroll
+    for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
+        if (pi >= P) break;
+        const uint32_t ra = limb_words_redc<NW>(wa, ks.k[pi]);
+        const uint32_t rb = limb_words_redc<NW>(wb, ks.k[pi]);
+        *oa = ra;
+        if (okb) oa[kPackT] = rb;
+        oa += wxp;
+    }
 }
 
 // ---------------------------------------------------------------- paper mode (NEXT-1)
