@@ -808,7 +808,7 @@ static uint32_t mac_v_rt(int slog) {
 template <int NW>
 static void launch_pack_key(const KeySrc &s, uint32_t nvec, const PrimeSet &pk, uint32_t P, uint32_t wxp, uint32_t *res,
                             cudaStream_t st) {
-    const dim3 grid((wxp + 2 * kPackT - 1) / (2 * kPackT), nvec);          // two limbs per thread
+    const dim3 grid((wxp + kPackL * kPackT - 1) / (kPackL * kPackT), nvec);   // kPackL limbs per thread
     pack_key_residues<NW><<<grid, kPackT, 0, st>>>(s, pk, P, wxp, res);
 }
 

@@ -211,12 +211,16 @@ __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeS
 // thread assembles its limb's NW words (big-endian bytes, readings A3/A4) from there and
 // reduces them modulo every prime.  res layout as pack_residues.
 constexpr int kPackT = 256;
+#ifndef PA_PACKL
+#define PA_PACKL 2
+#endif
+constexpr int kPackL = PA_PACKL;                               // limbs per thread in pack_key_residues
 template <int NW>
 __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
-    // a tile is 2 kPackT limbs, two per thread (limbs t and t + kPackT): the per-prime
-    // constants, loop and addressing are shared by both limbs' reductions
-    constexpr int TL = 2 * kPackT;
+    // a tile is kPackL kPackT limbs, kPackL per thread (limbs t + q kPackT): the per-prime
+    // constants, loop and addressing are shared by the limbs' reductions
+    constexpr int TL = kPackL * kPackT;
     constexpr int MAXW = TL * NW + 4;                         // staged words (LB <= 4 NW bytes per limb)
     __shared__ uint32_t sw[MAXW];
     const uint32_t iv = blockIdx.y;
@@ -296,28 +300,30 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
         for (int i = 0; i < NW; i++) any |= w[i];
         return any;
     };
-    const uint32_t ja = jt0 + threadIdx.x, jb = ja + kPackT;
-    if (ja >= wxp) return;
-    uint32_t wa[NW], wb[NW];
-    const uint32_t anya = extract(ja, wa), anyb = extract(jb, wb);
-    const bool okb = jb < wxp;
-    uint32_t *oa = res + (size_t)iv * P * wxp + ja;
-    if (!(anya | anyb)) {
-        for (uint32_t pi = 0; pi < P; pi++, oa += wxp) {
-            *oa = 0u;
-            if (okb) oa[kPackT] = 0u;
-        }
+    const uint32_t j0 = jt0 + threadIdx.x;
+    if (j0 >= wxp) return;
+    uint32_t w[kPackL][NW];
+    uint32_t any = 0;
+#pragma unroll
+    for (int q = 0; q < kPackL; q++) any |= extract(j0 + q * kPackT, w[q]);
+    uint32_t *o = res + (size_t)iv * P * wxp + j0;
+    if (!any) {
+        for (uint32_t pi = 0; pi < P; pi++, o += wxp)
+#pragma unroll
+            for (int q = 0; q < kPackL; q++)
+                if (j0 + q * kPackT < wxp) o[q * kPackT] = 0u;
         return;
     }
     // a zero limb reduces to p (== 0 mod p, inside the [0, 2p) range the column pass takes)
 #pragma unroll
     for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
         if (pi >= P) break;
-        const uint32_t ra = limb_words_redc<NW>(wa, ks.k[pi]);
-        const uint32_t rb = limb_words_redc<NW>(wb, ks.k[pi]);
-        *oa = ra;
-        if (okb) oa[kPackT] = rb;
-        oa += wxp;
+#pragma unroll
+        for (int q = 0; q < kPackL; q++) {
+            const uint32_t r = limb_words_redc<NW>(w[q], ks.k[pi]);
+            if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
+        }
+        o += wxp;
     }
 }
 
