@@ -1378,7 +1378,7 @@ static KeySrc key_src(const pa_ctx *c, const uint8_t *key_slice, uint32_t v0, ui
 template <int NW>
 static void launch_pack_bits(const KeySrc &s, const uint64_t *offs, uint32_t gamma, uint32_t B, uint32_t wx,
                              uint32_t nvec, const PrimeSet &pk, uint32_t P, uint32_t wxp, uint32_t *res, cudaStream_t st) {
-    const dim3 grid((wxp + kPackT - 1) / kPackT, nvec);
+    const dim3 grid((wxp + kPackL * kPackT - 1) / (kPackL * kPackT), nvec);
     pack_bits_residues<NW><<<grid, kPackT, 0, st>>>(s, offs, gamma, B, wx, pk, P, wxp, res);
 }
 

@@ -215,6 +215,31 @@ constexpr int kPackT = 256;
 #define PA_PACKL 2
 #endif
 constexpr int kPackL = PA_PACKL;                               // limbs per thread in pack_key_residues
+// Residues of kPackL limbs (j0 + q kPackT) modulo all P primes, stored P x wxp apart.
+// A zero limb among non-zero ones reduces to p (== 0 mod p, inside the [0, 2p) range the
+// column pass takes); an all-zero set stores zeros.
+template <int NW>
+__device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, uint32_t wxp, uint32_t P, uint32_t any,
+                                                     const uint32_t (&w)[kPackL][NW], const PrimeSet &ks) {
+    if (!any) {
+        for (uint32_t pi = 0; pi < P; pi++, o += wxp)
+#pragma unroll
+            for (int q = 0; q < kPackL; q++)
+                if (j0 + q * kPackT < wxp) o[q * kPackT] = 0u;
+        return;
+    }
+#pragma unroll
+    for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
+        if (pi >= P) break;
+#pragma unroll
+        for (int q = 0; q < kPackL; q++) {
+            const uint32_t r = limb_words_redc<NW>(w[q], ks.k[pi]);
+            if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
+        }
+        o += wxp;
+    }
+}
+
 template <int NW>
 __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
@@ -306,25 +331,7 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     uint32_t any = 0;
 #pragma unroll
     for (int q = 0; q < kPackL; q++) any |= extract(j0 + q * kPackT, w[q]);
-    uint32_t *o = res + (size_t)iv * P * wxp + j0;
-    if (!any) {
-        for (uint32_t pi = 0; pi < P; pi++, o += wxp)
-#pragma unroll
-            for (int q = 0; q < kPackL; q++)
-                if (j0 + q * kPackT < wxp) o[q * kPackT] = 0u;
-        return;
-    }
-    // a zero limb reduces to p (== 0 mod p, inside the [0, 2p) range the column pass takes)
-#pragma unroll
-    for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
-        if (pi >= P) break;
-#pragma unroll
-        for (int q = 0; q < kPackL; q++) {
-            const uint32_t r = limb_words_redc<NW>(w[q], ks.k[pi]);
-            if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
-        }
-        o += wxp;
-    }
+    store_residues_multi<NW>(res + (size_t)iv * P * wxp + j0, j0, wxp, P, any, w, ks);
 }
 
 // ---------------------------------------------------------------- paper mode (NEXT-1)
@@ -379,12 +386,13 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
                                                            uint32_t gamma, uint32_t B, uint32_t wx,
                                                            const PrimeSet ks, uint32_t P, uint32_t wxp,
                                                            uint32_t *__restrict__ res) {
-    constexpr int MAXW = kPackT * NW + 8;
+    constexpr int TL = kPackL * kPackT;                       // limbs per tile, kPackL per thread
+    constexpr int MAXW = TL * NW + 8;
     __shared__ uint32_t sw[MAXW];
     const uint32_t iv = blockIdx.y;
-    const uint32_t jt0 = blockIdx.x * kPackT;
+    const uint32_t jt0 = blockIdx.x * TL;
     const int64_t off = (int64_t)offs[iv];
-    const uint32_t jt1 = min(jt0 + kPackT, wx);
+    const uint32_t jt1 = min(jt0 + TL, wx);
     // key bits of the tile: [off + gamma - B jt1, off + gamma - B jt0), clipped at off
     int64_t blo = off + (int64_t)gamma - (int64_t)B * jt1 - 32;
     if (blo < off - 32) blo = off - 32;
@@ -406,14 +414,16 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
         }
     }
     __syncthreads();
-    const uint32_t j = jt0 + threadIdx.x;
-    if (j >= wxp) return;
-    uint32_t w[NW];
-    uint32_t any = 0;
-    if (j < wx) {
-        // word i of the limb = window bits [B j + 32 i, +32) = the 32 key bits whose MSB is key
-        // bit q_i = off + gamma - B j - 32 (i + 1): every word shares q_0's byte and bit shift
-        // and sits one staged word lower than the previous one
+    // word i of limb j = window bits [B j + 32 i, +32) = the 32 key bits whose MSB is key bit
+    // q_i = off + gamma - B j - 32 (i + 1): every word shares q_0's byte and bit shift and
+    // sits one staged word lower than the previous one
+    auto extract = [&](uint32_t j, uint32_t (&w)[NW]) -> uint32_t {
+        uint32_t any = 0;
+        if (j >= wx) {
+#pragma unroll
+            for (int i = 0; i < NW; i++) w[i] = 0u;
+            return 0u;
+        }
         const int64_t q0 = off + (int64_t)gamma - (int64_t)B * j - 32;
         const int64_t rb0 = (q0 >> 3) - 4 * gw0;               // staged byte of word 0
         const int sh = (int)(q0 & 7), bb = (int)(rb0 & 3);
@@ -435,11 +445,15 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
             a2 = a1;
             a1 = a0;
         }
-    } else {
+        return any;
+    };
+    const uint32_t j0 = jt0 + threadIdx.x;
+    if (j0 >= wxp) return;
+    uint32_t w[kPackL][NW];
+    uint32_t any = 0;
 #pragma unroll
-        for (int i = 0; i < NW; i++) w[i] = 0u;
-    }
-    store_residues<NW>(res + (size_t)iv * P * wxp + j, wxp, P, any, w, ks);
+    for (int q = 0; q < kPackL; q++) any |= extract(j0 + q * kPackT, w[q]);
+    store_residues_multi<NW>(res + (size_t)iv * P * wxp + j0, j0, wxp, P, any, w, ks);
 }
 
 // MH-only comparator: out[u] = bits [32 u, 32 u + 32) of x, the integer of key bits
