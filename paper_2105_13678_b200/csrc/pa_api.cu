@@ -1675,6 +1675,17 @@ extern "C" int pa_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *con
 // the MMH transforms.
 static constexpr int kCopyGroups = 8;
 
+// First block of copy group g of G: group sizes fall linearly (weights G, G-1, ..., 1), so the
+// last group -- whose transforms are all that is left to do once the last byte has arrived --
+// is the smallest (C4: 7, 6, 5, 4, 4, 2, 2, 1 blocks).  The H2D copy outruns nothing: the
+// GPU finishes each group's transforms before the next group's bytes land.
+static uint32_t group_begin(uint32_t nblk, int G, int g) {
+    const uint64_t W = (uint64_t)G * (G + 1) / 2;
+    uint64_t cum = 0;
+    for (int i = 0; i < g; i++) cum += (uint64_t)(G - i);
+    return (uint32_t)((nblk * cum + W / 2) / W);
+}
+
 static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
     // the copies may overwrite key_dev only after earlier work on the ctx stream is done
@@ -1687,8 +1698,8 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     const int G = whole ? 1 : (int)std::min<uint32_t>(kCopyGroups, nblk);
     const uint64_t R = c->pl.r / 8;
     for (int g = 0; g < G; g++) {
-        const uint64_t lo = G == 1 ? 0 : std::min<uint64_t>(nb, (uint64_t)(nblk * g / G) * R);
-        const uint64_t hi = G == 1 ? nb : std::min<uint64_t>(nb, (uint64_t)(nblk * (g + 1) / G) * R);
+        const uint64_t lo = G == 1 ? 0 : std::min<uint64_t>(nb, (uint64_t)group_begin(nblk, G, g) * R);
+        const uint64_t hi = G == 1 ? nb : std::min<uint64_t>(nb, (uint64_t)group_begin(nblk, G, g + 1) * R);
         if (hi > lo) CUDA_TRY(cudaMemcpyAsync(c->key_dev + lo, key_host + lo, hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
         CUDA_TRY(cudaEventRecord(c->copy_ev[g], c->copy_stream));
     }
@@ -1702,7 +1713,7 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     TRY(carry_reset(c));
     bool first = true;
     for (int g = 0; g < G; g++) {
-        const uint32_t v0 = nblk * g / G, v1 = nblk * (g + 1) / G;
+        const uint32_t v0 = group_begin(nblk, G, g), v1 = group_begin(nblk, G, g + 1);
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_ev[g], 0));
         if (v1 > v0) TRY(mmh_forward(c, c->key_dev, v0, v1));
         if (v1 > v0) TRY(mmh_mac(c, v0, v1, first, G == 1));
