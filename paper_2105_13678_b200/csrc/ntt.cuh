@@ -65,7 +65,9 @@ __host__ __device__ constexpr int bitrev(int q) {
 // in x[q] out.  tw[j] = omega_E^j, twp[j] its Shoup companion (j < E/2).
 // ZH: the upper half x[R/2..R) is known to be zero (a column whose non-zero rows all lie in
 // the first half): the first stage is then (a, a w), no sums or differences.
-template <int RLOG, int E, bool ZH = false>
+// LAZY: the last stage's outputs are left in [0, 4p) (no final reductions) -- for callers
+// whose next step is a Montgomery multiply, which takes any 32-bit operand.
+template <int RLOG, int E, bool ZH = false, bool LAZY = false>
 __device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const uint32_t *twp,
                                         uint32_t p, uint32_t p2) {
     constexpr int R = 1 << RLOG;
@@ -79,7 +81,13 @@ __device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const u
                     const int j = i * (E / (2 * h));
                     x[s + i + h] = (i == 0) ? x[s + i] : mul_shoup(x[s + i], tw[j], twp[j], p);
                 } else if (i == 0) {
-                    bfly_dif1(x[s], x[s + h], p2);
+                    if (LAZY && h == 1) {
+                        const uint32_t u = x[s], w = x[s + 1];
+                        x[s] = u + w;                   // < 4p
+                        x[s + 1] = u - w + p2;          // < 4p
+                    } else {
+                        bfly_dif1(x[s], x[s + h], p2);
+                    }
                 } else {
                     const int j = i * (E / (2 * h));
                     bfly_dif(x[s + i], x[s + i + h], tw[j], twp[j], p, p2);
@@ -103,8 +111,8 @@ struct Ctx32 {  // per-prime constants held in registers by a thread
 
 // Round rho >= 1 of a sub-DFT (recursive over rho).  Round rho-1 left its outputs in
 // shared memory; the last round leaves its outputs in x[] (group h, register mm <->
-// position v + TPV h + G_last * bitrev(mm)).
-template <int S_LOG, int E_LOG, int RHO, class SIdx>
+// position v + TPV h + G_last * bitrev(mm)), in [0, 2p), or [0, 4p) with LAZY.
+template <int S_LOG, int E_LOG, int RHO, bool LAZY = false, class SIdx>
 __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SIdx &sidx, int v,
                                             const uint32_t *tw, const uint32_t *twp,
                                             const uint32_t *rtw_p, const NttArgs &a,
@@ -125,7 +133,7 @@ __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SId
             for (int m = 0; m < R; m++) x[h * R + m] = sm[sidx(q + (S / R) * m)];
         }
 #pragma unroll
-        for (int h = 0; h < NG; h++) dft_reg<RL, E>(x + h * R, tw, twp, c.p, c.p2);
+        for (int h = 0; h < NG; h++) dft_reg<RL, E, false, LAZY && RHO == SP::Q - 1>(x + h * R, tw, twp, c.p, c.p2);
         if constexpr (RHO < SP::Q - 1) {
             __syncthreads();
 #pragma unroll
@@ -142,7 +150,7 @@ __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SId
                 }
             }
         }
-        rounds_rest<S_LOG, E_LOG, RHO + 1>(x, sm, sidx, v, tw, twp, rtw_p, a, c);
+        rounds_rest<S_LOG, E_LOG, RHO + 1, LAZY>(x, sm, sidx, v, tw, twp, rtw_p, a, c);
     }
 }
 

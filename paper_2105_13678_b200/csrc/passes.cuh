@@ -581,7 +581,9 @@ col_pass(const ColArgs A) {
             round0_finish<S_LOG, E_LOG, true>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         else
             round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
-        rounds_rest<S_LOG, E_LOG, 1>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+        // forward: the outputs meet a Montgomery multiply by the four-step twiddle next, so
+        // the last stage skips its reductions
+        rounds_rest<S_LOG, E_LOG, 1, MODE == COL_FWD>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         {
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
             constexpr int G = 1 << SP::glog(SP::Q - 1);
@@ -685,7 +687,7 @@ row_pass(const RowArgs A) {
             }
             __syncthreads();
             round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
-            rounds_rest<S_LOG, E_LOG, 1>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
+            rounds_rest<S_LOG, E_LOG, 1, true>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);   // mul_mont next
             constexpr int R = 1 << SP::rlog(SP::Q - 1);
             if constexpr (MODE == ROW_MAC) {
                 const uint32_t *ah = A.ahat + vbase + (size_t)k2 * S;
@@ -910,7 +912,7 @@ row_mac(const MacArgs A) {
             uint32_t *exch = PAD ? exb : xst;
             if constexpr (SP::Q > 1 && !PAD) __syncthreads();   // natural-order reads before in-place writes
             round0_finish<S_LOG, E_LOG>(x, exch, sidx, v, tw, twp, rtw_p, a, cx);
-            rounds_rest<S_LOG, E_LOG, 1>(x, exch, sidx, v, tw, twp, rtw_p, a, cx);
+            rounds_rest<S_LOG, E_LOG, 1, true>(x, exch, sidx, v, tw, twp, rtw_p, a, cx);   // mul_mont next
         }
         mbar_wait(&bars[NSX], k & 1);
         {
