@@ -66,8 +66,9 @@ __host__ __device__ constexpr int bitrev(int q) {
 // ZH: the upper half x[R/2..R) is known to be zero (a column whose non-zero rows all lie in
 // the first half): the first stage is then (a, a w), no sums or differences.
 // LAZY: the last stage's outputs are left in [0, 4p) (no final reductions) -- for callers
-// whose next step is a Montgomery multiply, which takes any 32-bit operand.
-template <int RLOG, int E, bool ZH = false, bool LAZY = false>
+// whose next step is a Montgomery multiply, which takes any 32-bit operand.  LAZY0: the
+// same except output 0, the one inter-round output that is not twiddled (k = bitrev(0) = 0).
+template <int RLOG, int E, bool ZH = false, bool LAZY = false, bool LAZY0 = false>
 __device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const uint32_t *twp,
                                         uint32_t p, uint32_t p2) {
     constexpr int R = 1 << RLOG;
@@ -81,10 +82,10 @@ __device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const u
                     const int j = i * (E / (2 * h));
                     x[s + i + h] = (i == 0) ? x[s + i] : mul_shoup(x[s + i], tw[j], twp[j], p);
                 } else if (i == 0) {
-                    if (LAZY && h == 1) {
+                    if ((LAZY || LAZY0) && h == 1) {
                         const uint32_t u = x[s], w = x[s + 1];
-                        x[s] = u + w;                   // < 4p
-                        x[s + 1] = u - w + p2;          // < 4p
+                        x[s] = (LAZY0 && !LAZY && s == 0) ? red2p(u + w, p2) : u + w;   // < 4p
+                        x[s + 1] = u - w + p2;                                          // < 4p
                     } else {
                         bfly_dif1(x[s], x[s + h], p2);
                     }
@@ -133,7 +134,8 @@ __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SId
             for (int m = 0; m < R; m++) x[h * R + m] = sm[sidx(q + (S / R) * m)];
         }
 #pragma unroll
-        for (int h = 0; h < NG; h++) dft_reg<RL, E, false, LAZY && RHO == SP::Q - 1>(x + h * R, tw, twp, c.p, c.p2);
+        for (int h = 0; h < NG; h++)
+            dft_reg<RL, E, false, LAZY && RHO == SP::Q - 1, (RHO < SP::Q - 1) && (T > 1)>(x + h * R, tw, twp, c.p, c.p2);
         if constexpr (RHO < SP::Q - 1) {
             __syncthreads();
 #pragma unroll
@@ -166,8 +168,9 @@ __device__ __forceinline__ void round0_finish(uint32_t *x, uint32_t *sm, const S
     constexpr int R = 1 << RL;
     constexpr int T = S / R;
     constexpr int NG = E / R;
+    // with a further round, every output but k = 0 is twiddled next (Montgomery): LAZY0
 #pragma unroll
-    for (int h = 0; h < NG; h++) dft_reg<RL, E, ZH>(x + h * R, tw, twp, c.p, c.p2);
+    for (int h = 0; h < NG; h++) dft_reg<RL, E, ZH, false, (SP::Q > 1) && (T > 1)>(x + h * R, tw, twp, c.p, c.p2);
     if constexpr (SP::Q > 1) {
 #pragma unroll
         for (int h = 0; h < NG; h++) {
