@@ -32,7 +32,7 @@ struct NttArgs {
     const uint32_t *regtw;     // [P][E/2] omega_E^j of this direction
     const uint32_t *regtwp;    // [P][E/2] Shoup companions
     uint32_t regtw_stride;     // E/2 entries per prime in the table (allocated for E=32)
-    const uint32_t *rtw;       // round twiddles (Montgomery form): [P][rtw_stride]
+    const uint32_t *rtw;       // round twiddles, Shoup pairs (w, floor(w 2^32/p)): [P][rtw_stride]
     uint32_t rtw_stride;
     uint32_t rtw_off[kMaxRounds];
     const uint32_t *ltw_lo;    // omega_L^(+-e_lo), e_lo < 2^h   (Montgomery form)
@@ -146,8 +146,10 @@ __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SId
                 for (int mm = 0; mm < R; mm++) {
                     const int k = bitrev<R>(mm);
                     uint32_t val = x[h * R + mm];
-                    if (T > 1 && k != 0)
-                        val = mul_mont(val, __ldg(rtw_p + a.rtw_off[RHO] + k * T + t), c.p, c.pinv);
+                    if (T > 1 && k != 0) {
+                        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(rtw_p + a.rtw_off[RHO]) + k * T + t);
+                        val = mul_shoup(val, w.x, w.y, c.p);
+                    }
                     sm[sidx(g + G * k + G * R * t)] = val;
                 }
             }
@@ -179,8 +181,10 @@ __device__ __forceinline__ void round0_finish(uint32_t *x, uint32_t *sm, const S
             for (int mm = 0; mm < R; mm++) {
                 const int k = bitrev<R>(mm);
                 uint32_t val = x[h * R + mm];
-                if (T > 1 && k != 0)
-                    val = mul_mont(val, __ldg(rtw_p + a.rtw_off[0] + k * T + t), c.p, c.pinv);
+                if (T > 1 && k != 0) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(rtw_p + a.rtw_off[0]) + k * T + t);
+                    val = mul_shoup(val, w.x, w.y, c.p);
+                }
                 sm[sidx(k + R * t)] = val;
             }
         }

@@ -312,7 +312,12 @@ static void round_tables(uint32_t p, uint32_t wL, int lg, int slog, int E_LOG, s
         off[rho] = (uint32_t)tab.size();
         for (uint32_t k = 0; k < R; k++) {
             uint64_t wk = powmod64(w, k, p), cur = 1;
-            for (uint32_t t = 0; t < T; t++) { tab.push_back(to_mont((uint32_t)cur, p)); cur = mulmod64(cur, wk, p); }
+            // Shoup pairs (w, floor(w 2^32 / p)), interleaved: one 8-byte load per twiddle
+            for (uint32_t t = 0; t < T; t++) {
+                tab.push_back((uint32_t)cur);
+                tab.push_back(shoup_of((uint32_t)cur, p));
+                cur = mulmod64(cur, wk, p);
+            }
         }
         glog += rl;
     }
