@@ -494,7 +494,7 @@ struct ColArgs {
     NttArgs nt;
     const uint32_t *src;     // FWD: residues [nvec][P][rows*N1];  INV: [P][L]
     uint32_t rows;           // FWD: rows holding non-zero limbs (<= N2)
-    const uint32_t *tw4;     // FWD: omega_L^(j1 k2) table [P][L] (Montgomery, canonical)
+    const uint2 *tw4;        // FWD: omega_L^(j1 k2) table [P][L], Shoup pairs (w, floor(w 2^32/p))
     uint32_t *dst;           // FWD: [nvec][P][L];  INV: [P][L]
     uint32_t nvec;           // vectors (blocks) per prime
     uint32_t units;          // (N1/32) * P * nvec
@@ -589,7 +589,7 @@ col_pass(const ColArgs A) {
             constexpr int G = 1 << SP::glog(SP::Q - 1);
             const size_t vb = ((size_t)v << N1_LOG) + j1;
             uint32_t *dst = ((MODE == COL_INV) ? A.dst + (size_t)pi * L : A.dst + ((size_t)iv * P + pi) * L) + vb;
-            const uint32_t *tw4 = A.tw4 + (size_t)pi * L + vb;
+            const uint2 *tw4 = A.tw4 + (size_t)pi * L + vb;
 #pragma unroll
             for (int h = 0; h < E / R; h++) {
 #pragma unroll
@@ -597,7 +597,10 @@ col_pass(const ColArgs A) {
                     const int rel = SP::TPV * h + G * bitrev<R>(mm);        // out_pos - v
                     const size_t o = (size_t)rel << N1_LOG;
                     uint32_t val = x[h * R + mm];
-                    if constexpr (MODE != COL_INV) val = mul_mont(val, __ldg(tw4 + o), cx.p, cx.pinv);
+                    if constexpr (MODE != COL_INV) {
+                        const uint2 w = __ldg(tw4 + o);
+                        val = mul_shoup(val, w.x, w.y, cx.p);
+                    }
                     else val = red1p(val, cx.p);
                     dst[o] = val;
                 }
