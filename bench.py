@@ -429,6 +429,62 @@ def main():
     nsteps_prof = args.steps
     stages = {kname: (v[0], v[1]) for kname, v in stages.items()}
 
+    e2e = None
+    if world == 1:
+        host_key = torch.from_numpy(key_full).pin_memory()
+        host_out = torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory()
+        for _ in range(2):
+            ctx.hash_host(host_key, host_out)
+        t = []
+        for _ in range(max(3, args.steps // 2)):
+            if not args.no_flush:
+                flush.fill_(1)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.hash_host(host_key, host_out)
+            bb.record(stream)
+            bb.synchronize()
+            t.append(a.elapsed_time(bb))
+        e2e_ms = statistics.median(t)
+        # end-to-end stream mode: a batch of pinned host keys, H2D overlapping compute
+        e2e_stream = None
+        if args.batch > 1:
+            hkeys = [host_key] + [torch.from_numpy(key_full).pin_memory() for _ in range(args.batch - 1)]
+            houts = [torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory() for _ in range(args.batch)]
+            ctx.hash_host_batch(hkeys, houts)
+            tsb = []
+            for _ in range(3):
+                a = torch.cuda.Event(enable_timing=True)
+                bb = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                ctx.hash_host_batch(hkeys, houts)
+                bb.record(stream)
+                bb.synchronize()
+                tsb.append(a.elapsed_time(bb))
+            msb = statistics.median(tsb)
+            e2e_stream = {"keys_per_batch": args.batch, "value": args.batch * w.n / (msb * 1e-3) / 1e6,
+                          "unit": "Mbps", "ms_per_key": msb / args.batch,
+                          "h2d_bytes_per_key": (w.n + 7) // 8, "d2h_bytes_per_key": (w.m + 7) // 8,
+                          "api": "pa_hash_host_batch (pinned host keys; H2D of key j overlaps the hash of key j-1)"}
+        # the PCIe floor: plain pinned copies of the same bytes (context for the e2e number)
+        kd = torch.empty_like(host_key, device=dev)
+        od = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
+        th2d, td2h = [], []
+        for _ in range(5):
+            a = torch.cuda.Event(enable_timing=True); bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream); kd.copy_(host_key, non_blocking=True); bb.record(stream); bb.synchronize()
+            th2d.append(a.elapsed_time(bb))
+            a.record(stream); host_out.copy_(od, non_blocking=True); bb.record(stream); bb.synchronize()
+            td2h.append(a.elapsed_time(bb))
+        e2e = {"value": w.n / (e2e_ms * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": e2e_ms,
+               "stream": e2e_stream,
+               "h2d_bytes_per_step": (w.n + 7) // 8, "d2h_bytes_per_step": (w.m + 7) // 8,
+               "api": "pa_hash_host (pinned host buffers, H2D + hash + D2H + sync)",
+               "h2d_copy_ms": min(th2d), "d2h_copy_ms": min(td2h),
+               "h2d_gbs": (w.n + 7) // 8 / (min(th2d) * 1e-3) / 1e9}
+
     # ---- stream mode (pa_hash_batch, NEXT-3): a batch of independent keys, MH / tail of one
     # key overlapping the MMH of the next; reported beside the single-key `value`
     stream_mode = None
@@ -538,62 +594,6 @@ def main():
             "what": "Toeplitz-hashing PA over GF(2) (Table 1, PAPER.md:57-71; SPEC.md:287-304): exact "
                     "single-prime NTT convolution of bit coefficients, r x r block split, parity of counts"}
         tctx.close()
-
-    e2e = None
-    if world == 1:
-        host_key = torch.from_numpy(key_full).pin_memory()
-        host_out = torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory()
-        for _ in range(2):
-            ctx.hash_host(host_key, host_out)
-        t = []
-        for _ in range(max(3, args.steps // 2)):
-            if not args.no_flush:
-                flush.fill_(1)
-            torch.cuda.synchronize()
-            a = torch.cuda.Event(enable_timing=True)
-            bb = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            ctx.hash_host(host_key, host_out)
-            bb.record(stream)
-            bb.synchronize()
-            t.append(a.elapsed_time(bb))
-        e2e_ms = statistics.median(t)
-        # end-to-end stream mode: a batch of pinned host keys, H2D overlapping compute
-        e2e_stream = None
-        if args.batch > 1:
-            hkeys = [host_key] + [torch.from_numpy(key_full).pin_memory() for _ in range(args.batch - 1)]
-            houts = [torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory() for _ in range(args.batch)]
-            ctx.hash_host_batch(hkeys, houts)
-            tsb = []
-            for _ in range(3):
-                a = torch.cuda.Event(enable_timing=True)
-                bb = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                ctx.hash_host_batch(hkeys, houts)
-                bb.record(stream)
-                bb.synchronize()
-                tsb.append(a.elapsed_time(bb))
-            msb = statistics.median(tsb)
-            e2e_stream = {"keys_per_batch": args.batch, "value": args.batch * w.n / (msb * 1e-3) / 1e6,
-                          "unit": "Mbps", "ms_per_key": msb / args.batch,
-                          "h2d_bytes_per_key": (w.n + 7) // 8, "d2h_bytes_per_key": (w.m + 7) // 8,
-                          "api": "pa_hash_host_batch (pinned host keys; H2D of key j overlaps the hash of key j-1)"}
-        # the PCIe floor: plain pinned copies of the same bytes (context for the e2e number)
-        kd = torch.empty_like(host_key, device=dev)
-        od = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
-        th2d, td2h = [], []
-        for _ in range(5):
-            a = torch.cuda.Event(enable_timing=True); bb = torch.cuda.Event(enable_timing=True)
-            a.record(stream); kd.copy_(host_key, non_blocking=True); bb.record(stream); bb.synchronize()
-            th2d.append(a.elapsed_time(bb))
-            a.record(stream); host_out.copy_(od, non_blocking=True); bb.record(stream); bb.synchronize()
-            td2h.append(a.elapsed_time(bb))
-        e2e = {"value": w.n / (e2e_ms * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": e2e_ms,
-               "stream": e2e_stream,
-               "h2d_bytes_per_step": (w.n + 7) // 8, "d2h_bytes_per_step": (w.m + 7) // 8,
-               "api": "pa_hash_host (pinned host buffers, H2D + hash + D2H + sync)",
-               "h2d_copy_ms": min(th2d), "d2h_copy_ms": min(td2h),
-               "h2d_gbs": (w.n + 7) // 8 / (min(th2d) * 1e-3) / 1e9}
 
     if rank != 0:
         if world > 1:
