@@ -420,3 +420,18 @@ def test_unaligned_key_and_output_pointers():
     assert bytes(ob[3:3 + ctx.nbytes_out].cpu().numpy()) == want
     assert int(ob[:3].sum()) == 0
     ctx.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,r,m", [(200_000, 1024, 5_000), (1 << 20, 2048, 30_000), (65_536, 1024, 2_000)])
+def test_many_blocks_few_units(n, r, m):
+    """Hundreds of blocks on a 2^10-point transform: the row MAC has only a handful of units,
+    so its grid splits each unit over many CTAs and adds into several accumulator slots,
+    which the inverse row pass sums (mac_grid in pa_api.cu)."""
+    PAContext = _pa()
+    key = key_bytes(n, 97)
+    ctx = PAContext(n, r, m, seed=13)
+    assert ctx.query()["mmh"]["log2_len"] == 10
+    got = bytes(ctx.hash(torch.from_numpy(key).cuda()).cpu().numpy())
+    assert got == oracle_seeded(key, n, r, m, 13)
+    ctx.close()
