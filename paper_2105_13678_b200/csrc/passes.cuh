@@ -769,7 +769,10 @@ __host__ __device__ constexpr int mac_v(int slog) {
 // exchange layout: a separate padded buffer (fewer instructions than the in-place XOR
 // swizzle, measured 118 vs 135 us for C4) whenever it fits; in place for 2^14-point rows
 __host__ __device__ constexpr int mac_pad(int slog) { return slog <= 13 ? 1 : 0; }
-template <int S_LOG, int PAD = mac_pad(S_LOG), int NSX = 2, int AIN = 0>
+#ifndef PA_MAC_NSX
+#define PA_MAC_NSX 2
+#endif
+template <int S_LOG, int PAD = mac_pad(S_LOG), int NSX = PA_MAC_NSX, int AIN = 0>
 constexpr size_t mac_smem_bytes() {
     return (size_t)(NSX + (AIN ? 0 : 1)) * mac_v(S_LOG) * (1 << S_LOG) * 4 + 4 * 8 +
            (PAD ? (size_t)mac_v(S_LOG) * ((1 << S_LOG) + (1 << S_LOG) / 32) * 4 : 0);
@@ -783,7 +786,7 @@ __host__ __device__ constexpr int mac_threads(int slog, int elog) { return mac_v
 __host__ __device__ constexpr int mac_minb(size_t smem_bytes) {
     return (int)(232448 / (smem_bytes + 1024)) < 1 ? 1 : ((int)(232448 / (smem_bytes + 1024)) > 8 ? 8 : (int)(232448 / (smem_bytes + 1024)));
 }
-template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = 2, int AIN = 0>
+template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = PA_MAC_NSX, int AIN = 0>
 __global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(mac_smem_bytes<S_LOG, PAD, NSX, AIN>()))
 row_mac(const MacArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
