@@ -23,4 +23,10 @@ for _ in range(15):
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record(s); ctx.hash_host(hk, ho); b.record(s); b.synchronize()
     t.append(a.elapsed_time(b))
-print("e2e ms median", round(statistics.median(t), 4), "min", round(min(t), 4))
+print("e2e ms median", round(statistics.median(t), 4), "min", round(min(t), 4), "max", round(max(t), 4))
+kd = torch.empty_like(hk, device="cuda")
+tc = []
+for _ in range(5):
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record(s); kd.copy_(hk, non_blocking=True); b.record(s); b.synchronize(); tc.append(a.elapsed_time(b))
+print("h2d ms", round(min(tc), 4))
