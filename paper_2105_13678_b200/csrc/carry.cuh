@@ -130,6 +130,35 @@ __device__ __forceinline__ uint32_t block_carries(int g, int pp, uint32_t cin, u
     return (C >> lane) & 1;
 }
 
+// block_carries for both block carry-ins at once: *c0 / *c1 = this thread's carry-in with
+// block carry-in 0 / 1, *bg = block generate.  One scan, so a caller that learns its carry-in
+// later (decoupled look-back) only selects.
+__device__ __forceinline__ void block_carries2(int g, int pp, uint32_t *c0, uint32_t *c1, uint32_t *bg) {
+    __shared__ uint32_t wc0[32], wc1[32];
+    __shared__ uint32_t wg2[32], wp2[32];
+    __shared__ uint32_t s_bg2;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t Gm = __ballot_sync(0xFFFFFFFFu, g), Pm = __ballot_sync(0xFFFFFFFFu, pp);
+    uint32_t co0;
+    (void)lane_carries(Gm, Pm, 0, co0);
+    if (lane == 0) { wg2[wid] = co0; wp2[wid] = (Pm == 0xFFFFFFFFu); }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        const uint32_t G2 = __ballot_sync(0xFFFFFFFFu, lane < nw ? wg2[lane] : 0);
+        const uint32_t P2 = __ballot_sync(0xFFFFFFFFu, lane < nw ? wp2[lane] : 1);
+        uint32_t co;
+        wc0[lane] = (lane_carries(G2, P2, 0, co) >> lane) & 1;
+        s_bg2 = co;                                           // same for every lane
+        wc1[lane] = (lane_carries(G2, P2, 1, co) >> lane) & 1;
+    }
+    __syncthreads();
+    uint32_t co;
+    *c0 = (lane_carries(Gm, Pm, wc0[wid], co) >> lane) & 1;
+    *c1 = (lane_carries(Gm, Pm, wc1[wid], co) >> lane) & 1;
+    *bg = s_bg2;
+}
+
 // Sources of 64-bit column sums for the carry kernel.
 struct SrcArr {
     const uint64_t *S;
@@ -483,8 +512,8 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     for (int v = 0; v < kCCV; v++) G = ((gm >> v) & 1u) | (((pm >> v) & 1u) & G);
     const int Pall = (pm == (1u << kCCV) - 1u);
     const int allp = __syncthreads_and(Pall);
-    uint32_t bg;
-    (void)block_carries((int)G, Pall, 0, &bg);
+    uint32_t bg, cc0, cc1;
+    block_carries2((int)G, Pall, &cc0, &cc1, &bg);          // both carry-ins before the look-back
     const uint32_t hi_last = s_hi[kCCT - 1];               // hi32 of the tile's last sum
     // the look-back flags carry their whole payload (ready bit + C_out), so relaxed gpu-scope
     // accesses suffice: no fence orders other data behind them
@@ -506,7 +535,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     }
     __syncthreads();
     const uint32_t cin = s_cin;
-    uint32_t c = block_carries((int)G, Pall, s_c1, nullptr);
+    uint32_t c = s_c1 ? cc1 : cc0;
 #pragma unroll
     for (int v = 0; v < kCCV; v++) {
         const uint32_t u = ub + v;

@@ -648,7 +648,10 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
     const size_t smem = 0;
     crt_coeffs<P><<<(ncoef + 127) / 128, 128, 0, st>>>(res, sd.L, ncoef, sd.crt, coef);
     CUDA_TRY(cudaGetLastError());
-    auto fn = crt_carry<P, RING>;
+#ifndef PA_CC_DBG
+#define PA_CC_DBG 0
+#endif
+    auto fn = crt_carry<P, RING, PA_CC_DBG>;            // PA_CC_DBG: timing-only ablations (carry.cuh)
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
         CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
