@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
                                                      uint32_t B, uint32_t gamma,
                                                      const uint32_t *__restrict__ addend, uint32_t n_addend,
                                                      uint32_t *__restrict__ out, uint32_t W, uint32_t cap,
-                                                     uint32_t *state, uint32_t Wfin) {
+                                                     uint32_t *state, uint32_t Wfin, uint32_t *__restrict__ obe) {
     (void)cap;
     // column sums of the tile's words, scatter form: a thread owns whole coefficients
     // (P words loaded from coefT, coalesced) and adds their P + 1 bit-shifted words into
@@ -536,15 +536,21 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     __syncthreads();
     const uint32_t cin = s_cin;
     uint32_t c = s_c1 ? cc1 : cc0;
+    // LINEAR with obe: the caller wants the W words as the MSB-first bit string of the whole
+    // W-word integer (m = alpha = 32 W, readings A5/A8): word u lands byte-swapped at W-1-u
+    auto store = [&](uint32_t u, uint32_t val) {
+        if (!RING && obe) obe[W - 1 - u] = __byte_perm(val, 0, 0x0123);
+        else out[u] = val;
+    };
 #pragma unroll
     for (int v = 0; v < kCCV; v++) {
         const uint32_t u = ub + v;
         const bool first = (threadIdx.x == 0 && v == 0);
         if (first) {
-            if (u < W) out[u] = w[v] + cin;
+            if (u < W) store(u, w[v] + cin);
             continue;
         }
-        if (u < W) out[u] = w[v] + c;
+        if (u < W) store(u, w[v] + c);
         c = ((gm >> v) & 1u) | (((pm >> v) & 1u) & c);
     }
     if (RING && !(DBG & 4)) {

@@ -642,7 +642,7 @@ static int launch_mac(int slog, const MacArgs &A, int grid, cudaStream_t st) {
 template <int P, bool RING>
 static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
                               const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint32_t *out, uint32_t W,
-                              uint32_t *state, uint32_t Wfin, cudaStream_t st) {
+                              uint32_t *state, uint32_t Wfin, cudaStream_t st, uint32_t *obe) {
     const uint32_t B = sd.pl.limb_bits;
     const uint32_t cap = (32u * kCCTile + 32u * P) / B + 3;
     const size_t smem = 0;
@@ -659,7 +659,7 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
     }
     const uint32_t ntiles = (W + kCCTile - 1) / kCCTile;
     fn<<<ntiles, kCCT, smem, st>>>(coef, sd.L, ncoef, B, (uint32_t)gamma, addend, n_addend, out, W, cap,
-                                      state, Wfin);
+                                      state, Wfin, obe);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
@@ -667,9 +667,9 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
 template <bool RING>
 static int launch_crt_carry(const uint32_t *res, const StageDev &sd, uint32_t ncoef, uint64_t gamma,
                             const uint32_t *addend, uint32_t n_addend, uint32_t *coef, uint32_t *out, uint32_t W,
-                            uint32_t *state, uint32_t Wfin, cudaStream_t st) {
+                            uint32_t *state, uint32_t Wfin, cudaStream_t st, uint32_t *obe = nullptr) {
 #define PA_CC_CASE(P) \
-    case P: return launch_crt_carry_t<P, RING>(res, sd, ncoef, gamma, addend, n_addend, coef, out, W, state, Wfin, st);
+    case P: return launch_crt_carry_t<P, RING>(res, sd, ncoef, gamma, addend, n_addend, coef, out, W, state, Wfin, st, obe);
     switch (sd.pl.nprimes) {
         PA_CC_CASE(2) PA_CC_CASE(3) PA_CC_CASE(4) PA_CC_CASE(5) PA_CC_CASE(6) PA_CC_CASE(7) PA_CC_CASE(8)
         PA_CC_CASE(9) PA_CC_CASE(10) PA_CC_CASE(11) PA_CC_CASE(12) PA_CC_CASE(13) PA_CC_CASE(14)
@@ -1513,13 +1513,18 @@ static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
         // only (b y + c) mod 2^alpha is needed: coefficients j with j B >= alpha cannot reach it
         const uint64_t ncoef = std::min<uint64_t>(std::min<uint64_t>(c->smh.L, cdiv(p.alpha, Bh) + cdiv(p.gamma, Bh) - 1),
                                                   cdiv(p.alpha, Bh));
+        // m = alpha, a whole number of words, aligned output: the carry kernel writes the
+        // output bits itself (byte-swapped words in reverse order), no extract pass
+        const bool direct = p.m == p.alpha && p.alpha % 32 == 0 && !((uintptr_t)out_bits & 3);
         TRY(launch_crt_carry<false>(c->acc_mh, c->smh, (uint32_t)ncoef, 0, c->c_words, W, c->coef, c->Z, W,
-                                    next_state(c), 0, c->stream));
+                                    next_state(c), 0, c->stream, direct ? reinterpret_cast<uint32_t *>(out_bits) : nullptr));
         c->launches += 2;
-        const uint64_t nb = cdiv(p.m, 8), nw = cdiv(nb, 4);
-        mh_extract<<<(uint32_t)cdiv(nw, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
-        c->launches++;
-        CUDA_TRY(cudaGetLastError());
+        if (!direct) {
+            const uint64_t nb = cdiv(p.m, 8), nw = cdiv(nb, 4);
+            mh_extract<<<(uint32_t)cdiv(nw, 256), 256, 0, c->stream>>>(c->Z, c->W_Z, p.alpha, p.m, out_bits, nb);
+            c->launches++;
+            CUDA_TRY(cudaGetLastError());
+        }
     }
     return PA_OK;
 }
