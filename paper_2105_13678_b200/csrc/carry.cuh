@@ -40,7 +40,10 @@ struct CrtK {
 //   fractional part away from 1.  All coefficients are independent (no Garner chain).
 // One thread per coefficient; word-major layout coef[w][j] (coalesced), P words each.
 template <int P>
-__global__ void __launch_bounds__(128) crt_coeffs(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
+#ifndef PA_CRT_MINB
+#define PA_CRT_MINB 1
+#endif
+__global__ void __launch_bounds__(128, PA_CRT_MINB) crt_coeffs(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
                                                   const CrtK K, uint32_t *__restrict__ coef) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= ncoef) return;
