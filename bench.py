@@ -40,6 +40,26 @@ def load_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
 
 
+def hbm_view(w, info: dict, ms_per_step: float, peaks: dict, paper: bool) -> dict:
+    """the step's bytes over the HBM peak, for two byte counts.
+    design = key + precomputed transforms (A^ for the k blocks, B^) + output, the bytes the
+    transform-domain design must stream once; min = key + the raw hash keys (k a_i of gamma bits,
+    b and c of alpha bits) + output, the bytes any implementation must touch.  The path is
+    ALU-bound (`roofline`), so these fractions are context, not its bound."""
+    key = (w.n + 7) // 8
+    out = (w.m + 7) // 8
+    k = info["k"]
+    mm, mh = info["mmh"], info["mh"]
+    hat = 4 * k * mm["nprimes"] * (1 << mm["log2_len"]) + 4 * mh["nprimes"] * (1 << mh["log2_len"])
+    raw = k * ((info["gamma"] + 7) // 8) + 2 * ((info["alpha"] + 7) // 8)
+    design, mn = key + hat + out, key + raw + out
+    gbs = lambda b: b / (ms_per_step * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    return {"design_bytes": design, "min_bytes": mn, "design_gbs": gbs(design), "min_gbs": gbs(mn),
+            "peak_gbs": peak, "design_frac": gbs(design) / peak, "min_frac": gbs(mn) / peak,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback"}
+
+
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock and clock-event reasons sampled DURING the timed region: an NVML
@@ -616,6 +636,7 @@ def main():
         "gpu_launches": launches_timed,
         "clocks": clocks,
         "roofline": roof,
+        "hbm": hbm_view(w, info, ms_per_step, peaks, paper),
         "stages_ms_per_step": {kk: v[0] / nsteps_prof for kk, v in sorted(stages.items())},
         "e2e": e2e,
         "stream": stream_mode if world == 1 else mr_stream,

@@ -66,6 +66,11 @@ def full(rep: str, stage: str, tag: str) -> None:
             val = float(v[0])
             unit = v[1] if len(v) > 1 else "byte"
             return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+        dur = rec.get("gpu__time_duration.sum", "0").split()
+        us = float(dur[0]) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(dur[1] if len(dur) > 1 else "usecond", 1.0)
+        dram = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
+        lines.append(f"  {'achieved DRAM GB/s (read+write / duration, SURVEY.md §8(d) item 4)':80s} "
+                     f"{dram / (us * 1e-6) / 1e9 if us else 0:.1f}")
         traffic[stage] = {"kernel": rec.get("Kernel Name"), "dram_bytes_per_launch":
                           mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
                           "dram_read": mb("dram__bytes_read.sum"), "dram_write": mb("dram__bytes_write.sum"),
