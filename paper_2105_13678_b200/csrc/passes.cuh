@@ -762,9 +762,15 @@ struct MacArgs {
     uint32_t slot_stride;     // so that no slot receives more than four partials of a unit
 };
 
-// rows per CTA: V*S = 2048 words per operand and stage, and V <= S/2 <= N2 (planner)
+// rows per CTA: V*S = kMacWords words per operand and stage, and V <= S/2 <= N2 (planner)
+#ifndef PA_MAC_WORDS
+#define PA_MAC_WORDS 2048
+#endif
+constexpr int kMacWords = PA_MAC_WORDS;
 __host__ __device__ constexpr int mac_v(int slog) {
-    return (slog >= 11 ? 1 : (2048 >> slog)) < (1 << (slog - 1)) ? (slog >= 11 ? 1 : (2048 >> slog)) : (1 << (slog - 1));
+    return ((1 << slog) >= kMacWords ? 1 : (kMacWords >> slog)) < (1 << (slog - 1))
+               ? ((1 << slog) >= kMacWords ? 1 : (kMacWords >> slog))
+               : (1 << (slog - 1));
 }
 // exchange layout: a separate padded buffer (fewer instructions than the in-place XOR
 // swizzle, measured 118 vs 135 us for C4) whenever it fits; in place for 2^14-point rows
