@@ -492,6 +492,15 @@ struct KInfo {
     int occ = 0;
 };
 
+// Launch attributes and occupancy are per device: callers keep one KInfo per device
+// (kMaxDevices) and pass the current device's entry.
+static constexpr int kMaxDevices = 16;
+static KInfo &kinfo_slot(KInfo (&tab)[kMaxDevices]) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+    return tab[d];
+}
+
 template <class F>
 static int kinfo(F *fn, int threads, size_t smem, KInfo &ki) {
     if (ki.occ) return PA_OK;
@@ -508,7 +517,8 @@ static int kinfo(F *fn, int threads, size_t smem, KInfo &ki) {
 template <int S_LOG, int N1_LOG, int MODE>
 static int launch_col_t(const ColArgs &A, cudaStream_t st) {
     constexpr int E_LOG = 5;
-    static KInfo ki;
+    static KInfo kis[kMaxDevices];
+    KInfo &ki = kinfo_slot(kis);
     auto fn = col_pass<S_LOG, E_LOG, N1_LOG, MODE>;
     TRY(kinfo(fn, 32 * (1 << (S_LOG - E_LOG)), (size_t)(1 << S_LOG) * 32 * 4, ki));
     const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
@@ -541,7 +551,8 @@ static int launch_row_t(const RowArgs &A0, cudaStream_t st) {
     // the inverse transforms a single vector: small CTAs (V S = 1024 words; 2048 measured
     // 21.0 vs 19.0 us for the C4 MMH inverse) give enough units
     constexpr int V = MODE == ROW_INV ? inv_v(S_LOG) : row_v(S_LOG);
-    static KInfo ki;
+    static KInfo kis[kMaxDevices];
+    KInfo &ki = kinfo_slot(kis);
     auto fn = row_pass<S_LOG, E_LOG, V, MODE>;
     constexpr int S = 1 << S_LOG;
     TRY(kinfo(fn, V * (S >> E_LOG), (size_t)V * (S + S / 32) * 4, ki));
@@ -581,7 +592,8 @@ static constexpr uint32_t kMacSlots = 4;
 template <int S_LOG>
 static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, uint32_t *nslot) {
     constexpr int E_LOG = 5;
-    static KInfo ki;
+    static KInfo kis[kMaxDevices];
+    KInfo &ki = kinfo_slot(kis);
     auto fn = row_mac<S_LOG, E_LOG>;
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
     const uint64_t full = (uint64_t)ki.occ * g_num_sms;
@@ -613,7 +625,8 @@ static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, 
 template <int S_LOG>
 static int launch_mac_t(const MacArgs &A, int grid, cudaStream_t st) {
     constexpr int E_LOG = 5;
-    static KInfo ki;
+    static KInfo kis[kMaxDevices];
+    KInfo &ki = kinfo_slot(kis);
     auto fn = row_mac<S_LOG, E_LOG>;
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
@@ -645,20 +658,14 @@ static int launch_crt_carry_t(const uint32_t *res, const StageDev &sd, uint32_t 
                               uint32_t *state, uint32_t Wfin, cudaStream_t st, uint32_t *obe) {
     const uint32_t B = sd.pl.limb_bits;
     const uint32_t cap = (32u * kCCTile + 32u * P) / B + 3;
-    const size_t smem = 0;
     crt_coeffs<P><<<(ncoef + 127) / 128, 128, 0, st>>>(res, sd.L, ncoef, sd.crt, coef);
     CUDA_TRY(cudaGetLastError());
 #ifndef PA_CC_DBG
 #define PA_CC_DBG 0
 #endif
     auto fn = crt_carry<P, RING, PA_CC_DBG>;            // PA_CC_DBG: timing-only ablations (carry.cuh)
-    static size_t smem_set = 0;
-    if (smem > 48 * 1024 && smem > smem_set) {
-        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
-    }
     const uint32_t ntiles = (W + kCCTile - 1) / kCCTile;
-    fn<<<ntiles, kCCT, smem, st>>>(coef, sd.L, ncoef, B, (uint32_t)gamma, addend, n_addend, out, W, cap,
+    fn<<<ntiles, kCCT, 0, st>>>(coef, sd.L, ncoef, B, (uint32_t)gamma, addend, n_addend, out, W, cap,
                                       state, Wfin, obe);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
