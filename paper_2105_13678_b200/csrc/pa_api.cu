@@ -1797,7 +1797,11 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
         c->launches = c->hgraph_launches;
         c->launches_total += c->launches;
     }
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    // synchronous call: poll rather than block, so the return does not wait on a thread
+    // wake-up (cudaStreamSynchronize may yield under the default scheduling heuristic)
+    cudaError_t q;
+    while ((q = cudaStreamQuery(c->stream)) == cudaErrorNotReady) { }
+    if (q != cudaSuccess) return set_err(PA_E_CUDA, "pa_hash_host: %s", cudaGetErrorString(q));
     if (c->pl.paper_k) return pa_ctx_status(c);
     return PA_OK;
 }
