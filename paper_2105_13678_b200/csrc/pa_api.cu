@@ -1763,6 +1763,15 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     return PA_OK;
 }
 
+// The synchronous host-buffer calls poll rather than block, so their return does not wait on
+// a thread wake-up (cudaStreamSynchronize may yield under the default scheduling heuristic).
+static int stream_poll(cudaStream_t st, const char *what) {
+    cudaError_t q;
+    while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) { }
+    if (q != cudaSuccess) return set_err(PA_E_CUDA, "%s: %s", what, cudaGetErrorString(q));
+    return PA_OK;
+}
+
 extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
     if (!c || !key_host || !out_host) return set_err(PA_E_PARAM, "NULL argument");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
@@ -1797,11 +1806,7 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
         c->launches = c->hgraph_launches;
         c->launches_total += c->launches;
     }
-    // synchronous call: poll rather than block, so the return does not wait on a thread
-    // wake-up (cudaStreamSynchronize may yield under the default scheduling heuristic)
-    cudaError_t q;
-    while ((q = cudaStreamQuery(c->stream)) == cudaErrorNotReady) { }
-    if (q != cudaSuccess) return set_err(PA_E_CUDA, "pa_hash_host: %s", cudaGetErrorString(q));
+    TRY(stream_poll(c->stream, "pa_hash_host"));
     if (c->pl.paper_k) return pa_ctx_status(c);
     return PA_OK;
 }
@@ -1863,8 +1868,7 @@ extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, ui
     c->launches = total;
     c->launches_total += total;
     TRY(rc);
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    return PA_OK;
+    return stream_poll(c->stream, "pa_hash_host_batch");
 }
 
 extern "C" int pa_ctx_set_profiling(pa_ctx *c, int enable) {
