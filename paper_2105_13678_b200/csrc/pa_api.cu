@@ -1424,9 +1424,11 @@ static int paper_pack(pa_ctx *c, const uint8_t *key) {
     ks.aligned = (((uintptr_t)key) & 3) == 0;
     {
         ProfScope ps(c, "mmh_reload_windows");
-        window_flags<<<c->T, 256, 0, c->stream>>>(ks, (uint32_t)p.gamma, c->T, c->wflags);
-        window_resolve<<<1, 32, 0, c->stream>>>(c->wflags, c->T, (uint32_t)p.k, (uint32_t)p.gamma, c->offs, c->status);
-        c->launches += 2;
+        uint32_t *done = next_state(c);                     // zeroed by carry_reset
+        if (!done) return set_err(PA_E_STATE, "carry slots exhausted");
+        window_flags<<<c->T, 256, 0, c->stream>>>(ks, (uint32_t)p.gamma, c->T, c->wflags, done, (uint32_t)p.k, c->offs,
+                                                  c->status);
+        c->launches += 1;
         CUDA_TRY(cudaGetLastError());
     }
     ProfScope ps(c, "mmh_pack");

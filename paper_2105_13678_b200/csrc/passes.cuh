@@ -344,12 +344,17 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
 // blockDim words and stops at the first chunk holding a zero bit: for keys of i.i.d.
 // bits that is the first chunk, so the check reads ~1 KB per window; an all-ones window
 // (the reload case) is scanned completely (correct, proportionally slower).
-__global__ void __launch_bounds__(256) window_flags(const KeySrc s, uint32_t gamma, uint32_t T, uint32_t *flags) {
+// The last CTA to finish (done counter, zeroed by the caller) then resolves the offsets:
+// offs[i] = bit offset of block i (the i-th window with a zero bit); status 1 if fewer than k
+// windows qualify (SPEC.md:74 InsufficientInput), else 0.
+__global__ void __launch_bounds__(256) window_flags(const KeySrc s, uint32_t gamma, uint32_t T, uint32_t *flags,
+                                                    uint32_t *done, uint32_t k, uint64_t *offs, uint32_t *status) {
+    __shared__ uint32_t s_last;
     const uint32_t t = blockIdx.x;
-    if (t >= T) return;
     const uint64_t lo = (uint64_t)t * gamma, hi = lo + gamma;  // window bits [lo, hi)
     const uint64_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
-    for (uint64_t base = w0; base < w1; base += blockDim.x) {
+    uint32_t found = 0;
+    for (uint64_t base = w0; base < w1 && !found; base += blockDim.x) {
         const uint64_t wi = base + threadIdx.x;
         uint32_t z = 0;
         if (wi < w1) {
@@ -358,22 +363,19 @@ __global__ void __launch_bounds__(256) window_flags(const KeySrc s, uint32_t gam
             if (p0 < lo) z &= 0xFFFFFFFFu >> (lo - p0);                 // positions before the window
             if (p0 + 32 > hi) z &= 0xFFFFFFFFu << (p0 + 32 - hi);       // positions after it
         }
-        if (__syncthreads_or(z != 0)) {
-            if (threadIdx.x == 0) flags[t] = 1u;
-            return;
-        }
+        found = __syncthreads_or(z != 0) ? 1u : 0u;
     }
-    if (threadIdx.x == 0) flags[t] = 0u;
-}
-
-// offs[i] = bit offset of block i (the i-th window with a zero bit); status 1 if fewer
-// than k windows qualify (SPEC.md:74 InsufficientInput), else 0.  One thread.
-__global__ void window_resolve(const uint32_t *flags, uint32_t T, uint32_t k, uint32_t gamma, uint64_t *offs,
-                               uint32_t *status) {
-    if (threadIdx.x || blockIdx.x) return;
+    if (threadIdx.x == 0) {
+        flags[t] = found;
+        __threadfence();
+        s_last = (atomicAdd(done, 1u) == T - 1);
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x) return;
+    __threadfence();
     uint32_t i = 0;
-    for (uint32_t t = 0; t < T && i < k; t++)
-        if (flags[t]) offs[i++] = (uint64_t)t * gamma;
+    for (uint32_t u = 0; u < T && i < k; u++)
+        if (((volatile uint32_t *)flags)[u]) offs[i++] = (uint64_t)u * gamma;
     *status = (i < k) ? 1u : 0u;
     for (; i < k; i++) offs[i] = 0;                            // output undefined; reads stay in bounds
 }
