@@ -1087,7 +1087,7 @@ static int run_toeplitz(pa_ctx *c, const uint8_t *key, uint8_t *out_bits) {
     {
         ProfScope ps(c, "tz_pack");
         const uint64_t tot = (uint64_t)nb << lr;
-        toeplitz_pack_bits<<<(uint32_t)std::min<uint64_t>(cdiv(tot, 256), (uint64_t)g_num_sms * 16), 256, 0,
+        toeplitz_pack_bits<<<(uint32_t)std::min<uint64_t>(cdiv(tot / 4, 256), (uint64_t)g_num_sms * 16), 256, 0,
                              c->stream>>>(key, p.n, tot, c->res);
         c->launches++;
         CUDA_TRY(cudaGetLastError());
@@ -1095,7 +1095,7 @@ static int run_toeplitz(pa_ctx *c, const uint8_t *key, uint8_t *out_bits) {
     TRY(tz_forward(c, c->res, nb, sd.pl.n_col / 2, c->scratch, c->tz_scale, "tz_fwd_col", "tz_fwd_row"));
     {
         ProfScope ps(c, "tz_mac");
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(L, 256), (uint64_t)g_num_sms * 8);
+        const uint32_t grid = (uint32_t)cdiv(L, 256);          // one element per thread
         switch (no) {
 #define PA_TZ(O) case O: launch_tz_mac<O>(c, grid); break;
             PA_TZ(1) PA_TZ(2) PA_TZ(3) PA_TZ(4) PA_TZ(5) PA_TZ(6) PA_TZ(7) PA_TZ(8)

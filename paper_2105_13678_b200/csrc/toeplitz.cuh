@@ -16,14 +16,21 @@
 namespace pa {
 
 // x_b[j] = key bit b r + j (MSB-first within bytes, reading A4), 0 beyond n; out [nb][r]
-// (the natural order the forward column pass reads, r = rows * N1).
+// (the natural order the forward column pass reads, r = rows * N1).  A thread expands one
+// nibble (4 coefficients) into one 16-byte store, so a warp writes 512 contiguous bytes.
 __global__ void __launch_bounds__(256) toeplitz_pack_bits(const uint8_t *__restrict__ key, uint64_t n,
                                                           uint64_t total, uint32_t *__restrict__ out) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t v = 0;
-        if (t < n) v = (__ldg(key + (t >> 3)) >> (7 - (t & 7))) & 1u;
-        out[t] = v;
+    const uint64_t nchunks = total >> 2;                     // total is a multiple of r >= 512
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nchunks;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t0 = i << 2;                          // first bit of the nibble
+        uint32_t nib = 0;
+        if (t0 < n) {
+            const uint32_t byte = __ldg(key + (t0 >> 3));
+            nib = (i & 1) ? (byte & 0xFu) : (byte >> 4);      // MSB-first: even chunk = high nibble
+            if (t0 + 4 > n) nib &= (0xF0u >> (n - t0)) & 0xFu;   // bits >= n are 0
+        }
+        reinterpret_cast<uint4 *>(out)[i] = make_uint4((nib >> 3) & 1u, (nib >> 2) & 1u, (nib >> 1) & 1u, nib & 1u);
     }
 }
 
@@ -51,7 +58,12 @@ __global__ void __launch_bounds__(256) toeplitz_pack_diag(const uint32_t *__rest
 // transform-domain sum over input blocks of every output block.  Eh holds T(e') L^-1 R
 // (Montgomery), Xh plain transforms, so mul_mont leaves T(x) T(e') / L.  For a fixed e the
 // E index window b .. b + O - 1 slides by one per input block: O registers, one new load.
+// The products are summed as plain 64-bit integers (one wide multiply-add each): x, w < p <
+// 2^30, so seven products stay below 3 p 2^32 and one REDC per seven blocks turns the group
+// into sum x w R^-1 mod p -- the same value as seven Montgomery products, at a fraction of
+// the instructions.
 constexpr int kTzMaxOut = 16;
+constexpr int kTzGroup = 7;
 template <int O>
 __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__ Xh, const uint32_t *__restrict__ Eh,
                                                     uint32_t nb, uint32_t L, uint32_t p, uint32_t pinv,
@@ -59,15 +71,27 @@ __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__
     const uint32_t p2 = 2 * p;
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < L; e += gridDim.x * blockDim.x) {
         uint32_t a[O], w[O];
+        uint64_t t[O];
 #pragma unroll
         for (int o = 0; o < O; o++) {
             a[o] = 0;
+            t[o] = 0;
             w[o] = __ldg(Eh + (size_t)(O - 1 - o) * L + e);        // w[o] = E[b + O - 1 - o] at b = 0
         }
+        uint32_t g = 0;
+#pragma unroll 7
         for (uint32_t b = 0; b < nb; b++) {
             const uint32_t x = __ldg(Xh + (size_t)b * L + e);
 #pragma unroll
-            for (int o = 0; o < O; o++) a[o] = red2p(a[o] + mul_mont(x, w[o], p, pinv), p2);
+            for (int o = 0; o < O; o++) t[o] = mad_wide(x, w[o], t[o]);
+            if (++g == kTzGroup) {
+                g = 0;
+#pragma unroll
+                for (int o = 0; o < O; o++) {
+                    a[o] = red2p(a[o] + red2p(redc64(t[o], p, pinv), p2), p2);
+                    t[o] = 0;
+                }
+            }
             if (b + 1 < nb) {
 #pragma unroll
                 for (int o = O - 1; o > 0; o--) w[o] = w[o - 1];
@@ -75,7 +99,10 @@ __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__
             }
         }
 #pragma unroll
-        for (int o = 0; o < O; o++) acc[(size_t)o * L + e] = red1p(a[o], p);
+        for (int o = 0; o < O; o++) {
+            a[o] = red2p(a[o] + red2p(redc64(t[o], p, pinv), p2), p2);
+            acc[(size_t)o * L + e] = red1p(a[o], p);
+        }
     }
 }
 
