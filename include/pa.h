@@ -190,6 +190,13 @@ int pa_ctx_rekey(pa_ctx *ctx, uint64_t seed);
  * output is then undefined). */
 int pa_ctx_status(pa_ctx *ctx);
 
+/* Paper mode: consumption statistics of the last hash (SPEC.md pa_run "stats: consumed_bits,
+ * rejected_blocks"; the reload rule of PAPER.md:130,147-148): *consumed_bits = key bits up to
+ * the end of the k-th usable window, *rejected_windows = all-ones windows cast away before it.
+ * Synchronizes the context stream.  PA_E_STATE if the context is not in paper mode,
+ * PA_E_INSUFFICIENT_INPUT as pa_ctx_status.  Outputs may be NULL. */
+int pa_ctx_paper_stats(pa_ctx *ctx, uint64_t *consumed_bits, uint64_t *rejected_windows);
+
 /* Free everything the context owns; NULL is a no-op. */
 void pa_ctx_destroy(pa_ctx *ctx);
 

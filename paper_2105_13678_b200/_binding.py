@@ -79,6 +79,7 @@ pa_mmh_partial = _sig("pa_mmh_partial", i32, vp, vp, vp)
 pa_mh_merge = _sig("pa_mh_merge", i32, vp, vp, u32, vp)
 pa_ctx_destroy = _sig("pa_ctx_destroy", None, vp)
 pa_ctx_status = _sig("pa_ctx_status", i32, vp)
+pa_ctx_paper_stats = _sig("pa_ctx_paper_stats", i32, vp, ctypes.POINTER(u64), ctypes.POINTER(u64))
 pa_ctx_rekey = _sig("pa_ctx_rekey", i32, vp, u64)
 pa_ctx_query = _sig("pa_ctx_query", i32, vp, ctypes.POINTER(pa_info))
 pa_ctx_set_stream = _sig("pa_ctx_set_stream", i32, vp, vp)
@@ -99,7 +100,7 @@ pa_derive_paper_params = _sig("pa_derive_paper_params", i32, u64, ctypes.c_doubl
 EXPORTED = ["pa_ctx_create", "pa_ctx_create_ex", "pa_hash", "pa_hash_host", "pa_hash_batch", "pa_hash_host_batch", "pa_mmh_partial", "pa_mh_merge",
             "pa_ctx_destroy", "pa_ctx_status", "pa_ctx_rekey", "pa_ctx_query", "pa_ctx_set_stream", "pa_ctx_set_profiling",
             "pa_ctx_stage_times", "pa_plan", "pa_philox4x64_10", "pa_expand_a", "pa_expand_bc",
-            "pa_last_error", "pa_derive_security_coefficient", "pa_select_block_count", "pa_select_gamma",
+            "pa_last_error", "pa_ctx_paper_stats", "pa_derive_security_coefficient", "pa_select_block_count", "pa_select_gamma",
             "pa_derive_paper_params"]
 
 

@@ -1365,6 +1365,18 @@ extern "C" int pa_ctx_status(pa_ctx *c) {
     return PA_OK;
 }
 
+extern "C" int pa_ctx_paper_stats(pa_ctx *c, uint64_t *consumed_bits, uint64_t *rejected_windows) {
+    if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    if (!c->pl.paper_k) return set_err(PA_E_STATE, "paper stats: not a paper-mode context");
+    TRY(pa_ctx_status(c));                                   // synchronizes; insufficient input
+    uint64_t last = 0;
+    CUDA_TRY(cudaMemcpy(&last, c->offs + (c->pl.k - 1), 8, cudaMemcpyDeviceToHost));
+    const uint64_t consumed = last + c->pl.gamma;
+    if (consumed_bits) *consumed_bits = consumed;
+    if (rejected_windows) *rejected_windows = consumed / c->pl.gamma - c->pl.k;
+    return PA_OK;
+}
+
 extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
     if (!c || !info) return set_err(PA_E_PARAM, "NULL argument");
     memset(info, 0, sizeof *info);

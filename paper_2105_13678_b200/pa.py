@@ -132,6 +132,13 @@ class PAContext:
         mode) found fewer than paper_k usable windows."""
         B.check(B.pa_ctx_status(self._h))
 
+    def paper_stats(self) -> tuple[int, int]:
+        """pa_ctx_paper_stats: (consumed key bits, rejected all-ones windows) of the last
+        paper-mode hash (SPEC.md pa_run stats)."""
+        cb, rw = ctypes.c_uint64(), ctypes.c_uint64()
+        B.check(B.pa_ctx_paper_stats(self._h, ctypes.byref(cb), ctypes.byref(rw)))
+        return cb.value, rw.value
+
     def query(self) -> dict:
         info = B.pa_info()
         B.check(B.pa_ctx_query(self._h, ctypes.byref(info)))

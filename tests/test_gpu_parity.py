@@ -290,6 +290,8 @@ def test_paper_mode_parity(gamma, k, extra, allones):
     got = bytes(out.cpu().numpy())
     want = hashes.pa_hash_paper_seeded(key, n, gamma, k, m, seed)
     assert got == want
+    _, used = hashes.paper_blocks(key, n, gamma, k)                # windows the oracle consumed
+    assert ctx.paper_stats() == (used * gamma, used - k)
     assert bytes(ctx.hash_host(key)) == want
     ctx.close()
 
