@@ -90,6 +90,15 @@ def derive_paper_params(target_n: int, ratio: float, t: int, epsilon: float) -> 
     return dict(zip(("gamma", "k", "n", "s", "m"), (x.value for x in v)))
 
 
+def stream_partition(total_bits: int, n: int) -> tuple[int, int]:
+    """A long key stream cut into successive jobs of n bits (SURVEY.md §8(f) NEXT-3 "remainder
+    reporting"; SPEC.md pa_stream): (jobs, remainder bits).  A trailing partial job is reported
+    as the remainder, never padded (padding would break the uniform-input assumption)."""
+    if n < 1 or total_bits < 0:
+        raise ValueError("n >= 1 and total_bits >= 0 required")
+    return total_bits // n, total_bits % n
+
+
 def shard_ranges(k: int, G: int) -> list[tuple[int, int]]:
     """Rank g owns blocks [floor(k g / G), floor(k (g+1) / G))."""
     return [(k * g // G, k * (g + 1) // G) for g in range(G)]
@@ -114,6 +123,7 @@ class PAContext:
         h = ctypes.c_void_p()
         B.check(B.pa_ctx_create_ex(ctypes.byref(prm), ctypes.byref(h)))
         self._h = h
+        self.mode = "paper" if paper_k else ("mh_only" if mh_only else ("toeplitz" if toeplitz else "mmh_mh"))
         self.info = self.query()
         self.n, self.r, self.m = n, r, m
         self.gamma, self.alpha, self.k = self.info["gamma"], self.info["alpha"], self.info["k"]
@@ -329,3 +339,32 @@ def stream_gather_merge(partial_fn, merge_fn, key_slices, group=None):
 def stream_hash(ctx: PAContext, key_slices, group=None):
     """Rotating-root stream hash with a shard context (pa_mmh_partial / pa_mh_merge)."""
     return stream_gather_merge(ctx.mmh_partial, ctx.mh_merge, key_slices, group)
+
+
+def stream_pa(ctx: PAContext, key, total_bits: int, seeds=None):
+    """Privacy amplification over a long key stream (r-bit mode, n a multiple of 8): job j
+    hashes key bits [j n, (j+1) n) with the context's function, or with a fresh function
+    re-drawn from seeds[j] on the GPU (pa_ctx_rekey, NEXT-2).  Without seeds the jobs go
+    through pa_hash_batch (two buffer sets / streams).  Returns (outputs, stats) with stats
+    {jobs, consumed_bits, remainder_bits}; the remainder is reported, not hashed."""
+    n = ctx.info["n"]
+    if ctx.mode != "mmh_mh" or ctx.block_range != (0, ctx.info["k"]):
+        raise B.PAError(B.PA_E_STATE, "stream_pa: whole-key MMH-MH contexts (r-bit mode) only")
+    if n % 8:
+        raise B.PAError(B.PA_E_PARAM, "stream_pa: n must be a multiple of 8 (byte-aligned jobs)")
+    jobs, rem = stream_partition(total_bits, n)
+    key = ctx._dev_u8(key, 1)
+    nb = n // 8
+    if key.numel() < jobs * nb:
+        raise B.PAError(B.PA_E_PARAM, "stream_pa: key shorter than total_bits")
+    slices = [key[j * nb:(j + 1) * nb] for j in range(jobs)]
+    if seeds is None:
+        outs = ctx.hash_batch(slices) if jobs > 1 else [ctx.hash(sl) for sl in slices]
+    else:
+        if len(seeds) < jobs:
+            raise B.PAError(B.PA_E_PARAM, "stream_pa: one seed per job")
+        outs = []
+        for j, sl in enumerate(slices):
+            ctx.rekey(seeds[j])
+            outs.append(ctx.hash(sl))
+    return outs, {"jobs": jobs, "consumed_bits": jobs * n, "remainder_bits": rem}

@@ -186,3 +186,11 @@ def test_toeplitz_plan():
         P.plan(100, 16, 10, toeplitz=True)            # r is chosen by the planner
     with pytest.raises(B.PAError):
         P.plan(100, 0, 10, toeplitz=True, limb_bits=8)
+
+
+@pytest.mark.parametrize("total,n,jobs,rem", [
+    (2 * 1000 + 5, 1000, 2, 5),        # SPEC.md pa_stream: 2 full jobs + 5 leftover bits
+    (0, 1000, 0, 0),                   # empty input: no jobs, no remainder
+    (12, 12, 1, 0), (11, 12, 0, 11), (260_000_000 * 3 + 7, 260_000_000, 3, 7)])
+def test_stream_partition(total, n, jobs, rem):
+    assert P.stream_partition(total, n) == (jobs, rem)

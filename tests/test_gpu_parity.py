@@ -437,3 +437,26 @@ def test_many_blocks_few_units(n, r, m):
     got = bytes(ctx.hash(torch.from_numpy(key).cuda()).cpu().numpy())
     assert got == oracle_seeded(key, n, r, m, 13)
     ctx.close()
+
+
+@pytest.mark.gpu
+def test_stream_pa_jobs_and_remainder():
+    """NEXT-3 remainder reporting: a long key cut into n-bit jobs (fixed function via
+    pa_hash_batch, or a fresh function per job via pa_ctx_rekey), each job equal to the
+    oracle on its slice; the trailing partial job is reported, not hashed."""
+    from paper_2105_13678_b200.pa import stream_pa
+    PAContext = _pa()
+    n, r, m = 40_000, 1024, 3_000
+    total = 3 * n + 777
+    stream = key_bytes(total, 4242)
+    ctx = PAContext(n, r, m, seed=21)
+    outs, st = stream_pa(ctx, torch.from_numpy(stream).cuda(), total)
+    assert st == {"jobs": 3, "consumed_bits": 3 * n, "remainder_bits": 777}
+    for j, o in enumerate(outs):
+        sl = stream[j * n // 8:(j + 1) * n // 8]
+        assert bytes(o.cpu().numpy()) == oracle_seeded(sl, n, r, m, 21), j
+    outs, st = stream_pa(ctx, torch.from_numpy(stream).cuda(), total, seeds=[100, 101, 102])
+    for j, o in enumerate(outs):
+        sl = stream[j * n // 8:(j + 1) * n // 8]
+        assert bytes(o.cpu().numpy()) == oracle_seeded(sl, n, r, m, 100 + j), j
+    ctx.close()
