@@ -1303,6 +1303,9 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
 // ---- fresh hash keys per job (NEXT-2): expand a_i, b, c from `seed` on the GPU (reading
 // A7, bit-identical to pa_expand_a / pa_expand_bc) and recompute the transforms of the a_i
 // and of b.  Asynchronous on the context stream; later hashes use the new function.
+#ifndef PA_EXP_CTAS
+#define PA_EXP_CTAS 8                              // expand_keys_first CTAs per SM (full occupancy)
+#endif
 extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
     if (c->pl.toeplitz) return set_err(PA_E_STATE, "rekey: not for the Toeplitz comparator");
@@ -1318,7 +1321,7 @@ extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
     c->launches = 0;
     {
         ProfScope ps(c, "rekey_expand");
-        const uint32_t grid = (uint32_t)g_num_sms * 4;
+        const uint32_t grid = (uint32_t)g_num_sms * PA_EXP_CTAS;
         if (c->nblk) {
             CUDA_TRY(cudaMemsetAsync(c->rekey_ok, 0, (size_t)c->nblk * 4, c->stream));
             expand_keys_first<<<grid, 256, 0, c->stream>>>(seed, p.b0, p.gamma, Wa32, c->nblk, 0, c->a_words_dev,

@@ -350,7 +350,10 @@ def test_rekey_fresh_keys_on_gpu():
     # created with that seed; seed 32048 makes block 0's first gamma=17 draw all ones, so
     # the device rejection/redraw path is exercised
     PAContext = _pa()
-    for (n, r, m, s1, s2) in [(300_001, 4096, 20_000, 5, 77), (1_000, 16, 10, 9, 32048)]:
+    # gamma = 19937 (624 words per a_i, even: every vector takes the coalesced 64-bit store
+    # path of expand_keys_first) and 44497 (1391 words, odd: odd vectors store word by word)
+    for (n, r, m, s1, s2) in [(300_001, 4096, 20_000, 5, 77), (1_000, 16, 10, 9, 32048),
+                              (200_003, 16384, 30_000, 6, 78), (300_007, 32768, 50_000, 7, 79)]:
         key = key_bytes(n, s1 + s2)
         ctx = PAContext(n, r, m, seed=s1)
         kd = torch.from_numpy(key).cuda()
