@@ -1740,28 +1740,18 @@ static uint32_t group_begin(uint32_t nblk, int G, int g) {
     return (uint32_t)((nblk * cum + W / 2) / W);
 }
 
-static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
+static int grouped_copy_hash(pa_ctx *c, const uint8_t *key_host, uint8_t *key_dev, uint8_t *out_dev,
+                             uint8_t *out_host) {
+    // copy_stream is already ordered after every earlier user of key_dev
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
-    // the copies may overwrite key_dev only after earlier work on the ctx stream is done
-    CUDA_TRY(cudaEventRecord(c->copy_ev[kCopyGroups], c->stream));
-    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[kCopyGroups], 0));
     const uint32_t nblk = c->nblk;
-    // paper mode: the reload rule needs the whole key before any block offset is known;
-    // MH-only: one product over the whole key
-    const bool whole = c->pl.paper_k || c->pl.mh_only || c->pl.toeplitz;
-    const int G = whole ? 1 : (int)std::min<uint32_t>(kCopyGroups, nblk);
+    const int G = (int)std::min<uint32_t>(kCopyGroups, nblk);
     const uint64_t R = c->pl.r / 8;
     for (int g = 0; g < G; g++) {
         const uint64_t lo = G == 1 ? 0 : std::min<uint64_t>(nb, (uint64_t)group_begin(nblk, G, g) * R);
         const uint64_t hi = G == 1 ? nb : std::min<uint64_t>(nb, (uint64_t)group_begin(nblk, G, g + 1) * R);
-        if (hi > lo) CUDA_TRY(cudaMemcpyAsync(c->key_dev + lo, key_host + lo, hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
+        if (hi > lo) CUDA_TRY(cudaMemcpyAsync(key_dev + lo, key_host + lo, hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
         CUDA_TRY(cudaEventRecord(c->copy_ev[g], c->copy_stream));
-    }
-    if (whole) {
-        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_ev[0], 0));
-        TRY(hash_enqueue(c, c->key_dev, c->out_dev));
-        CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
-        return PA_OK;
     }
     c->launches = 0;
     TRY(carry_reset(c));
@@ -1769,15 +1759,34 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     for (int g = 0; g < G; g++) {
         const uint32_t v0 = group_begin(nblk, G, g), v1 = group_begin(nblk, G, g + 1);
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_ev[g], 0));
-        if (v1 > v0) TRY(mmh_forward(c, c->key_dev, v0, v1));
+        if (v1 > v0) TRY(mmh_forward(c, key_dev, v0, v1));
         if (v1 > v0) TRY(mmh_mac(c, v0, v1, first, G == 1));
         first = false;
     }
     uint32_t *y = nullptr;
     TRY(mmh_tail(c, &y));
-    TRY(run_mh(c, y, c->out_dev));
-    CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
+    TRY(run_mh(c, y, out_dev));
+    CUDA_TRY(cudaMemcpyAsync(out_host, out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
     return PA_OK;
+}
+
+static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
+    const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
+    // the copies may overwrite key_dev only after earlier work on the ctx stream is done
+    CUDA_TRY(cudaEventRecord(c->copy_ev[kCopyGroups], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[kCopyGroups], 0));
+    // paper mode: the reload rule needs the whole key before any block offset is known;
+    // MH-only: one product over the whole key
+    const bool whole = c->pl.paper_k || c->pl.mh_only || c->pl.toeplitz;
+    if (whole) {
+        CUDA_TRY(cudaMemcpyAsync(c->key_dev, key_host, nb, cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(cudaEventRecord(c->copy_ev[0], c->copy_stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_ev[0], 0));
+        TRY(hash_enqueue(c, c->key_dev, c->out_dev));
+        CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
+        return PA_OK;
+    }
+    return grouped_copy_hash(c, key_host, c->key_dev, c->out_dev, out_host);
 }
 
 // The synchronous host-buffer calls poll rather than block, so their return does not wait on
@@ -1866,6 +1875,16 @@ extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, ui
     for (uint32_t j = 0; j < count && rc == PA_OK; j++) {
         const int s = (int)(j & 1);
         if (j >= 2 && cudaStreamWaitEvent(c->copy_stream, c->hb_done[s], 0) != cudaSuccess) rc = set_err(PA_E_CUDA, "event wait failed");
+        if (rc != PA_OK) break;
+        if (j + 1 == count) {
+            // the last key: copied in block groups, its transforms starting as groups land, so
+            // only the last group's work, the tails and the D2H follow the last byte (the drain)
+            if (s) swap_bufs(c);
+            rc = grouped_copy_hash(c, keys_host[j], kbuf[s], obuf[s], outs_host[j]);
+            total += c->launches;
+            if (s) swap_bufs(c);
+            break;
+        }
         if (rc == PA_OK && cudaMemcpyAsync(kbuf[s], keys_host[j], nb, cudaMemcpyHostToDevice, c->copy_stream) != cudaSuccess)
             rc = set_err(PA_E_CUDA, "H2D copy failed");
         if (rc == PA_OK && cudaEventRecord(c->hb_copy[s], c->copy_stream) != cudaSuccess) rc = set_err(PA_E_CUDA, "event record failed");

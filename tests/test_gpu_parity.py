@@ -324,10 +324,14 @@ def test_hash_host_batch():
         ctx = PAContext(n, r, m, seed=seed)
         keys = [key_bytes(n, 200 + j) for j in range(5)]
         pinned = [torch.from_numpy(k).pin_memory() for k in keys]
-        for hk in (keys, pinned):
-            outs = ctx.hash_host_batch(hk)
-            for k, o in zip(keys, outs):
-                assert bytes(np.asarray(o)) == oracle_seeded(k, n, r, m, seed)
+        want = [oracle_seeded(k, n, r, m, seed) for k in keys]
+        # the last key of a batch is copied in block groups: last on buffer set 0 (5 keys),
+        # set 1 (2 keys) and the single-key batch
+        for cnt in (5, 2, 1):
+            for hk in (keys[:cnt], pinned[:cnt]):
+                outs = ctx.hash_host_batch(hk)
+                for w, o in zip(want, outs):
+                    assert bytes(np.asarray(o)) == w
         ctx.close()
 
 
