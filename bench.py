@@ -326,11 +326,17 @@ def main():
     key_full = key_bytes(w.n, w.key_seed)
     lo, hi = (0, w.nbytes) if paper else key_slice_bytes(w.n, w.r, (b0, b1))
     key_dev = torch.from_numpy(key_full[lo:hi].copy()).to(dev)
+    # S0 (untimed in the step): context creation -- plan, host tables, hash-key
+    # expansion and the precomputed transforms -- timed once by wall clock
+    torch.cuda.synchronize()
+    t_create = time.perf_counter()
     if paper:
         ctx = PAContext(w.n, 0, w.m, w.gamma, seed=w.hash_seed, limb_bits=args.limb_bits, paper_k=w.k)
     else:
         ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None,
                         limb_bits=args.limb_bits)
+    torch.cuda.synchronize()
+    ctx_create_ms = (time.perf_counter() - t_create) * 1e3
     info = ctx.query()
     out = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -642,6 +648,7 @@ def main():
         "stream": stream_mode if world == 1 else mr_stream,
         "comparators": comparators,
         "fresh_keys": fresh,
+        "ctx_create_ms": ctx_create_ms,
     }
     if verified is not None:
         line["verified_vs_whole_key"] = verified

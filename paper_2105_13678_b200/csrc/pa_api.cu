@@ -550,7 +550,9 @@ static int launch_row_t(const RowArgs &A0, cudaStream_t st) {
     constexpr int E_LOG = 5;
     // the inverse transforms a single vector: small CTAs (V S = 1024 words; 2048 measured
     // 21.0 vs 19.0 us for the C4 MMH inverse) give enough units
-    constexpr int V = MODE == ROW_INV ? inv_v(S_LOG) : row_v(S_LOG);
+    // ROW_STORE (precomputed transforms, comparators): half the rows of the MAC-era default
+    // (C4 re-key: 108 -> 102 us for the 372 vectors of 2^9-point rows)
+    constexpr int V = MODE == ROW_INV ? inv_v(S_LOG) : MODE == ROW_STORE ? (row_v(S_LOG) > 1 ? row_v(S_LOG) / 2 : 1) : row_v(S_LOG);
     static KInfo kis[kMaxDevices];
     KInfo &ki = kinfo_slot(kis);
     auto fn = row_pass<S_LOG, E_LOG, V, MODE>;
