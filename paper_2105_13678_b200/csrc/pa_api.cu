@@ -868,6 +868,24 @@ template <class Src>
 static int launch_pack(const Src &src, uint32_t B, uint32_t grid, const PrimeSet &pk, uint32_t P, uint32_t nvec,
                        uint32_t wxp, uint32_t *res, cudaStream_t st) {
     const int nw = B <= 56 ? 0 : (int)((B + 31) / 32);
+    const uint32_t tiles = (uint32_t)cdiv(wxp, (uint64_t)kPackL * kPackT);
+    if (nw >= 2 && nvec <= 65535 && (uint64_t)tiles * nvec >= 2ull * g_num_sms) {
+        // many vectors (re-key): kPackL limbs per thread; the single-vector MH pack keeps
+        // one limb per thread (more CTAs for its ~170 tiles)
+        const dim3 tg(tiles, nvec);
+        switch (nw) {
+            case 2: pack_residues_tiled<Src, 2><<<tg, kPackT, 0, st>>>(src, pk, P, wxp, res); break;
+            case 3: pack_residues_tiled<Src, 3><<<tg, kPackT, 0, st>>>(src, pk, P, wxp, res); break;
+            case 4: pack_residues_tiled<Src, 4><<<tg, kPackT, 0, st>>>(src, pk, P, wxp, res); break;
+            case 5: pack_residues_tiled<Src, 5><<<tg, kPackT, 0, st>>>(src, pk, P, wxp, res); break;
+            case 6: pack_residues_tiled<Src, 6><<<tg, kPackT, 0, st>>>(src, pk, P, wxp, res); break;
+            case 7: pack_residues_tiled<Src, 7><<<tg, kPackT, 0, st>>>(src, pk, P, wxp, res); break;
+            case 8: pack_residues_tiled<Src, 8><<<tg, kPackT, 0, st>>>(src, pk, P, wxp, res); break;
+            default: return set_err(PA_E_PARAM, "unsupported limb width %u", B);
+        }
+        CUDA_TRY(cudaGetLastError());
+        return PA_OK;
+    }
     switch (nw) {
         case 0: pack_residues<Src, 0><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;
         case 2: pack_residues<Src, 2><<<grid, 256, 0, st>>>(src, pk, P, nvec, wxp, res); break;

@@ -334,6 +334,32 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     store_residues_multi<NW>(res + (size_t)iv * P * wxp + j0, j0, wxp, P, any, w, ks);
 }
 
+// S1 for many word-sourced vectors (pa_ctx_rekey's a_i): CTA (tile of kPackL kPackT limbs,
+// vector blockIdx.y), kPackL limbs per thread sharing the per-prime loop (pack_key_residues'
+// scheme without the byte staging).  res layout as pack_residues.
+template <class Src, int NW>
+__global__ void __launch_bounds__(kPackT) pack_residues_tiled(const Src src, const PrimeSet ks, uint32_t P,
+                                                              uint32_t wxp, uint32_t *__restrict__ res) {
+    const uint32_t iv = blockIdx.y;
+    const uint32_t j0 = blockIdx.x * (kPackL * kPackT) + threadIdx.x;
+    if (j0 >= wxp) return;
+    uint32_t w[kPackL][NW];
+    uint32_t any = 0;
+#pragma unroll
+    for (int q = 0; q < kPackL; q++) {
+        const uint32_t j = j0 + q * kPackT;
+        if (j < wxp) {
+            src.template words<NW>(iv, j, w[q]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < NW; i++) w[q][i] = 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < NW; i++) any |= w[q][i];
+    }
+    store_residues_multi<NW>(res + (size_t)iv * P * wxp + j0, j0, wxp, P, any, w, ks);
+}
+
 // ---------------------------------------------------------------- paper mode (NEXT-1)
 // Algorithm 1 as written: gamma-bit windows t = key bits
 // [t gamma, (t+1) gamma) (MSB-first); a window equal to 2^gamma - 1 is cast
