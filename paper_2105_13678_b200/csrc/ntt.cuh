@@ -35,6 +35,7 @@ struct NttArgs {
     const uint32_t *rtw;       // round twiddles, Shoup pairs (w, floor(w 2^32/p)): [P][rtw_stride]
     uint32_t rtw_stride;
     uint32_t rtw_off[kMaxRounds];
+    uint32_t rtw_off4[kMaxRounds];   // the same pass's offsets for 16-element threads (E_LOG = 4)
     const uint32_t *ltw_lo;    // omega_L^(+-e_lo), e_lo < 2^h   (Montgomery form)
     const uint32_t *ltw_hi;    // omega_L^(+-e_hi 2^h)
     uint32_t ltw_lo_stride, ltw_hi_stride, ltw_h;

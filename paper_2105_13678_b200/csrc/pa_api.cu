@@ -471,6 +471,7 @@ static NttArgs ntt_args(const StageDev &sd, int dir, int pass /*0 col, 1 row*/, 
     a.rtw = sd.rtw;
     a.rtw_stride = sd.rtw_stride;
     for (int r = 0; r < kMaxRounds; r++) a.rtw_off[r] = sd.rtw_off[elog - 4][pass * 2 + dir][r];
+    for (int r = 0; r < kMaxRounds; r++) a.rtw_off4[r] = sd.rtw_off[0][pass * 2 + dir][r];
     a.ltw_lo = sd.ltw_lo[dir];
     a.ltw_hi = sd.ltw_hi[dir];
     a.ltw_lo_stride = sd.ltw_lo_n;
@@ -514,17 +515,35 @@ static int kinfo(F *fn, int threads, size_t smem, KInfo &ki) {
     return PA_OK;
 }
 
-template <int S_LOG, int N1_LOG, int MODE>
-static int launch_col_t(const ColArgs &A, cudaStream_t st) {
-    constexpr int E_LOG = 5;
+template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
+static int launch_col_e(const ColArgs &A0, cudaStream_t st) {
     static KInfo kis[kMaxDevices];
     KInfo &ki = kinfo_slot(kis);
     auto fn = col_pass<S_LOG, E_LOG, N1_LOG, MODE>;
     TRY(kinfo(fn, 32 * (1 << (S_LOG - E_LOG)), (size_t)(1 << S_LOG) * 32 * 4, ki));
+    ColArgs A = A0;
+    if (E_LOG == 4)
+        for (int r = 0; r < kMaxRounds; r++) A.nt.rtw_off[r] = A.nt.rtw_off4[r];
     const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
+}
+
+// A pass with few units (the single-vector MH forward and both inverses: one unit per CTA)
+// is as long as one unit takes; 16-element threads (twice the threads per column) halve
+// that.  Many-unit passes keep 32 elements per thread (fewer instructions per point).
+// Measured on C4: the MMH inverse (192 units) 20.8 -> 18.9 us with E = 16, but the MH
+// passes (352 units) slower (forward 14.8 -> 18.9 us), so only passes below 1.5 units per SM.
+#ifndef PA_COL_E4_UNITS
+#define PA_COL_E4_UNITS 3                          // E = 16 while 2 units <= this x SMs
+#endif
+template <int S_LOG, int N1_LOG, int MODE>
+static int launch_col_t(const ColArgs &A, cudaStream_t st) {
+    if constexpr (S_LOG == 8) {
+        if (2ull * A.units <= (uint64_t)PA_COL_E4_UNITS * g_num_sms) return launch_col_e<S_LOG, 4, N1_LOG, MODE>(A, st);
+    }
+    return launch_col_e<S_LOG, 5, N1_LOG, MODE>(A, st);
 }
 
 // (column log, row log) pairs the planner produces (plan_product: MMH and single-vector rules)
