@@ -535,8 +535,11 @@ template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
 #ifndef PA_COL8_MINB
 #define PA_COL8_MINB 4
 #endif
+#ifndef PA_COL8E4_MINB
+#define PA_COL8E4_MINB 2
+#endif
 __global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)),
-                                  S_LOG == 8 ? (E_LOG == 5 ? PA_COL8_MINB : 2) : (S_LOG < 8 ? 3 : 1))
+                                  S_LOG == 8 ? (E_LOG == 5 ? PA_COL8_MINB : PA_COL8E4_MINB) : (S_LOG < 8 ? 3 : 1))
 col_pass(const ColArgs A) {
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int E = SP::E;
