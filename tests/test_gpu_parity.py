@@ -90,6 +90,21 @@ def test_limb_width_invariance(B):
     assert gpu_hash(key, n, r, m, 77, limb_bits=B) == oracle_seeded(key, n, r, m, 77)
 
 
+@pytest.mark.parametrize("B", [64, 96, 168])
+def test_many_vector_pack_paths(B):
+    # 318 blocks: the a_i of context creation and of pa_ctx_rekey go through the tiled
+    # two-limbs-per-thread pack (pack_residues_tiled, >= 2 tiles per SM); the key through
+    # pack_key_residues with a ragged last block
+    n, r, m = 1_300_001, 4096, 5_000
+    key = key_bytes(n, 3 * B)
+    kd = torch.from_numpy(key).cuda()
+    ctx = _pa()(n, r, m, seed=21, limb_bits=B)
+    assert bytes(ctx.hash(kd).cpu().numpy()) == oracle_seeded(key, n, r, m, 21)
+    ctx.rekey(22)
+    assert bytes(ctx.hash(kd).cpu().numpy()) == oracle_seeded(key, n, r, m, 22)
+    ctx.close()
+
+
 @pytest.mark.parametrize("kind,pos", [("zero", 0), ("ones", 0), ("alt", 0), ("bit", 0), ("bit", 2047),
                                       ("bit", 2048), ("bit", 65_535)])
 def test_special_keys(kind, pos):
