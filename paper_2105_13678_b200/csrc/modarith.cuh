@@ -21,6 +21,8 @@ struct alignas(16) PrimeK {  // per-prime constants passed to kernels
     uint32_t pinv;         // p^{-1} mod 2^32   (Montgomery, R = 2^32)
     uint32_t r2;           // R^2 mod p         (to Montgomery form)
     uint32_t pw[8];        // 2^(32 i) mod p, i < 8 (multiword limb reduction)
+    uint32_t pw24[10];     // 2^(24 j) mod p, j < 10 (the same, over 24-bit chunks)
+    uint32_t pad_[2];
 };
 
 // All primes of a stage by value: passed as a kernel parameter, so the per-prime constants

@@ -375,6 +375,7 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cuda
         pk[i].pinv = inv;
         pk[i].r2 = (uint32_t)powmod64(2, 64, p);
         for (int w = 0; w < 8; w++) pk[i].pw[w] = (uint32_t)powmod64(2, 32ull * w, p);
+        for (int w = 0; w < 10; w++) pk[i].pw24[w] = (uint32_t)powmod64(2, 24ull * w, p);
         const uint32_t g = primitive_root(p);
         const uint32_t wf = (uint32_t)powmod64(g, (p - 1) >> lg, p);     // omega_L
         const uint32_t wi = inv_mod(wf, p);

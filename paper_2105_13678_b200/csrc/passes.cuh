@@ -159,6 +159,30 @@ __device__ __forceinline__ uint32_t limb_words_redc(const uint32_t (&w)[NW], con
     return s;
 }
 
+// The same from the limb's 24-bit chunks c_j (NC <= 10): sum_j c_j (2^(24 j) mod p) < 10 2^54
+// fits one 64-bit accumulator far below p 2^32, so a single REDC gives v 2^-32 mod p in
+// (0, 2p) -- one multiply-add per chunk and one reduction per (limb, prime), against a
+// reduction per three 32-bit words.
+template <int NW>
+__host__ __device__ constexpr int chunks24() { return (32 * NW + 23) / 24; }
+template <int NW>
+__device__ __forceinline__ void limb_chunks24(const uint32_t (&w)[NW], uint32_t (&c)[chunks24<NW>()]) {
+#pragma unroll
+    for (int j = 0; j < chunks24<NW>(); j++) {
+        const int i = (24 * j) >> 5, sh = (24 * j) & 31;
+        const uint32_t lo = w[i], hi = (i + 1 < NW) ? w[i + 1] : 0u;
+        c[j] = __funnelshift_r(lo, hi, sh) & 0xFFFFFFu;
+    }
+}
+template <int NC>
+__device__ __forceinline__ uint32_t limb_chunks_redc(const uint32_t (&c)[NC], const PrimeK &k) {
+    static_assert(NC <= 10, "pw24 holds 10 chunk weights");
+    uint64_t t = 0;
+#pragma unroll
+    for (int j = 0; j < NC; j++) t = mad_wide(c[j], k.pw24[j], t);
+    return redc64(t, k.p, k.pinv);
+}
+
 // The residues of one multiword limb modulo all P primes, stored P x wxp apart from o.
 template <int NW>
 __device__ __forceinline__ void store_residues(uint32_t *o, uint32_t wxp, uint32_t P, uint32_t any,
@@ -215,6 +239,9 @@ constexpr int kPackT = 256;
 #define PA_PACKL 2
 #endif
 constexpr int kPackL = PA_PACKL;                               // limbs per thread in pack_key_residues
+#ifndef PA_PACK_CHUNK24
+#define PA_PACK_CHUNK24 1                      // reduce limbs over 24-bit chunks (one REDC per prime)
+#endif
 // Residues of kPackL limbs (j0 + q kPackT) modulo all P primes, stored P x wxp apart.
 // A zero limb among non-zero ones reduces to p (== 0 mod p, inside the [0, 2p) range the
 // column pass takes); an all-zero set stores zeros.
@@ -228,6 +255,25 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
                 if (j0 + q * kPackT < wxp) o[q * kPackT] = 0u;
         return;
     }
+#if PA_PACK_CHUNK24
+    if constexpr (NW <= 7) {
+        constexpr int NC = chunks24<NW>();
+        uint32_t c[kPackL][NC];
+#pragma unroll
+        for (int q = 0; q < kPackL; q++) limb_chunks24<NW>(w[q], c[q]);
+#pragma unroll
+        for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
+            if (pi >= P) break;
+#pragma unroll
+            for (int q = 0; q < kPackL; q++) {
+                const uint32_t r = limb_chunks_redc<NC>(c[q], ks.k[pi]);
+                if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
+            }
+            o += wxp;
+        }
+        return;
+    }
+#endif
 #pragma unroll
     for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
         if (pi >= P) break;
