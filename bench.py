@@ -461,7 +461,8 @@ def main():
         host_out = torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory()
         for _ in range(2):
             ctx.hash_host(host_key, host_out)
-        t = []
+        t, t_copy = [], []
+        kd_probe = torch.empty_like(host_key, device=dev)
         for _ in range(max(3, args.steps // 2)):
             if not args.no_flush:
                 flush.fill_(1)
@@ -473,6 +474,13 @@ def main():
             bb.record(stream)
             bb.synchronize()
             t.append(a.elapsed_time(bb))
+            # the host link is shared with the box's other GPUs: a plain copy of the same key
+            # right after each e2e sample shows the PCIe bandwidth that sample saw
+            a.record(stream)
+            kd_probe.copy_(host_key, non_blocking=True)
+            bb.record(stream)
+            bb.synchronize()
+            t_copy.append(a.elapsed_time(bb))
         e2e_ms = statistics.median(t)
         # end-to-end stream mode: a batch of pinned host keys, H2D overlapping compute
         e2e_stream = None
@@ -509,6 +517,8 @@ def main():
                "h2d_bytes_per_step": (w.n + 7) // 8, "d2h_bytes_per_step": (w.m + 7) // 8,
                "api": "pa_hash_host (pinned host buffers, H2D + hash + D2H + sync)",
                "h2d_copy_ms": min(th2d), "d2h_copy_ms": min(td2h),
+               "samples_ms": [round(x, 4) for x in t],
+               "h2d_copy_ms_interleaved": statistics.median(t_copy),
                "h2d_gbs": (w.n + 7) // 8 / (min(th2d) * 1e-3) / 1e9}
 
     # ---- stream mode (pa_hash_batch, NEXT-3): a batch of independent keys, MH / tail of one
