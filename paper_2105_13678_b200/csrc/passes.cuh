@@ -271,18 +271,19 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
             }
             o += wxp;
         }
-        return;
-    }
+    } else
 #endif
+    {
 #pragma unroll
-    for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
-        if (pi >= P) break;
+        for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
+            if (pi >= P) break;
 #pragma unroll
-        for (int q = 0; q < kPackL; q++) {
-            const uint32_t r = limb_words_redc<NW>(w[q], ks.k[pi]);
-            if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
+            for (int q = 0; q < kPackL; q++) {
+                const uint32_t r = limb_words_redc<NW>(w[q], ks.k[pi]);
+                if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
+            }
+            o += wxp;
         }
-        o += wxp;
     }
 }
 
