@@ -347,6 +347,13 @@ def test_hash_host_batch():
                 outs = ctx.hash_host_batch(hk)
                 for w, o in zip(want, outs):
                     assert bytes(np.asarray(o)) == w
+        # pinned output buffers (the bench's e2e form), single key and batch
+        pouts = [torch.zeros(ctx.nbytes_out, dtype=torch.uint8).pin_memory() for _ in keys]
+        ctx.hash_host(pinned[0], pouts[0])
+        assert bytes(pouts[0].numpy()) == want[0]
+        ctx.hash_host_batch(pinned, pouts)
+        for w, o in zip(want, pouts):
+            assert bytes(o.numpy()) == w
         ctx.close()
 
 
