@@ -15,6 +15,8 @@ from oracle.hashes import (bits_to_field_blocks, key_blocks, mh_eval, mmh_eval,
                            pa_run_paper)
 from synth import key_bytes, special_key
 
+import philox_ref  # noqa: E402  (tests/ is on sys.path under pytest)
+
 
 # ------------------------------------------------------------------ SPEC examples
 def test_mmh_spec_examples():
@@ -81,6 +83,33 @@ def test_pa_run_matches_straight_line():
         z = ((b * y + c) % 2 ** g) // 2 ** (g - m)
         assert out == [int(ch) for ch in format(z, f"0{m}b")]
         assert consumed == pos
+
+
+@pytest.mark.parametrize("n,r,m", [(1000, 64, 50), (4096, 256, 300), (3001, 512, 520), (2048, 1024, 1)])
+def test_rbit_pa_hash_m_below_gamma_straight_line(n, r, m):
+    # The library's r-bit shape with m < gamma, where the paper fixes alpha = gamma
+    # (reading A1 reduces to it): an independent straight-line
+    # Algorithm 1 with general % and bit strings -- key bits MSB-first, zero-extended to
+    # k r bits (A3, A4), x_i the r-bit windows, y = sum a_i x_i % p,
+    # z = ((b y + c) % 2^gamma) // 2^(gamma - m), output bits MSB-first (A5).
+    pp = hashes.plan_params(n, r, m)
+    g, k = pp["gamma"], pp["k"]
+    assert m < g and pp["alpha"] == g
+    rng = random.Random(n + r + m)
+    key = bytes(rng.getrandbits(8) for _ in range((n + 7) // 8))
+    p = 2 ** g - 1
+    a = [rng.randrange(p) for _ in range(k)]
+    b, c = rng.getrandbits(g) | 1, rng.getrandbits(g)
+    bits = "".join(format(byte, "08b") for byte in key)[:n].ljust(k * r, "0")
+    xs = [int(bits[i * r:(i + 1) * r], 2) for i in range(k)]
+    y = sum(ai * xi for ai, xi in zip(a, xs)) % p
+    z = ((b * y + c) % 2 ** g) // 2 ** (g - m)
+    zb = format(z, f"0{m}b").ljust(-(-m // 8) * 8, "0")
+    want = bytes(int(zb[8 * t:8 * t + 8], 2) for t in range(len(zb) // 8))
+    assert hashes.pa_hash(key, n, r, m, g, a, b, c) == want
+    # and the seeded entry point uses alpha = gamma for b and c
+    a2, b2, c2 = seeds.expand_hash_keys(11, k, g, g)
+    assert hashes.pa_hash_seeded(key, n, r, m, 11) == hashes.pa_hash(key, n, r, m, g, a2, b2, c2)
 
 
 # ---------------------------------------------------------- brute-force universality
@@ -187,6 +216,48 @@ def test_seed_expansion_contract():
     # raw Philox words, little-endian, masked: numpy stream key (seed, i)
     w = np.random.Philox(key=np.array([1234, 3], dtype=np.uint64)).random_raw(2)
     assert a[3] == (int(w[0]) | (int(w[1]) << 64)) & ((1 << 89) - 1)
+
+
+def test_philox_stream_equals_written_out_definition():
+    # numpy.random.Philox (the oracle's generator, reading A7) against Philox4x64-10 written
+    # out from its definition (tests/philox_ref.py), on the stream keys the oracle uses:
+    # a_i (seed, i), b (seed, 2^63), c (seed, 2^63 + 1), and a key with every bit set
+    for key in [(0, 0), (1234, 3), (0x5EED0004, seeds.STREAM_B), (0x5EED0004, seeds.STREAM_C),
+                (2**64 - 1, 2**64 - 1)]:
+        want = philox_ref.stream_words(*key, 11)
+        assert [int(v) for v in seeds._philox(*key).random_raw(11)] == want
+
+
+@pytest.mark.parametrize("seed,alpha", [(0x5EED0001, 104_858), (0x5EED0004, 26_000_000 // 1000),
+                                        (7, 1), (7, 64), (7, 65), (2**64 - 1, 200)])
+def test_expand_b_c_pinned_to_reference_streams(seed, alpha):
+    # PAPER.md:142 "b, c in Z_{2^gamma}, gcd(b,2) = 1"; reading A7: b = draw of stream
+    # (seed, 2^63) with bit 0 forced, c = draw of stream (seed, 2^63 + 1) as drawn.  The
+    # words come from the written-out Philox, not from numpy, so a key-conversion slip
+    # (2^63 + 1 rounded to 2^63 gives c the stream of b) fails here.
+    nw = (alpha + 63) // 64
+    b_ref = philox_ref.draw(philox_ref.stream_words(seed, 1 << 63, nw), alpha) | 1
+    c_ref = philox_ref.draw(philox_ref.stream_words(seed, (1 << 63) + 1, nw), alpha)
+    assert seeds.expand_b(seed, alpha) == b_ref
+    assert seeds.expand_c(seed, alpha) == c_ref
+    if alpha >= 64:
+        # the two streams differ (c is not b's stream with bit 0 as drawn)
+        assert c_ref != philox_ref.draw(philox_ref.stream_words(seed, 1 << 63, nw), alpha)
+
+
+def test_expand_a_pinned_to_reference_stream():
+    # a_i: ceil(gamma/64) words of stream (seed, i), all-ones rejected
+    for seed, i, g in [(99, 0, 89), (99, 30, 521), (2**63, 5, 4423), (5, 1, 3)]:
+        ws = philox_ref.stream_words(seed, i, 64 * ((g + 63) // 64))
+        nw = (g + 63) // 64
+        allones = (1 << g) - 1
+        t = 0
+        while True:
+            v = philox_ref.draw(ws[t * nw:(t + 1) * nw], g)
+            t += 1
+            if v != allones:
+                break
+        assert seeds.expand_a(seed, i, g) == v
 
 
 def test_seed_rejection_of_all_ones():
