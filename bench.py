@@ -176,16 +176,35 @@ def stage_ops(info: dict, stage: str) -> float:
     return 0.0
 
 
+def int_peak(peaks: dict, nsm: int = 148) -> tuple[float, str, dict]:
+    """The integer roofline denominator in Gop/s (int32 lane-ops).  Measured: the Shoup
+    butterfly mix of microbench/int_peak.cu (6 SASS instructions, 3 FMA-pipe + 3 ALU-pipe),
+    in lane-ops per SM per clock on a B200, x SMs x sm_max_mhz (profiles/int_peak.json).
+    Fallback: the issue model, 1 warp-instruction per clock per SMSP."""
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    try:
+        ip = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))
+        per_clk = float(ip["ops"]["shoup_butterfly"]["lane_ops_per_sm_clk"])
+        pipes = {k: round(v["lane_ops_per_sm_clk"], 2) for k, v in ip["ops"].items()}
+        return (per_clk * ip.get("sms", nsm) * sm_mhz * 1e6 / 1e9,
+                f"measured: Shoup butterfly mix {per_clk:.1f} lane-ops/SM/clk (microbench/int_peak.cu on "
+                f"{ip.get('gpu', 'B200')}, profiles/int_peak.json) x {ip.get('sms', nsm)} SMs x {sm_mhz:.0f} MHz",
+                pipes)
+    except Exception:
+        return (nsm * 4 * 32 * sm_mhz * 1e6 / 1e9,
+                f"issue model (no profiles/int_peak.json): {nsm} SMs x 4 SMSP x 32 lanes x 1 instr/clk x "
+                f"{sm_mhz:.0f} MHz", {})
+
+
 def roofline(info: dict, stages: dict, peaks: dict, steps: int) -> dict:
-    """Dominant kernel stage -> achieved int32 Gop/s vs the issue-rate peak.
+    """Dominant kernel stage -> achieved int32 Gop/s vs the measured integer peak.
     `stages` maps stage -> (ms per step, launches per step), from CUDA events recorded
     on the context stream around each launch (pa_ctx_set_profiling)."""
     name, (ms, cnt) = max(stages.items(), key=lambda kv: kv[1][0])
     per_launch_ms = ms / max(cnt, 1)
     ops = stage_ops(info, name)
-    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    nsm = 148
-    peak = nsm * 4 * 32 * sm_mhz * 1e6 / 1e9          # Gop/s: 1 warp-instr/clk/SMSP x 32 lanes
+    peak, note, pipes = int_peak(peaks)
+    issue_peak = 148 * 4 * 32 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
     achieved = ops / (per_launch_ms * 1e-3) / 1e9 if ops else None
     traffic = None
     try:
@@ -196,9 +215,10 @@ def roofline(info: dict, stages: dict, peaks: dict, steps: int) -> dict:
     share = ms / sum(v[0] for v in stages.values())
     return {"bound": "alu", "kernel": name, "achieved": achieved, "peak": peak, "unit": "Gop/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "ms_per_launch": per_launch_ms, "share_of_step": share,
-            "peak_note": f"int32 lane-ops: {nsm} SMs x 4 SMSP x 32 lanes x 1 instr/clk x {sm_mhz:.0f} MHz "
-                         "(B300_MICROARCH.md issue model; IMAD and ALU pipes each half rate)"}
+            "ms_per_launch": per_launch_ms, "share_of_step": share, "peak_source": note,
+            "issue_model_peak": issue_peak,
+            "issue_model_frac": (achieved / issue_peak) if achieved else None,
+            "measured_lane_ops_per_sm_clk": pipes}
 
 
 # --------------------------------------------------------------------------- CPU oracle
@@ -384,7 +404,7 @@ def main():
         ctx = PAContext(w.n, 0, w.m, w.gamma, seed=w.hash_seed, limb_bits=args.limb_bits, paper_k=w.k)
     else:
         ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None,
-                        limb_bits=args.limb_bits)
+                        limb_bits=args.limb_bits, throughput_only=True)
     torch.cuda.synchronize()
     ctx_create_ms = (time.perf_counter() - t_create) * 1e3
     info = ctx.query()
@@ -405,7 +425,7 @@ def main():
         res = distributed_hash(ctx, key_dev)
         torch.cuda.synchronize()
         if rank == 0:
-            whole = PAContext(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits)
+            whole = PAContext(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits, throughput_only=True)
             ref = torch.empty(whole.nbytes_out, dtype=torch.uint8, device=dev)
             whole.hash(torch.from_numpy(key_full).to(dev), ref)
             torch.cuda.synchronize()
@@ -464,7 +484,7 @@ def main():
         if args.verify:
             ok = torch.ones(1, dtype=torch.int32, device=dev)
             for j, o in outs_j.items():
-                whole = PAContext(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits)
+                whole = PAContext(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits, throughput_only=True)
                 ref = torch.empty(whole.nbytes_out, dtype=torch.uint8, device=dev)
                 whole.hash(torch.from_numpy(roll_slice(j)).to(dev), ref)
                 torch.cuda.synchronize()

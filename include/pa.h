@@ -85,6 +85,11 @@ typedef struct {
                                   pa_mmh_partial / pa_mh_merge call */
     uint32_t launches_total; /* kernel launches enqueued since creation (mod 2^32),
                                 precompute included */
+    uint32_t insecure_length; /* 1 when m >= gamma (MMH-MH contexts): alpha = m > gamma and
+                                 the output is longer than the gamma bits of entropy y can
+                                 carry -- a throughput configuration, security-vacuous
+                                 (PAPER.md:143 requires gamma > beta; reading A1).  strict
+                                 contexts reject it instead. */
 } pa_info;
 
 typedef struct {

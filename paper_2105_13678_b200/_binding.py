@@ -45,7 +45,8 @@ class pa_stage_plan(ctypes.Structure):
 class pa_info(ctypes.Structure):
     _fields_ = [("n", u64), ("r", u64), ("m", u64), ("gamma", u64), ("alpha", u64), ("k", u64),
                 ("block_begin", u64), ("block_end", u64), ("mmh", pa_stage_plan), ("mh", pa_stage_plan),
-                ("device_bytes", u64), ("kernels_per_hash", u32), ("launches_total", u32)]
+                ("device_bytes", u64), ("kernels_per_hash", u32), ("launches_total", u32),
+                ("insecure_length", u32)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("mmh", "mh")}

@@ -486,7 +486,9 @@ static NttArgs ntt_args(const StageDev &sd, int dir, int pass /*0 col, 1 row*/, 
 }
 
 // ====================================================================== launchers
-static int g_num_sms = 0;
+// SM count of the device the current pa_* call runs on: set per call by DevGuard from the
+// context (a process may drive several GPUs), read by the launchers for grid sizing
+static thread_local int g_num_sms = 0;
 
 struct KInfo {
     int threads = 0;
@@ -727,6 +729,7 @@ struct HashBufs {
 struct pa_ctx {
     Plan pl{};
     int device = 0;
+    int num_sms = 0;                          // SMs of `device` (grid sizing)
     cudaStream_t stream = nullptr;
     DevAlloc da;
     StageDev smmh, smh;
@@ -779,6 +782,24 @@ struct pa_ctx {
     uint32_t bgraph_launches = 0;
 };
 static constexpr int kCarrySlots = 8;
+
+// Every pa_* call on a context runs on the context's device: the guard makes it current
+// (restoring the caller's device on return) and selects its SM count for the launchers.
+struct DevGuard {
+    int prev = -1;
+    bool switched = false;
+    explicit DevGuard(const pa_ctx *c) {
+        if (!c) return;
+        g_num_sms = c->num_sms;
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != c->device && cudaSetDevice(c->device) == cudaSuccess)
+            switched = true;
+    }
+    ~DevGuard() {
+        if (switched) cudaSetDevice(prev);
+    }
+    DevGuard(const DevGuard &) = delete;
+    DevGuard &operator=(const DevGuard &) = delete;
+};
 
 // exchange the active per-hash buffers (and stream) with the alternate set
 static void swap_bufs(pa_ctx *c) {
@@ -1270,6 +1291,7 @@ extern "C" int pa_plan(const pa_params *prm, pa_info *info) {
         info->n = p.n; info->r = p.r; info->m = p.m; info->gamma = p.gamma; info->alpha = p.alpha;
         info->k = p.k; info->block_begin = p.b0; info->block_end = p.b1;
         info->mmh = p.mmh; info->mh = p.mh;
+        info->insecure_length = (!p.mh_only && !p.toeplitz && p.m >= p.gamma) ? 1u : 0u;
         const uint64_t nb = p.b1 - p.b0;
         info->device_bytes = 4ull * (3 * nb + 3) * p.mmh.nprimes * (1ull << p.mmh.log2_len) +
                              4ull * 5 * p.mh.nprimes * (1ull << p.mh.log2_len);
@@ -1288,10 +1310,11 @@ extern "C" int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out) {
     c->stream = (cudaStream_t)prm->stream;
     int rc = PA_OK;
     if (cudaGetDevice(&c->device) != cudaSuccess) rc = set_err(PA_E_CUDA, "no CUDA device");
-    if (rc == PA_OK && !g_num_sms) {
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, c->device) != cudaSuccess) rc = set_err(PA_E_CUDA, "cudaGetDeviceProperties failed");
-        else g_num_sms = prop.multiProcessorCount;
+    if (rc == PA_OK) {
+        int nsm = 0;
+        if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || nsm <= 0)
+            rc = set_err(PA_E_CUDA, "cudaDeviceGetAttribute(multiProcessorCount) failed");
+        c->num_sms = g_num_sms = nsm;
     }
     if (rc == PA_OK) rc = ctx_alloc_and_precompute(c, prm);
     if (rc != PA_OK) {
@@ -1314,6 +1337,7 @@ extern "C" pa_ctx *pa_ctx_create(uint64_t n, uint64_t r, uint64_t m, uint64_t p,
 
 extern "C" void pa_ctx_destroy(pa_ctx *c) {
     if (!c) return;
+    DevGuard dg_(c);
     cudaStreamSynchronize(c->stream);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->evpool) cudaEventDestroy(e);
@@ -1348,6 +1372,7 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
 #endif
 extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    DevGuard dg_(c);
     if (c->pl.toeplitz) return set_err(PA_E_STATE, "rekey: not for the Toeplitz comparator");
     const Plan &p = c->pl;
     const uint32_t Wa32 = (uint32_t)cdiv(p.gamma, 32), Wal32 = (uint32_t)cdiv(p.alpha, 32);
@@ -1400,6 +1425,7 @@ extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
 
 extern "C" int pa_ctx_status(pa_ctx *c) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    DevGuard dg_(c);
     uint32_t st = 0;
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemcpy(&st, c->status, 4, cudaMemcpyDeviceToHost));
@@ -1410,6 +1436,7 @@ extern "C" int pa_ctx_status(pa_ctx *c) {
 
 extern "C" int pa_ctx_paper_stats(pa_ctx *c, uint64_t *consumed_bits, uint64_t *rejected_windows) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    DevGuard dg_(c);
     if (!c->pl.paper_k) return set_err(PA_E_STATE, "paper stats: not a paper-mode context");
     TRY(pa_ctx_status(c));                                   // synchronizes; insufficient input
     uint64_t last = 0;
@@ -1427,6 +1454,7 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
     info->n = p.n; info->r = p.r; info->m = p.m; info->gamma = p.gamma; info->alpha = p.alpha;
     info->k = p.k; info->block_begin = p.b0; info->block_end = p.b1;
     info->mmh = p.mmh; info->mh = p.mh;
+    info->insecure_length = (!p.mh_only && !p.toeplitz && p.m >= p.gamma) ? 1u : 0u;
     info->device_bytes = c->da.bytes;
     info->kernels_per_hash = c->launches;
     info->launches_total = c->launches_total;
@@ -1435,6 +1463,7 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
 
 extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    DevGuard dg_(c);
     if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
     if (c->hgraph_exec) { cudaGraphExecDestroy(c->hgraph_exec); c->hgraph_exec = nullptr; }
     if (c->bgraph_exec) { cudaGraphExecDestroy(c->bgraph_exec); c->bgraph_exec = nullptr; }
@@ -1627,6 +1656,7 @@ static bool graphs_enabled(const pa_ctx *c) {
 
 extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     if (!c || !key_bits || !out_bits) return set_err(PA_E_PARAM, "NULL argument");
+    DevGuard dg_(c);
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     if (!graphs_enabled(c)) {
         const int rc = hash_enqueue(c, key_bits, out_bits);
@@ -1656,6 +1686,7 @@ extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
 
 extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
     if (!c || !key_slice || !y_out) return set_err(PA_E_PARAM, "NULL argument");
+    DevGuard dg_(c);
     if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     c->launches = 0;
     TRY(carry_reset(c));
@@ -1669,6 +1700,7 @@ extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_o
 
 extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits) {
     if (!c || !y_parts || !out_bits || G == 0) return set_err(PA_E_PARAM, "bad argument");
+    DevGuard dg_(c);
     if (G > (1u << 24)) return set_err(PA_E_PARAM, "too many parts");
     if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     c->launches = 0;
@@ -1729,6 +1761,7 @@ static int batch_enqueue(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *
 
 extern "C" int pa_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
     if (!c || (count && (!keys || !outs))) return set_err(PA_E_PARAM, "NULL argument");
+    DevGuard dg_(c);
     if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     for (uint32_t j = 0; j < count; j++)
@@ -1829,6 +1862,16 @@ static int hash_host_enqueue(pa_ctx *c, const uint8_t *key_host, uint8_t *out_ho
     return grouped_copy_hash(c, key_host, c->key_dev, c->out_dev, out_host);
 }
 
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory?
+static bool host_pinned(const void *p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();                               // clear the sticky-free error state
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 // The synchronous host-buffer calls poll rather than block, so their return does not wait on
 // a thread wake-up (cudaStreamSynchronize may yield under the default scheduling heuristic).
 static int stream_poll(cudaStream_t st, const char *what) {
@@ -1840,6 +1883,7 @@ static int stream_poll(cudaStream_t st, const char *what) {
 
 extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
     if (!c || !key_host || !out_host) return set_err(PA_E_PARAM, "NULL argument");
+    DevGuard dg_(c);
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
     if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
@@ -1848,7 +1892,9 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
         CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
     }
-    if (!graphs_enabled(c)) {
+    // copies from / to pageable host memory synchronise with the host, which stream capture
+    // forbids: such buffers take the direct (uncaptured) path
+    if (!graphs_enabled(c) || !host_pinned(key_host) || !host_pinned(out_host)) {
         const int rc = hash_host_enqueue(c, key_host, out_host);
         c->launches_total += c->launches;
         TRY(rc);
@@ -1884,6 +1930,7 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
 extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, uint8_t *const *outs_host,
                                   uint32_t count) {
     if (!c || (count && (!keys_host || !outs_host))) return set_err(PA_E_PARAM, "NULL argument");
+    DevGuard dg_(c);
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     if (c->pl.paper_k || c->pl.mh_only || c->pl.toeplitz)
         return set_err(PA_E_STATE, "paper mode / comparators: use pa_hash_host per key");
@@ -1949,12 +1996,14 @@ extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, ui
 
 extern "C" int pa_ctx_set_profiling(pa_ctx *c, int enable) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    DevGuard dg_(c);
     c->prof = enable != 0;
     return PA_OK;
 }
 
 extern "C" int pa_ctx_stage_times(pa_ctx *c, const char **names, double *ms, uint32_t *launches, int max) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
+    DevGuard dg_(c);
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     for (auto &r : c->recs) {
         float t = 0;

@@ -7,10 +7,15 @@ handle"; SPEC.md:161 split-merge) is host logic and lives here too.
 from __future__ import annotations
 
 import ctypes
+import warnings
 
 import numpy as np
 
 from . import _binding as B
+
+
+class InsecureLengthWarning(UserWarning):
+    """m >= gamma: the output is longer than its entropy (reading A1)."""
 
 
 def _words(v: int, bits: int) -> np.ndarray:
@@ -110,7 +115,8 @@ class PAContext:
 
     def __init__(self, n: int, r: int, m: int, gamma: int = 0, seed: int = 0, *,
                  block_range=None, a=None, b=None, c=None, stream=None, limb_bits: int = 0,
-                 strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False):
+                 strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False,
+                 throughput_only: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise B.PAError(B.PA_E_CUDA, "no CUDA device: the library has no CPU path")
@@ -131,6 +137,12 @@ class PAContext:
         self.nbytes_in = (n + 7) // 8
         self.nbytes_out = (m + 7) // 8
         self.y_words = (self.gamma + 31) // 32
+        self.insecure_length = bool(self.info.get("insecure_length", 0))
+        if self.insecure_length and not throughput_only:
+            warnings.warn(f"m = {m} >= gamma = {self.gamma}: alpha = m and the output is longer than the "
+                          "gamma bits of entropy y carries (security-vacuous, reading A1; PAPER.md:143 needs "
+                          "gamma > m).  Pass strict=True to reject, throughput_only=True to silence.",
+                          InsecureLengthWarning, stacklevel=2)
 
     # ------------------------------------------------------------------ queries
     def rekey(self, seed: int) -> None:
@@ -204,32 +216,55 @@ class PAContext:
         B.check(B.pa_hash_batch(self._h, kp, op, len(keys)))
         return outs
 
+    def _host_u8(self, buf, nbytes: int, what: str, writable: bool = False) -> int:
+        """Pointer of a host buffer the C call reads (keys) or writes (outputs): a CPU uint8
+        torch tensor or numpy array, C-contiguous, with at least ``nbytes`` bytes.  Anything
+        else is rejected -- never converted, so no pointer to a temporary copy reaches C."""
+        torch = self._torch
+        if isinstance(buf, torch.Tensor):
+            if buf.device.type != "cpu":
+                raise ValueError(f"{what}: expected a host (CPU) tensor, got {buf.device}")
+            if buf.dtype != torch.uint8 or not buf.is_contiguous():
+                raise ValueError(f"{what}: expected a contiguous uint8 tensor")
+            if buf.numel() < nbytes:
+                raise ValueError(f"{what}: {buf.numel()} bytes, need {nbytes}")
+            return buf.data_ptr()
+        if isinstance(buf, np.ndarray):
+            if buf.dtype != np.uint8 or not buf.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"{what}: expected a C-contiguous uint8 numpy array")
+            if writable and not buf.flags["WRITEABLE"]:
+                raise ValueError(f"{what}: array is read-only")
+            if buf.size < nbytes:
+                raise ValueError(f"{what}: {buf.size} bytes, need {nbytes}")
+            return buf.ctypes.data
+        raise ValueError(f"{what}: expected a uint8 numpy array or CPU torch tensor, got {type(buf).__name__}")
+
     def hash_host_batch(self, keys_host, outs_host=None):
         """pa_hash_host_batch: host keys (numpy uint8 / pinned torch CPU tensors) -> host
         outputs, H2D of key j overlapping the hash of key j-1.  Synchronous."""
-        torch = self._torch
-
-        def ptr(x):
-            return x.data_ptr() if isinstance(x, torch.Tensor) else np.ascontiguousarray(x).ctypes.data
-        keys_host = [k if isinstance(k, torch.Tensor) else np.ascontiguousarray(k, dtype=np.uint8) for k in keys_host]
+        keys_host = list(keys_host)
         if outs_host is None:
             outs_host = [np.zeros(self.nbytes_out, dtype=np.uint8) for _ in keys_host]
-        kp = (ctypes.c_void_p * len(keys_host))(*[ptr(k) for k in keys_host])
-        op = (ctypes.c_void_p * len(outs_host))(*[ptr(o) for o in outs_host])
+        outs_host = list(outs_host)
+        if len(outs_host) != len(keys_host):
+            raise ValueError("keys and outs differ in length")
+        kp = (ctypes.c_void_p * len(keys_host))(
+            *[self._host_u8(k, self.nbytes_in, f"key {j}") for j, k in enumerate(keys_host)])
+        op = (ctypes.c_void_p * len(outs_host))(
+            *[self._host_u8(o, self.nbytes_out, f"output {j}", True) for j, o in enumerate(outs_host)])
         B.check(B.pa_hash_host_batch(self._h, kp, op, len(keys_host)))
         return outs_host
 
     def hash_host(self, key_host, out_host=None):
-        """pa_hash_host: host buffers (numpy uint8 / pinned torch CPU tensor), synchronous."""
-        torch = self._torch
-        if isinstance(key_host, torch.Tensor):
-            kp = key_host.data_ptr()
-        else:
-            key_host = np.ascontiguousarray(key_host, dtype=np.uint8)
-            kp = key_host.ctypes.data
+        """pa_hash_host: host buffers (numpy uint8 / pinned torch CPU tensor), synchronous.
+        Pageable buffers work (the library then skips graph capture); pinned ones give full
+        PCIe bandwidth."""
+        if isinstance(key_host, (bytes, bytearray)):
+            key_host = np.frombuffer(bytes(key_host), dtype=np.uint8)
+        kp = self._host_u8(key_host, self.nbytes_in, "key")
         if out_host is None:
             out_host = np.zeros(self.nbytes_out, dtype=np.uint8)
-        op = out_host.data_ptr() if isinstance(out_host, torch.Tensor) else out_host.ctypes.data
+        op = self._host_u8(out_host, self.nbytes_out, "output", True)
         B.check(B.pa_hash_host(self._h, ctypes.c_void_p(kp), ctypes.c_void_p(op)))
         return out_host
 

@@ -194,3 +194,40 @@ def test_toeplitz_plan():
     (12, 12, 1, 0), (11, 12, 0, 11), (260_000_000 * 3 + 7, 260_000_000, 3, 7)])
 def test_stream_partition(total, n, jobs, rem):
     assert P.stream_partition(total, n) == (jobs, rem)
+
+
+def test_insecure_length_flag():
+    # reading A1: m >= gamma is accepted (alpha = m) but flagged; strict rejects it
+    assert P.plan(260_000_000, 1 << 23, 26_000_000)["insecure_length"] == 1     # C4: m > gamma
+    assert P.plan(10_485_760, 1 << 20, 1_048_576)["insecure_length"] == 0       # C2: m < gamma
+    assert P.plan(4096, 4096, 4423)["insecure_length"] == 1                     # m == gamma
+
+
+def _host_checker():
+    import torch
+    ctx = P.PAContext.__new__(P.PAContext)      # the argument checks only (no GPU)
+    ctx._torch = torch
+    return ctx, torch
+
+
+def test_host_buffer_checks_reject_bad_buffers():
+    # pa_hash_host reads ceil(n/8) and writes ceil(m/8) bytes through raw
+    # pointers, so short, strided, non-uint8, read-only or device buffers must be rejected
+    ctx, torch = _host_checker()
+    ok = np.zeros(100, np.uint8)
+    assert ctx._host_u8(ok, 100, "key") == ok.ctypes.data
+    assert ctx._host_u8(torch.zeros(100, dtype=torch.uint8), 64, "key") > 0
+    bad = [np.zeros(99, np.uint8),                       # short
+           np.zeros(200, np.uint8)[::2],                 # strided
+           np.zeros(100, np.uint16),                     # wrong dtype
+           torch.zeros(200, dtype=torch.uint8)[::2],     # non-contiguous tensor
+           torch.zeros(100, dtype=torch.int32),          # wrong tensor dtype
+           [0] * 100]                                    # not a buffer
+    for b in bad:
+        with pytest.raises(ValueError):
+            ctx._host_u8(b, 100, "buf")
+    ro = np.zeros(100, np.uint8)
+    ro.flags.writeable = False
+    assert ctx._host_u8(ro, 100, "key") > 0              # a key may be read-only
+    with pytest.raises(ValueError):
+        ctx._host_u8(ro, 100, "out", writable=True)      # an output may not

@@ -489,3 +489,43 @@ def test_stream_pa_jobs_and_remainder():
         sl = stream[j * n // 8:(j + 1) * n // 8]
         assert bytes(o.cpu().numpy()) == oracle_seeded(sl, n, r, m, 100 + j), j
     ctx.close()
+
+
+def test_hash_host_pageable_buffers_on_user_stream():
+    # on a non-default stream pa_hash_host is captured as a CUDA graph; copies
+    # from pageable (numpy) memory cannot be captured, so those buffers take the direct path
+    PAContext = _pa()
+    n, r, m, seed = 300_001, 4096, 20_000, 23
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = PAContext(n, r, m, seed=seed)
+        for ks in (7, 8):
+            key = key_bytes(n, ks)
+            out = np.zeros((m + 7) // 8, np.uint8)
+            ctx.hash_host(key, out)                                       # numpy key and output
+            assert bytes(out) == oracle_seeded(key, n, r, m, seed)
+            o2 = ctx.hash_host_batch([key, key_bytes(n, ks + 10)])       # pageable batch
+            assert bytes(o2[0]) == oracle_seeded(key, n, r, m, seed)
+            assert bytes(o2[1]) == oracle_seeded(key_bytes(n, ks + 10), n, r, m, seed)
+        # pinned key, pageable output and the reverse
+        hk = torch.from_numpy(key_bytes(n, 9)).pin_memory()
+        o3 = ctx.hash_host(hk, np.zeros((m + 7) // 8, np.uint8))
+        ho = torch.empty((m + 7) // 8, dtype=torch.uint8).pin_memory()
+        ctx.hash_host(key_bytes(n, 9), ho)
+        assert bytes(o3) == bytes(ho.numpy()) == oracle_seeded(key_bytes(n, 9), n, r, m, seed)
+        ctx.close()
+
+
+def test_context_on_other_current_device_is_used():
+    # every call runs on the context's device and the caller's current device is
+    # restored (on a one-GPU box this checks the guard is transparent)
+    PAContext = _pa()
+    n, r, m, seed = 100_003, 1024, 5_000, 3
+    key = key_bytes(n, 4)
+    ctx = PAContext(n, r, m, seed=seed)
+    dev_before = torch.cuda.current_device()
+    out = ctx.hash(torch.from_numpy(key).cuda())
+    torch.cuda.synchronize()
+    assert torch.cuda.current_device() == dev_before
+    assert bytes(out.cpu().numpy()) == oracle_seeded(key, n, r, m, seed)
+    ctx.close()
