@@ -23,9 +23,10 @@ constexpr int kIters = 4096;
 
 enum Op { OP_IMAD, OP_IMAD_WIDE, OP_IMAD_HI, OP_IADD3, OP_LOP3, OP_SHF, OP_PRMT, OP_VIADDMNMX,
           OP_MIX_IMAD_IADD3, OP_BFLY, OP_COUNT };
-static const char *kNames[OP_COUNT] = {"IMAD", "IMAD.WIDE.U32", "IMAD.HI.U32", "IADD3", "LOP3", "SHF", "PRMT",
+static const char *kNames[OP_COUNT] = {"IMAD", "mad.wide.u32 chain step (IMAD.WIDE.U32 + IADD3 + IADD3.X/IMAD.X)", "IMAD.HI.U32", "IADD3", "LOP3", "SHF", "PRMT",
                                        "VIADDMNMX", "IMAD+IADD3 1:1", "shoup_butterfly"};
-// lane-operations (SASS instructions x 32 lanes / 32) per chain step
+// lane-operations (SASS instructions x 32 lanes / 32) per chain step; the mad.wide.u32 step
+// is counted as one (ptxas emits it as IMAD.WIDE.U32 with a zero addend plus a 64-bit add)
 static const int kInstrPerStep[OP_COUNT] = {1, 1, 1, 1, 1, 1, 1, 1, 2, 6};
 
 template <int OP>
