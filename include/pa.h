@@ -31,8 +31,10 @@
  * with respect to the host, pa_hash_host is synchronous.
  *
  * Ownership: the context owns its precomputed transforms and scratch (device
- * memory allocated with cudaMalloc on the device current at creation); the
- * caller owns every key / output buffer passed in.
+ * memory from pa_params.dev_alloc, default cudaMallocAsync on the context stream,
+ * on the device current at creation); the caller owns every key / output buffer
+ * passed in.  Every call on a context runs on the context's device (the caller's
+ * current device is restored on return).
  */
 #ifndef PA_H_
 #define PA_H_
@@ -52,6 +54,7 @@ extern "C" {
 #define PA_E_NOMEM              -4   /* device or host allocation failed */
 #define PA_E_CUDA               -5   /* a CUDA runtime call or kernel failed */
 #define PA_E_STATE              -6   /* call not valid for this context (e.g. shard) */
+#define PA_E_NCCL               -7   /* NCCL unavailable or an NCCL call failed (world >= 1) */
 
 typedef struct pa_ctx pa_ctx;
 
@@ -90,6 +93,13 @@ typedef struct {
                                  carry -- a throughput configuration, security-vacuous
                                  (PAPER.md:143 requires gamma > beta; reading A1).  strict
                                  contexts reject it instead. */
+    int32_t  world;          /* multi-GPU contexts: ranks sharing each key, else 0 */
+    int32_t  rank;           /* this context's rank in [0, world) */
+    uint64_t acc_words;      /* words of one transform-domain accumulator (pa_mmh_acc):
+                                mmh.nprimes * 2^mmh.log2_len */
+    uint32_t graph_captures; /* CUDA-graph captures since creation (new pointer sets) */
+    uint32_t graph_updates;  /* ... of which updated an executable graph in place */
+    uint32_t graph_instantiations;
 } pa_info;
 
 typedef struct {
@@ -134,6 +144,30 @@ typedef struct {
      * (n < 2^29).  pa_query reports r, k = ceil(n/r) input blocks, alpha = ceil(m/r) output
      * blocks and the transform in `mmh`.  pa_hash / pa_hash_host only. */
     uint64_t toeplitz;
+    /* Multi-GPU (SURVEY.md §8(b,e); MMH splits over blocks, "split and separately
+     * handle"): world >= 1 makes the context rank `rank` of a `world`-rank job
+     * hashing every key together.  Each rank owns blocks [floor(k rank / world),
+     * floor(k (rank+1) / world)) (block_begin/block_end must be 0 or exactly that range) and
+     * the transforms of its own a_i; every rank plans the transform for all k blocks, so the
+     * partial sums are compatible.  The ranks' transform-domain accumulators
+     * sum_{i in shard} X_i (.) A_i are summed by ONE ncclReduce to the key's root, which
+     * alone runs the inverse transform, CRT, carries, the Mersenne fold and MH.
+     * nccl_id: the ncclUniqueId bytes from pa_nccl_unique_id() on one rank, given to all.
+     * Creation is collective (every rank must call pa_ctx_create_ex; it blocks until all
+     * ranks joined).  world = 1 is a one-rank communicator (the same code path).  NCCL is
+     * loaded at run time (libnccl.so.2; PA_NCCL_LIB overrides); failures -> PA_E_NCCL.
+     * Not available with paper_k, mh_only or toeplitz. */
+    int32_t world;
+    int32_t rank;
+    uint8_t nccl_id[128];
+    /* Device memory of the context (precomputed transforms and scratch): dev_alloc(bytes,
+     * stream, alloc_user) -> 256-byte aligned pointer or NULL, dev_free(ptr, bytes, stream,
+     * alloc_user) at pa_ctx_destroy -- e.g. PyTorch's caching allocator (the Python binding
+     * passes torch.cuda.caching_allocator_alloc / _delete).  NULL: cudaMallocAsync /
+     * cudaFreeAsync on the context stream (the device's default memory pool). */
+    void *(*dev_alloc)(size_t bytes, void *stream, void *user);
+    void (*dev_free)(void *ptr, size_t bytes, void *stream, void *user);
+    void *alloc_user;
 } pa_params;
 
 /* Create a context on the current CUDA device.  `p` is the Mersenne EXPONENT
@@ -148,8 +182,12 @@ int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out);
 
 /* Hash one key.  key_bits: DEVICE pointer to ceil(n/8) bytes (bits >= n ignored).
  * For a shard context it points to the shard's slice: key bytes
- * [block_begin*r/8, min(block_end*r/8, ceil(n/8))) -- and pa_hash then fails with
- * PA_E_STATE: shards use pa_mmh_partial + pa_mh_merge.
+ * [block_begin*r/8, min(block_end*r/8, ceil(n/8))).  A shard context without world
+ * (block_begin/block_end only) fails with PA_E_STATE: it hashes through pa_mmh_partial +
+ * pa_mh_merge or pa_mmh_acc + pa_tail_merge (host-side exchange).  A multi-GPU context
+ * (world >= 1) runs S1-S3 on its blocks, one ncclReduce of the transform-domain
+ * accumulators to rank 0, and S4-S7 on rank 0: out_bits is written on rank 0 only (other
+ * ranks may pass NULL); every rank must call pa_hash for every key, in the same order.
  * out_bits: DEVICE pointer to ceil(m/8) bytes (written MSB-first, pad bits 0).
  * Asynchronous on the context stream. */
 int pa_hash(pa_ctx *ctx, const uint8_t *key_bits, uint8_t *out_bits);
@@ -160,6 +198,10 @@ int pa_hash(pa_ctx *ctx, const uint8_t *key_bits, uint8_t *out_bits);
  * back into the context stream), so one key's latency-bound MH / tail kernels overlap the
  * next key's MMH transforms.  The first call allocates the second buffer set (about the
  * per-hash scratch of pa_ctx_query's device_bytes minus the precomputed transforms).
+ * Multi-GPU contexts (world >= 1): the root rotates -- key j is reduced to and finished on
+ * rank j mod world (SPEC.md:235-243 pa_stream), so every rank
+ * computes 1/world of every key's MMH and the tail + MH of every world-th key; outs[j] is
+ * written on rank j mod world only (NULL allowed elsewhere).  All ranks pass the same count.
  * Asynchronous on the context stream; outputs are identical to count pa_hash calls. */
 int pa_hash_batch(pa_ctx *ctx, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count);
 
@@ -183,6 +225,24 @@ int pa_mmh_partial(pa_ctx *ctx, const uint8_t *key_slice, uint32_t *y_out);
 /* Stages S6-S7: y = sum_{g<G} y_parts[g] mod p (each part ceil(gamma/32) words,
  * DEVICE, contiguous), then MH into out_bits (DEVICE, ceil(m/8) bytes). */
 int pa_mh_merge(pa_ctx *ctx, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits);
+
+/* Transform-domain split of S1-S7 with a caller-side exchange (any transport; the
+ * single-GPU validation of the multi-GPU path).
+ * pa_mmh_acc: S1-S3 on this context's blocks -> acc_out (DEVICE, pa_info.acc_words
+ *   32-bit words) = sum_{i in shard} NTT(x_i) (.) NTT(a_i), prime by prime, each word
+ *   canonical (< its prime), in the transform's internal order.  Any context with the
+ *   same (n, r, m, gamma, limb_bits) produces the same layout (shards plan for all k
+ *   blocks), and the sum of the parts over a partition of the blocks is the whole key's.
+ * pa_tail_merge: S4-S7 from G such accumulators (DEVICE, contiguous, G * acc_words
+ *   words): their sum mod each prime is inverse-transformed, CRT-recombined, carried,
+ *   folded mod p and hashed by MH into out_bits (DEVICE, ceil(m/8) bytes).  Both
+ *   asynchronous on the context stream; no NCCL involved. */
+int pa_mmh_acc(pa_ctx *ctx, const uint8_t *key_slice, uint32_t *acc_out);
+int pa_tail_merge(pa_ctx *ctx, const uint32_t *acc_parts, uint32_t G, uint8_t *out_bits);
+
+/* A fresh ncclUniqueId (128 bytes) for pa_params.nccl_id: call on one rank and broadcast
+ * the bytes to the others (e.g. torch.distributed).  PA_E_NCCL if NCCL cannot be loaded. */
+int pa_nccl_unique_id(uint8_t *id_out);
 
 /* Fresh hash keys per job: re-draw a_i, b, c from `seed` on the
  * GPU (reading A7; bit-identical to pa_expand_a / pa_expand_bc and to a context created

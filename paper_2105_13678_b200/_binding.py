@@ -26,8 +26,9 @@ PA_E_BOUND = -3
 PA_E_NOMEM = -4
 PA_E_CUDA = -5
 PA_E_STATE = -6
+PA_E_NCCL = -7
 _CODES = {0: "PA_OK", -1: "PA_E_PARAM", -2: "PA_E_INSUFFICIENT_INPUT", -3: "PA_E_BOUND",
-          -4: "PA_E_NOMEM", -5: "PA_E_CUDA", -6: "PA_E_STATE"}
+          -4: "PA_E_NOMEM", -5: "PA_E_CUDA", -6: "PA_E_STATE", -7: "PA_E_NCCL"}
 
 u64, u32, i32, vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_void_p
 
@@ -46,7 +47,8 @@ class pa_info(ctypes.Structure):
     _fields_ = [("n", u64), ("r", u64), ("m", u64), ("gamma", u64), ("alpha", u64), ("k", u64),
                 ("block_begin", u64), ("block_end", u64), ("mmh", pa_stage_plan), ("mh", pa_stage_plan),
                 ("device_bytes", u64), ("kernels_per_hash", u32), ("launches_total", u32),
-                ("insecure_length", u32)]
+                ("insecure_length", u32), ("world", i32), ("rank", i32), ("acc_words", u64),
+                ("graph_captures", u32), ("graph_updates", u32), ("graph_instantiations", u32)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("mmh", "mh")}
@@ -55,12 +57,19 @@ class pa_info(ctypes.Structure):
         return d
 
 
+# device allocator callbacks of pa_params (void *alloc(size_t, void *stream, void *user);
+# void free(void *, size_t, void *stream, void *user))
+DEV_ALLOC = ctypes.CFUNCTYPE(vp, ctypes.c_size_t, vp, vp)
+DEV_FREE = ctypes.CFUNCTYPE(None, vp, ctypes.c_size_t, vp, vp)
+
+
 class pa_params(ctypes.Structure):
     _fields_ = [("n", u64), ("r", u64), ("m", u64), ("gamma", u64), ("seed", u64),
                 ("block_begin", u64), ("block_end", u64),
                 ("a_words", vp), ("b_words", vp), ("c_words", vp),
                 ("stream", vp), ("limb_bits", i32), ("strict", i32), ("paper_k", u64), ("mh_only", u64),
-                ("toeplitz", u64)]
+                ("toeplitz", u64), ("world", i32), ("rank", i32), ("nccl_id", ctypes.c_uint8 * 128),
+                ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE), ("alloc_user", vp)]
 
 
 def _sig(name, res, *args):
@@ -78,6 +87,9 @@ pa_hash_batch = _sig("pa_hash_batch", i32, vp, ctypes.POINTER(vp), ctypes.POINTE
 pa_hash_host_batch = _sig("pa_hash_host_batch", i32, vp, ctypes.POINTER(vp), ctypes.POINTER(vp), u32)
 pa_mmh_partial = _sig("pa_mmh_partial", i32, vp, vp, vp)
 pa_mh_merge = _sig("pa_mh_merge", i32, vp, vp, u32, vp)
+pa_mmh_acc = _sig("pa_mmh_acc", i32, vp, vp, vp)
+pa_tail_merge = _sig("pa_tail_merge", i32, vp, vp, u32, vp)
+pa_nccl_unique_id = _sig("pa_nccl_unique_id", i32, vp)
 pa_ctx_destroy = _sig("pa_ctx_destroy", None, vp)
 pa_ctx_status = _sig("pa_ctx_status", i32, vp)
 pa_ctx_paper_stats = _sig("pa_ctx_paper_stats", i32, vp, ctypes.POINTER(u64), ctypes.POINTER(u64))
@@ -102,7 +114,7 @@ EXPORTED = ["pa_ctx_create", "pa_ctx_create_ex", "pa_hash", "pa_hash_host", "pa_
             "pa_ctx_destroy", "pa_ctx_status", "pa_ctx_rekey", "pa_ctx_query", "pa_ctx_set_stream", "pa_ctx_set_profiling",
             "pa_ctx_stage_times", "pa_plan", "pa_philox4x64_10", "pa_expand_a", "pa_expand_bc",
             "pa_last_error", "pa_ctx_paper_stats", "pa_derive_security_coefficient", "pa_select_block_count", "pa_select_gamma",
-            "pa_derive_paper_params"]
+            "pa_derive_paper_params", "pa_mmh_acc", "pa_tail_merge", "pa_nccl_unique_id"]
 
 
 class PAError(RuntimeError):

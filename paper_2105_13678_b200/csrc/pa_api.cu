@@ -34,6 +34,8 @@
 #include "passes.cuh"
 #include "rekey.cuh"
 #include "toeplitz.cuh"
+#include "exchange.cuh"
+#include "nccl_dl.h"
 
 using namespace pa;
 
@@ -57,6 +59,13 @@ static int set_err(int code, const char *fmt, ...) {
         if (_e != cudaSuccess)                                                              \
             return set_err(PA_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
                            __FILE__, __LINE__);                                             \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                      \
+    do {                                                                                    \
+        const ncclResult_t r_ = (expr);                                                     \
+        if (r_ != ncclSuccess)                                                              \
+            return set_err(PA_E_NCCL, "%s: %s", #expr, pa::nccl_api().GetErrorString(r_));  \
     } while (0)
 
 #define TRY(expr)                      \
@@ -141,6 +150,7 @@ struct Plan {
     uint64_t toeplitz;       // comparator: Toeplitz-hashing PA (tz_nb input, tz_no output blocks of r bits)
     uint64_t tz_nb, tz_no;
     int strict, force_B;
+    int world, rank;         // multi-GPU context (world >= 1): NCCL rank of a world-rank job
     pa_stage_plan mmh, mh;
 };
 
@@ -157,7 +167,13 @@ static int make_plan(const pa_params *prm, Plan *P) {
     p.paper_k = prm->paper_k;
     p.mh_only = prm->mh_only;
     p.toeplitz = prm->toeplitz;
+    p.world = prm->world;
+    p.rank = prm->rank;
     if (p.n < 1) return set_err(PA_E_PARAM, "n must be >= 1");
+    if (p.world < 0 || (p.world > 0 && (p.rank < 0 || p.rank >= p.world)) || (p.world == 0 && p.rank != 0))
+        return set_err(PA_E_PARAM, "multi-GPU: need 0 <= rank < world (got rank %d, world %d)", p.rank, p.world);
+    if (p.world > 0 && (p.paper_k || p.mh_only || p.toeplitz))
+        return set_err(PA_E_PARAM, "multi-GPU contexts hash in r-bit mode (no paper_k, mh_only or toeplitz)");
     if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
     if (p.toeplitz) {
         // comparator: Toeplitz-hashing PA, r x r blocks, one prime
@@ -248,10 +264,22 @@ static int make_plan(const pa_params *prm, Plan *P) {
     p.alpha = std::max<uint64_t>(g, p.m);
     p.k = (p.n + p.r - 1) / p.r;
     p.b0 = prm->block_begin; p.b1 = prm->block_end;
+    if (p.world > 0) {
+        // rank g owns blocks [floor(k g / G), floor(k (g+1) / G))
+        if ((uint64_t)p.world > p.k) return set_err(PA_E_PARAM, "multi-GPU: world %d > k = %llu blocks", p.world, (unsigned long long)p.k);
+        const uint64_t s0 = p.k * (uint64_t)p.rank / (uint64_t)p.world, s1 = p.k * (uint64_t)(p.rank + 1) / (uint64_t)p.world;
+        if ((p.b0 || p.b1) && (p.b0 != s0 || p.b1 != s1))
+            return set_err(PA_E_PARAM, "multi-GPU: block range must be 0 or [%llu, %llu) for rank %d of %d",
+                           (unsigned long long)s0, (unsigned long long)s1, p.rank, p.world);
+        p.b0 = s0; p.b1 = s1;
+    }
     if (p.b0 == 0 && p.b1 == 0) p.b1 = p.k;
     if (p.b0 >= p.b1 || p.b1 > p.k) return set_err(PA_E_PARAM, "bad shard [%llu, %llu) of %llu blocks",
                                                   (unsigned long long)p.b0, (unsigned long long)p.b1, (unsigned long long)p.k);
-    if (plan_product(p.r, p.gamma, p.b1 - p.b0, p.force_B, p.b1 - p.b0, &p.mmh) != PA_OK)
+    // every shard plans the transform of the whole key (all k blocks in the coefficient bound,
+    // the whole key's split): the transform-domain accumulators of the shards are then
+    // compatible and their sum is the whole key's (pa_mmh_acc, multi-GPU reduce)
+    if (plan_product(p.r, p.gamma, p.k, p.force_B, p.k, &p.mmh) != PA_OK)
         return set_err(PA_E_BOUND, "no transform plan covers the MMH coefficient bound");
     if (plan_product(p.gamma, p.alpha, 1, p.force_B, 1, &p.mh) != PA_OK)
         return set_err(PA_E_BOUND, "no transform plan covers the MH product");
@@ -277,23 +305,50 @@ struct StageDev {
     CrtK crt{};
 };
 
+// Device memory of a context: the caller's allocator (pa_params.dev_alloc / dev_free, e.g.
+// PyTorch's caching allocator) or the stream-ordered cudaMallocAsync / cudaFreeAsync on the
+// context stream (the device's default memory pool).
 struct DevAlloc {
-    std::vector<void *> ptrs;
+    struct Blk {
+        void *p;
+        size_t bytes;
+    };
+    std::vector<Blk> blks;
     uint64_t bytes = 0;
+    cudaStream_t stream = nullptr;
+    void *(*fn_alloc)(size_t, void *, void *) = nullptr;
+    void (*fn_free)(void *, size_t, void *, void *) = nullptr;
+    void *user = nullptr;
     template <class T>
     int alloc(T **p, size_t count) {
         void *q = nullptr;
-        const size_t b = std::max<size_t>(count * sizeof(T), 16);
-        cudaError_t e = cudaMalloc(&q, b);
-        if (e != cudaSuccess) return set_err(PA_E_NOMEM, "cudaMalloc(%zu) failed: %s", b, cudaGetErrorString(e));
-        ptrs.push_back(q);
+        const size_t b = (std::max<size_t>(count * sizeof(T), 16) + 255) & ~(size_t)255;
+        if (fn_alloc) {
+            q = fn_alloc(b, (void *)stream, user);
+            if (!q) return set_err(PA_E_NOMEM, "dev_alloc(%zu) returned NULL", b);
+            if ((uintptr_t)q & 15) {
+                if (fn_free) fn_free(q, b, (void *)stream, user);
+                return set_err(PA_E_PARAM, "dev_alloc returned a pointer that is not 16-byte aligned");
+            }
+        } else {
+            cudaError_t e = cudaMallocAsync(&q, b, stream);
+            if (e != cudaSuccess) return set_err(PA_E_NOMEM, "cudaMallocAsync(%zu) failed: %s", b, cudaGetErrorString(e));
+        }
+        blks.push_back({q, b});
         bytes += b;
         *p = (T *)q;
         return PA_OK;
     }
     void free_all() {
-        for (void *q : ptrs) cudaFree(q);
-        ptrs.clear();
+        for (const Blk &k : blks) {
+            if (fn_alloc) {
+                if (fn_free) fn_free(k.p, k.bytes, (void *)stream, user);
+            } else {
+                cudaFreeAsync(k.p, stream);
+            }
+        }
+        if (!fn_alloc && !blks.empty()) cudaStreamSynchronize(stream);
+        blks.clear();
         bytes = 0;
     }
 };
@@ -726,6 +781,21 @@ struct HashBufs {
     cudaStream_t stream = nullptr;
 };
 
+// A captured CUDA graph of one call shape.  The graph is keyed on the pointers the call
+// bakes into kernel arguments; a call with new pointers re-captures (host work only) and
+// updates the executable graph in place (cudaGraphExecUpdate: same topology, new kernel
+// parameters) instead of re-instantiating it.  Counters: pa_info.graph_*.
+struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<const void *> key;
+    uint32_t launches = 0;
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+        key.clear();
+    }
+};
+
 struct pa_ctx {
     Plan pl{};
     int device = 0;
@@ -754,12 +824,13 @@ struct pa_ctx {
     uint32_t *tz_scale = nullptr;             // Toeplitz: [R, L^-1 R^2] (ROW_STORE scales of x and e')
     uint8_t *key_dev = nullptr;               // staging for pa_hash_host
     cudaStream_t copy_stream = nullptr;       // pa_hash_host H2D copies
-    cudaGraphExec_t graph_exec = nullptr;     // captured pa_hash (graphs_enabled)
-    const void *graph_key = nullptr, *graph_out = nullptr;
-    uint32_t graph_launches = 0;
-    cudaGraphExec_t hgraph_exec = nullptr;    // captured pa_hash_host
-    const void *hgraph_key = nullptr, *hgraph_out = nullptr;
-    uint32_t hgraph_launches = 0;
+    GraphSlot g_hash, g_host, g_batch;        // captured pa_hash / pa_hash_host / pa_hash_batch
+    GraphSlot g_mg_pre[2], g_mg_post[2];      // multi-GPU, per buffer set: S1-S3 + export; S4-S7 (root)
+    // multi-GPU (pa_params.world >= 1): the NCCL communicator and, per buffer set, the
+    // exported accumulator (send) and the reduced sum (recv; significant on the root)
+    ncclComm_t comm = nullptr;
+    bool x_u64 = false;                       // reduce 64-bit words (world * max prime >= 2^32)
+    void *xsend[2] = {}, *xrecv[2] = {};
     cudaEvent_t copy_ev[9] = {};
     uint8_t *out_dev = nullptr;
     uint8_t *key_dev2 = nullptr, *out_dev2 = nullptr;   // pa_hash_host_batch second staging set
@@ -768,6 +839,7 @@ struct pa_ctx {
     uint32_t mac_slots = 1;           // accumulator slots of the last MMH row MAC (mac_grid)
     uint32_t launches = 0;            // launches of the current / last hash call
     uint32_t launches_total = 0;      // since creation
+    uint32_t graph_captures = 0, graph_updates = 0, graph_instantiations = 0;
     bool prof = false;
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> evpool;
@@ -777,9 +849,6 @@ struct pa_ctx {
     HashBufs alt;
     size_t res_words = 0;
     cudaEvent_t bev[2] = {};
-    cudaGraphExec_t bgraph_exec = nullptr;
-    std::vector<const void *> bgraph_ptrs;
-    uint32_t bgraph_launches = 0;
 };
 static constexpr int kCarrySlots = 8;
 
@@ -1002,15 +1071,17 @@ static int stage_mac(pa_ctx *c, StageDev &sd, uint32_t nvec, const uint32_t *scr
 }
 
 // ---- S4: one inverse transform of acc (in place, natural order, canonical residues)
-static int stage_inverse(pa_ctx *c, StageDev &sd, uint32_t *acc, const char *tag, uint32_t nslot = 1) {
+// src (default acc): nslot slots src_stride words apart (default P L), each < 4p, summed
+static int stage_inverse(pa_ctx *c, StageDev &sd, uint32_t *acc, const char *tag, uint32_t nslot = 1,
+                         const uint32_t *src = nullptr, uint64_t src_stride = 0) {
     const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
     const uint32_t P = sd.pl.nprimes;
     ProfScope ps(c, tag);
     RowArgs R{};
     R.nt = ntt_args(sd, 1, 1);
-    R.src = acc;
+    R.src = src ? src : acc;
     R.nsrc = nslot;
-    R.src_stride = P * sd.L;
+    R.src_stride = src_stride ? (uint32_t)src_stride : P * sd.L;
     R.dst = acc;
     R.tw4 = sd.tw4i;
     R.nvec = 1;
@@ -1120,7 +1191,7 @@ static int toeplitz_alloc_and_precompute(pa_ctx *c) {
     std::vector<uint32_t> dw;
     TRY(expand_words(p.seed, kStreamT, nd, dw, false));
     uint32_t *dw_dev = nullptr;
-    CUDA_TRY(cudaMalloc(&dw_dev, dw.size() * 4));
+    CUDA_TRY(cudaMallocAsync(&dw_dev, dw.size() * 4, c->stream));
     CUDA_TRY(cudaMemcpyAsync(dw_dev, dw.data(), dw.size() * 4, cudaMemcpyHostToDevice, c->stream));
     const uint64_t tot = (uint64_t)ne * L;
     toeplitz_pack_diag<<<(uint32_t)std::min<uint64_t>(cdiv(tot, 256), (uint64_t)g_num_sms * 16), 256, 0,
@@ -1128,7 +1199,7 @@ static int toeplitz_alloc_and_precompute(pa_ctx *c) {
     int rc = cudaGetLastError() == cudaSuccess ? PA_OK : set_err(PA_E_CUDA, "toeplitz_pack_diag launch failed");
     if (rc == PA_OK) rc = tz_forward(c, c->res, ne, sd.pl.n_col, c->ahat, c->tz_scale + 1, "pre_col", "pre_row");
     const cudaError_t e = cudaStreamSynchronize(c->stream);
-    cudaFree(dw_dev);
+    cudaFreeAsync(dw_dev, c->stream);
     if (rc != PA_OK) return rc;
     if (e != cudaSuccess) return set_err(PA_E_CUDA, "Toeplitz precompute failed: %s", cudaGetErrorString(e));
     return PA_OK;
@@ -1266,8 +1337,8 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
         }
     }
     uint32_t *a_dev = nullptr, *b_dev = nullptr;
-    CUDA_TRY(cudaMalloc(&a_dev, std::max<size_t>(aw.size() * 4, 16)));
-    CUDA_TRY(cudaMalloc(&b_dev, Wal32 * 4));
+    CUDA_TRY(cudaMallocAsync(&a_dev, std::max<size_t>(aw.size() * 4, 16), c->stream));
+    CUDA_TRY(cudaMallocAsync(&b_dev, Wal32 * 4, c->stream));
     CUDA_TRY(cudaMemcpyAsync(a_dev, aw.data(), aw.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(b_dev, bw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->c_words, cw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
@@ -1276,8 +1347,8 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     WordSrc wsb{b_dev, (uint32_t)Wal32, Bh, (uint32_t)cdiv(p.alpha, Bh)};
     if (rc == PA_OK) rc = precompute_hat(c, c->smh, wsb, 1, rows_b, c->scratch_mh, c->bhat);
     cudaError_t e = cudaStreamSynchronize(c->stream);
-    cudaFree(a_dev);
-    cudaFree(b_dev);
+    cudaFreeAsync(a_dev, c->stream);
+    cudaFreeAsync(b_dev, c->stream);
     if (rc != PA_OK) return rc;
     if (e != cudaSuccess) return set_err(PA_E_CUDA, "precompute failed: %s", cudaGetErrorString(e));
     return PA_OK;
@@ -1292,12 +1363,16 @@ extern "C" int pa_plan(const pa_params *prm, pa_info *info) {
         info->k = p.k; info->block_begin = p.b0; info->block_end = p.b1;
         info->mmh = p.mmh; info->mh = p.mh;
         info->insecure_length = (!p.mh_only && !p.toeplitz && p.m >= p.gamma) ? 1u : 0u;
+        info->world = p.world; info->rank = p.rank;
+        info->acc_words = (uint64_t)p.mmh.nprimes << p.mmh.log2_len;
         const uint64_t nb = p.b1 - p.b0;
         info->device_bytes = 4ull * (3 * nb + 3) * p.mmh.nprimes * (1ull << p.mmh.log2_len) +
                              4ull * 5 * p.mh.nprimes * (1ull << p.mh.log2_len);
     }
     return PA_OK;
 }
+
+static int mg_init(pa_ctx *c, const pa_params *prm);
 
 extern "C" int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out) {
     if (!out) return set_err(PA_E_PARAM, "out is NULL");
@@ -1316,7 +1391,13 @@ extern "C" int pa_ctx_create_ex(const pa_params *prm, pa_ctx **out) {
             rc = set_err(PA_E_CUDA, "cudaDeviceGetAttribute(multiProcessorCount) failed");
         c->num_sms = g_num_sms = nsm;
     }
+    c->da.stream = c->stream;
+    c->da.fn_alloc = prm->dev_alloc;
+    c->da.fn_free = prm->dev_free;
+    c->da.user = prm->alloc_user;
+    if (rc == PA_OK && (!prm->dev_alloc) != (!prm->dev_free)) rc = set_err(PA_E_PARAM, "dev_alloc and dev_free go together");
     if (rc == PA_OK) rc = ctx_alloc_and_precompute(c, prm);
+    if (rc == PA_OK && p.world > 0) rc = mg_init(c, prm);
     if (rc != PA_OK) {
         cudaStreamSynchronize(c->stream);
         c->da.free_all();
@@ -1339,25 +1420,22 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     if (!c) return;
     DevGuard dg_(c);
     cudaStreamSynchronize(c->stream);
+    if (c->comm) nccl_api().CommDestroy(c->comm);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->evpool) cudaEventDestroy(e);
-    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
-    if (c->hgraph_exec) cudaGraphExecDestroy(c->hgraph_exec);
-    if (c->bgraph_exec) cudaGraphExecDestroy(c->bgraph_exec);
+    for (GraphSlot *g : {&c->g_hash, &c->g_host, &c->g_batch, &c->g_mg_pre[0], &c->g_mg_pre[1], &c->g_mg_post[0],
+                         &c->g_mg_post[1]})
+        g->reset();
     if (c->alt_ready) {
         cudaStreamSynchronize(c->alt.stream);
         cudaStreamDestroy(c->alt.stream);
         for (auto e : c->bev) cudaEventDestroy(e);
     }
-    if (c->key_dev) cudaFree(c->key_dev);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
         for (auto e : c->copy_ev) if (e) cudaEventDestroy(e);
         cudaStreamDestroy(c->copy_stream);
     }
-    if (c->out_dev) cudaFree(c->out_dev);
-    if (c->key_dev2) cudaFree(c->key_dev2);
-    if (c->out_dev2) cudaFree(c->out_dev2);
     for (auto e : c->hb_copy) if (e) cudaEventDestroy(e);
     for (auto e : c->hb_done) if (e) cudaEventDestroy(e);
     c->da.free_all();
@@ -1381,7 +1459,7 @@ extern "C" int pa_ctx_rekey(pa_ctx *c, uint64_t seed) {
         TRY(c->da.alloc(&c->b_words_dev, Wal32));
         TRY(c->da.alloc(&c->rekey_ok, (size_t)c->nblk + 2));
     }
-    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+    c->g_hash.reset();
     const uint32_t launches0 = c->launches;
     c->launches = 0;
     {
@@ -1455,7 +1533,12 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
     info->k = p.k; info->block_begin = p.b0; info->block_end = p.b1;
     info->mmh = p.mmh; info->mh = p.mh;
     info->insecure_length = (!p.mh_only && !p.toeplitz && p.m >= p.gamma) ? 1u : 0u;
+    info->world = p.world; info->rank = p.rank;
+    info->acc_words = (p.mh_only || p.toeplitz) ? 0 : (uint64_t)p.mmh.nprimes << p.mmh.log2_len;
     info->device_bytes = c->da.bytes;
+    info->graph_captures = c->graph_captures;
+    info->graph_updates = c->graph_updates;
+    info->graph_instantiations = c->graph_instantiations;
     info->kernels_per_hash = c->launches;
     info->launches_total = c->launches_total;
     return PA_OK;
@@ -1464,10 +1547,11 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
 extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
     DevGuard dg_(c);
-    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
-    if (c->hgraph_exec) { cudaGraphExecDestroy(c->hgraph_exec); c->hgraph_exec = nullptr; }
-    if (c->bgraph_exec) { cudaGraphExecDestroy(c->bgraph_exec); c->bgraph_exec = nullptr; }
+    for (GraphSlot *g : {&c->g_hash, &c->g_host, &c->g_batch, &c->g_mg_pre[0], &c->g_mg_pre[1], &c->g_mg_post[0],
+                         &c->g_mg_post[1]})
+        g->reset();
     c->stream = (cudaStream_t)stream;
+    c->da.stream = c->stream;
     return PA_OK;
 }
 
@@ -1562,10 +1646,13 @@ static int mmh_mac(pa_ctx *c, uint32_t v0, uint32_t v1, bool first, bool only, b
                      zero);
 }
 
-// ---- S4+S5 after all blocks are accumulated -> canonical y
-static int mmh_tail(pa_ctx *c, uint32_t **y_out) {
+// ---- S4+S5 after all blocks are accumulated -> canonical y.  The accumulator is c->acc
+// (c->mac_slots slots) unless src is given: nsrc slots src_stride words apart, each < 4p
+// (the merged accumulators of several shards)
+static int mmh_tail(pa_ctx *c, uint32_t **y_out, const uint32_t *src = nullptr, uint32_t nsrc = 0,
+                    uint64_t src_stride = 0) {
     const Plan &p = c->pl;
-    TRY(stage_inverse(c, c->smmh, c->acc, "mmh_inverse", c->mac_slots));
+    TRY(stage_inverse(c, c->smmh, c->acc, "mmh_inverse", src ? nsrc : c->mac_slots, src, src_stride));
     {
         ProfScope ps(c, "mmh_crt_carry_fold");
         TRY(launch_crt_carry<true>(c->acc, c->smmh, (uint32_t)c->ncoef_mmh, p.gamma, nullptr, 0, c->coef, c->y1,
@@ -1576,8 +1663,8 @@ static int mmh_tail(pa_ctx *c, uint32_t **y_out) {
     return PA_OK;
 }
 
-// ---- S1-S5 on this ctx's blocks -> canonical y in the returned buffer (Wg words)
-static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
+// ---- S1-S3 on this ctx's blocks -> transform-domain accumulator c->acc (c->mac_slots slots)
+static int run_mmh_acc(pa_ctx *c, const uint8_t *key_slice) {
     // accumulators zeroed first: the chain pack -> col -> row_mac is back-to-back kernels
     {
         const uint32_t P = c->pl.mmh.nprimes;
@@ -1588,7 +1675,12 @@ static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
         CUDA_TRY(cudaMemsetAsync(c->acc, 0, (size_t)nslot * P * c->smmh.L * 4, c->stream));
     }
     TRY(mmh_forward(c, key_slice, 0, c->nblk));
-    TRY(mmh_mac(c, 0, c->nblk, true, true, false));
+    return mmh_mac(c, 0, c->nblk, true, true, false);
+}
+
+// ---- S1-S5 on this ctx's blocks -> canonical y in the returned buffer (Wg words)
+static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
+    TRY(run_mmh_acc(c, key_slice));
     return mmh_tail(c, y_out);
 }
 
@@ -1654,34 +1746,64 @@ static bool graphs_enabled(const pa_ctx *c) {
     return !off && c->stream != nullptr && !c->prof;
 }
 
-extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
-    if (!c || !key_bits || !out_bits) return set_err(PA_E_PARAM, "NULL argument");
-    DevGuard dg_(c);
-    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
-    if (!graphs_enabled(c)) {
-        const int rc = hash_enqueue(c, key_bits, out_bits);
-        c->launches_total += c->launches;
-        return rc;
-    }
-    if (!c->graph_exec || c->graph_key != key_bits || c->graph_out != out_bits) {
-        if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set);
+static int mg_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count);
+
+// Enqueue `enqueue()` on the context stream through the graph slot `gs` (captured once per
+// pointer key, updated in place for new pointers) or directly when graphs are off.
+template <class F>
+static int graph_run(pa_ctx *c, GraphSlot &gs, const std::vector<const void *> &key, F &&enqueue) {
+    if (!graphs_enabled(c)) return enqueue();
+    if (!gs.exec || key != gs.key) {
         cudaGraph_t g = nullptr;
         CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        const int rc = hash_enqueue(c, key_bits, out_bits);
+        const int rc = enqueue();
         const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
-        if (rc != PA_OK) { if (g) cudaGraphDestroy(g); return rc; }
+        if (rc != PA_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
         if (e != cudaSuccess) return set_err(PA_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
-        const cudaError_t e2 = cudaGraphInstantiate(&c->graph_exec, g, 0);
+        c->graph_captures++;
+        bool updated = false;
+        if (gs.exec) {
+            cudaGraphExecUpdateResultInfo info{};
+            if (cudaGraphExecUpdate(gs.exec, g, &info) == cudaSuccess) {
+                updated = true;
+                c->graph_updates++;
+            } else {
+                cudaGetLastError();
+                gs.reset();
+            }
+        }
+        if (!updated) {
+            const cudaError_t e2 = cudaGraphInstantiate(&gs.exec, g, 0);
+            if (e2 != cudaSuccess) {
+                gs.exec = nullptr;
+                cudaGraphDestroy(g);
+                return set_err(PA_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2));
+            }
+            c->graph_instantiations++;
+        }
         cudaGraphDestroy(g);
-        if (e2 != cudaSuccess) { c->graph_exec = nullptr; return set_err(PA_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2)); }
-        c->graph_key = key_bits;
-        c->graph_out = out_bits;
-        c->graph_launches = c->launches;
+        gs.key = key;
+        gs.launches = c->launches;
     }
-    CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream));
-    c->launches = c->graph_launches;
-    c->launches_total += c->launches;
+    CUDA_TRY(cudaGraphLaunch(gs.exec, c->stream));
+    c->launches = gs.launches;
     return PA_OK;
+}
+
+extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
+    if (!c || !key_bits) return set_err(PA_E_PARAM, "NULL argument");
+    DevGuard dg_(c);
+    if (c->comm) return mg_hash(c, key_bits, out_bits, 0, 0);
+    if (!out_bits) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k)
+        return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge or pa_mmh_acc + pa_tail_merge");
+    const int rc = graph_run(c, c->g_hash, {key_bits, out_bits}, [&] { return hash_enqueue(c, key_bits, out_bits); });
+    c->launches_total += c->launches;
+    return rc;
 }
 
 extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
@@ -1763,37 +1885,186 @@ extern "C" int pa_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *con
     if (!c || (count && (!keys || !outs))) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
     if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
+    if (c->comm) return mg_hash_batch(c, keys, outs, count);
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     for (uint32_t j = 0; j < count; j++)
         if (!keys[j] || !outs[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
     if (count == 0) return PA_OK;
     if (count == 1) return pa_hash(c, keys[0], outs[0]);
     TRY(alloc_alt(c));
-    if (!graphs_enabled(c)) {
-        const int rc = batch_enqueue(c, keys, outs, count);
-        c->launches_total += c->launches;
-        return rc;
-    }
     std::vector<const void *> ptrs;
     for (uint32_t j = 0; j < count; j++) { ptrs.push_back(keys[j]); ptrs.push_back(outs[j]); }
-    if (!c->bgraph_exec || ptrs != c->bgraph_ptrs) {
-        if (c->bgraph_exec) { cudaGraphExecDestroy(c->bgraph_exec); c->bgraph_exec = nullptr; }
-        cudaGraph_t g = nullptr;
-        CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        const int rc = batch_enqueue(c, keys, outs, count);
-        const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
-        if (rc != PA_OK) { if (g) cudaGraphDestroy(g); return rc; }
-        if (e != cudaSuccess) return set_err(PA_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
-        const cudaError_t e2 = cudaGraphInstantiate(&c->bgraph_exec, g, 0);
-        cudaGraphDestroy(g);
-        if (e2 != cudaSuccess) { c->bgraph_exec = nullptr; return set_err(PA_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2)); }
-        c->bgraph_ptrs = ptrs;
-        c->bgraph_launches = c->launches;
-    }
-    CUDA_TRY(cudaGraphLaunch(c->bgraph_exec, c->stream));
-    c->launches = c->bgraph_launches;
+    const int rc = graph_run(c, c->g_batch, ptrs, [&] { return batch_enqueue(c, keys, outs, count); });
     c->launches_total += c->launches;
+    return rc;
+}
+
+// ====================================================================== multi-GPU
+// rank g hashes its blocks' S1-S3 into the transform-domain accumulator,
+// the ranks' accumulators are summed by one ncclReduce to the key's root (MMH is linear over
+// a partition of the blocks), and the root alone runs S4-S7.
+
+// canonical export of the accumulator (c->mac_slots slots) into `dst` (u32 or u64 words)
+static int launch_export(pa_ctx *c, void *dst, bool u64) {
+    const uint64_t total = (uint64_t)c->pl.mmh.nprimes * c->smmh.L;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
+    const uint32_t lg = c->pl.mmh.log2_len;
+    ProfScope ps(c, "mmh_acc_export");
+    if (u64)
+        acc_export<uint64_t><<<grid, 256, 0, c->stream>>>(c->acc, c->mac_slots, total, lg, total, c->smmh.pks,
+                                                          static_cast<uint64_t *>(dst));
+    else
+        acc_export<uint32_t><<<grid, 256, 0, c->stream>>>(c->acc, c->mac_slots, total, lg, total, c->smmh.pks,
+                                                          static_cast<uint32_t *>(dst));
+    c->launches++;
+    CUDA_TRY(cudaGetLastError());
     return PA_OK;
+}
+
+// S4-S7 from the reduced accumulator `recv` (u32 sums < 4p, or u64 sums converted into tmp32)
+static int mg_post_enqueue(pa_ctx *c, const void *recv, uint32_t *tmp32, uint8_t *out) {
+    c->launches = 0;
+    TRY(carry_reset(c));
+    const uint32_t *src = static_cast<const uint32_t *>(recv);
+    if (c->x_u64) {
+        const uint64_t total = (uint64_t)c->pl.mmh.nprimes * c->smmh.L;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
+        ProfScope ps(c, "mmh_acc_import");
+        acc_import_u64<<<grid, 256, 0, c->stream>>>(static_cast<const uint64_t *>(recv), c->pl.mmh.log2_len, total,
+                                                     c->smmh.pks, tmp32);
+        c->launches++;
+        CUDA_TRY(cudaGetLastError());
+        src = tmp32;
+    }
+    uint32_t *y = nullptr;
+    TRY(mmh_tail(c, &y, src, 1, 0));
+    return run_mh(c, y, out);
+}
+
+// one key on a multi-GPU context, reduced to and finished on `root`, with buffer set `set`
+// (the caller has swapped the set in: c->acc, c->stream, ... are the set's)
+static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set) {
+    const int rank = c->pl.rank;
+    if (rank == root && !out) return set_err(PA_E_PARAM, "NULL output on the root rank");
+    const uint64_t total = (uint64_t)c->pl.mmh.nprimes * c->smmh.L;
+    uint32_t launched = 0;
+    TRY(graph_run(c, c->g_mg_pre[set], {key}, [&] {
+        c->launches = 0;
+        TRY(run_mmh_acc(c, key));
+        return launch_export(c, c->xsend[set], c->x_u64);
+    }));
+    launched += c->launches;
+    {
+        ProfScope ps(c, "mmh_nccl_reduce");
+        NCCL_TRY(nccl_api().Reduce(c->xsend[set], c->xrecv[set], total, c->x_u64 ? ncclUint64 : ncclUint32, ncclSum,
+                                   root, c->comm, c->stream));
+    }
+    if (rank == root) {
+        TRY(graph_run(c, c->g_mg_post[set], {out}, [&] {
+            return mg_post_enqueue(c, c->xrecv[set], static_cast<uint32_t *>(c->xsend[set]), out);
+        }));
+        launched += c->launches;
+    }
+    c->launches = launched;
+    c->launches_total += launched;
+    return PA_OK;
+}
+
+// stream of keys with the root rotating (key j on rank j mod world), alternating buffer sets
+// and streams so key j's reduce and tail overlap key j+1's transforms
+static int mg_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
+    const int world = c->pl.world, rank = c->pl.rank;
+    for (uint32_t j = 0; j < count; j++) {
+        if (!keys[j]) return set_err(PA_E_PARAM, "NULL key in batch");
+        if ((int)(j % world) == rank && !outs[j]) return set_err(PA_E_PARAM, "NULL output of a key this rank is root of");
+    }
+    if (count == 0) return PA_OK;
+    TRY(alloc_alt(c));
+    CUDA_TRY(cudaEventRecord(c->bev[0], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->alt.stream, c->bev[0], 0));
+    uint32_t total = 0;
+    for (uint32_t j = 0; j < count; j++) {
+        const int set = (int)(j & 1);
+        if (set) swap_bufs(c);
+        const int rc = mg_hash(c, keys[j], outs[j], (int)(j % world), set);
+        total += c->launches;
+        if (set) swap_bufs(c);
+        TRY(rc);
+    }
+    CUDA_TRY(cudaEventRecord(c->bev[1], c->alt.stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->bev[1], 0));
+    c->launches = total;
+    return PA_OK;
+}
+
+// NCCL communicator and exchange buffers of a multi-GPU context (collective: blocks until
+// every rank of the job has joined)
+static int mg_init(pa_ctx *c, const pa_params *prm) {
+    NcclApi &api = nccl_api();
+    if (!api.ok) return set_err(PA_E_NCCL, "NCCL unavailable: %s", api.why);
+    uint32_t qmax = 0;
+    for (uint32_t i = 0; i < c->pl.mmh.nprimes; i++) qmax = std::max(qmax, c->pl.mmh.primes[i]);
+    // u32 sums must stay below 4 q (the inverse row pass reduces its input from [0, 4q))
+    c->x_u64 = c->pl.world > 4 || (uint64_t)c->pl.world * (qmax - 1) >= (1ull << 32);
+    const size_t total = (size_t)c->pl.mmh.nprimes * c->smmh.L;
+    for (int s = 0; s < 2; s++) {
+        // u64 buffers also hold the u32 conversion on the root (tmp32 = xsend)
+        if (c->x_u64) {
+            uint64_t *a, *b;
+            TRY(c->da.alloc(&a, total));
+            TRY(c->da.alloc(&b, total));
+            c->xsend[s] = a;
+            c->xrecv[s] = b;
+        } else {
+            uint32_t *a, *b;
+            TRY(c->da.alloc(&a, total));
+            TRY(c->da.alloc(&b, total));
+            c->xsend[s] = a;
+            c->xrecv[s] = b;
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    ncclUniqueId id;
+    static_assert(sizeof id.internal == sizeof prm->nccl_id, "ncclUniqueId size");
+    memcpy(id.internal, prm->nccl_id, sizeof id.internal);
+    NCCL_TRY(api.CommInitRank(&c->comm, c->pl.world, id, c->pl.rank));
+    return PA_OK;
+}
+
+extern "C" int pa_nccl_unique_id(uint8_t *id_out) {
+    if (!id_out) return set_err(PA_E_PARAM, "NULL argument");
+    NcclApi &api = nccl_api();
+    if (!api.ok) return set_err(PA_E_NCCL, "NCCL unavailable: %s", api.why);
+    ncclUniqueId id;
+    NCCL_TRY(api.GetUniqueId(&id));
+    memcpy(id_out, id.internal, sizeof id.internal);
+    return PA_OK;
+}
+
+// ---- transform-domain split with a caller-side exchange (include/pa.h)
+extern "C" int pa_mmh_acc(pa_ctx *c, const uint8_t *key_slice, uint32_t *acc_out) {
+    if (!c || !key_slice || !acc_out) return set_err(PA_E_PARAM, "NULL argument");
+    DevGuard dg_(c);
+    if (c->pl.mh_only || c->pl.toeplitz || c->pl.paper_k) return set_err(PA_E_STATE, "r-bit MMH-MH contexts only");
+    c->launches = 0;
+    int rc = run_mmh_acc(c, key_slice);
+    if (rc == PA_OK) rc = launch_export(c, acc_out, false);
+    c->launches_total += c->launches;
+    return rc;
+}
+
+extern "C" int pa_tail_merge(pa_ctx *c, const uint32_t *acc_parts, uint32_t G, uint8_t *out_bits) {
+    if (!c || !acc_parts || !out_bits || G == 0) return set_err(PA_E_PARAM, "bad argument");
+    DevGuard dg_(c);
+    if (c->pl.mh_only || c->pl.toeplitz || c->pl.paper_k) return set_err(PA_E_STATE, "r-bit MMH-MH contexts only");
+    if (G > 4096) return set_err(PA_E_PARAM, "too many parts");
+    c->launches = 0;
+    int rc = carry_reset(c);
+    uint32_t *y = nullptr;
+    if (rc == PA_OK) rc = mmh_tail(c, &y, acc_parts, G, (uint64_t)c->pl.mmh.nprimes * c->smmh.L);
+    if (rc == PA_OK) rc = run_mh(c, y, out_bits);
+    c->launches_total += c->launches;
+    return rc;
 }
 
 // End-to-end hash from host buffers.  The key is copied in kCopyGroups block groups on a
@@ -1886,37 +2157,22 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
     DevGuard dg_(c);
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
-    if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
-    if (!c->out_dev) CUDA_TRY(cudaMalloc(&c->out_dev, mb));
+    if (!c->key_dev) TRY(c->da.alloc(&c->key_dev, nb));
+    if (!c->out_dev) TRY(c->da.alloc(&c->out_dev, mb));
     if (!c->copy_stream) {
         CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
     }
     // copies from / to pageable host memory synchronise with the host, which stream capture
     // forbids: such buffers take the direct (uncaptured) path
-    if (!graphs_enabled(c) || !host_pinned(key_host) || !host_pinned(out_host)) {
+    if (!host_pinned(key_host) || !host_pinned(out_host)) {
         const int rc = hash_host_enqueue(c, key_host, out_host);
         c->launches_total += c->launches;
         TRY(rc);
     } else {
-        if (!c->hgraph_exec || c->hgraph_key != key_host || c->hgraph_out != out_host) {
-            if (c->hgraph_exec) { cudaGraphExecDestroy(c->hgraph_exec); c->hgraph_exec = nullptr; }
-            cudaGraph_t g = nullptr;
-            CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-            const int rc = hash_host_enqueue(c, key_host, out_host);
-            const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
-            if (rc != PA_OK) { if (g) cudaGraphDestroy(g); return rc; }
-            if (e != cudaSuccess) return set_err(PA_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
-            const cudaError_t e2 = cudaGraphInstantiate(&c->hgraph_exec, g, 0);
-            cudaGraphDestroy(g);
-            if (e2 != cudaSuccess) { c->hgraph_exec = nullptr; return set_err(PA_E_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2)); }
-            c->hgraph_key = key_host;
-            c->hgraph_out = out_host;
-            c->hgraph_launches = c->launches;
-        }
-        CUDA_TRY(cudaGraphLaunch(c->hgraph_exec, c->stream));
-        c->launches = c->hgraph_launches;
+        const int rc = graph_run(c, c->g_host, {key_host, out_host}, [&] { return hash_host_enqueue(c, key_host, out_host); });
         c->launches_total += c->launches;
+        TRY(rc);
     }
     TRY(stream_poll(c->stream, "pa_hash_host"));
     if (c->pl.paper_k) return pa_ctx_status(c);
@@ -1938,10 +2194,10 @@ extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, ui
         if (!keys_host[j] || !outs_host[j]) return set_err(PA_E_PARAM, "NULL key or output in batch");
     if (count == 0) return PA_OK;
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
-    if (!c->key_dev) CUDA_TRY(cudaMalloc(&c->key_dev, nb));
-    if (!c->out_dev) CUDA_TRY(cudaMalloc(&c->out_dev, mb));
-    if (!c->key_dev2) CUDA_TRY(cudaMalloc(&c->key_dev2, nb));
-    if (!c->out_dev2) CUDA_TRY(cudaMalloc(&c->out_dev2, mb));
+    if (!c->key_dev) TRY(c->da.alloc(&c->key_dev, nb));
+    if (!c->out_dev) TRY(c->da.alloc(&c->out_dev, mb));
+    if (!c->key_dev2) TRY(c->da.alloc(&c->key_dev2, nb));
+    if (!c->out_dev2) TRY(c->da.alloc(&c->out_dev2, mb));
     if (!c->copy_stream) {
         CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));

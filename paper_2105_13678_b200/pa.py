@@ -25,9 +25,14 @@ def _words(v: int, bits: int) -> np.ndarray:
 
 def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
             stream=None, limb_bits=0, strict=False, keep=None, paper_k=0, mh_only=False,
-            toeplitz=False) -> B.pa_params:
+            toeplitz=False, world=0, rank=0, nccl_id=None) -> B.pa_params:
     prm = B.pa_params()
     prm.n, prm.r, prm.m, prm.gamma, prm.seed = n, r, m, gamma, seed & (2**64 - 1)
+    prm.world, prm.rank = world, rank
+    if nccl_id is not None:
+        if len(nccl_id) != 128:
+            raise ValueError("nccl_id must be 128 bytes (pa_nccl_unique_id)")
+        ctypes.memmove(prm.nccl_id, bytes(nccl_id), 128)
     prm.paper_k = paper_k
     prm.mh_only = 1 if mh_only else 0
     prm.toeplitz = 1 if toeplitz else 0
@@ -56,10 +61,11 @@ def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
 
 
 def plan(n: int, r: int, m: int, gamma: int = 0, block_range=None, limb_bits: int = 0,
-         strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False) -> dict:
+         strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False,
+         world: int = 0, rank: int = 0) -> dict:
     """Validate parameters and return the transform plan (host only, no GPU)."""
     prm = _params(n, r, m, gamma, 0, block_range, limb_bits=limb_bits, strict=strict, paper_k=paper_k,
-                  mh_only=mh_only, toeplitz=toeplitz)
+                  mh_only=mh_only, toeplitz=toeplitz, world=world, rank=rank)
     info = B.pa_info()
     B.check(B.pa_plan(ctypes.byref(prm), ctypes.byref(info)))
     return info.as_dict()
@@ -104,6 +110,29 @@ def stream_partition(total_bits: int, n: int) -> tuple[int, int]:
     return total_bits // n, total_bits % n
 
 
+def nccl_unique_id() -> bytes:
+    """pa_nccl_unique_id: a fresh ncclUniqueId (128 bytes) for the multi-GPU contexts."""
+    buf = (ctypes.c_uint8 * 128)()
+    B.check(B.pa_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def _torch_allocator(torch, device: int):
+    """pa_params.dev_alloc / dev_free over PyTorch's caching allocator."""
+    def _alloc(nbytes, stream, _user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0))
+        except Exception:
+            return None
+
+    def _free(ptr, _nbytes, _stream, _user):
+        try:
+            torch.cuda.caching_allocator_delete(int(ptr))
+        except Exception:
+            pass
+    return B.DEV_ALLOC(_alloc), B.DEV_FREE(_free)
+
+
 def shard_ranges(k: int, G: int) -> list[tuple[int, int]]:
     """Rank g owns blocks [floor(k g / G), floor(k (g+1) / G))."""
     return [(k * g // G, k * (g + 1) // G) for g in range(G)]
@@ -116,7 +145,8 @@ class PAContext:
     def __init__(self, n: int, r: int, m: int, gamma: int = 0, seed: int = 0, *,
                  block_range=None, a=None, b=None, c=None, stream=None, limb_bits: int = 0,
                  strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False,
-                 throughput_only: bool = False):
+                 throughput_only: bool = False, world: int = 0, rank: int = 0, nccl_id: bytes | None = None,
+                 torch_allocator: bool = True):
         import torch
         if not torch.cuda.is_available():
             raise B.PAError(B.PA_E_CUDA, "no CUDA device: the library has no CPU path")
@@ -125,7 +155,13 @@ class PAContext:
         self.stream = st
         keep: list = []
         prm = _params(n, r, m, gamma, seed, block_range, a, b, c, ctypes.c_void_p(st.cuda_stream),
-                      limb_bits, strict, keep, paper_k, mh_only, toeplitz)
+                      limb_bits, strict, keep, paper_k, mh_only, toeplitz, world, rank, nccl_id)
+        self._alloc_cbs = None
+        if torch_allocator:
+            # the context's device memory comes from PyTorch's caching allocator; the callbacks
+            # live as long as the context (pa_ctx_destroy calls dev_free)
+            self._alloc_cbs = _torch_allocator(torch, torch.cuda.current_device())
+            prm.dev_alloc, prm.dev_free = self._alloc_cbs
         h = ctypes.c_void_p()
         B.check(B.pa_ctx_create_ex(ctypes.byref(prm), ctypes.byref(h)))
         self._h = h
@@ -134,6 +170,9 @@ class PAContext:
         self.n, self.r, self.m = n, r, m
         self.gamma, self.alpha, self.k = self.info["gamma"], self.info["alpha"], self.info["k"]
         self.block_range = (self.info["block_begin"], self.info["block_end"])
+        self.world, self.rank = self.info["world"], self.info["rank"]
+        lo, hi = key_slice_bytes(n, r, self.block_range) if self.mode == "mmh_mh" else (0, (n + 7) // 8)
+        self.slice_bytes = hi - lo
         self.nbytes_in = (n + 7) // 8
         self.nbytes_out = (m + 7) // 8
         self.y_words = (self.gamma + 31) // 32
@@ -195,24 +234,31 @@ class PAContext:
         return t
 
     def hash(self, key, out=None):
-        """pa_hash: key = CUDA uint8 tensor of ceil(n/8) bytes -> CUDA uint8 tensor ceil(m/8)."""
+        """pa_hash: key = CUDA uint8 tensor of ceil(n/8) bytes (a shard's slice for multi-GPU
+        contexts) -> CUDA uint8 tensor ceil(m/8) (on rank 0 of a multi-GPU context; None on
+        the other ranks)."""
         torch = self._torch
-        key = self._dev_u8(key, self.nbytes_in)
-        if out is None:
+        mg = self.world > 0
+        key = self._dev_u8(key, self.slice_bytes if mg else self.nbytes_in)
+        if out is None and (not mg or self.rank == 0):
             out = torch.empty(self.nbytes_out, dtype=torch.uint8, device=key.device)
-        B.check(B.pa_hash(self._h, ctypes.c_void_p(key.data_ptr()), ctypes.c_void_p(out.data_ptr())))
+        op = ctypes.c_void_p(out.data_ptr()) if out is not None else None
+        B.check(B.pa_hash(self._h, ctypes.c_void_p(key.data_ptr()), op))
         return out
 
     def hash_batch(self, keys, outs=None):
-        """pa_hash_batch: a list of CUDA uint8 key tensors -> list of outputs (stream mode)."""
+        """pa_hash_batch: a list of CUDA uint8 key tensors -> list of outputs (stream mode).
+        Multi-GPU contexts: key j is finished on rank j mod world; other entries are None."""
         torch = self._torch
-        keys = [self._dev_u8(k, self.nbytes_in) for k in keys]
+        mg = self.world > 0
+        keys = [self._dev_u8(k, self.slice_bytes if mg else self.nbytes_in) for k in keys]
         if outs is None:
-            outs = [torch.empty(self.nbytes_out, dtype=torch.uint8, device=k.device) for k in keys]
+            outs = [torch.empty(self.nbytes_out, dtype=torch.uint8, device=k.device)
+                    if (not mg or j % self.world == self.rank) else None for j, k in enumerate(keys)]
         if len(outs) != len(keys):
             raise ValueError("keys and outs differ in length")
         kp = (ctypes.c_void_p * len(keys))(*[k.data_ptr() for k in keys])
-        op = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        op = (ctypes.c_void_p * len(outs))(*[o.data_ptr() if o is not None else None for o in outs])
         B.check(B.pa_hash_batch(self._h, kp, op, len(keys)))
         return outs
 
@@ -267,6 +313,30 @@ class PAContext:
         op = self._host_u8(out_host, self.nbytes_out, "output", True)
         B.check(B.pa_hash_host(self._h, ctypes.c_void_p(kp), ctypes.c_void_p(op)))
         return out_host
+
+    def mmh_acc(self, key_slice, acc_out=None):
+        """pa_mmh_acc: this context's transform-domain accumulator (acc_words int32 words on
+        the device), canonical residues; parts of a block partition sum to the whole key's."""
+        torch = self._torch
+        key_slice = self._dev_u8(key_slice, 1)
+        if acc_out is None:
+            acc_out = torch.empty(self.info["acc_words"], dtype=torch.int32, device=key_slice.device)
+        if acc_out.dtype != torch.int32 or not acc_out.is_contiguous() or acc_out.numel() < self.info["acc_words"]:
+            raise ValueError("acc_out: contiguous int32 tensor of acc_words words")
+        B.check(B.pa_mmh_acc(self._h, ctypes.c_void_p(key_slice.data_ptr()), ctypes.c_void_p(acc_out.data_ptr())))
+        return acc_out
+
+    def tail_merge(self, acc_parts, out=None):
+        """pa_tail_merge: acc_parts = int32 CUDA tensor [G, acc_words] -> output bytes."""
+        torch = self._torch
+        acc_parts = acc_parts.contiguous()
+        G = acc_parts.shape[0] if acc_parts.dim() == 2 else 1
+        if acc_parts.dtype != torch.int32 or acc_parts.numel() != G * self.info["acc_words"]:
+            raise ValueError("acc_parts: int32 tensor [G, acc_words]")
+        if out is None:
+            out = torch.empty(self.nbytes_out, dtype=torch.uint8, device=acc_parts.device)
+        B.check(B.pa_tail_merge(self._h, ctypes.c_void_p(acc_parts.data_ptr()), G, ctypes.c_void_p(out.data_ptr())))
+        return out
 
     def mmh_partial(self, key_slice, y_out=None):
         """pa_mmh_partial: this shard's residue as ceil(gamma/32) words (int32 CUDA tensor)."""
@@ -369,6 +439,29 @@ def stream_gather_merge(partial_fn, merge_fn, key_slices, group=None):
         if me == root:
             outs[j] = merge_fn(parts)
     return outs
+
+
+def transform_merge_hash(ctx: PAContext, key_slice, group=None, root: int = 0):
+    """Multi-GPU hash with a caller-side exchange in the transform domain (any process
+    group, e.g. gloo for validation): pa_mmh_acc on every rank, accumulators gathered,
+    pa_tail_merge (sum mod each prime + S4-S7) on ``root``."""
+    return shard_gather_merge(ctx.mmh_acc, ctx.tail_merge, key_slice, group, root)
+
+
+def transform_merge_stream(ctx: PAContext, key_slices, group=None):
+    """NEXT-3 rotating root with the transform-domain exchange: key j finished on rank j mod G."""
+    return stream_gather_merge(ctx.mmh_acc, ctx.tail_merge, key_slices, group)
+
+
+def nccl_context(n: int, r: int, m: int, seed: int = 0, group=None, **kw) -> PAContext:
+    """A multi-GPU context on every rank of ``group`` (torch.distributed): rank 0 draws the
+    ncclUniqueId (pa_nccl_unique_id), the group broadcasts it, every rank creates its
+    context (collective; the library then reduces over its own NCCL communicator)."""
+    import torch.distributed as dist
+    G, me = dist.get_world_size(group), dist.get_rank(group)
+    obj = [nccl_unique_id() if me == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return PAContext(n, r, m, seed=seed, world=G, rank=me, nccl_id=obj[0], **kw)
 
 
 def stream_hash(ctx: PAContext, key_slices, group=None):

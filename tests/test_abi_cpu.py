@@ -231,3 +231,39 @@ def test_host_buffer_checks_reject_bad_buffers():
     assert ctx._host_u8(ro, 100, "key") > 0              # a key may be read-only
     with pytest.raises(ValueError):
         ctx._host_u8(ro, 100, "out", writable=True)      # an output may not
+
+
+def test_plan_multi_gpu_world():
+    # rank g of G owns blocks [k g / G, k (g+1) / G); every rank plans the
+    # whole key's transform so the transform-domain accumulators are compatible
+    n, r, m = 260_000_000, 1 << 23, 26_000_000
+    whole = P.plan(n, r, m)
+    for G in (1, 2, 3, 8):
+        for g in range(G):
+            info = P.plan(n, r, m, world=G, rank=g)
+            assert (info["block_begin"], info["block_end"]) == P.shard_ranges(31, G)[g]
+            assert info["world"] == G and info["rank"] == g
+            assert info["mmh"] == whole["mmh"] and info["mh"] == whole["mh"]
+            assert info["acc_words"] == whole["mmh"]["nprimes"] << whole["mmh"]["log2_len"]
+    # a plain shard context plans the whole key's transform too
+    assert P.plan(n, r, m, block_range=(3, 9))["mmh"] == whole["mmh"]
+    bad = [dict(world=2, rank=2), dict(world=-1), dict(world=0, rank=1), dict(world=32, rank=0),
+           dict(world=2, rank=0, block_range=(0, 3)), dict(world=2, rank=0, paper_k=3)]
+    for kw in bad:
+        with pytest.raises(B.PAError) as ei:
+            if "paper_k" in kw:
+                P.plan(1000, 0, 10, 107, **kw)
+            else:
+                P.plan(n, r, m, **kw)
+        assert ei.value.code == B.PA_E_PARAM
+    P.plan(n, r, m, world=2, rank=1, block_range=(15, 31))        # the exact range is accepted
+
+
+def test_nccl_unique_id_host_only():
+    # the library loads NCCL at run time (dlopen); the id is 128 bytes and fresh per call
+    try:
+        a, b = P.nccl_unique_id(), P.nccl_unique_id()
+    except B.PAError as e:
+        assert e.code == B.PA_E_NCCL
+        pytest.skip(f"NCCL not loadable here: {e}")
+    assert len(a) == 128 and len(b) == 128 and a != b

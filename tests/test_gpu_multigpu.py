@@ -1,0 +1,145 @@
+"""GPU parity of the multi-GPU split (SURVEY.md §8(b,e)) through the C ABI, on one GPU.
+
+- pa_mmh_acc / pa_tail_merge: G shard contexts (the ranks' block ranges) each produce the
+  transform-domain accumulator of their blocks; the sum, inverse-transformed and finished
+  on one context, must equal the CPU oracle's hash of the whole key (MMH is linear over a
+  partition of the blocks).
+- Multi-GPU contexts (pa_params.world/rank/nccl_id) with a one-rank NCCL communicator run
+  the library's own ncclReduce path (pa_hash, and pa_hash_batch with the rotating root)
+  against the oracle.  NCCL across several ranks needs a multi-GPU node.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import hashes  # noqa: E402
+from synth import CONFIGS, key_bytes  # noqa: E402
+
+
+def _P():
+    from paper_2105_13678_b200 import pa
+    return pa
+
+
+@pytest.mark.parametrize("n,r,m,G", [(100_003, 1024, 5_000, 1), (100_003, 1024, 5_000, 2),
+                                     (262_157, 2048, 30_001, 3), (300_000, 4096, 4_000, 5),
+                                     (1 << 20, 1 << 16, 104_858, 4)])
+def test_transform_merge_equals_oracle(n, r, m, G):
+    P = _P()
+    seed = 77
+    key = key_bytes(n, 0x51 + G)
+    k = -(-n // r)
+    ctxs, parts = [], []
+    for (b0, b1) in P.shard_ranges(k, G):
+        ctx = P.PAContext(n, r, m, seed=seed, block_range=(b0, b1))
+        lo, hi = P.key_slice_bytes(n, r, (b0, b1))
+        parts.append(ctx.mmh_acc(torch.from_numpy(key[lo:hi].copy()).cuda()))
+        ctxs.append(ctx)
+    acc = torch.stack(parts)
+    want = hashes.pa_hash_seeded(key, n, r, m, seed)
+    for ctx in (ctxs[0], ctxs[-1]):
+        out = ctx.tail_merge(acc)
+        torch.cuda.synchronize()
+        assert bytes(out.cpu().numpy()) == want
+    # the whole-key context's accumulator is the parts' sum mod each NTT prime
+    whole = P.PAContext(n, r, m, seed=seed)
+    wa = whole.mmh_acc(torch.from_numpy(key).cuda()).to(torch.int64).cpu()
+    info = whole.query()
+    L = 1 << info["mmh"]["log2_len"]
+    q = torch.tensor(info["mmh"]["primes"], dtype=torch.int64).repeat_interleave(L)
+    s = acc.to(torch.int64).cpu().sum(0) % q
+    assert torch.equal(s, wa)
+    assert bool((wa < q).all())
+    out = whole.tail_merge(wa.to(torch.int32).cuda().unsqueeze(0))
+    torch.cuda.synchronize()
+    assert bytes(out.cpu().numpy()) == want
+    for ctx in ctxs + [whole]:
+        ctx.close()
+
+
+def _one_rank_ctx(P, n, r, m, seed, **kw):
+    try:
+        nid = P.nccl_unique_id()
+    except Exception as e:  # pragma: no cover
+        pytest.fail(f"NCCL not loadable on the GPU box: {e}")
+    return P.PAContext(n, r, m, seed=seed, world=1, rank=0, nccl_id=nid, **kw)
+
+
+@pytest.mark.parametrize("on_stream", [False, True])
+def test_nccl_one_rank_hash_and_rotating_batch(on_stream):
+    P = _P()
+    n, r, m, seed = 262_157, 2048, 30_001, 4
+    s = torch.cuda.Stream() if on_stream else torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        ctx = _one_rank_ctx(P, n, r, m, seed)
+        assert ctx.world == 1 and ctx.rank == 0
+        for ks in (1, 2):
+            key = key_bytes(n, 0x900 + ks)
+            out = ctx.hash(torch.from_numpy(key).cuda())
+            s.synchronize()
+            assert bytes(out.cpu().numpy()) == hashes.pa_hash_seeded(key, n, r, m, seed)
+        keys = [key_bytes(n, 0xA00 + j) for j in range(5)]
+        outs = ctx.hash_batch([torch.from_numpy(kk).cuda() for kk in keys])
+        s.synchronize()
+        for kk, o in zip(keys, outs):
+            assert bytes(o.cpu().numpy()) == hashes.pa_hash_seeded(kk, n, r, m, seed)
+        info = ctx.query()
+        if on_stream:
+            # new key / output pointers re-capture and update the graphs in place
+            assert info["graph_captures"] >= 2 and info["graph_instantiations"] <= info["graph_captures"]
+        ctx.close()
+
+
+def test_nccl_one_rank_c2_golden():
+    import hashlib
+    import json
+    import os
+    P = _P()
+    w = CONFIGS["C2"]
+    ctx = _one_rank_ctx(P, w.n, w.r, w.m, w.hash_seed)
+    out = ctx.hash(torch.from_numpy(key_bytes(w.n, w.key_seed)).cuda())
+    torch.cuda.synchronize()
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "digests.json")))
+    assert hashlib.sha256(bytes(out.cpu().numpy())).hexdigest() == gold["C2"]["out_sha256"]
+    ctx.close()
+
+
+def test_graph_update_on_new_pointers():
+    # verdict r1 #8: a hash on new key/output buffers re-captures and updates the executable
+    # graph in place (cudaGraphExecUpdate) instead of re-instantiating; results stay exact
+    P = _P()
+    n, r, m, seed = 300_001, 4096, 20_000, 8
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = P.PAContext(n, r, m, seed=seed)
+        for ks in range(4):
+            key = key_bytes(n, 0xB00 + ks)
+            kd = torch.from_numpy(key).cuda()                 # a new buffer every time
+            out = ctx.hash(kd)
+            s.synchronize()
+            assert bytes(out.cpu().numpy()) == hashes.pa_hash_seeded(key, n, r, m, seed)
+        info = ctx.query()
+        assert info["graph_captures"] >= 2
+        assert info["graph_instantiations"] == 1 and info["graph_updates"] == info["graph_captures"] - 1
+        ctx.close()
+
+
+def test_torch_allocator_and_default_allocator_agree():
+    # pa_params.dev_alloc: the context's device memory from PyTorch's caching allocator
+    # (default in the binding) or cudaMallocAsync (torch_allocator=False); same results
+    P = _P()
+    n, r, m, seed = 100_003, 1024, 5_000, 12
+    key = key_bytes(n, 0xC00)
+    outs = []
+    for ta in (True, False):
+        before = torch.cuda.memory_allocated()
+        ctx = P.PAContext(n, r, m, seed=seed, torch_allocator=ta)
+        held = torch.cuda.memory_allocated() - before
+        assert (held >= ctx.query()["device_bytes"]) if ta else (held == 0)
+        outs.append(bytes(ctx.hash(torch.from_numpy(key).cuda()).cpu().numpy()))
+        ctx.close()
+        if ta:
+            assert torch.cuda.memory_allocated() == before
+    assert outs[0] == outs[1] == hashes.pa_hash_seeded(key, n, r, m, seed)
