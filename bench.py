@@ -644,6 +644,33 @@ def main():
 
     # ---- fresh hash keys per job (NEXT-2): pa_ctx_rekey (device Philox expansion + transforms
     # of the a_i and b) before every hash -- the "cold" throughput of a new function per job
+    # ---- graph re-binding (verdict r1 #8): pa_hash on alternating output buffers, so every
+    # call sees a new pointer set and re-captures + updates its executable graph in place
+    # (cudaGraphExecUpdate), against the same calls on one buffer (plain replay)
+    graph_rebind = None
+    if world == 1 and not paper:
+        outs2 = [torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev) for _ in range(2)]
+        i0 = ctx.query()
+        torch.cuda.synchronize()
+        res_t = {}
+        for mode in ("same", "alternating"):
+            tl = []
+            for j in range(max(6, args.steps // 2)):
+                o = outs2[0] if mode == "same" else outs2[j & 1]
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ctx.hash(key_dev, o)
+                torch.cuda.synchronize()
+                tl.append((time.perf_counter() - t0) * 1e3)
+            res_t[mode] = statistics.median(tl[2:])
+        i1 = ctx.query()
+        graph_rebind = {"host_wall_ms_same_pointers": res_t["same"],
+                        "host_wall_ms_new_pointers": res_t["alternating"],
+                        "captures": i1["graph_captures"] - i0["graph_captures"],
+                        "updates": i1["graph_updates"] - i0["graph_updates"],
+                        "instantiations": i1["graph_instantiations"] - i0["graph_instantiations"],
+                        "what": "wall time of pa_hash + synchronize; new pointers re-capture and cudaGraphExecUpdate"}
+
     fresh = None
     if world == 1:
         for j in range(2):
@@ -757,6 +784,7 @@ def main():
         "stream": stream_mode if world == 1 else mr_stream,
         "comparators": comparators,
         "fresh_keys": fresh,
+        "graph_rebind": graph_rebind,
         "ctx_create_ms": ctx_create_ms,
     }
     if verified is not None:
