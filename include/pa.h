@@ -313,6 +313,17 @@ int pa_select_gamma(uint64_t target_n, uint64_t k, uint64_t *gamma, int *exceeds
 int pa_derive_paper_params(uint64_t target_n, double ratio, uint64_t t, double epsilon, uint64_t *gamma,
                            uint64_t *k, uint64_t *n, uint64_t *s, uint64_t *m);
 
+/* Bounds-asserting debug build (built with -DPA_DEBUG into _pa_debug.so): every global
+ * access site of the kernels is checked against the live device ranges (context
+ * allocations + the caller's buffers of the current call) and every shared-memory index
+ * against the launch's shared memory; a violation prints the site and traps.
+ * pa_debug_build: 1 in that build, 0 in the release build.  pa_debug_selftest: (debug
+ * build) counts, without trapping, one out-of-range global address and one out-of-range
+ * shared index and returns PA_OK when exactly those two are caught; PA_E_STATE otherwise
+ * or in the release build. */
+int pa_debug_build(void);
+int pa_debug_selftest(void);
+
 /* Code of the last failure on this thread; copies its message into buf. */
 int pa_last_error(char *buf, size_t len);
 

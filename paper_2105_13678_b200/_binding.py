@@ -90,6 +90,8 @@ pa_mh_merge = _sig("pa_mh_merge", i32, vp, vp, u32, vp)
 pa_mmh_acc = _sig("pa_mmh_acc", i32, vp, vp, vp)
 pa_tail_merge = _sig("pa_tail_merge", i32, vp, vp, u32, vp)
 pa_nccl_unique_id = _sig("pa_nccl_unique_id", i32, vp)
+pa_debug_build = _sig("pa_debug_build", i32)
+pa_debug_selftest = _sig("pa_debug_selftest", i32)
 pa_ctx_destroy = _sig("pa_ctx_destroy", None, vp)
 pa_ctx_status = _sig("pa_ctx_status", i32, vp)
 pa_ctx_paper_stats = _sig("pa_ctx_paper_stats", i32, vp, ctypes.POINTER(u64), ctypes.POINTER(u64))
@@ -114,7 +116,8 @@ EXPORTED = ["pa_ctx_create", "pa_ctx_create_ex", "pa_hash", "pa_hash_host", "pa_
             "pa_ctx_destroy", "pa_ctx_status", "pa_ctx_rekey", "pa_ctx_query", "pa_ctx_set_stream", "pa_ctx_set_profiling",
             "pa_ctx_stage_times", "pa_plan", "pa_philox4x64_10", "pa_expand_a", "pa_expand_bc",
             "pa_last_error", "pa_ctx_paper_stats", "pa_derive_security_coefficient", "pa_select_block_count", "pa_select_gamma",
-            "pa_derive_paper_params", "pa_mmh_acc", "pa_tail_merge", "pa_nccl_unique_id"]
+            "pa_derive_paper_params", "pa_mmh_acc", "pa_tail_merge", "pa_nccl_unique_id", "pa_debug_build",
+            "pa_debug_selftest"]
 
 
 class PAError(RuntimeError):

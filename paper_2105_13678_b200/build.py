@@ -9,6 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "pa_api.cu")
 OUT = os.path.join(HERE, "_pa.so")
+OUT_DEBUG = os.path.join(HERE, "_pa_debug.so")     # -DPA_DEBUG: bounds-asserting build (csrc/debug.cuh)
 DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + \
        [os.path.join(ROOT, "include", "pa.h")]
 
@@ -23,17 +24,18 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    out = OUT_DEBUG if debug else OUT
     newest = max(os.path.getmtime(d) for d in DEPS)
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", SRC]
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+        return out
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DPA_DEBUG"] if debug else []), "-o", out + ".tmp", SRC]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))

@@ -2,6 +2,7 @@
 // cp.async.bulk) completed on shared-memory mbarriers, for sm_100a.
 #pragma once
 #include <cstdint>
+#include "debug.cuh"
 
 namespace pa {
 
@@ -37,6 +38,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 
 // bytes must be a multiple of 16, both addresses 16-byte aligned
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {
+    PA_CK(src_gmem, bytes);
+    PA_SMEM_PTR_CK(dst_smem, bytes);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(dst_smem)),

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128, PA_CRT_MINB) crt_coeffs(const uint32_t *_
     uint64_t slo = 1ull << 40, shi = 0;                // bias 2^-24
 #pragma unroll
     for (int i = 0; i < P; i++) {
-        const uint32_t r = res[(size_t)i * L + j];
+        const uint32_t r = PA_AT(res + (size_t)i * L + j);
         y[i] = red1p(mul_mont(r, K.qinv[i], K.p[i], K.pinv[i]), K.p[i]);
         const uint64_t q = (uint64_t)y[i] * K.G[i];
         slo += q;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(128, PA_CRT_MINB) crt_coeffs(const uint32_t *_
         const uint64_t km = (uint64_t)k * K.M[w];
         // subtract low word of k M (its high part carries into the next word via `borrow`)
         const int64_t d = (int64_t)(uint32_t)v - (int64_t)(uint32_t)km + borrow;
-        out[(size_t)w * ncoef] = (uint32_t)d;
+        PA_AT(out + (size_t)w * ncoef) = (uint32_t)d;
         borrow = (d >> 32) - (int64_t)(km >> 32);       // arithmetic shift: -1 on underflow
     }
 }
@@ -166,7 +166,7 @@ __device__ __forceinline__ void block_carries2(int g, int pp, uint32_t *c0, uint
 struct SrcArr {
     const uint64_t *S;
     uint32_t n;            // words present; S_u = 0 for u >= n
-    __device__ __forceinline__ uint64_t operator()(uint32_t u) const { return u < n ? S[u] : 0ull; }
+    __device__ __forceinline__ uint64_t operator()(uint32_t u) const { return u < n ? PA_AT(S + u) : 0ull; }
 };
 // Sum of G residues (S6): S_u = sum_g parts[g][u].
 struct SrcParts {
@@ -175,7 +175,7 @@ struct SrcParts {
     __device__ __forceinline__ uint64_t operator()(uint32_t u) const {
         uint64_t s = 0;
         if (u < Wg)
-            for (uint32_t g = 0; g < G; g++) s += parts[(size_t)g * Wg + u];
+            for (uint32_t g = 0; g < G; g++) s += PA_AT(parts + (size_t)g * Wg + u);
         return s;
     }
 };
@@ -224,12 +224,14 @@ __global__ void __launch_bounds__(kCarryT) carry_mw(const Src src, uint32_t W, u
         const uint32_t ntiles = (W + kCarryTile - 1) / kCarryTile;
         uint32_t cin = 0;
         if (tile > 0) {
+            PA_CK(vs + tile, 4);
             vs[tile] = 1u | (bg << 1) | ((uint32_t)allp << 2);
             __threadfence();
             uint32_t accG = 0, accP = 1;
             int64_t j = (int64_t)tile - 1;
             for (;;) {
                 if (j < 0) { cin = accG; break; }
+                PA_CK(vs + j, 4);
                 const uint32_t st = vs[j];
                 if (st == 0) continue;
                 if (st & 8u) { cin = accG | (accP & ((st >> 4) & 1u)); break; }
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(kCarryT) carry_mw(const Src src, uint32_t W, u
 #pragma unroll
     for (int j = 0; j < kCarryV; j++) {
         const uint32_t u = u0 + j;
-        if (u < W) out[u] = w[j] + c;
+        if (u < W) PA_AT(out + u) = w[j] + c;
         c = ((gm >> j) & 1u) | (((pm >> j) & 1u) & c);
     }
 }
@@ -271,12 +273,12 @@ __device__ __forceinline__ void fin_ripple(uint32_t *y, uint32_t Wtot, uint32_t 
         if (threadIdx.x == 0) s_first = 0xFFFFFFFFu;
         __syncthreads();
         const uint32_t u = base + threadIdx.x;
-        const uint32_t v = (u < Wtot) ? y[u] : 0u;
+        const uint32_t v = (u < Wtot) ? PA_AT(y + u) : 0u;
         if (u < Wtot && v != 0xFFFFFFFFu) atomicMin(&s_first, u);
         __syncthreads();
         const uint32_t f = s_first;
-        if (u < Wtot && u < f) y[u] = 0u;
-        if (u == f) y[u] = v + 1u;
+        if (u < Wtot && u < f) PA_AT(y + u) = 0u;
+        if (u == f) PA_AT(y + u) = v + 1u;
         __syncthreads();
         if (f != 0xFFFFFFFFu) return;     // carry absorbed (uniform)
     }
@@ -293,7 +295,7 @@ __device__ void mersenne_finish_dev(uint32_t *y, uint32_t Wtot, uint64_t gamma) 
         __syncthreads();
         for (uint32_t t = threadIdx.x; t < nT; t += blockDim.x) {
             const uint32_t i = gw + t;
-            const uint32_t lo = y[i], hi = (i + 1 < Wtot) ? y[i + 1] : 0u;
+            const uint32_t lo = PA_AT(y + i), hi = (i + 1 < Wtot) ? PA_AT(y + i + 1) : 0u;
             const uint32_t v = gs ? __funnelshift_r(lo, hi, gs) : lo;
             T[t] = v;
             if (v) atomicOr(&s_nz, 1u);
@@ -302,15 +304,16 @@ __device__ void mersenne_finish_dev(uint32_t *y, uint32_t Wtot, uint64_t gamma) 
         if (!s_nz) break;
         for (uint32_t t = threadIdx.x; t < nT; t += blockDim.x) {     // clear bits >= gamma
             const uint32_t i = gw + t;
-            if (t == 0 && gs) y[i] &= (1u << gs) - 1u;
-            else y[i] = 0u;
+            if (t == 0 && gs) PA_AT(y + i) &= (1u << gs) - 1u;
+            else PA_AT(y + i) = 0u;
         }
         __syncthreads();
         if (threadIdx.x == 0) {                           // y += T (short add)
             uint64_t cy = 0;
             for (uint32_t t = 0; t < nT && t < Wtot; t++) {
-                const uint64_t s = (uint64_t)y[t] + T[t] + cy;
-                y[t] = (uint32_t)s;
+                PA_IDX_CK(t, 64);
+                const uint64_t s = (uint64_t)PA_AT(y + t) + T[t] + cy;
+                PA_AT(y + t) = (uint32_t)s;
                 cy = s >> 32;
             }
             s_carry = (uint32_t)cy;
@@ -327,12 +330,12 @@ __device__ void mersenne_finish_dev(uint32_t *y, uint32_t Wtot, uint64_t gamma) 
         const uint32_t u = base + threadIdx.x;
         if (u < Wg) {
             const uint32_t want = (u == Wg - 1 && gs) ? ((1u << gs) - 1u) : 0xFFFFFFFFu;
-            if (y[u] != want) atomicOr(&s_bad, 1u);
+            if (PA_AT(y + u) != want) atomicOr(&s_bad, 1u);
         }
         __syncthreads();
         if (s_bad) return;
     }
-    for (uint32_t u = threadIdx.x; u < Wg; u += blockDim.x) y[u] = 0u;
+    for (uint32_t u = threadIdx.x; u < Wg; u += blockDim.x) PA_AT(y + u) = 0u;
 }
 
 __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict__ y, uint32_t Wtot, uint64_t gamma) {
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     constexpr uint32_t cbits = 32 * P;
     __shared__ uint32_t s_tile, s_cin, s_c1, s_last;
     __shared__ uint32_t s_hi[kCCT];
-    if (threadIdx.x == 0) s_tile = atomicAdd(&state[0], 1u);
+    if (threadIdx.x == 0) { PA_CK(state, 8); s_tile = atomicAdd(&state[0], 1u); }
     for (uint32_t i = threadIdx.x; i < kCCTile; i += blockDim.x) s_clo[i] = s_chi[i] = 0u;
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -428,6 +431,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
         for (int i = 0; i <= P; i++) {
             const int64_t wi = wq + i;
             if (wi < 0 || wi >= (int64_t)kCCTile) continue;
+            PA_IDX_CK(wi, kCCTile);
             const uint32_t lo = (i > 0) ? m[i - 1] : 0u, hi = (i < P) ? m[i] : 0u;
             const uint32_t val = s ? __funnelshift_l(lo, hi, s) : hi;
             if (val) {
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
         for (uint32_t j = ja + threadIdx.x; j <= jb; j += blockDim.x) {
             uint32_t c[P];
 #pragma unroll
-            for (int w = 0; w < P; w++) c[w] = (DBG & 1) ? 0u : __ldg(coefT + (size_t)w * ncoef + j);
+            for (int w = 0; w < P; w++) c[w] = (DBG & 1) ? 0u : PA_LDG(coefT + (size_t)w * ncoef + j);
             const int64_t pos = (int64_t)B * j - base;        // ring / linear bit of the piece
             int64_t len = cbits;
             if (RING && pos + len > (int64_t)gamma) len = (int64_t)gamma - pos;
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
                 const int cut = (int)((int64_t)gamma - pos);
                 uint32_t c[P], h[P];
 #pragma unroll
-                for (int w = 0; w < P; w++) c[w] = coefT[(size_t)w * ncoef + j];
+                for (int w = 0; w < P; w++) c[w] = PA_AT(coefT + (size_t)w * ncoef + j);
                 // h = c >> cut (the part above the ring top), placed at ring bit 0
                 const int cw = cut >> 5, cs = cut & 31;
 #pragma unroll
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     for (int v = 0; v < kCCV; v++) {
         const uint32_t u = ub + v;
         const uint32_t iw = threadIdx.x * kCCV + v;
-        S[v] = (((uint64_t)s_chi[iw] << 32) | s_clo[iw]) + ((!RING && addend && u < n_addend) ? addend[u] : 0ull);
+        S[v] = (((uint64_t)s_chi[iw] << 32) | s_clo[iw]) + ((!RING && addend && u < n_addend) ? PA_AT(addend + u) : 0ull);
     }
     // ---- carries inside the tile (cin of word u0 handled separately, see above)
     uint32_t w[kCCV];
@@ -542,8 +546,8 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     // LINEAR with obe: the caller wants the W words as the MSB-first bit string of the whole
     // W-word integer (m = alpha = 32 W, readings A5/A8): word u lands byte-swapped at W-1-u
     auto store = [&](uint32_t u, uint32_t val) {
-        if (!RING && obe) obe[W - 1 - u] = __byte_perm(val, 0, 0x0123);
-        else out[u] = val;
+        if (!RING && obe) PA_AT(obe + (W - 1 - u)) = __byte_perm(val, 0, 0x0123);
+        else PA_AT(out + u) = val;
     };
 #pragma unroll
     for (int v = 0; v < kCCV; v++) {
@@ -582,7 +586,7 @@ __global__ void mh_extract(const uint32_t *__restrict__ Z, uint64_t nwz, uint64_
     if (4 * q >= nbytes) return;
     const int64_t lowb = (int64_t)alpha - 32 * (int64_t)(q + 1);   // Z bit of the word's LSB
     uint32_t v;
-    auto zw = [&](int64_t wi) -> uint32_t { return (wi >= 0 && (uint64_t)wi < nwz) ? Z[wi] : 0u; };
+    auto zw = [&](int64_t wi) -> uint32_t { return (wi >= 0 && (uint64_t)wi < nwz) ? PA_AT(Z + wi) : 0u; };
     if (lowb >= 0) {
         const int64_t wi = lowb >> 5;
         v = __funnelshift_r(zw(wi), zw(wi + 1), (int)(lowb & 31));
@@ -593,12 +597,12 @@ __global__ void mh_extract(const uint32_t *__restrict__ Z, uint64_t nwz, uint64_
     if (valid < 32) v &= valid <= 0 ? 0u : ~((1u << (32 - valid)) - 1u);
     const uint32_t be = __byte_perm(v, 0, 0x0123);
     if (4 * q + 4 <= nbytes && !(reinterpret_cast<uintptr_t>(out) & 3)) {
-        reinterpret_cast<uint32_t *>(out)[q] = be;                 // coalesced word store
+        PA_AT(reinterpret_cast<uint32_t *>(out) + q) = be;                 // coalesced word store
         return;
     }
 #pragma unroll
     for (int b = 0; b < 4; b++)
-        if (4 * q + b < nbytes) out[4 * q + b] = (uint8_t)(be >> (8 * b));
+        if (4 * q + b < nbytes) PA_AT(out + 4 * q + b) = (uint8_t)(be >> (8 * b));
 }
 
 }  // namespace pa

@@ -26,10 +26,10 @@ __global__ void __launch_bounds__(256) acc_export(const uint32_t *__restrict__ a
         const uint32_t q = ks.k[pi].p, q2 = ks.k[pi].p2;
         uint32_t v = 0;
         for (uint32_t s = 0; s < nslot; s++) {
-            const uint32_t a = red1p(red2p(acc[s * slot_stride + e], q2), q);   // < 4q -> < q
+            const uint32_t a = red1p(red2p(PA_AT(acc + s * slot_stride + e), q2), q);   // < 4q -> < q
             v = red1p(v + a, q);
         }
-        out[e] = (T)v;
+        PA_AT(out + e) = (T)v;
     }
 }
 
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) acc_import_u64(const uint64_t *__restrict
                                                       const PrimeSet ks, uint32_t *__restrict__ out) {
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = ks.k[e >> log2L].p;
-        out[e] = (uint32_t)(in[e] % q);
+        PA_AT(out + e) = (uint32_t)(PA_AT(in + e) % q);
     }
 }
 

@@ -10,6 +10,7 @@
 // operations; 4p < 2^32 so a sum of two never overflows.
 #pragma once
 #include <cstdint>
+#include "debug.cuh"
 
 namespace pa {
 

@@ -102,8 +102,8 @@ __device__ __forceinline__ void dft_reg(uint32_t *x, const uint32_t *tw, const u
 // omega_L^e (direction of the tables) in Montgomery form, canonical (< p).
 __device__ __forceinline__ uint32_t ltw_mont(const NttArgs &a, int pi, uint32_t e, uint32_t p,
                                              uint32_t pinv) {
-    const uint32_t lo = __ldg(a.ltw_lo + (size_t)pi * a.ltw_lo_stride + (e & ((1u << a.ltw_h) - 1)));
-    const uint32_t hi = __ldg(a.ltw_hi + (size_t)pi * a.ltw_hi_stride + (e >> a.ltw_h));
+    const uint32_t lo = PA_LDG(a.ltw_lo + (size_t)pi * a.ltw_lo_stride + (e & ((1u << a.ltw_h) - 1)));
+    const uint32_t hi = PA_LDG(a.ltw_hi + (size_t)pi * a.ltw_hi_stride + (e >> a.ltw_h));
     return red1p(mul_mont(lo, hi, p, pinv), p);
 }
 
@@ -132,7 +132,7 @@ __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SId
         for (int h = 0; h < NG; h++) {
             const int q = v + SP::TPV * h;
 #pragma unroll
-            for (int m = 0; m < R; m++) x[h * R + m] = sm[sidx(q + (S / R) * m)];
+            for (int m = 0; m < R; m++) { PA_SMEM_PTR_CK(sm + sidx(q + (S / R) * m), 4); x[h * R + m] = sm[sidx(q + (S / R) * m)]; }
         }
 #pragma unroll
         for (int h = 0; h < NG; h++)
@@ -148,9 +148,10 @@ __device__ __forceinline__ void rounds_rest(uint32_t *x, uint32_t *sm, const SId
                     const int k = bitrev<R>(mm);
                     uint32_t val = x[h * R + mm];
                     if (T > 1 && k != 0) {
-                        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(rtw_p + a.rtw_off[RHO]) + k * T + t);
+                        const uint2 w = PA_LDG(reinterpret_cast<const uint2 *>(rtw_p + a.rtw_off[RHO]) + k * T + t);
                         val = mul_shoup(val, w.x, w.y, c.p);
                     }
+                    PA_SMEM_PTR_CK(sm + sidx(g + G * k + G * R * t), 4);
                     sm[sidx(g + G * k + G * R * t)] = val;
                 }
             }
@@ -183,9 +184,10 @@ __device__ __forceinline__ void round0_finish(uint32_t *x, uint32_t *sm, const S
                 const int k = bitrev<R>(mm);
                 uint32_t val = x[h * R + mm];
                 if (T > 1 && k != 0) {
-                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(rtw_p + a.rtw_off[0]) + k * T + t);
+                    const uint2 w = PA_LDG(reinterpret_cast<const uint2 *>(rtw_p + a.rtw_off[0]) + k * T + t);
                     val = mul_shoup(val, w.x, w.y, c.p);
                 }
+                PA_SMEM_PTR_CK(sm + sidx(k + R * t), 4);
                 sm[sidx(k + R * t)] = val;
             }
         }

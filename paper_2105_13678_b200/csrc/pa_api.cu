@@ -82,6 +82,70 @@ extern "C" int pa_last_error(char *buf, size_t len) {
     return g_err;
 }
 
+// ====================================================================== debug build
+// PA_DEBUG (debug.cuh): the device-side table of valid global ranges -- every allocation of
+// every context on the device, plus the caller's buffers of the current call.  Uploaded
+// (after a device synchronize) whenever it changes; graphs are off in this build.
+#ifdef PA_DEBUG
+#include <mutex>
+namespace {
+struct DbgDev {
+    std::vector<pa::DbgRange> perm, user;
+};
+std::mutex g_dbg_mu;
+std::map<int, DbgDev> g_dbg_dev;
+void dbg_upload_locked(int dev) {
+    DbgDev &d = g_dbg_dev[dev];
+    std::vector<pa::DbgRange> all = d.perm;
+    for (const auto &r : d.user) if (all.size() < (size_t)pa::kDbgMaxRanges) all.push_back(r);
+    if (all.size() > (size_t)pa::kDbgMaxRanges) all.resize(pa::kDbgMaxRanges);
+    const uint32_t n = (uint32_t)all.size();
+    cudaDeviceSynchronize();
+    if (n) cudaMemcpyToSymbol(pa::g_dbg_ranges, all.data(), n * sizeof(pa::DbgRange));
+    cudaMemcpyToSymbol(pa::g_dbg_n, &n, sizeof n);
+}
+}  // namespace
+static void dbg_add(const void *p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_dbg_mu);
+    g_dbg_dev[dev].perm.push_back({(uint64_t)p, (uint64_t)p + bytes});
+    dbg_upload_locked(dev);
+}
+static void dbg_remove(const void *p) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_dbg_mu);
+    auto &v = g_dbg_dev[dev].perm;
+    for (size_t i = 0; i < v.size(); i++)
+        if (v[i].lo == (uint64_t)p) { v.erase(v.begin() + i); break; }
+    dbg_upload_locked(dev);
+}
+// the caller's buffers of this call (replaces those of the previous call)
+static void dbg_user(std::initializer_list<std::pair<const void *, uint64_t>> bufs) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_dbg_mu);
+    auto &u = g_dbg_dev[dev].user;
+    u.clear();
+    for (const auto &b : bufs)
+        if (b.first && b.second) u.push_back({(uint64_t)b.first, (uint64_t)b.first + b.second});
+    dbg_upload_locked(dev);
+}
+static void dbg_user_add(const void *p, uint64_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_dbg_mu);
+    if (p && bytes) g_dbg_dev[dev].user.push_back({(uint64_t)p, (uint64_t)p + bytes});
+    dbg_upload_locked(dev);
+}
+#else
+static inline void dbg_add(const void *, size_t) {}
+static inline void dbg_remove(const void *) {}
+static inline void dbg_user(std::initializer_list<std::pair<const void *, uint64_t>>) {}
+static inline void dbg_user_add(const void *, uint64_t) {}
+#endif
+
 // ====================================================================== planning
 static constexpr int kMinLog2L = 10;
 static constexpr int kMaxLog2L = 23;
@@ -336,11 +400,13 @@ struct DevAlloc {
         }
         blks.push_back({q, b});
         bytes += b;
+        dbg_add(q, b);
         *p = (T *)q;
         return PA_OK;
     }
     void free_all() {
         for (const Blk &k : blks) {
+            dbg_remove(k.p);
             if (fn_alloc) {
                 if (fn_free) fn_free(k.p, k.bytes, (void *)stream, user);
             } else {
@@ -1192,6 +1258,7 @@ static int toeplitz_alloc_and_precompute(pa_ctx *c) {
     TRY(expand_words(p.seed, kStreamT, nd, dw, false));
     uint32_t *dw_dev = nullptr;
     CUDA_TRY(cudaMallocAsync(&dw_dev, dw.size() * 4, c->stream));
+    dbg_add(dw_dev, dw.size() * 4);
     CUDA_TRY(cudaMemcpyAsync(dw_dev, dw.data(), dw.size() * 4, cudaMemcpyHostToDevice, c->stream));
     const uint64_t tot = (uint64_t)ne * L;
     toeplitz_pack_diag<<<(uint32_t)std::min<uint64_t>(cdiv(tot, 256), (uint64_t)g_num_sms * 16), 256, 0,
@@ -1199,6 +1266,7 @@ static int toeplitz_alloc_and_precompute(pa_ctx *c) {
     int rc = cudaGetLastError() == cudaSuccess ? PA_OK : set_err(PA_E_CUDA, "toeplitz_pack_diag launch failed");
     if (rc == PA_OK) rc = tz_forward(c, c->res, ne, sd.pl.n_col, c->ahat, c->tz_scale + 1, "pre_col", "pre_row");
     const cudaError_t e = cudaStreamSynchronize(c->stream);
+    dbg_remove(dw_dev);
     cudaFreeAsync(dw_dev, c->stream);
     if (rc != PA_OK) return rc;
     if (e != cudaSuccess) return set_err(PA_E_CUDA, "Toeplitz precompute failed: %s", cudaGetErrorString(e));
@@ -1339,6 +1407,8 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     uint32_t *a_dev = nullptr, *b_dev = nullptr;
     CUDA_TRY(cudaMallocAsync(&a_dev, std::max<size_t>(aw.size() * 4, 16), c->stream));
     CUDA_TRY(cudaMallocAsync(&b_dev, Wal32 * 4, c->stream));
+    dbg_add(a_dev, std::max<size_t>(aw.size() * 4, 16));
+    dbg_add(b_dev, Wal32 * 4);
     CUDA_TRY(cudaMemcpyAsync(a_dev, aw.data(), aw.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(b_dev, bw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->c_words, cw.data(), Wal32 * 4, cudaMemcpyHostToDevice, c->stream));
@@ -1347,6 +1417,8 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     WordSrc wsb{b_dev, (uint32_t)Wal32, Bh, (uint32_t)cdiv(p.alpha, Bh)};
     if (rc == PA_OK) rc = precompute_hat(c, c->smh, wsb, 1, rows_b, c->scratch_mh, c->bhat);
     cudaError_t e = cudaStreamSynchronize(c->stream);
+    dbg_remove(a_dev);
+    dbg_remove(b_dev);
     cudaFreeAsync(a_dev, c->stream);
     cudaFreeAsync(b_dev, c->stream);
     if (rc != PA_OK) return rc;
@@ -1742,6 +1814,10 @@ static int hash_enqueue(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
 // captured once into a CUDA graph per (key, out) pointer pair and replayed: no host
 // launch overhead, no inter-kernel launch gaps.  PA_NO_GRAPH=1 disables it.
 static bool graphs_enabled(const pa_ctx *c) {
+#ifdef PA_DEBUG
+    (void)c;
+    return false;                         // the range table is uploaded per call
+#endif
     static const bool off = getenv("PA_NO_GRAPH") && atoi(getenv("PA_NO_GRAPH"));
     return !off && c->stream != nullptr && !c->prof;
 }
@@ -1794,9 +1870,19 @@ static int graph_run(pa_ctx *c, GraphSlot &gs, const std::vector<const void *> &
     return PA_OK;
 }
 
+// bytes of the key (slice) a call on this context reads
+static uint64_t key_slice_len(const pa_ctx *c) {
+    const Plan &p = c->pl;
+    const uint64_t nb = cdiv(p.n, 8);
+    if (p.paper_k || p.mh_only || p.toeplitz) return nb;
+    const uint64_t R = p.r / 8;
+    return std::min(p.b1 * R, nb) - std::min(p.b0 * R, nb);
+}
+
 extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     if (!c || !key_bits) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
+    dbg_user({{key_bits, key_slice_len(c)}, {out_bits, cdiv(c->pl.m, 8)}});
     if (c->comm) return mg_hash(c, key_bits, out_bits, 0, 0);
     if (!out_bits) return set_err(PA_E_PARAM, "NULL argument");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k)
@@ -1809,6 +1895,7 @@ extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
 extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_out) {
     if (!c || !key_slice || !y_out) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
+    dbg_user({{key_slice, key_slice_len(c)}, {y_out, c->Wg * 4}});
     if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     c->launches = 0;
     TRY(carry_reset(c));
@@ -1823,6 +1910,7 @@ extern "C" int pa_mmh_partial(pa_ctx *c, const uint8_t *key_slice, uint32_t *y_o
 extern "C" int pa_mh_merge(pa_ctx *c, const uint32_t *y_parts, uint32_t G, uint8_t *out_bits) {
     if (!c || !y_parts || !out_bits || G == 0) return set_err(PA_E_PARAM, "bad argument");
     DevGuard dg_(c);
+    dbg_user({{y_parts, (uint64_t)G * c->Wg * 4}, {out_bits, cdiv(c->pl.m, 8)}});
     if (G > (1u << 24)) return set_err(PA_E_PARAM, "too many parts");
     if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     c->launches = 0;
@@ -1884,6 +1972,11 @@ static int batch_enqueue(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *
 extern "C" int pa_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
     if (!c || (count && (!keys || !outs))) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
+    dbg_user({});
+    for (uint32_t j = 0; j < count; j++) {
+        dbg_user_add(keys[j], key_slice_len(c));
+        dbg_user_add(outs[j], cdiv(c->pl.m, 8));
+    }
     if (c->pl.mh_only || c->pl.toeplitz) return set_err(PA_E_STATE, "comparator context: use pa_hash");
     if (c->comm) return mg_hash_batch(c, keys, outs, count);
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
@@ -2045,6 +2138,7 @@ extern "C" int pa_nccl_unique_id(uint8_t *id_out) {
 extern "C" int pa_mmh_acc(pa_ctx *c, const uint8_t *key_slice, uint32_t *acc_out) {
     if (!c || !key_slice || !acc_out) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
+    dbg_user({{key_slice, key_slice_len(c)}, {acc_out, 4ull * c->pl.mmh.nprimes * c->smmh.L}});
     if (c->pl.mh_only || c->pl.toeplitz || c->pl.paper_k) return set_err(PA_E_STATE, "r-bit MMH-MH contexts only");
     c->launches = 0;
     int rc = run_mmh_acc(c, key_slice);
@@ -2056,6 +2150,7 @@ extern "C" int pa_mmh_acc(pa_ctx *c, const uint8_t *key_slice, uint32_t *acc_out
 extern "C" int pa_tail_merge(pa_ctx *c, const uint32_t *acc_parts, uint32_t G, uint8_t *out_bits) {
     if (!c || !acc_parts || !out_bits || G == 0) return set_err(PA_E_PARAM, "bad argument");
     DevGuard dg_(c);
+    dbg_user({{acc_parts, 4ull * G * c->pl.mmh.nprimes * c->smmh.L}, {out_bits, cdiv(c->pl.m, 8)}});
     if (c->pl.mh_only || c->pl.toeplitz || c->pl.paper_k) return set_err(PA_E_STATE, "r-bit MMH-MH contexts only");
     if (G > 4096) return set_err(PA_E_PARAM, "too many parts");
     c->launches = 0;
@@ -2352,4 +2447,48 @@ extern "C" int pa_expand_bc(uint64_t seed, uint64_t alpha, uint32_t *b_out, uint
     TRY(expand_words(seed, kStreamC, alpha, w, false));
     memcpy(c_out, w.data(), w.size() * 4);
     return PA_OK;
+}
+
+// ====================================================================== debug-build probes
+extern "C" int pa_debug_build(void) {
+#ifdef PA_DEBUG
+    return 1;
+#else
+    return 0;
+#endif
+}
+
+#ifdef PA_DEBUG
+// soft-mode probe: one registered range, one address past its end, one smem index past the
+// dynamic allocation -> exactly 2 violations counted
+__global__ void dbg_selftest_k(const uint32_t *inside, const uint32_t *past_end) {
+    extern __shared__ uint32_t dsm[];
+    PA_CK(inside, 4);
+    PA_CK(past_end, 4);
+    PA_SMEM_CK(8);                       // launched with 32 bytes of dynamic smem: index 8 is out
+    PA_SMEM_CK(7);
+    if (threadIdx.x == 1024) dsm[0] = 0;  // keeps dsm referenced
+}
+#endif
+
+extern "C" int pa_debug_selftest(void) {
+#ifdef PA_DEBUG
+    uint32_t *buf = nullptr;
+    CUDA_TRY(cudaMalloc(&buf, 64));
+    dbg_add(buf, 64);
+    const uint32_t one = 1, zero = 0;
+    CUDA_TRY(cudaMemcpyToSymbol(pa::g_dbg_soft, &one, 4));
+    CUDA_TRY(cudaMemcpyToSymbol(pa::g_dbg_violations, &zero, 4));
+    dbg_selftest_k<<<1, 1, 32>>>(buf + 15, buf + 16);
+    CUDA_TRY(cudaDeviceSynchronize());
+    uint32_t nv = 0;
+    CUDA_TRY(cudaMemcpyFromSymbol(&nv, pa::g_dbg_violations, 4));
+    CUDA_TRY(cudaMemcpyToSymbol(pa::g_dbg_soft, &zero, 4));
+    dbg_remove(buf);
+    cudaFree(buf);
+    if (nv != 2) return set_err(PA_E_STATE, "debug self-test counted %u violations, expected 2", nv);
+    return PA_OK;
+#else
+    return set_err(PA_E_STATE, "not a PA_DEBUG build");
+#endif
 }

@@ -29,13 +29,13 @@ __device__ __forceinline__ uint32_t key_word(const KeySrc &s, int64_t widx) {
     const int64_t base = widx * 4;
     if (base < 0) return 0;
     if (s.aligned && base + 4 < (int64_t)s.nbytes)
-        return __ldg(reinterpret_cast<const uint32_t *>(s.key) + widx);
+        return PA_LDG(reinterpret_cast<const uint32_t *>(s.key) + widx);
     uint32_t w = 0;
 #pragma unroll
     for (int b = 0; b < 4; b++) {
         const int64_t pos = base + b;
         if (pos < (int64_t)s.nbytes) {
-            uint32_t v = s.key[pos];
+            uint32_t v = PA_AT(s.key + pos);
             if (pos == (int64_t)s.nbytes - 1) v &= s.last_mask;
             w |= v << (8 * b);
         }
@@ -104,9 +104,9 @@ __device__ __forceinline__ uint64_t word_limb(const WordSrc &s, uint32_t vec, ui
     const uint32_t wi = (uint32_t)(bit >> 5);
     const int sh = (int)(bit & 31);
     const uint32_t *base = s.w + (size_t)vec * s.words;
-    const uint32_t a0 = wi < s.words ? __ldg(base + wi) : 0u;
-    const uint32_t a1 = wi + 1 < s.words ? __ldg(base + wi + 1) : 0u;
-    const uint32_t a2 = wi + 2 < s.words ? __ldg(base + wi + 2) : 0u;
+    const uint32_t a0 = wi < s.words ? PA_LDG(base + wi) : 0u;
+    const uint32_t a1 = wi + 1 < s.words ? PA_LDG(base + wi + 1) : 0u;
+    const uint32_t a2 = wi + 2 < s.words ? PA_LDG(base + wi + 2) : 0u;
     const uint64_t v = ((uint64_t)__funnelshift_r(a1, a2, sh) << 32) | __funnelshift_r(a0, a1, sh);
     return s.limb_bits >= 64 ? v : (v & ((1ull << s.limb_bits) - 1));
 }
@@ -122,10 +122,10 @@ __device__ __forceinline__ void word_limb_words(const WordSrc &s, uint32_t vec, 
     const uint32_t wi = (uint32_t)(bit >> 5);
     const int sh = (int)(bit & 31);
     const uint32_t *base = s.w + (size_t)vec * s.words;
-    uint32_t prev = wi < s.words ? __ldg(base + wi) : 0u;
+    uint32_t prev = wi < s.words ? PA_LDG(base + wi) : 0u;
 #pragma unroll
     for (int i = 0; i < NW; i++) {
-        const uint32_t nx = wi + i + 1 < s.words ? __ldg(base + wi + i + 1) : 0u;
+        const uint32_t nx = wi + i + 1 < s.words ? PA_LDG(base + wi + i + 1) : 0u;
         uint32_t v = __funnelshift_r(prev, nx, sh);
         const int left = (int)s.limb_bits - 32 * i;          // limb bits from this word up
         if (left <= 0) v = 0;
@@ -191,11 +191,11 @@ __device__ __forceinline__ void store_residues(uint32_t *o, uint32_t wxp, uint32
 #pragma unroll
         for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
             if (pi >= P) break;
-            *o = limb_words_redc<NW>(w, ks.k[pi]);
+            PA_AT(o) = limb_words_redc<NW>(w, ks.k[pi]);
             o += wxp;
         }
     } else {
-        for (uint32_t pi = 0; pi < P; pi++, o += wxp) *o = 0u;
+        for (uint32_t pi = 0; pi < P; pi++, o += wxp) PA_AT(o) = 0u;
     }
 }
 
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeS
             const uint64_t v = src(iv, j);
 #pragma unroll
             for (uint32_t pi = 0; pi < kMaxPrimes; pi++)
-                if (pi < P) o[(size_t)pi * wxp] = v ? limb_redc(v, ks.k[pi].p, ks.k[pi].pinv) : 0u;
+                if (pi < P) PA_AT(o + (size_t)pi * wxp) = v ? limb_redc(v, ks.k[pi].p, ks.k[pi].pinv) : 0u;
         } else {
             uint32_t w[NW];
             src.template words<NW>(iv, j, w);
@@ -252,7 +252,7 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
         for (uint32_t pi = 0; pi < P; pi++, o += wxp)
 #pragma unroll
             for (int q = 0; q < kPackL; q++)
-                if (j0 + q * kPackT < wxp) o[q * kPackT] = 0u;
+                if (j0 + q * kPackT < wxp) PA_AT(o + q * kPackT) = 0u;
         return;
     }
 #if PA_PACK_CHUNK24
@@ -267,7 +267,7 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
 #pragma unroll
             for (int q = 0; q < kPackL; q++) {
                 const uint32_t r = limb_chunks_redc<NC>(c[q], ks.k[pi]);
-                if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
+                if (j0 + q * kPackT < wxp) PA_AT(o + q * kPackT) = r;
             }
             o += wxp;
         }
@@ -280,7 +280,7 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
 #pragma unroll
             for (int q = 0; q < kPackL; q++) {
                 const uint32_t r = limb_words_redc<NW>(w[q], ks.k[pi]);
-                if (j0 + q * kPackT < wxp) o[q * kPackT] = r;
+                if (j0 + q * kPackT < wxp) PA_AT(o + q * kPackT) = r;
             }
             o += wxp;
         }
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
 #pragma unroll
         for (int u = 0; u < KU; u++) {
             const int k = threadIdx.x + u * kPackT;
-            v[u] = (k < nw) ? __ldg(kw + k) : 0u;
+            v[u] = (k < nw) ? PA_LDG(kw + k) : 0u;
         }
     } else {
         for (int u = 0; u < KU; u++) {
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
 #pragma unroll
     for (int u = 0; u < KU; u++) {
         const int k = threadIdx.x + u * kPackT;
-        if (k < nw) sw[k] = v[u];
+        if (k < nw) { PA_IDX_CK(k, MAXW); sw[k] = v[u]; }
     }
     __syncthreads();
     // limb j's NW words (big-endian bytes, readings A3/A4).  Byte offsets relative to the
@@ -345,9 +345,11 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
         const int hi = (int)(s.blk_bytes - (uint32_t)LB * j) - base;
         const int sh = (hi & 3) * 8;
         const int wtop = (hi >> 2) - 1;                       // staged word holding byte hi - 4
+        PA_IDX_CK(wtop + 1, MAXW);
         uint32_t nxt = sw[wtop + 1];
 #pragma unroll
         for (int i = 0; i < NW; i++) {
+            PA_IDX_CK(max(wtop - i, 0), MAXW);
             const uint32_t cur = sw[max(wtop - i, 0)];
             w[i] = __byte_perm(__funnelshift_r(cur, nxt, sh), 0, 0x0123);
             nxt = cur;
@@ -439,7 +441,7 @@ __global__ void __launch_bounds__(256) window_flags(const KeySrc s, uint32_t gam
         found = __syncthreads_or(z != 0) ? 1u : 0u;
     }
     if (threadIdx.x == 0) {
-        flags[t] = found;
+        PA_AT(flags + t) = found;
         __threadfence();
         s_last = (atomicAdd(done, 1u) == T - 1);
     }
@@ -448,9 +450,9 @@ __global__ void __launch_bounds__(256) window_flags(const KeySrc s, uint32_t gam
     __threadfence();
     uint32_t i = 0;
     for (uint32_t u = 0; u < T && i < k; u++)
-        if (((volatile uint32_t *)flags)[u]) offs[i++] = (uint64_t)u * gamma;
+        if (((volatile uint32_t *)flags)[u]) { PA_CK(offs + i, 8); offs[i++] = (uint64_t)u * gamma; }
     *status = (i < k) ? 1u : 0u;
-    for (; i < k; i++) offs[i] = 0;                            // output undefined; reads stay in bounds
+    for (; i < k; i++) PA_AT(offs + i) = 0;                            // output undefined; reads stay in bounds
 }
 
 // S1 in paper mode: block iv = the gamma-bit window at key bit offs[iv]; limb j, word w =
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(kPackT) pack_bits_residues(const KeySrc s, con
 #pragma unroll
         for (int u = 0; u < KU; u++) {
             const int k = threadIdx.x + u * kPackT;
-            if (k < nw && k < MAXW) sw[k] = v[u];
+            if (k < nw && k < MAXW) { PA_IDX_CK(k, MAXW); sw[k] = v[u]; }
         }
     }
     __syncthreads();
@@ -546,7 +548,7 @@ __global__ void key_to_words(const KeySrc s, uint64_t n, uint32_t W, uint32_t *_
     const uint64_t be = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
     uint32_t v = (uint32_t)(be >> (32 - sh));
     if (q < 0) v &= 0xFFFFFFFFu >> (-q);                        // positions before bit 0 of the key
-    out[u] = v;
+    PA_AT(out + u) = v;
 }
 
 struct KeyLimbs {
@@ -629,8 +631,8 @@ col_pass(const ColArgs A) {
             cx.p = pk.p; cx.p2 = pk.p2; cx.pinv = pk.pinv;
 #pragma unroll
             for (int j = 0; j < E / 2; j++) {
-                tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j * (32 / E));
-                twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j * (32 / E));
+                tw[j] = PA_LDG(a.regtw + pi * a.regtw_stride + j * (32 / E));
+                twp[j] = PA_LDG(a.regtwp + pi * a.regtw_stride + j * (32 / E));
             }
             rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
         }
@@ -648,7 +650,7 @@ col_pass(const ColArgs A) {
                     (void)dummy;
                     const int rel = SP::TPV * h + (SP::S / R) * m;          // in_pos - v
                     uint32_t val = 0;
-                    if (MODE == COL_INV || (uint32_t)(v + rel) < rows) val = src[(size_t)rel << N1_LOG];
+                    if (MODE == COL_INV || (uint32_t)(v + rel) < rows) val = PA_AT(src + ((size_t)rel << N1_LOG));
                     x[h * R + m] = val;
                 }
             }
@@ -677,11 +679,11 @@ col_pass(const ColArgs A) {
                     const size_t o = (size_t)rel << N1_LOG;
                     uint32_t val = x[h * R + mm];
                     if constexpr (MODE != COL_INV) {
-                        const uint2 w = __ldg(tw4 + o);
+                        const uint2 w = PA_LDG(tw4 + o);
                         val = mul_shoup(val, w.x, w.y, cx.p);
                     }
                     else val = red1p(val, cx.p);
-                    dst[o] = val;
+                    PA_AT(dst + o) = val;
                 }
             }
         }
@@ -731,8 +733,8 @@ row_pass(const RowArgs A) {
         uint32_t tw[E / 2], twp[E / 2];
 #pragma unroll
         for (int j = 0; j < E / 2; j++) {
-            tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j * (32 / E));
-            twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j * (32 / E));
+            tw[j] = PA_LDG(a.regtw + pi * a.regtw_stride + j * (32 / E));
+            twp[j] = PA_LDG(a.regtwp + pi * a.regtw_stride + j * (32 / E));
         }
         const uint32_t *rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
         uint32_t acc[E];
@@ -750,7 +752,7 @@ row_pass(const RowArgs A) {
                 for (int h = 0; h < E / R; h++)
 #pragma unroll
                     for (int m = 0; m < R; m++) {
-                        const uint32_t t = src[in_pos<S_LOG, E_LOG>(v, h, m)];
+                        const uint32_t t = PA_AT(src + in_pos<S_LOG, E_LOG>(v, h, m));
                         // ROW_INV input: accumulators merged with red.add, in [0, 4p)
                         x[h * R + m] = (MODE == ROW_INV) ? red2p(t, cx.p2) : t;
                     }
@@ -764,7 +766,7 @@ row_pass(const RowArgs A) {
                     for (int h = 0; h < E / R; h++)
 #pragma unroll
                         for (int m = 0; m < R; m++)
-                            x[h * R + m] = red2p(x[h * R + m] + red2p(sq[in_pos<S_LOG, E_LOG>(v, h, m)], cx.p2), cx.p2);
+                            x[h * R + m] = red2p(x[h * R + m] + red2p(PA_AT(sq + in_pos<S_LOG, E_LOG>(v, h, m)), cx.p2), cx.p2);
                 }
             }
             __syncthreads();
@@ -778,7 +780,7 @@ row_pass(const RowArgs A) {
 #pragma unroll
                     for (int mm = 0; mm < R; mm++) {
                         const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
-                        acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], __ldg(ah + k1), cx.p, cx.pinv), cx.p2);
+                        acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], PA_LDG(ah + k1), cx.p, cx.pinv), cx.p2);
                     }
             } else if constexpr (MODE == ROW_STORE) {
                 const uint32_t sc = A.scale[pi];
@@ -788,7 +790,7 @@ row_pass(const RowArgs A) {
 #pragma unroll
                     for (int mm = 0; mm < R; mm++) {
                         const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
-                        dst[k1] = red1p(mul_mont(x[h * R + mm], sc, cx.p, cx.pinv), cx.p);
+                        PA_AT(dst + k1) = red1p(mul_mont(x[h * R + mm], sc, cx.p, cx.pinv), cx.p);
                     }
             } else {
                 uint32_t *dst = A.dst + vbase + (size_t)k2 * S;
@@ -797,8 +799,8 @@ row_pass(const RowArgs A) {
 #pragma unroll
                     for (int mm = 0; mm < R; mm++) {
                         const uint32_t j1 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
-                        const uint32_t w = __ldg(A.tw4 + (size_t)pi * L + (size_t)k2 * S + j1);
-                        dst[j1] = mul_mont(x[h * R + mm], w, cx.p, cx.pinv);
+                        const uint32_t w = PA_LDG(A.tw4 + (size_t)pi * L + (size_t)k2 * S + j1);
+                        PA_AT(dst + j1) = mul_mont(x[h * R + mm], w, cx.p, cx.pinv);
                     }
             }
         }
@@ -808,7 +810,7 @@ row_pass(const RowArgs A) {
 #pragma unroll
             for (int h = 0; h < E / R; h++)
 #pragma unroll
-                for (int mm = 0; mm < R; mm++) dst[out_pos<S_LOG, E_LOG>(v, h, mm)] = acc[h * R + mm];
+                for (int mm = 0; mm < R; mm++) PA_AT(dst + out_pos<S_LOG, E_LOG>(v, h, mm)) = acc[h * R + mm];
         }
         __syncthreads();
     }
@@ -947,6 +949,7 @@ row_mac(const MacArgs A) {
     uint32_t *const dslot = A.dst + (size_t)(blockIdx.x % A.nslot) * A.slot_stride;   // mode 0 slot
     auto flush_one = [&](uint32_t *d, uint32_t v) {
         v = red1p(v, cx.p);
+        PA_CK(d, 4);
         if (A.mode == 0) atomicAdd(d, v);
         else if (A.mode == 1) *d = v;
         else *d = red1p(*d + v, cx.p);
@@ -974,8 +977,8 @@ row_mac(const MacArgs A) {
                 cx = Ctx32{pk.p, pk.p2, pk.pinv};
 #pragma unroll
                 for (int j = 0; j < E / 2; j++) {
-                    tw[j] = __ldg(a.regtw + pi * a.regtw_stride + j * (32 / E));
-                    twp[j] = __ldg(a.regtwp + pi * a.regtw_stride + j * (32 / E));
+                    tw[j] = PA_LDG(a.regtw + pi * a.regtw_stride + j * (32 / E));
+                    twp[j] = PA_LDG(a.regtwp + pi * a.regtw_stride + j * (32 / E));
                 }
                 rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
             }
@@ -993,7 +996,7 @@ row_mac(const MacArgs A) {
 #pragma unroll
             for (int h = 0; h < E / R; h++)
 #pragma unroll
-                for (int m = 0; m < R; m++) x[h * R + m] = xst[w * S + in_pos<S_LOG, E_LOG>(v, h, m)];
+                for (int m = 0; m < R; m++) { PA_SMEM_PTR_CK((xst + w * S + in_pos<S_LOG, E_LOG>(v, h, m)), 4); x[h * R + m] = xst[w * S + in_pos<S_LOG, E_LOG>(v, h, m)]; }
         }
         if constexpr (AIN) {
             __syncthreads();                             // X stage s read: A^(it) may land there
@@ -1015,7 +1018,7 @@ row_mac(const MacArgs A) {
                 for (int mm = 0; mm < R; mm++) {
                     const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
                     if constexpr (DBG == 3) acc[h * R + mm] += x[h * R + mm];
-                    else acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], arow[k1], cx.p, cx.pinv), cx.p2);
+                    else acc[h * R + mm] = red2p(acc[h * R + mm] + mul_mont(x[h * R + mm], (PA_SMEM_PTR_CK(arow + k1, 4), arow[k1]), cx.p, cx.pinv), cx.p2);
                 }
         }
         __syncthreads();                                 // X stage s and A^ are free

@@ -5,6 +5,7 @@
 // by device kernels so a context can be re-keyed without a host round trip.
 #pragma once
 #include <cstdint>
+#include "debug.cuh"
 
 namespace pa {
 
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kExpT) expand_keys_first(uint64_t seed, uint64
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const int q = 32 * k + lane;                    // word q of the warp's 128
-                o64[q] = sw[(q & 3) * 33 + (q >> 2)];
+                PA_AT(o64 + q) = sw[(q & 3) * 33 + (q >> 2)];
             }
             __syncwarp();
         } else if (live) {
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(kExpT) expand_keys_first(uint64_t seed, uint64
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     const uint64_t i32 = 8 * blk + 2 * e + h;
-                    if (i32 < nw32) o[i32] = (uint32_t)(r[e] >> (32 * h));
+                    if (i32 < nw32) PA_AT(o + i32) = (uint32_t)(r[e] >> (32 * h));
                 }
         }
     }
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(256) expand_keys_dev(uint64_t seed, uint64_t s
                     uint32_t v = (uint32_t)(r[e] >> (32 * h));
                     if (i32 == nw32 - 1) v &= topmask;
                     if (i32 == 0 && force_odd) v |= 1u;
-                    o[i32] = v;
+                    PA_AT(o + i32) = v;
                     allones &= (v == (i32 == nw32 - 1 ? topmask : 0xFFFFFFFFu));
                 }
             }

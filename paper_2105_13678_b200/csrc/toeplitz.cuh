@@ -26,11 +26,11 @@ __global__ void __launch_bounds__(256) toeplitz_pack_bits(const uint8_t *__restr
         const uint64_t t0 = i << 2;                          // first bit of the nibble
         uint32_t nib = 0;
         if (t0 < n) {
-            const uint32_t byte = __ldg(key + (t0 >> 3));
+            const uint32_t byte = PA_LDG(key + (t0 >> 3));
             nib = (i & 1) ? (byte & 0xFu) : (byte >> 4);      // MSB-first: even chunk = high nibble
             if (t0 + 4 > n) nib &= (0xF0u >> (n - t0)) & 0xFu;   // bits >= n are 0
         }
-        reinterpret_cast<uint4 *>(out)[i] = make_uint4((nib >> 3) & 1u, (nib >> 2) & 1u, (nib >> 1) & 1u, nib & 1u);
+        PA_AT(reinterpret_cast<uint4 *>(out) + i) = make_uint4((nib >> 3) & 1u, (nib >> 2) & 1u, (nib >> 1) & 1u, nib & 1u);
     }
 }
 
@@ -48,9 +48,9 @@ __global__ void __launch_bounds__(256) toeplitz_pack_diag(const uint32_t *__rest
         uint32_t v = 0;
         if (s + 1 < L) {
             const int64_t idx = (int64_t)m + ((int64_t)dp - (int64_t)(O - 1)) * (int64_t)r + (int64_t)r - 2 - (int64_t)s;
-            if (idx >= 0 && (uint64_t)idx < nd) v = (__ldg(dw + (idx >> 5)) >> (idx & 31)) & 1u;
+            if (idx >= 0 && (uint64_t)idx < nd) v = (PA_LDG(dw + (idx >> 5)) >> (idx & 31)) & 1u;
         }
-        out[t] = v;
+        PA_AT(out + t) = v;
     }
 }
 
@@ -76,12 +76,12 @@ __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__
         for (int o = 0; o < O; o++) {
             a[o] = 0;
             t[o] = 0;
-            w[o] = __ldg(Eh + (size_t)(O - 1 - o) * L + e);        // w[o] = E[b + O - 1 - o] at b = 0
+            w[o] = PA_LDG(Eh + (size_t)(O - 1 - o) * L + e);        // w[o] = E[b + O - 1 - o] at b = 0
         }
         uint32_t g = 0;
 #pragma unroll 7
         for (uint32_t b = 0; b < nb; b++) {
-            const uint32_t x = __ldg(Xh + (size_t)b * L + e);
+            const uint32_t x = PA_LDG(Xh + (size_t)b * L + e);
 #pragma unroll
             for (int o = 0; o < O; o++) t[o] = mad_wide(x, w[o], t[o]);
             if (++g == kTzGroup) {
@@ -95,13 +95,13 @@ __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__
             if (b + 1 < nb) {
 #pragma unroll
                 for (int o = O - 1; o > 0; o--) w[o] = w[o - 1];
-                w[0] = __ldg(Eh + (size_t)(b + O) * L + e);
+                w[0] = PA_LDG(Eh + (size_t)(b + O) * L + e);
             }
         }
 #pragma unroll
         for (int o = 0; o < O; o++) {
             a[o] = red2p(a[o] + red2p(redc64(t[o], p, pinv), p2), p2);
-            acc[(size_t)o * L + e] = red1p(a[o], p);
+            PA_AT(acc + (size_t)o * L + e) = red1p(a[o], p);
         }
     }
 }
@@ -116,11 +116,11 @@ __global__ void __launch_bounds__(256) toeplitz_extract(const uint32_t *__restri
     for (uint64_t wq = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wq * 32 < m; wq += nwarps) {
         const uint64_t j = wq * 32 + lane;
         uint32_t bit = 0;
-        if (j < m) bit = __ldg(acc + (j >> log2r) * L + (r - 1) + (j & (r - 1))) & 1u;
+        if (j < m) bit = PA_LDG(acc + (j >> log2r) * L + (r - 1) + (j & (r - 1))) & 1u;
         const uint32_t mask = __brev(__ballot_sync(0xFFFFFFFFu, bit));   // bit 31 = output bit 32 wq
         if (lane < 4) {
             const uint64_t q = wq * 4 + lane;
-            if (q < nbytes) out[q] = (uint8_t)(mask >> (24 - 8 * lane));
+            if (q < nbytes) PA_AT(out + q) = (uint8_t)(mask >> (24 - 8 * lane));
         }
     }
 }

@@ -267,3 +267,12 @@ def test_nccl_unique_id_host_only():
         assert e.code == B.PA_E_NCCL
         pytest.skip(f"NCCL not loadable here: {e}")
     assert len(a) == 128 and len(b) == 128 and a != b
+
+
+def test_debug_build_flag():
+    # release _pa.so reports 0 and refuses the self-test; the bounds-asserting build
+    # (_pa_debug.so, -DPA_DEBUG) is exercised on the GPU by tests/test_gpu_multigpu.py
+    if os.environ.get("PA_DEV_LIB"):
+        pytest.skip("a development library is loaded")
+    assert B.pa_debug_build() == 0
+    assert B.pa_debug_selftest() == B.PA_E_STATE

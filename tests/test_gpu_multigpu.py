@@ -143,3 +143,13 @@ def test_torch_allocator_and_default_allocator_agree():
         if ta:
             assert torch.cuda.memory_allocated() == before
     assert outs[0] == outs[1] == hashes.pa_hash_seeded(key, n, r, m, seed)
+
+
+def test_debug_build_catches_out_of_range():
+    # under the bounds-asserting build (PA_DEV_LIB=.../_pa_debug.so, scripts/gpu_debug.sh)
+    # the checker must catch one out-of-range global address and one shared index
+    from paper_2105_13678_b200 import _binding as B
+    if B.pa_debug_build() != 1:
+        pytest.skip("release build loaded (run the suite with PA_DEV_LIB=_pa_debug.so)")
+    torch.cuda.init()
+    assert B.pa_debug_selftest() == B.PA_OK
