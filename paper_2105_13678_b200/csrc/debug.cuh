@@ -47,11 +47,13 @@ __device__ __forceinline__ uint32_t dbg_dyn_smem_bytes() {
 
 }  // namespace pa
 namespace pa {
+// static shared memory lies below the dynamic array, which ends at its base + the launch's
+// dynamic size: a shared access is in bounds iff it ends at or below that end
 __device__ __forceinline__ void dbg_smem_check(const void *p, uint64_t bytes, const char *what, const char *file, int line) {
-    uint32_t tot;
-    asm("mov.u32 %0, %%total_smem_size;" : "=r"(tot));
+    extern __shared__ __align__(16) uint8_t pa_dbg_dyn_base[];
+    const uint32_t end = (uint32_t)__cvta_generic_to_shared(pa_dbg_dyn_base) + dbg_dyn_smem_bytes();
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    if ((uint64_t)a + bytes > tot) dbg_fail(what, file, line, a, tot);
+    if ((uint64_t)a + bytes > end) dbg_fail(what, file, line, a, end);
 }
 __device__ __forceinline__ void dbg_idx_check(int64_t i, int64_t n, const char *what, const char *file, int line) {
     if (i < 0 || i >= n) dbg_fail(what, file, line, (uint64_t)i, (uint64_t)n);
