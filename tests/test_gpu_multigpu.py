@@ -86,7 +86,8 @@ def test_nccl_one_rank_hash_and_rotating_batch(on_stream):
         for kk, o in zip(keys, outs):
             assert bytes(o.cpu().numpy()) == hashes.pa_hash_seeded(kk, n, r, m, seed)
         info = ctx.query()
-        if on_stream:
+        from paper_2105_13678_b200 import _binding as B
+        if on_stream and not B.pa_debug_build():          # the debug build captures no graphs
             # new key / output pointers re-capture and update the graphs in place
             assert info["graph_captures"] >= 2 and info["graph_instantiations"] <= info["graph_captures"]
         ctx.close()
@@ -121,6 +122,9 @@ def test_graph_update_on_new_pointers():
             s.synchronize()
             assert bytes(out.cpu().numpy()) == hashes.pa_hash_seeded(key, n, r, m, seed)
         info = ctx.query()
+        from paper_2105_13678_b200 import _binding as B
+        if B.pa_debug_build():
+            pytest.skip("the bounds-asserting build captures no graphs")
         assert info["graph_captures"] >= 2
         assert info["graph_instantiations"] == 1 and info["graph_updates"] == info["graph_captures"] - 1
         ctx.close()
