@@ -45,6 +45,7 @@ template <int P>
 #endif
 __global__ void __launch_bounds__(128, PA_CRT_MINB) crt_coeffs(const uint32_t *__restrict__ res, uint32_t L, uint32_t ncoef,
                                                   const CrtK K, uint32_t *__restrict__ coef) {
+    PA_TMARK(0x4000 | P, 0);
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= ncoef) return;
     uint32_t y[P];
@@ -308,15 +309,35 @@ __device__ void mersenne_finish_dev(uint32_t *y, uint32_t Wtot, uint64_t gamma) 
             else PA_AT(y + i) = 0u;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {                           // y += T (short add)
-            uint64_t cy = 0;
-            for (uint32_t t = 0; t < nT && t < Wtot; t++) {
-                PA_IDX_CK(t, 64);
-                const uint64_t s = (uint64_t)PA_AT(y + t) + T[t] + cy;
-                PA_AT(y + t) = (uint32_t)s;
-                cy = s >> 32;
+        // y += T (short add, nT <= 64 words) by the first two warps: one word per lane, the
+        // carries by generate/propagate ballots, warp 0's carry-out into warp 1; the carry out
+        // of word lim-1 (= the carry into lane lim) continues in fin_ripple
+        {
+            __shared__ uint32_t s_Cw[2], s_co[2];
+            const uint32_t t = threadIdx.x;
+            const uint32_t lim = min(nT, Wtot);
+            uint64_t sum = 0;
+            uint32_t Gm = 0, Pm = 0;
+            if (t < 64) {
+                const uint32_t yv = (t < lim) ? PA_AT(y + t) : 0u;
+                sum = (uint64_t)yv + ((t < lim) ? T[t] : 0u);
+                Gm = __ballot_sync(0xFFFFFFFFu, (uint32_t)(sum >> 32));
+                Pm = __ballot_sync(0xFFFFFFFFu, (uint32_t)sum == 0xFFFFFFFFu);
+                if (t == 0) {
+                    uint32_t co;
+                    s_Cw[0] = lane_carries(Gm, Pm, 0, co);
+                    s_co[0] = co;
+                }
             }
-            s_carry = (uint32_t)cy;
+            __syncthreads();
+            if (t == 32) {
+                uint32_t co;
+                s_Cw[1] = lane_carries(Gm, Pm, s_co[0], co);
+                s_co[1] = co;
+            }
+            __syncthreads();
+            if (t < 64 && t < lim) PA_AT(y + t) = (uint32_t)sum + ((s_Cw[t >> 5] >> (t & 31)) & 1u);
+            if (t == 0) s_carry = (lim < 64) ? ((s_Cw[lim >> 5] >> (lim & 31)) & 1u) : s_co[1];
         }
         __syncthreads();
         if (s_carry && nT < Wtot) fin_ripple(y, Wtot, nT);
@@ -354,7 +375,10 @@ __global__ void __launch_bounds__(kFinT) mersenne_finish_k(uint32_t *__restrict_
 // A tile whose carry-out does not depend on C_in (it generates, or some word does not
 // propagate) publishes C_out before waiting for its predecessor, so the chain is
 // almost never serial.  RING: the last CTA to finish runs the Mersenne finish.
-// state: [0] ticket, [1] done counter, [2 + t] tile t: bit 31 ready, bits 0..30 C_out.
+// state: [0] ticket, [kFlagStride] done counter, [kFlagStride (2 + t)] tile t: bit 31 ready,
+// bits 0..30 C_out -- one 128-byte line per word, so the publishers' stores and the
+// successors' polls of different tiles (and the two counters) do not contend for a line.
+constexpr uint32_t kFlagStride = 32;
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t *p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -409,7 +433,9 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     constexpr uint32_t cbits = 32 * P;
     __shared__ uint32_t s_tile, s_cin, s_c1, s_last;
     __shared__ uint32_t s_hi[kCCT];
-    if (threadIdx.x == 0) { PA_CK(state, 8); s_tile = atomicAdd(&state[0], 1u); }
+    constexpr uint32_t kKid = 0x5000 | P | (RING ? 0x80 : 0);
+    PA_TMARK(kKid, 0);
+    if (threadIdx.x == 0) { PA_CK(state, 4); s_tile = atomicAdd(&state[0], 1u); }
     for (uint32_t i = threadIdx.x; i < kCCTile; i += blockDim.x) s_clo[i] = s_chi[i] = 0u;
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -491,6 +517,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
         }
     }
     __syncthreads();
+    PA_TMARK_B(kKid, 2, 0x100000 | tile);
     uint64_t S[kCCV];
 #pragma unroll
     for (int v = 0; v < kCCV; v++) {
@@ -521,24 +548,28 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     const int allp = __syncthreads_and(Pall);
     uint32_t bg, cc0, cc1;
     block_carries2((int)G, Pall, &cc0, &cc1, &bg);          // both carry-ins before the look-back
+    PA_TMARK_B(kKid, 3, 0x100000 | tile);
     const uint32_t hi_last = s_hi[kCCT - 1];               // hi32 of the tile's last sum
     // the look-back flags carry their whole payload (ready bit + C_out), so relaxed gpu-scope
     // accesses suffice: no fence orders other data behind them
-    uint32_t *vs = state + 2;
+    uint32_t *vs = state + 2 * kFlagStride;
     if (threadIdx.x == 0) {
         const bool indep = bg || !allp;
         const uint32_t cout_indep = hi_last + bg;
-        if (indep) st_relaxed_gpu(vs + tile, 0x80000000u | cout_indep);
+        PA_TMARK_B(kKid, 10 + (indep ? 1 : 0) + (allp ? 2 : 0) + (bg ? 4 : 0), 0x100000 | tile);
+        if (indep) st_relaxed_gpu(vs + kFlagStride * tile, 0x80000000u | cout_indep);
         uint32_t cin = 0;
         if (tile > 0 && !(DBG & 2)) {
             uint32_t st;
-            while (!((st = ld_relaxed_gpu(vs + tile - 1)) & 0x80000000u)) { }
+            PA_CK(vs + kFlagStride * (tile - 1), 4);
+            while (!((st = ld_relaxed_gpu(vs + kFlagStride * (tile - 1))) & 0x80000000u)) __nanosleep(32);
             cin = st & 0x7FFFFFFFu;
         }
         const uint32_t c1 = (uint32_t)(((uint64_t)w[0] + cin) >> 32);     // thread 0 owns word u0
         s_cin = cin;
         s_c1 = c1;
-        if (!indep) st_relaxed_gpu(vs + tile, 0x80000000u | (hi_last + (bg | ((uint32_t)allp & c1))));
+        PA_TMARK_B(kKid, 4, 0x100000 | tile);
+        if (!indep) st_relaxed_gpu(vs + kFlagStride * tile, 0x80000000u | (hi_last + (bg | ((uint32_t)allp & c1))));
     }
     __syncthreads();
     const uint32_t cin = s_cin;
@@ -563,18 +594,24 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     if (RING && !(DBG & 4)) {
         // the CTA barrier orders every thread's output stores before thread 0's fence, which
         // (cumulatively) publishes them before the done-counter increment
+        // acq_rel atomic (cumulative release of what bar.sync made thread 0 observe; acquire
+        // for the last CTA) instead of a full sequentially-consistent fence per CTA
         __syncthreads();
         if (threadIdx.x == 0) {
-            __threadfence();
             const uint32_t ntiles = (W + kCCTile - 1) / kCCTile;
-            s_last = (atomicAdd(&state[1], 1u) == ntiles - 1);
+            uint32_t old;
+            PA_CK(state + kFlagStride, 4);
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(state + kFlagStride) : "memory");
+            s_last = (old == ntiles - 1);
         }
         __syncthreads();
         if (s_last) {
-            __threadfence();
+            __threadfence();                                  // one CTA: acquire for every thread
             mersenne_finish_dev(out, Wfin, gamma);
+            PA_TMARK_B(kKid, 6, 0x100000 | tile);
         }
     }
+    PA_TMARK_B(kKid, 5, 0x100000 | tile);
 }
 
 // ---------------------------------------------------------------- MH output

@@ -84,3 +84,34 @@ __device__ __forceinline__ void dbg_dsmem_check(int64_t i, const char *what, con
 #define PA_LDG(...) __ldg(__VA_ARGS__)
 #define PA_AT(...) (*(__VA_ARGS__))
 #endif
+
+// ---- timeline profiling build (-DPA_TPROF, development only; scripts/tprof.py): thread 0
+// of every CTA of the instrumented kernels appends (kernel id, CTA, phase, SM, globaltimer,
+// clock64) records; pa_tprof_dump copies them out.  Nothing in the release build.
+#ifdef PA_TPROF
+namespace pa {
+struct TRec {
+    uint32_t kid, blk, phase, sm;
+    uint64_t t, clk;
+};
+constexpr uint32_t kTMax = 1u << 20;
+__device__ TRec g_trec[kTMax];
+__device__ uint32_t g_tn;
+__device__ __forceinline__ void tmark(uint32_t kid, uint32_t phase, uint32_t blk = 0xFFFFFFFFu) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        uint64_t t, clk;
+        uint32_t sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(clk));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        const uint32_t i = atomicAdd(&g_tn, 1u);
+        if (i < kTMax) g_trec[i] = TRec{kid, blk != 0xFFFFFFFFu ? blk : blockIdx.x + blockIdx.y * gridDim.x, phase, sm, t, clk};
+    }
+}
+}  // namespace pa
+#define PA_TMARK(kid, phase) ::pa::tmark((uint32_t)(kid), (uint32_t)(phase))
+#define PA_TMARK_B(kid, phase, blk) ::pa::tmark((uint32_t)(kid), (uint32_t)(phase), (uint32_t)(blk))
+#else
+#define PA_TMARK(kid, phase) ((void)0)
+#define PA_TMARK_B(kid, phase, blk) ((void)0)
+#endif

@@ -1363,7 +1363,8 @@ static int ctx_alloc_and_precompute(pa_ctx *c, const pa_params *prm) {
     TRY(c->da.alloc(&c->coef, std::max<size_t>((size_t)Pm * Lm, (size_t)Ph * Lh)));
     TRY(c->da.alloc(&c->y1, std::max<uint64_t>(c->W_fold, c->Wg)));
     TRY(c->da.alloc(&c->Z, c->W_Z));
-    c->cstate_stride = (uint32_t)(cdiv(Smax, std::min(kCarryTile, kCCTile)) + 2);
+    // crt_carry: ticket, done counter and one flag per tile, each on its own 128-byte line
+    c->cstate_stride = (uint32_t)((cdiv(Smax, std::min(kCarryTile, kCCTile)) + 2) * kFlagStride);
     TRY(c->da.alloc(&c->cstate, (size_t)c->cstate_stride * kCarrySlots));
     TRY(c->da.alloc(&c->status, 4));
     CUDA_TRY(cudaMemsetAsync(c->status, 0, 4, c->stream));
@@ -2492,3 +2493,21 @@ extern "C" int pa_debug_selftest(void) {
     return set_err(PA_E_STATE, "not a PA_DEBUG build");
 #endif
 }
+
+#ifdef PA_TPROF
+// timeline profiling build only (scripts/tprof.py; not part of include/pa.h)
+extern "C" int pa_tprof_reset(void) {
+    const uint32_t z = 0;
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyToSymbol(pa::g_tn, &z, 4));
+    return PA_OK;
+}
+extern "C" int pa_tprof_dump(void *host, uint32_t max_records) {
+    uint32_t n = 0;
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(&n, pa::g_tn, 4));
+    n = std::min(std::min(n, pa::kTMax), max_records);
+    if (n) CUDA_TRY(cudaMemcpyFromSymbol(host, pa::g_trec, (size_t)n * sizeof(pa::TRec)));
+    return (int)n;
+}
+#endif

@@ -207,6 +207,7 @@ template <class Src, int NW>
 __global__ void __launch_bounds__(256) pack_residues(const Src src, const PrimeSet ks,
                                                      uint32_t P, uint32_t nvec, uint32_t wxp,
                                                      uint32_t *__restrict__ res) {
+    PA_TMARK(0x7000 | NW, 0);
     const uint64_t total = (uint64_t)nvec * wxp;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
@@ -290,6 +291,7 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
 template <int NW>
 __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
+    PA_TMARK(0x6000 | NW, 0);
     // a tile is kPackL kPackT limbs, kPackL per thread (limbs t + q kPackT): the per-prime
     // constants, loop and addressing are shared by the limbs' reductions
     constexpr int TL = kPackL * kPackT;
@@ -590,6 +592,7 @@ template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
 __global__ void __launch_bounds__(32 * (1 << (S_LOG - E_LOG)),
                                   S_LOG == 8 ? (E_LOG == 5 ? PA_COL8_MINB : PA_COL8E4_MINB) : (S_LOG < 8 ? 3 : 1))
 col_pass(const ColArgs A) {
+    PA_TMARK(0x1000 | (S_LOG << 8) | (E_LOG << 4) | MODE, 0);
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int E = SP::E;
     constexpr uint32_t N1 = 1u << N1_LOG;
@@ -709,6 +712,7 @@ struct RowArgs {
 template <int S_LOG, int E_LOG, int V, int MODE>
 __global__ void __launch_bounds__(V * (1 << (S_LOG - E_LOG)))
 row_pass(const RowArgs A) {
+    PA_TMARK(0x2000 | (S_LOG << 8) | (E_LOG << 4) | MODE, 0);
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int S = SP::S, E = SP::E;
     constexpr int RS = S + S / 32;                       // padded row stride in smem
@@ -876,6 +880,7 @@ __host__ __device__ constexpr int mac_minb(size_t smem_bytes) {
 template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = PA_MAC_NSX, int AIN = 0>
 __global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(mac_smem_bytes<S_LOG, PAD, NSX, AIN>()))
 row_mac(const MacArgs A) {
+    PA_TMARK(0x3000 | (S_LOG << 8) | (E_LOG << 4), 0);
     using SP = SubPlan<S_LOG, E_LOG>;
     constexpr int S = SP::S, E = SP::E;
     constexpr int V = mac_v(S_LOG);
