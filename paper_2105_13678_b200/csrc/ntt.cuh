@@ -32,6 +32,11 @@ struct NttArgs {
     const uint32_t *regtw;     // [P][E/2] omega_E^j of this direction
     const uint32_t *regtwp;    // [P][E/2] Shoup companions
     uint32_t regtw_stride;     // E/2 entries per prime in the table (allocated for E=32)
+    // the same omega_32^j Shoup pairs by value: kernel parameters live in the constant bank,
+    // so a warp-uniform prime index reads them as uniform constant loads (no per-thread
+    // registers or global loads for the in-register DFT twiddles)
+    uint32_t ctw[kMaxPrimes][16];
+    uint32_t ctwp[kMaxPrimes][16];
     const uint32_t *rtw;       // round twiddles, Shoup pairs (w, floor(w 2^32/p)): [P][rtw_stride]
     uint32_t rtw_stride;
     uint32_t rtw_off[kMaxRounds];
@@ -110,6 +115,24 @@ __device__ __forceinline__ uint32_t ltw_mont(const NttArgs &a, int pi, uint32_t 
 struct Ctx32 {  // per-prime constants held in registers by a thread
     uint32_t p, p2, pinv;
 };
+
+#ifndef PA_CTW
+#define PA_CTW 1
+#endif
+// omega_E^j (j < E/2) of prime pi for an in-register radix-E DFT (E <= 32)
+template <int E>
+__device__ __forceinline__ void load_regtw(const NttArgs &a, uint32_t pi, uint32_t *tw, uint32_t *twp) {
+#pragma unroll
+    for (int j = 0; j < E / 2; j++) {
+#if PA_CTW
+        tw[j] = a.ctw[pi][j * (32 / E)];
+        twp[j] = a.ctwp[pi][j * (32 / E)];
+#else
+        tw[j] = PA_LDG(a.regtw + pi * a.regtw_stride + j * (32 / E));
+        twp[j] = PA_LDG(a.regtwp + pi * a.regtw_stride + j * (32 / E));
+#endif
+    }
+}
 
 // Round rho >= 1 of a sub-DFT (recursive over rho).  Round rho-1 left its outputs in
 // shared memory; the last round leaves its outputs in x[] (group h, register mm <->

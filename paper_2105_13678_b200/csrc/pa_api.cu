@@ -359,6 +359,7 @@ struct StageDev {
     PrimeSet pks{};                     // host copy, passed by value to the pack kernels
     uint32_t *scale = nullptr;
     uint32_t *regtw[2] = {}, *regtwp[2] = {};
+    uint32_t ctw[2][kMaxPrimes][16] = {}, ctwp[2][kMaxPrimes][16] = {};   // host copies (NttArgs by value)
     uint32_t *rtw = nullptr;            // [P][stride]: col fwd, col inv, row fwd, row inv
     uint32_t rtw_stride = 0;
     uint32_t rtw_off[2][4][kMaxRounds] = {};   // [E_LOG - 4][col fwd, col inv, row fwd, row inv]
@@ -511,6 +512,8 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cuda
                 const uint32_t t = (uint32_t)powmod64(w32, j, p);
                 regtw[dir].push_back(t);
                 regtwp[dir].push_back(shoup_of(t, p));
+                sd.ctw[dir][i][j] = t;
+                sd.ctwp[dir][i][j] = shoup_of(t, p);
             }
             uint64_t cur = 1;
             for (uint32_t e = 0; e < sd.ltw_lo_n; e++) { lo[dir].push_back(to_mont((uint32_t)cur, p)); cur = mulmod64(cur, wL, p); }
@@ -590,6 +593,8 @@ static NttArgs ntt_args(const StageDev &sd, int dir, int pass /*0 col, 1 row*/, 
     a.regtw = sd.regtw[dir];
     a.regtwp = sd.regtwp[dir];
     a.regtw_stride = 16;
+    memcpy(a.ctw, sd.ctw[dir], sizeof a.ctw);
+    memcpy(a.ctwp, sd.ctwp[dir], sizeof a.ctwp);
     a.rtw = sd.rtw;
     a.rtw_stride = sd.rtw_stride;
     for (int r = 0; r < kMaxRounds; r++) a.rtw_off[r] = sd.rtw_off[elog - 4][pass * 2 + dir][r];

@@ -632,11 +632,7 @@ col_pass(const ColArgs A) {
             cur_pi = (int)pi;
             const PrimeK pk = a.pk[pi];
             cx.p = pk.p; cx.p2 = pk.p2; cx.pinv = pk.pinv;
-#pragma unroll
-            for (int j = 0; j < E / 2; j++) {
-                tw[j] = PA_LDG(a.regtw + pi * a.regtw_stride + j * (32 / E));
-                twp[j] = PA_LDG(a.regtwp + pi * a.regtw_stride + j * (32 / E));
-            }
+            load_regtw<E>(a, pi, tw, twp);
             rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
         }
         uint32_t x[E];
@@ -735,11 +731,7 @@ row_pass(const RowArgs A) {
         const PrimeK pk = a.pk[pi];
         const Ctx32 cx{pk.p, pk.p2, pk.pinv};
         uint32_t tw[E / 2], twp[E / 2];
-#pragma unroll
-        for (int j = 0; j < E / 2; j++) {
-            tw[j] = PA_LDG(a.regtw + pi * a.regtw_stride + j * (32 / E));
-            twp[j] = PA_LDG(a.regtwp + pi * a.regtw_stride + j * (32 / E));
-        }
+        load_regtw<E>(a, pi, tw, twp);
         const uint32_t *rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
         uint32_t acc[E];
 #pragma unroll
@@ -980,11 +972,7 @@ row_mac(const MacArgs A) {
                 cur_pi = pi;
                 const PrimeK pk = a.pk[pi];
                 cx = Ctx32{pk.p, pk.p2, pk.pinv};
-#pragma unroll
-                for (int j = 0; j < E / 2; j++) {
-                    tw[j] = PA_LDG(a.regtw + pi * a.regtw_stride + j * (32 / E));
-                    twp[j] = PA_LDG(a.regtwp + pi * a.regtw_stride + j * (32 / E));
-                }
+                load_regtw<E>(a, pi, tw, twp);
                 rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
             }
             have_unit = true;
