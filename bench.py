@@ -173,6 +173,11 @@ def stage_ops(info: dict, stage: str) -> float:
         return INT_OPS_PER_BFLY * bfly(mh, 1, mh["n_row"]) + INT_OPS_PER_MAC * mh["nprimes"] * (1 << mh["log2_len"])
     if stage == "mh_inverse":
         return INT_OPS_PER_BFLY * bfly(mh, 1, 1 << mh["log2_len"])
+    if stage == "mh_row_mac_inv":      # forward row DFT + MAC + inverse row DFT (row_macinv)
+        return (2 * INT_OPS_PER_BFLY * bfly(mh, 1, mh["n_row"]) +
+                INT_OPS_PER_MAC * mh["nprimes"] * (1 << mh["log2_len"]))
+    if stage == "mh_inverse_col":
+        return INT_OPS_PER_BFLY * bfly(mh, 1, mh["n_col"])
     return 0.0
 
 

@@ -732,6 +732,32 @@ static int launch_row(int slog, const RowArgs &A, cudaStream_t st) {
     return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
 }
 
+template <int S_LOG>
+static int launch_macinv_t(const MacInvArgs &A0, cudaStream_t st) {
+    constexpr int E_LOG = 5;
+    constexpr int V = inv_v(S_LOG);                     // as the inverse row pass
+    static KInfo kis[kMaxDevices];
+    KInfo &ki = kinfo_slot(kis);
+    auto fn = row_macinv<S_LOG, E_LOG, V>;
+    constexpr int S = 1 << S_LOG;
+    TRY(kinfo(fn, V * (S >> E_LOG), (size_t)V * (S + S / 32) * 4, ki));
+    MacInvArgs A = A0;
+    A.units = (A.fw.n2 / V) * A.fw.nprimes;
+    const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
+    fn<<<grid, ki.threads, ki.smem, st>>>(A);
+    CUDA_TRY(cudaGetLastError());
+    return PA_OK;
+}
+
+static int launch_macinv(int slog, const MacInvArgs &A, cudaStream_t st) {
+    switch (slog) {
+#define PA_LMI(S) case S: return launch_macinv_t<S>(A, st);
+        PA_LMI(5) PA_LMI(6) PA_LMI(7) PA_LMI(8) PA_LMI(9) PA_LMI(10) PA_LMI(11) PA_LMI(12) PA_LMI(13) PA_LMI(14)
+#undef PA_LMI
+    }
+    return set_err(PA_E_PARAM, "unsupported row length 2^%d", slog);
+}
+
 // Grid of the row MAC.  Mode 0 splits the (unit, vector) iterations evenly: a unit then
 // spans at most ceil(grid / nunits) + 1 consecutive CTAs, and CTA b adds its canonical
 // partials (< p) into slot b mod nslot, so a slot sees at most four partials of a unit
@@ -1165,6 +1191,39 @@ static int stage_inverse(pa_ctx *c, StageDev &sd, uint32_t *acc, const char *tag
     A.units = (sd.pl.n_row / 32) * P;
     TRY(launch_col<COL_INV>(clog, rlog, A, c->stream));
     c->launches += 2;
+    return PA_OK;
+}
+
+// ---- S3+S4 of a single vector (the MH product): forward row DFT x hat, inverse row DFT
+// (one kernel, row_macinv), then the inverse column pass -> canonical residues in dst,
+// natural order
+static int stage_macinv(pa_ctx *c, StageDev &sd, const uint32_t *scratch, const uint32_t *hat, uint32_t *dst,
+                        const char *tag_row, const char *tag_col) {
+    const int clog = __builtin_ctz(sd.pl.n_col), rlog = __builtin_ctz(sd.pl.n_row);
+    const uint32_t P = sd.pl.nprimes;
+    {
+        ProfScope ps(c, tag_row);
+        MacInvArgs M{};
+        M.fw = ntt_args(sd, 0, 1);
+        M.iv = ntt_args(sd, 1, 1);
+        M.src = scratch;
+        M.bhat = hat;
+        M.tw4 = sd.tw4i;
+        M.dst = dst;
+        TRY(launch_macinv(rlog, M, c->stream));
+        c->launches++;
+    }
+    {
+        ProfScope ps(c, tag_col);
+        ColArgs A{};
+        A.nt = ntt_args(sd, 1, 0);
+        A.src = dst;
+        A.dst = dst;
+        A.nvec = 1;
+        A.units = (sd.pl.n_row / 32) * P;
+        TRY(launch_col<COL_INV>(clog, rlog, A, c->stream));
+        c->launches++;
+    }
     return PA_OK;
 }
 
@@ -1763,13 +1822,20 @@ static int run_mmh(pa_ctx *c, const uint8_t *key_slice, uint32_t **y_out) {
 }
 
 // ---- S7 on canonical y -> out_bits
+#ifndef PA_MH_MACINV
+#define PA_MH_MACINV 1            // fused single-vector row MAC + inverse row pass (row_macinv)
+#endif
 static int run_mh(pa_ctx *c, const uint32_t *y, uint8_t *out_bits) {
     const Plan &p = c->pl;
     const uint32_t Bh = p.mh.limb_bits;
     WordSrc ws{y, (uint32_t)c->Wg, Bh, (uint32_t)cdiv(p.gamma, Bh)};
     TRY(stage_pack_col(c, c->smh, WordLimbs{ws}, 1, c->rows_mh, c->res, c->scratch_mh, "mh_pack", "mh_fwd_col"));
+#if PA_MH_MACINV
+    TRY(stage_macinv(c, c->smh, c->scratch_mh, c->bhat, c->acc_mh, "mh_row_mac_inv", "mh_inverse_col"));
+#else
     TRY(stage_mac(c, c->smh, 1, c->scratch_mh, c->bhat, c->acc_mh, true, "mh_fwd_row_mac", false));
     TRY(stage_inverse(c, c->smh, c->acc_mh, "mh_inverse"));
+#endif
     const uint32_t W = (uint32_t)c->W_Z;
     {
         ProfScope ps(c, "mh_crt_carry_extract");

@@ -812,6 +812,85 @@ row_pass(const RowArgs A) {
     }
 }
 
+// ---------------------------------------------------------------- single-vector row MAC + inverse row
+// S7 (Eq. 4), the MH product b y: the single vector's forward row DFT,
+// the transform-domain product with B^ (b's precomputed transform), the inverse row DFT
+// and the inverse four-step twiddle, in one pass over each row.  With one vector there is
+// nothing to accumulate across CTAs, so the row stays on chip between the two DFTs (one
+// shared-memory reorder from the forward DFT's output positions to the inverse DFT's input
+// positions) instead of a store, a kernel boundary and a reload.  Output as ROW_INV.
+struct MacInvArgs {
+    NttArgs fw;               // forward row tables
+    NttArgs iv;               // inverse row tables
+    const uint32_t *src;      // [P][L] forward column-pass output
+    const uint32_t *bhat;     // [P][L] precomputed transform (Montgomery, x 1/L)
+    const uint32_t *tw4;      // omega_L^(-j1 k2) [P][L] (Montgomery, canonical)
+    uint32_t *dst;            // [P][L]
+    uint32_t units;           // (N2 / V) * P
+};
+
+template <int S_LOG, int E_LOG, int V>
+__global__ void __launch_bounds__(V * (1 << (S_LOG - E_LOG)))
+row_macinv(const MacInvArgs A) {
+    PA_TMARK(0x2800 | (S_LOG << 4) | E_LOG, 0);
+    using SP = SubPlan<S_LOG, E_LOG>;
+    constexpr int S = SP::S, E = SP::E;
+    constexpr int RS = S + S / 32;                       // padded row stride in smem
+    extern __shared__ uint32_t sm[];
+    const int w = threadIdx.x / SP::TPV;
+    const int v = threadIdx.x % SP::TPV;
+    const uint32_t L = 1u << A.fw.log2L;
+    const uint32_t P = A.fw.nprimes;
+    auto sidx = [w](int pos) { return w * RS + pos + (pos >> 5); };
+    constexpr int R0 = 1 << SP::rlog(0);
+    constexpr int RL = 1 << SP::rlog(SP::Q - 1);
+    for (uint32_t u = blockIdx.x; u < A.units; u += gridDim.x) {
+        const uint32_t pi = u % P;
+        const uint32_t k2 = (u / P) * V + w;             // row index
+        const PrimeK pk = A.fw.pk[pi];
+        const Ctx32 cx{pk.p, pk.p2, pk.pinv};
+        const size_t rb = (size_t)pi * L + (size_t)k2 * S;
+        uint32_t tw[E / 2], twp[E / 2];
+        uint32_t x[E];
+#pragma unroll
+        for (int h = 0; h < E / R0; h++)
+#pragma unroll
+            for (int m = 0; m < R0; m++) x[h * R0 + m] = PA_AT(A.src + rb + in_pos<S_LOG, E_LOG>(v, h, m));
+        load_regtw<E>(A.fw, pi, tw, twp);
+        __syncthreads();                                 // the previous row's shared reads are done
+        round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, A.fw.rtw + (size_t)pi * A.fw.rtw_stride, A.fw, cx);
+        rounds_rest<S_LOG, E_LOG, 1, true>(x, sm, sidx, v, tw, twp, A.fw.rtw + (size_t)pi * A.fw.rtw_stride, A.fw, cx);
+        __syncthreads();                                 // last-round shared reads before the reorder
+#pragma unroll
+        for (int h = 0; h < E / RL; h++)
+#pragma unroll
+            for (int mm = 0; mm < RL; mm++) {
+                const int k1 = out_pos<S_LOG, E_LOG>(v, h, mm);
+                PA_SMEM_PTR_CK(sm + sidx(k1), 4);
+                sm[sidx(k1)] = mul_mont(x[h * RL + mm], PA_LDG(A.bhat + rb + k1), cx.p, cx.pinv);   // (0, 2p)
+            }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < E / R0; h++)
+#pragma unroll
+            for (int m = 0; m < R0; m++) {
+                PA_SMEM_PTR_CK(sm + sidx(in_pos<S_LOG, E_LOG>(v, h, m)), 4);
+                x[h * R0 + m] = sm[sidx(in_pos<S_LOG, E_LOG>(v, h, m))];
+            }
+        load_regtw<E>(A.iv, pi, tw, twp);
+        __syncthreads();                                 // reorder reads before round 0's writes
+        round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, A.iv.rtw + (size_t)pi * A.iv.rtw_stride, A.iv, cx);
+        rounds_rest<S_LOG, E_LOG, 1, true>(x, sm, sidx, v, tw, twp, A.iv.rtw + (size_t)pi * A.iv.rtw_stride, A.iv, cx);
+#pragma unroll
+        for (int h = 0; h < E / RL; h++)
+#pragma unroll
+            for (int mm = 0; mm < RL; mm++) {
+                const uint32_t j1 = (uint32_t)out_pos<S_LOG, E_LOG>(v, h, mm);
+                PA_AT(A.dst + rb + j1) = mul_mont(x[h * RL + mm], PA_LDG(A.tw4 + rb + j1), cx.p, cx.pinv);
+            }
+    }
+}
+
 // ---------------------------------------------------------------- row pass + MAC
 // S2+S3 (Eq. 2): second NTT pass of every block and the transform-
 // domain multiply-accumulate acc += X_i (.) A^_i, for all blocks i.
