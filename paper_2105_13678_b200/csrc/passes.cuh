@@ -636,28 +636,43 @@ col_pass(const ColArgs A) {
             rtw_p = a.rtw + (size_t)pi * a.rtw_stride;
         }
         uint32_t x[E];
+        // round 0's first stage pairs rows q and q + S/2: with all non-zero rows in the
+        // first half (the zero-padded upper half of every packed vector) it is (a, a w), and the
+        // upper half (m >= R/2 in every group) is neither loaded nor read.  Its loads are left
+        // out of this branch altogether: a predicated-off load still holds its destination
+        // register on the scoreboard, and a later reuse of that register waited on it.
+        const bool zh = MODE == COL_FWD && 2 * rows <= (1u << S_LOG);
         {
             constexpr int R = 1 << SP::rlog(0);
             const uint32_t *src = ((MODE == COL_INV) ? A.src + (size_t)pi * L
                                                      : A.src + ((size_t)iv * P + pi) * ((size_t)rows * N1)) +
                                   ((size_t)v << N1_LOG) + j1;
+            if (zh) {
 #pragma unroll
-            for (int h = 0; h < E / R; h++) {
+                for (int h = 0; h < E / R; h++) {
 #pragma unroll
-                for (int m = 0; m < R; m++) {
-                    constexpr int dummy = 0;
-                    (void)dummy;
-                    const int rel = SP::TPV * h + (SP::S / R) * m;          // in_pos - v
-                    uint32_t val = 0;
-                    if (MODE == COL_INV || (uint32_t)(v + rel) < rows) val = PA_AT(src + ((size_t)rel << N1_LOG));
-                    x[h * R + m] = val;
+                    for (int m = 0; m < R; m++) {
+                        const int rel = SP::TPV * h + (SP::S / R) * m;      // in_pos - v, < S/2 iff m < R/2
+                        uint32_t val = 0;
+                        if (m < R / 2 && (uint32_t)(v + rel) < rows) val = PA_AT(src + ((size_t)rel << N1_LOG));
+                        x[h * R + m] = val;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < E / R; h++) {
+#pragma unroll
+                    for (int m = 0; m < R; m++) {
+                        const int rel = SP::TPV * h + (SP::S / R) * m;      // in_pos - v
+                        uint32_t val = 0;
+                        if (MODE == COL_INV || (uint32_t)(v + rel) < rows) val = PA_AT(src + ((size_t)rel << N1_LOG));
+                        x[h * R + m] = val;
+                    }
                 }
             }
         }
         __syncthreads();    // previous unit's last-round smem reads are done
-        // round 0's first stage pairs rows q and q + S/2: with all non-zero rows in the
-        // first half (the zero-padded upper half of every packed vector) it is (a, a w)
-        if (MODE == COL_FWD && 2 * rows <= (1u << S_LOG))
+        if (zh)
             round0_finish<S_LOG, E_LOG, true>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         else
             round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
