@@ -100,6 +100,7 @@ typedef struct {
     uint32_t graph_captures; /* CUDA-graph captures since creation (new pointer sets) */
     uint32_t graph_updates;  /* ... of which updated an executable graph in place */
     uint32_t graph_instantiations;
+    uint32_t tz_group_blocks;/* Toeplitz contexts: input blocks per accumulation group */
 } pa_info;
 
 typedef struct {
@@ -140,9 +141,12 @@ typedef struct {
      * n + m - 1 diagonal bits d drawn from `seed` (reading A15).  Exact integer NTT
      * convolution mod one 30-bit prime, r x r block split (r = min(2^22, 2^ceil(log2 max(n,
      * m))), at least 512; limb_bits != 0 forces r = 2^limb_bits, 9..22).  r, gamma, shards,
-     * paper_k, mh_only must be 0; n below the prime
-     * (n < 2^29).  pa_query reports r, k = ceil(n/r) input blocks, alpha = ceil(m/r) output
-     * blocks and the transform in `mmh`.  pa_hash / pa_hash_host only. */
+     * paper_k, mh_only must be 0; m < 2^31.  Each output bit is the parity of a count <= n:
+     * with n below the prime one accumulation is exact; otherwise the input blocks are summed
+     * in groups of floor((prime - 1) / r) blocks (each group's counts exact) and the groups'
+     * parities XORed.  Output blocks are accumulated kTzMaxOut (16) at a time.  pa_query
+     * reports r, k = ceil(n/r) input blocks, alpha = ceil(m/r) output blocks, the transform in
+     * `mmh` and the group size in tz_group_blocks.  pa_hash / pa_hash_host only. */
     uint64_t toeplitz;
     /* Multi-GPU (SURVEY.md §8(b,e); MMH splits over blocks, "split and separately
      * handle"): world >= 1 makes the context rank `rank` of a `world`-rank job
@@ -168,6 +172,10 @@ typedef struct {
     void *(*dev_alloc)(size_t bytes, void *stream, void *user);
     void (*dev_free)(void *ptr, size_t bytes, void *stream, void *user);
     void *alloc_user;
+    /* Toeplitz comparator only: input blocks per accumulation group, at most the automatic
+     * floor((prime - 1) / r) (0 = automatic).  Smaller groups exercise the grouped (parity
+     * XOR) path at small n; the output does not depend on it. */
+    uint64_t tz_group_blocks;
 } pa_params;
 
 /* Create a context on the current CUDA device.  `p` is the Mersenne EXPONENT

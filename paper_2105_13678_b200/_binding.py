@@ -48,7 +48,8 @@ class pa_info(ctypes.Structure):
                 ("block_begin", u64), ("block_end", u64), ("mmh", pa_stage_plan), ("mh", pa_stage_plan),
                 ("device_bytes", u64), ("kernels_per_hash", u32), ("launches_total", u32),
                 ("insecure_length", u32), ("world", i32), ("rank", i32), ("acc_words", u64),
-                ("graph_captures", u32), ("graph_updates", u32), ("graph_instantiations", u32)]
+                ("graph_captures", u32), ("graph_updates", u32), ("graph_instantiations", u32),
+                ("tz_group_blocks", u32)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("mmh", "mh")}
@@ -69,7 +70,8 @@ class pa_params(ctypes.Structure):
                 ("a_words", vp), ("b_words", vp), ("c_words", vp),
                 ("stream", vp), ("limb_bits", i32), ("strict", i32), ("paper_k", u64), ("mh_only", u64),
                 ("toeplitz", u64), ("world", i32), ("rank", i32), ("nccl_id", ctypes.c_uint8 * 128),
-                ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE), ("alloc_user", vp)]
+                ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE), ("alloc_user", vp),
+                ("tz_group_blocks", u64)]
 
 
 def _sig(name, res, *args):

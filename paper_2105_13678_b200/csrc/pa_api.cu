@@ -213,6 +213,7 @@ struct Plan {
     uint64_t mh_only;        // comparator: MH-only PA over the whole n-bit key
     uint64_t toeplitz;       // comparator: Toeplitz-hashing PA (tz_nb input, tz_no output blocks of r bits)
     uint64_t tz_nb, tz_no;
+    uint32_t tz_group = 0;   // input blocks per accumulation (counts below the prime)
     int strict, force_B;
     int world, rank;         // multi-GPU context (world >= 1): NCCL rank of a world-rank job
     pa_stage_plan mmh, mh;
@@ -243,8 +244,7 @@ static int make_plan(const pa_params *prm, Plan *P) {
         // comparator: Toeplitz-hashing PA, r x r blocks, one prime
         if (prm->gamma || prm->r || p.paper_k || p.mh_only || prm->block_begin || prm->block_end)
             return set_err(PA_E_PARAM, "Toeplitz PA takes no gamma, r, paper_k, mh_only or shard");
-        if (p.n >= (1ull << 29) || p.m >= (1ull << 31))
-            return set_err(PA_E_PARAM, "Toeplitz PA: n < 2^29 (counts below the prime), m < 2^31");
+        if (p.m >= (1ull << 31)) return set_err(PA_E_PARAM, "Toeplitz PA: m < 2^31");
         const uint64_t big = std::max(p.n, p.m);
         int lr = 9;
         while (lr < 22 && (1ull << lr) < big) lr++;
@@ -256,14 +256,20 @@ static int make_plan(const pa_params *prm, Plan *P) {
         p.r = 1ull << lr;
         p.tz_nb = cdiv(p.n, p.r);
         p.tz_no = cdiv(p.m, p.r);
-        if (p.tz_no > (uint64_t)kTzMaxOut) return set_err(PA_E_PARAM, "Toeplitz PA: m <= %d * 2^22", kTzMaxOut);
         p.k = p.tz_nb;
         p.alpha = p.tz_no;
         p.gamma = 0;
         p.b0 = 0; p.b1 = p.k;
         uint32_t prime = 0;
+        // a prime above n keeps every count exact in one accumulation; else the largest prime
+        // of the transform length, and the input blocks are summed in groups of
+        // floor((prime - 1) / r) blocks whose counts stay below it (parities XORed)
         for (uint32_t q : kPrimes) if (two_adic(q) >= lg && q > p.n) { prime = q; break; }
+        if (!prime)
+            for (uint32_t q : kPrimes) if (two_adic(q) >= lg && q > p.r && q > prime) prime = q;
         if (!prime) return set_err(PA_E_BOUND, "no NTT prime for Toeplitz length 2^%d", lg);
+        p.tz_group = (uint32_t)std::min<uint64_t>((prime - 1) / p.r, p.tz_nb);
+        if (prm->tz_group_blocks) p.tz_group = (uint32_t)std::min<uint64_t>(prm->tz_group_blocks, p.tz_group);
         pa_stage_plan &sp = p.mmh;
         sp = pa_stage_plan{};
         sp.limb_bits = 1;
@@ -1338,10 +1344,11 @@ static int toeplitz_alloc_and_precompute(pa_ctx *c) {
 }
 
 template <int O>
-static void launch_tz_mac(const pa_ctx *c, uint32_t grid) {
+static void launch_tz_mac(const pa_ctx *c, uint32_t grid, uint32_t b0, uint32_t b1, uint32_t o0) {
     const StageDev &sd = c->smmh;
-    toeplitz_mac<O><<<grid, 256, 0, c->stream>>>(c->scratch, c->ahat, (uint32_t)c->pl.tz_nb, sd.L, sd.pl.primes[0],
-                                                 sd.pks.k[0].pinv, c->acc);
+    const uint32_t ebase = b0 - o0 + (uint32_t)c->pl.tz_no - O;        // >= 0: o0 + O <= no
+    toeplitz_mac<O><<<grid, 256, 0, c->stream>>>(c->scratch, c->ahat, b0, b1, ebase, sd.L, sd.pl.primes[0],
+                                                 sd.pks.k[0].pinv, c->acc + (size_t)o0 * sd.L);
 }
 
 static int run_toeplitz(pa_ctx *c, const uint8_t *key, uint8_t *out_bits) {
@@ -1357,27 +1364,35 @@ static int run_toeplitz(pa_ctx *c, const uint8_t *key, uint8_t *out_bits) {
         CUDA_TRY(cudaGetLastError());
     }
     TRY(tz_forward(c, c->res, nb, sd.pl.n_col / 2, c->scratch, c->tz_scale, "tz_fwd_col", "tz_fwd_row"));
-    {
-        ProfScope ps(c, "tz_mac");
-        const uint32_t grid = (uint32_t)cdiv(L, 256);          // one element per thread
-        switch (no) {
-#define PA_TZ(O) case O: launch_tz_mac<O>(c, grid); break;
-            PA_TZ(1) PA_TZ(2) PA_TZ(3) PA_TZ(4) PA_TZ(5) PA_TZ(6) PA_TZ(7) PA_TZ(8)
-            PA_TZ(9) PA_TZ(10) PA_TZ(11) PA_TZ(12) PA_TZ(13) PA_TZ(14) PA_TZ(15) PA_TZ(16)
+    // input blocks in groups whose counts stay below the prime (one group unless n >= prime),
+    // output blocks in groups of at most kTzMaxOut per MAC launch
+    const uint32_t gb = std::max<uint32_t>(1, p.tz_group);
+    for (uint32_t b0 = 0; b0 < nb; b0 += gb) {
+        const uint32_t b1 = std::min(nb, b0 + gb);
+        {
+            ProfScope ps(c, "tz_mac");
+            const uint32_t grid = (uint32_t)cdiv(L, 256);      // one element per thread
+            for (uint32_t o0 = 0; o0 < no; o0 += kTzMaxOut) {
+                const uint32_t O = std::min<uint32_t>(kTzMaxOut, no - o0);
+                switch (O) {
+#define PA_TZ(Q) case Q: launch_tz_mac<Q>(c, grid, b0, b1, o0); break;
+                    PA_TZ(1) PA_TZ(2) PA_TZ(3) PA_TZ(4) PA_TZ(5) PA_TZ(6) PA_TZ(7) PA_TZ(8)
+                    PA_TZ(9) PA_TZ(10) PA_TZ(11) PA_TZ(12) PA_TZ(13) PA_TZ(14) PA_TZ(15) PA_TZ(16)
 #undef PA_TZ
-            default: return set_err(PA_E_PARAM, "Toeplitz: %u output blocks", no);
+                }
+                c->launches++;
+                CUDA_TRY(cudaGetLastError());
+            }
         }
-        c->launches++;
-        CUDA_TRY(cudaGetLastError());
-    }
-    for (uint32_t o = 0; o < no; o++) TRY(stage_inverse(c, sd, c->acc + (size_t)o * L, "tz_inverse"));
-    {
-        ProfScope ps(c, "tz_extract");
-        const uint64_t nbytes = cdiv(p.m, 8), nwarp = cdiv(p.m, 32);
-        toeplitz_extract<<<(uint32_t)std::min<uint64_t>(cdiv(nwarp, 8), (uint64_t)g_num_sms * 16), 256, 0,
-                           c->stream>>>(c->acc, lr, L, p.m, out_bits, nbytes);
-        c->launches++;
-        CUDA_TRY(cudaGetLastError());
+        for (uint32_t o = 0; o < no; o++) TRY(stage_inverse(c, sd, c->acc + (size_t)o * L, "tz_inverse"));
+        {
+            ProfScope ps(c, "tz_extract");
+            const uint64_t nbytes = cdiv(p.m, 8), nwarp = cdiv(p.m, 32);
+            toeplitz_extract<<<(uint32_t)std::min<uint64_t>(cdiv(nwarp, 8), (uint64_t)g_num_sms * 16), 256, 0,
+                               c->stream>>>(c->acc, lr, L, p.m, out_bits, nbytes, b0 > 0 ? 1u : 0u);
+            c->launches++;
+            CUDA_TRY(cudaGetLastError());
+        }
     }
     return PA_OK;
 }
@@ -1502,6 +1517,7 @@ extern "C" int pa_plan(const pa_params *prm, pa_info *info) {
         info->insecure_length = (!p.mh_only && !p.toeplitz && p.m >= p.gamma) ? 1u : 0u;
         info->world = p.world; info->rank = p.rank;
         info->acc_words = (uint64_t)p.mmh.nprimes << p.mmh.log2_len;
+        info->tz_group_blocks = p.toeplitz ? p.tz_group : 0u;
         const uint64_t nb = p.b1 - p.b0;
         info->device_bytes = 4ull * (3 * nb + 3) * p.mmh.nprimes * (1ull << p.mmh.log2_len) +
                              4ull * 5 * p.mh.nprimes * (1ull << p.mh.log2_len);
@@ -1676,6 +1692,7 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
     info->graph_captures = c->graph_captures;
     info->graph_updates = c->graph_updates;
     info->graph_instantiations = c->graph_instantiations;
+    info->tz_group_blocks = p.toeplitz ? p.tz_group : 0u;
     info->kernels_per_hash = c->launches;
     info->launches_total = c->launches_total;
     return PA_OK;

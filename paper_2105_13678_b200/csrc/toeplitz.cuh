@@ -54,21 +54,25 @@ __global__ void __launch_bounds__(256) toeplitz_pack_diag(const uint32_t *__rest
     }
 }
 
-// acc[o][e] = sum_b Xh[b][e] * Eh[b - o + O - 1][e] mod p for o < O (canonical), i.e. the
-// transform-domain sum over input blocks of every output block.  Eh holds T(e') L^-1 R
-// (Montgomery), Xh plain transforms, so mul_mont leaves T(x) T(e') / L.  For a fixed e the
-// E index window b .. b + O - 1 slides by one per input block: O registers, one new load.
+// acc[o'][e] = sum_{b in [b0, b1)} Xh[b][e] * Eh[b - o + no - 1][e] mod p for the output blocks
+// o = o0 + o' (o' < O) of a group, i.e. the transform-domain sum over the input blocks of a
+// group (canonical).  Eh holds T(e') L^-1 R (Montgomery), Xh plain transforms, so mul_mont
+// leaves T(x) T(e') / L.  ebase = b0 - o0 + no - O: for a fixed e the E index window
+// ebase + (b - b0) .. + O - 1 slides by one per input block: O registers, one new load.
 // The products are summed as plain 64-bit integers (one wide multiply-add each): x, w < p <
 // 2^30, so seven products stay below 3 p 2^32 and one REDC per seven blocks turns the group
 // into sum x w R^-1 mod p -- the same value as seven Montgomery products, at a fraction of
 // the instructions.
-constexpr int kTzMaxOut = 16;
+constexpr int kTzMaxOut = 16;                 // output blocks per MAC launch (O registers)
 constexpr int kTzGroup = 7;
 template <int O>
 __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__ Xh, const uint32_t *__restrict__ Eh,
-                                                    uint32_t nb, uint32_t L, uint32_t p, uint32_t pinv,
-                                                    uint32_t *__restrict__ acc) {
+                                                    uint32_t b0, uint32_t b1, uint32_t ebase, uint32_t L, uint32_t p,
+                                                    uint32_t pinv, uint32_t *__restrict__ acc) {
     const uint32_t p2 = 2 * p;
+    const uint32_t nb = b1 - b0;
+    Xh += (size_t)b0 * L;
+    Eh += (size_t)ebase * L;
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < L; e += gridDim.x * blockDim.x) {
         uint32_t a[O], w[O];
         uint64_t t[O];
@@ -76,7 +80,7 @@ __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__
         for (int o = 0; o < O; o++) {
             a[o] = 0;
             t[o] = 0;
-            w[o] = PA_LDG(Eh + (size_t)(O - 1 - o) * L + e);        // w[o] = E[b + O - 1 - o] at b = 0
+            w[o] = PA_LDG(Eh + (size_t)(O - 1 - o) * L + e);        // w[o] = E[ebase + b + O - 1 - o] at b = b0
         }
         uint32_t g = 0;
 #pragma unroll 7
@@ -108,8 +112,12 @@ __global__ void __launch_bounds__(256) toeplitz_mac(const uint32_t *__restrict__
 
 // Output bit j < m = parity of coefficient r - 1 + (j mod r) of block j / r (canonical
 // residues = exact counts < p).  One warp per 32 output bits: ballot, emitted MSB-first.
+// With several input-block groups (their counts each below p, the sum possibly not) every
+// group's parities are XORed into the output (xor_in): the parity of a sum is the XOR of the
+// parities.
 __global__ void __launch_bounds__(256) toeplitz_extract(const uint32_t *__restrict__ acc, uint32_t log2r, uint32_t L,
-                                                        uint64_t m, uint8_t *__restrict__ out, uint64_t nbytes) {
+                                                        uint64_t m, uint8_t *__restrict__ out, uint64_t nbytes,
+                                                        uint32_t xor_in) {
     const uint64_t r = 1ull << log2r;
     const int lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -120,7 +128,10 @@ __global__ void __launch_bounds__(256) toeplitz_extract(const uint32_t *__restri
         const uint32_t mask = __brev(__ballot_sync(0xFFFFFFFFu, bit));   // bit 31 = output bit 32 wq
         if (lane < 4) {
             const uint64_t q = wq * 4 + lane;
-            if (q < nbytes) PA_AT(out + q) = (uint8_t)(mask >> (24 - 8 * lane));
+            if (q < nbytes) {
+                const uint8_t v = (uint8_t)(mask >> (24 - 8 * lane));
+                PA_AT(out + q) = xor_in ? (uint8_t)(PA_AT(out + q) ^ v) : v;
+            }
         }
     }
 }

@@ -179,9 +179,17 @@ def test_toeplitz_plan():
     assert small["r"] == 512 and small["k"] == 1 and small["alpha"] == 1
     forced = P.plan(5000, 0, 1500, toeplitz=True, limb_bits=9)
     assert forced["k"] == 10 and forced["alpha"] == 3
-    for kw in (dict(n=1 << 29, m=10), dict(n=100, m=17 << 22)):
-        with pytest.raises(B.PAError):
-            P.plan(kw["n"], 0, kw["m"], toeplitz=True)
+    assert info["tz_group_blocks"] == 62                       # n below the prime: one accumulation
+    # n above every NTT prime of the length (C5: 2^31 key bits): the input blocks are summed in
+    # groups whose counts stay below the prime, floor((p - 1) / r) blocks each; m > 16 r is
+    # accumulated 16 output blocks at a time
+    big = P.plan(1 << 31, 0, 214_748_365, toeplitz=True)
+    q = big["mmh"]["primes"][0]
+    assert big["r"] == 1 << 22 and big["k"] == 512 and big["alpha"] == 52 and q < 1 << 31
+    assert big["tz_group_blocks"] == (q - 1) // (1 << 22) and big["tz_group_blocks"] * (1 << 22) < q
+    assert P.plan(1 << 31, 0, 10, toeplitz=True, tz_group_blocks=3)["tz_group_blocks"] == 3
+    with pytest.raises(B.PAError):
+        P.plan(100, 0, 1 << 31, toeplitz=True)                # m < 2^31
     with pytest.raises(B.PAError):
         P.plan(100, 16, 10, toeplitz=True)            # r is chosen by the planner
     with pytest.raises(B.PAError):

@@ -12,9 +12,9 @@ from synth import CONFIGS, key_bytes
 pytestmark = pytest.mark.gpu
 
 
-def _hash(n, m, seed, key, limb_bits=0):
+def _hash(n, m, seed, key, limb_bits=0, tz_group_blocks=0):
     from paper_2105_13678_b200 import PAContext
-    ctx = PAContext(n, 0, m, 0, seed=seed, toeplitz=True, limb_bits=limb_bits)
+    ctx = PAContext(n, 0, m, 0, seed=seed, toeplitz=True, limb_bits=limb_bits, tz_group_blocks=tz_group_blocks)
     out = torch.empty(ctx.nbytes_out, dtype=torch.uint8, device="cuda")
     ctx.hash(torch.from_numpy(np.frombuffer(key, dtype=np.uint8).copy()).cuda(), out)
     torch.cuda.synchronize()
@@ -40,6 +40,18 @@ def test_toeplitz_block_split_whole(n, m, lr):
     got, info = _hash(n, m, 7, key, limb_bits=lr)
     assert info["r"] == 1 << lr and info["k"] == -(-n // (1 << lr)) and info["alpha"] == -(-m // (1 << lr))
     assert got == OT.toeplitz_pa_seeded(key, n, m, 7)
+
+
+@pytest.mark.parametrize("n,m,lr,grp", [(40_000, 20_000, 9, 1), (40_000, 20_000, 9, 3), (5_000, 9_500, 9, 2),
+                                        (70_001, 10_000, 10, 5), (600, 5000, 9, 1)])
+def test_toeplitz_input_groups_and_many_output_blocks(n, m, lr, grp):
+    """Input blocks accumulated in groups of `grp` (each group's counts exact, parities XORed:
+    the path n >= prime takes with groups of floor((prime - 1) / r) blocks) and more than 16
+    output blocks (MAC launches of at most 16 accumulators), against the oracle."""
+    key = key_bytes(n, 0x900 + n)
+    got, info = _hash(n, m, 5, key, limb_bits=lr, tz_group_blocks=grp)
+    assert info["tz_group_blocks"] == grp and info["alpha"] == -(-m // (1 << lr))
+    assert got == OT.toeplitz_pa_seeded(key, n, m, 5)
 
 
 def test_toeplitz_special_keys():
