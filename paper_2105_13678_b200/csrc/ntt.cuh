@@ -207,7 +207,11 @@ __device__ __forceinline__ void round0_finish(uint32_t *x, uint32_t *sm, const S
                 const int k = bitrev<R>(mm);
                 uint32_t val = x[h * R + mm];
                 if (T > 1 && k != 0) {
+#if defined(PA_COL_DBG) && (PA_COL_DBG & 2)
+                    const uint2 w = make_uint2(k * 7u + t, k * 11u + t);   // timing-only ablation
+#else
                     const uint2 w = PA_LDG(reinterpret_cast<const uint2 *>(rtw_p + a.rtw_off[0]) + k * T + t);
+#endif
                     val = mul_shoup(val, w.x, w.y, c.p);
                 }
                 PA_SMEM_PTR_CK(sm + sidx(k + R * t), 4);

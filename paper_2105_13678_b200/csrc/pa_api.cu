@@ -650,6 +650,9 @@ static int kinfo(F *fn, int threads, size_t smem, KInfo &ki) {
     return PA_OK;
 }
 
+#ifndef PA_COL_LANES
+#define PA_COL_LANES 1
+#endif
 template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
 static int launch_col_e(const ColArgs &A0, cudaStream_t st) {
     static KInfo kis[kMaxDevices];
@@ -660,6 +663,9 @@ static int launch_col_e(const ColArgs &A0, cudaStream_t st) {
     if (E_LOG == 4)
         for (int r = 0; r < kMaxRounds; r++) A.nt.rtw_off[r] = A.nt.rtw_off4[r];
     const int grid = (int)std::min<uint64_t>(A.units, (uint64_t)ki.occ * g_num_sms);
+    // co-resident CTAs share their SM slot's units round robin (col_pass) when the grid is
+    // the full occupancy and every CTA of a slot gets work
+    A.lanes = (PA_COL_LANES && grid == ki.occ * g_num_sms && A.units >= (uint64_t)grid * 2) ? (uint32_t)ki.occ : 1u;
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;

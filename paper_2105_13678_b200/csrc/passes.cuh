@@ -577,6 +577,7 @@ struct ColArgs {
     uint32_t *dst;           // FWD: [nvec][P][L];  INV: [P][L]
     uint32_t nvec;           // vectors (blocks) per prime
     uint32_t units;          // (N1/32) * P * nvec
+    uint32_t lanes;          // co-resident CTAs per SM slot (launcher: grid = lanes * slots), else 1
 };
 
 // One CTA = 32 adjacent columns (one lane each) x S/E threads per column.  The row
@@ -605,8 +606,16 @@ col_pass(const ColArgs A) {
     const uint32_t nvec = A.nvec;
     const uint32_t rows = A.rows;
     const uint32_t units = A.units;
-    const uint32_t u0 = (uint32_t)(((uint64_t)blockIdx.x * units) / gridDim.x);
-    const uint32_t u1 = (uint32_t)(((uint64_t)(blockIdx.x + 1) * units) / gridDim.x);
+    // CTAs b, b + slots, b + 2 slots, ... of a full-occupancy grid are resident on one SM (the
+    // first wave fills SM (b mod slots) with them): they share one contiguous unit range and
+    // take its units round robin, so the co-resident CTAs work on the same (column group,
+    // prime) for successive vectors and read the same four-step twiddles (one L1-resident
+    // tile instead of one per CTA).  Any placement gives the same results.
+    const uint32_t lanes = A.lanes;
+    const uint32_t slots = gridDim.x / lanes;
+    const uint32_t slot = blockIdx.x % slots, lane = blockIdx.x / slots;
+    const uint32_t u0 = (uint32_t)(((uint64_t)slot * units) / slots) + lane;
+    const uint32_t u1 = (uint32_t)(((uint64_t)(slot + 1) * units) / slots);
     auto sidx = [c](int pos) { return pos * 32 + c; };
 
     uint32_t tw[E / 2], twp[E / 2];
@@ -622,10 +631,13 @@ col_pass(const ColArgs A) {
         pi = pair0 % P;
         cg = pair0 / P;
     }
-    for (uint32_t u = u0; u < u1; u++) {
-        if (u != u0 && ++iv == nvec) {
-            iv = 0;
-            if (++pi == P) { pi = 0; cg++; }
+    for (uint32_t u = u0; u < u1; u += lanes) {
+        if (u != u0) {
+            iv += lanes;
+            while (iv >= nvec) {
+                iv -= nvec;
+                if (++pi == P) { pi = 0; cg++; }
+            }
         }
         const uint32_t j1 = cg * 32 + c;
         if ((int)pi != cur_pi) {
@@ -644,8 +656,13 @@ col_pass(const ColArgs A) {
         const bool zh = MODE == COL_FWD && 2 * rows <= (1u << S_LOG);
         {
             constexpr int R = 1 << SP::rlog(0);
+#if defined(PA_COL_DBG) && (PA_COL_DBG & 4)
+            const uint32_t *src = ((MODE == COL_INV) ? A.src + (size_t)pi * L
+                                                     : A.src + ((size_t)0 * P + pi) * ((size_t)rows * N1)) +
+#else
             const uint32_t *src = ((MODE == COL_INV) ? A.src + (size_t)pi * L
                                                      : A.src + ((size_t)iv * P + pi) * ((size_t)rows * N1)) +
+#endif
                                   ((size_t)v << N1_LOG) + j1;
             if (zh) {
 #pragma unroll
@@ -693,7 +710,11 @@ col_pass(const ColArgs A) {
                     const size_t o = (size_t)rel << N1_LOG;
                     uint32_t val = x[h * R + mm];
                     if constexpr (MODE != COL_INV) {
+#if defined(PA_COL_DBG) && (PA_COL_DBG & 1)
+                        const uint2 w = make_uint2(j1 + 3u, (j1 + 3u) * 5u);   // timing-only ablation
+#else
                         const uint2 w = PA_LDG(tw4 + o);
+#endif
                         val = mul_shoup(val, w.x, w.y, cx.p);
                     }
                     else val = red1p(val, cx.p);
