@@ -23,7 +23,8 @@ struct alignas(16) PrimeK {  // per-prime constants passed to kernels
     uint32_t r2;           // R^2 mod p         (to Montgomery form)
     uint32_t pw[8];        // 2^(32 i) mod p, i < 8 (multiword limb reduction)
     uint32_t pw24[10];     // 2^(24 j) mod p, j < 10 (the same, over 24-bit chunks)
-    uint32_t pad_[2];
+    uint32_t pw28[10];     // 2^(28 j) mod p, j < 10 (over 28-bit chunks)
+    uint32_t pad_[4];
 };
 
 // All primes of a stage by value: passed as a kernel parameter, so the per-prime constants

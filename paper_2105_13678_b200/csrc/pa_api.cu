@@ -504,6 +504,7 @@ static int setup_stage(DevAlloc &da, const pa_stage_plan &pl, StageDev &sd, cuda
         pk[i].r2 = (uint32_t)powmod64(2, 64, p);
         for (int w = 0; w < 8; w++) pk[i].pw[w] = (uint32_t)powmod64(2, 32ull * w, p);
         for (int w = 0; w < 10; w++) pk[i].pw24[w] = (uint32_t)powmod64(2, 24ull * w, p);
+        for (int w = 0; w < 10; w++) pk[i].pw28[w] = (uint32_t)powmod64(2, 28ull * w, p);
         const uint32_t g = primitive_root(p);
         const uint32_t wf = (uint32_t)powmod64(g, (p - 1) >> lg, p);     // omega_L
         const uint32_t wi = inv_mod(wf, p);
@@ -1058,11 +1059,23 @@ static uint32_t mac_v_rt(int slog) {
     }
 }
 
+#ifndef PA_PACK_CW28
+#define PA_PACK_CW28 1                 // key limbs reduced over 28-bit chunks where that saves one
+#endif
 template <int NW>
 static void launch_pack_key(const KeySrc &s, uint32_t nvec, const PrimeSet &pk, uint32_t P, uint32_t wxp, uint32_t *res,
                             cudaStream_t st) {
     const dim3 grid((wxp + kPackL * kPackT - 1) / (kPackL * kPackT), nvec);   // kPackL limbs per thread
-    pack_key_residues<NW><<<grid, kPackT, 0, st>>>(s, pk, P, wxp, res);
+    // a limb of B <= 28 (NW - 1) + 28 bits... : ceil(B / 28) 28-bit chunks when that is fewer
+    // than the ceil(32 NW / 24) 24-bit ones (B = 168: 6 against 8)
+    constexpr int NCLO = (32 * (NW - 1) + 8 + 27) / 28;       // chunks of the narrowest B with NW words
+    const uint32_t B = 8 * s.limb_bytes;
+    if (PA_PACK_CW28 && NCLO <= 10 && B <= 28u * NCLO)
+        pack_key_residues<NW, (NCLO <= 10 ? NCLO : 10)><<<grid, kPackT, 0, st>>>(s, pk, P, wxp, res);
+    else if (PA_PACK_CW28 && (32 * NW + 27) / 28 <= 10)
+        pack_key_residues<NW, ((32 * NW + 27) / 28 <= 10 ? (32 * NW + 27) / 28 : 10)><<<grid, kPackT, 0, st>>>(s, pk, P, wxp, res);
+    else
+        pack_key_residues<NW><<<grid, kPackT, 0, st>>>(s, pk, P, wxp, res);
 }
 
 static int launch_pack(const KeyLimbs &src, uint32_t B, uint32_t grid, const PrimeSet &pk, uint32_t P, uint32_t nvec,

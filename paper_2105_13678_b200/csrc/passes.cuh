@@ -183,6 +183,27 @@ __device__ __forceinline__ uint32_t limb_chunks_redc(const uint32_t (&c)[NC], co
     return redc64(t, k.p, k.pinv);
 }
 
+// The same over NC 28-bit chunks (key limbs; B <= 28 NC): sum_j c_j (2^(28 j) mod p) <=
+// 10 (2^28 - 1)(p - 1) < p 2^32, so one REDC still gives v 2^-32 mod p in (0, 2p); a 168-bit
+// limb takes 6 multiply-adds per prime instead of the 8 of its 24-bit chunks.
+template <int NW, int NC>
+__device__ __forceinline__ void limb_chunks28(const uint32_t (&w)[NW], uint32_t (&c)[NC]) {
+#pragma unroll
+    for (int j = 0; j < NC; j++) {
+        const int i = (28 * j) >> 5, sh = (28 * j) & 31;
+        const uint32_t lo = i < NW ? w[i] : 0u, hi = (i + 1 < NW) ? w[i + 1] : 0u;
+        c[j] = __funnelshift_r(lo, hi, sh) & 0xFFFFFFFu;
+    }
+}
+template <int NC>
+__device__ __forceinline__ uint32_t limb_chunks28_redc(const uint32_t (&c)[NC], const PrimeK &k) {
+    static_assert(NC <= 10, "pw28 holds 10 chunk weights");
+    uint64_t t = 0;
+#pragma unroll
+    for (int j = 0; j < NC; j++) t = mad_wide(c[j], k.pw28[j], t);
+    return redc64(t, k.p, k.pinv);
+}
+
 // The residues of one multiword limb modulo all P primes, stored P x wxp apart from o.
 template <int NW>
 __device__ __forceinline__ void store_residues(uint32_t *o, uint32_t wxp, uint32_t P, uint32_t any,
@@ -246,7 +267,8 @@ constexpr int kPackL = PA_PACKL;                               // limbs per thre
 // Residues of kPackL limbs (j0 + q kPackT) modulo all P primes, stored P x wxp apart.
 // A zero limb among non-zero ones reduces to p (== 0 mod p, inside the [0, 2p) range the
 // column pass takes); an all-zero set stores zeros.
-template <int NW>
+// NC28 > 0: the limbs hold at most 28 NC28 bits; reduce them over 28-bit chunks.
+template <int NW, int NC28 = 0>
 __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, uint32_t wxp, uint32_t P, uint32_t any,
                                                      const uint32_t (&w)[kPackL][NW], const PrimeSet &ks) {
     if (!any) {
@@ -254,6 +276,22 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
 #pragma unroll
             for (int q = 0; q < kPackL; q++)
                 if (j0 + q * kPackT < wxp) PA_AT(o + q * kPackT) = 0u;
+        return;
+    }
+    if constexpr (NC28 > 0) {
+        uint32_t c[kPackL][NC28];
+#pragma unroll
+        for (int q = 0; q < kPackL; q++) limb_chunks28<NW, NC28>(w[q], c[q]);
+#pragma unroll
+        for (uint32_t pi = 0; pi < kMaxPrimes; pi++) {
+            if (pi >= P) break;
+#pragma unroll
+            for (int q = 0; q < kPackL; q++) {
+                const uint32_t r = limb_chunks28_redc<NC28>(c[q], ks.k[pi]);
+                if (j0 + q * kPackT < wxp) PA_AT(o + q * kPackT) = r;
+            }
+            o += wxp;
+        }
         return;
     }
 #if PA_PACK_CHUNK24
@@ -288,7 +326,7 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
     }
 }
 
-template <int NW>
+template <int NW, int NC28 = 0>
 __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
     PA_TMARK(0x6000 | NW, 0);
@@ -382,7 +420,7 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     uint32_t any = 0;
 #pragma unroll
     for (int q = 0; q < kPackL; q++) any |= extract(j0 + q * kPackT, w[q]);
-    store_residues_multi<NW>(res + (size_t)iv * P * wxp + j0, j0, wxp, P, any, w, ks);
+    store_residues_multi<NW, NC28>(res + (size_t)iv * P * wxp + j0, j0, wxp, P, any, w, ks);
 }
 
 // S1 for many word-sourced vectors (pa_ctx_rekey's a_i): CTA (tile of kPackL kPackT limbs,
