@@ -55,16 +55,18 @@ for rep in range(3):
                "last_start_us": (int(e["t"].max()) - t0) / 1e3,
                "until_next_kernel_us": ((nxt - ts) / 1e3) if nxt else None}
         if (kid & 0xF000) == 0x5000:
+            # carry tiles: every phase mark carries the tile (0x100000 | tile); times relative to
+            # phase 7 (ticket known) of the same tile, on the global timer (ns)
             ph = {}
-            for p in (2, 3, 4, 5):
+            base = r[(r["kid"] == kid) & (r["phase"] == 7)]
+            bt = {int(b): int(t) for b, t in zip(base["blk"], base["t"])}
+            ph["ticket_us_after_first_start_median"] = float(np.median([(bt[k] - ts) / 1e3 for k in bt])) if bt else None
+            for p in (8, 9, 18, 2, 3, 4, 5):
                 a = r[(r["kid"] == kid) & (r["phase"] == p)]
-                b = r[(r["kid"] == kid) & (r["phase"] == 0)]
-                if len(a) == len(b) and len(a):
-                    ia = np.argsort(a["blk"]); ib = np.argsort(b["blk"])
-                    d = (a["clk"][ia].astype(np.int64) - b["clk"][ib].astype(np.int64))
-                    ph[f"phase{p}_cycles_median"] = float(np.median(d))
-                    ph[f"phase{p}_cycles_max"] = float(d.max())
-                    ph[f"phase{p}_end_us_max"] = (int(a["t"].max()) - t0) / 1e3
+                d = [(int(t) - bt[int(b)]) / 1e3 for b, t in zip(a["blk"], a["t"]) if int(b) in bt]
+                if d:
+                    ph[f"phase{p}_us_median"] = round(float(np.median(d)), 2)
+                    ph[f"phase{p}_us_max"] = round(float(max(d)), 2)
             row.update(ph)
         rows.append(row)
     res[rep] = rows
