@@ -439,6 +439,7 @@ __global__ void __launch_bounds__(kCCT) crt_carry(const uint32_t *__restrict__ c
     for (uint32_t i = threadIdx.x; i < kCCTile; i += blockDim.x) s_clo[i] = s_chi[i] = 0u;
     __syncthreads();
     const uint32_t tile = s_tile;
+    PA_TMARK_B(kKid, 7, 0x100000 | tile);               // ticket known (scripts/tprof.py phase base)
     const uint32_t u0 = tile * kCCTile;
     const uint32_t ub = u0 + threadIdx.x * kCCV;            // this thread's first word
     const uint32_t nchunks = (DBG & 8) ? 0u : RING ? (uint32_t)(((uint64_t)B * ncoef + gamma - 1) / gamma) : 1u;
