@@ -371,6 +371,8 @@ def main():
                     help="skip the MH-only PA comparator measurement")
     ap.add_argument("--only-device", action="store_true",
                     help="timed device steps only (no per-stage pass, no e2e): for ncu launch lists")
+    ap.add_argument("--p2p", action="store_true",
+                    help="N>1: exchange the accumulators over peer memory (pa_params.p2p) instead of ncclReduce")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo only to validate the multi-rank path)")
     ap.add_argument("--same-device", action="store_true",
@@ -432,7 +434,8 @@ def main():
     if paper:
         ctx = PAContext(w.n, 0, w.m, w.gamma, seed=w.hash_seed, limb_bits=args.limb_bits, paper_k=w.k)
     elif lib_nccl:
-        ctx = nccl_context(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits, throughput_only=True)
+        ctx = nccl_context(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits, throughput_only=True,
+                           p2p=args.p2p)
     else:
         ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None,
                         limb_bits=args.limb_bits, throughput_only=True)
@@ -775,9 +778,10 @@ def main():
                    "alpha": info["alpha"],
                    "mmh_plan": {kk: info["mmh"][kk] for kk in ("limb_bits", "nprimes", "log2_len", "n_col", "n_row")},
                    "mh_plan": {kk: info["mh"][kk] for kk in ("limb_bits", "nprimes", "log2_len", "n_col", "n_row")},
-                   "parallelism": (f"blocks sharded over {world} ranks; transform-domain accumulators summed by one "
-                                   "ncclReduce (library NCCL) to rank 0, which runs the inverse, CRT, carries, fold "
-                                   "and MH") if lib_nccl else (f"{world} ranks, gloo exchange (validation)" if world > 1
+                   "parallelism": (f"blocks sharded over {world} ranks; transform-domain accumulators " +
+                                   ("added by each rank's row MAC into rank 0's receive buffer over peer memory "
+                                    "(p2p)" if args.p2p else "summed by one ncclReduce (library NCCL) to rank 0") +
+                                   ", which runs the inverse, CRT, carries, fold and MH") if lib_nccl else (f"{world} ranks, gloo exchange (validation)" if world > 1
                                                                 else "one GPU"),
                    "l2": "flushed (256 MiB write) before every timed step" if not args.no_flush else "not flushed"},
         "gpu_launches": launches_timed,

@@ -101,6 +101,8 @@ typedef struct {
     uint32_t graph_updates;  /* ... of which updated an executable graph in place */
     uint32_t graph_instantiations;
     uint32_t tz_group_blocks;/* Toeplitz contexts: input blocks per accumulation group */
+    uint32_t p2p;            /* multi-GPU contexts: 1 = accumulators exchanged over peer memory
+                                (pa_params.p2p), 0 = ncclReduce */
 } pa_info;
 
 typedef struct {
@@ -176,6 +178,17 @@ typedef struct {
      * floor((prime - 1) / r) (0 = automatic).  Smaller groups exercise the grouped (parity
      * XOR) path at small n; the output does not depend on it. */
     uint64_t tz_group_blocks;
+    /* Multi-GPU contexts (world >= 1): exchange the transform-domain accumulators over peer
+     * memory instead of an ncclReduce.  Each rank's row multiply-accumulate adds its canonical
+     * partial sums with 64-bit atomics straight into the key root's receive buffer (NVLink peer
+     * stores, overlapping the transforms; the compute and the collective are one kernel), and
+     * 32-bit counters in each GPU's own memory order the uses of a receive buffer (the root
+     * zeroes and frees it after its import; ranks wait for that before their next atomics).
+     * The buffers (cudaMalloc) are shared through CUDA IPC handles all-gathered once over the
+     * context's NCCL communicator at creation.  Ranks must issue the same sequence of
+     * pa_hash / pa_hash_batch calls.  Requires peer access between the GPUs (one node);
+     * creation fails with PA_E_CUDA otherwise.  0: ncclReduce (default). */
+    int32_t p2p;
 } pa_params;
 
 /* Create a context on the current CUDA device.  `p` is the Mersenne EXPONENT
@@ -334,6 +347,10 @@ int pa_debug_selftest(void);
 
 /* Code of the last failure on this thread; copies its message into buf. */
 int pa_last_error(char *buf, size_t len);
+
+/* sizeof(pa_params) and sizeof(pa_info) as compiled into the library (host only): bindings
+ * check their struct mirrors against them.  Outputs may be NULL.  Returns PA_OK. */
+int pa_abi_sizes(uint64_t *params_bytes, uint64_t *info_bytes);
 
 #ifdef __cplusplus
 }

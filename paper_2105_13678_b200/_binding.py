@@ -49,7 +49,7 @@ class pa_info(ctypes.Structure):
                 ("device_bytes", u64), ("kernels_per_hash", u32), ("launches_total", u32),
                 ("insecure_length", u32), ("world", i32), ("rank", i32), ("acc_words", u64),
                 ("graph_captures", u32), ("graph_updates", u32), ("graph_instantiations", u32),
-                ("tz_group_blocks", u32)]
+                ("tz_group_blocks", u32), ("p2p", u32)]
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("mmh", "mh")}
@@ -71,7 +71,7 @@ class pa_params(ctypes.Structure):
                 ("stream", vp), ("limb_bits", i32), ("strict", i32), ("paper_k", u64), ("mh_only", u64),
                 ("toeplitz", u64), ("world", i32), ("rank", i32), ("nccl_id", ctypes.c_uint8 * 128),
                 ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE), ("alloc_user", vp),
-                ("tz_group_blocks", u64)]
+                ("tz_group_blocks", u64), ("p2p", i32)]
 
 
 def _sig(name, res, *args):
@@ -108,6 +108,7 @@ pa_philox4x64_10 = _sig("pa_philox4x64_10", i32, u64, u64, u64, vp)
 pa_expand_a = _sig("pa_expand_a", i32, u64, u64, u64, vp)
 pa_expand_bc = _sig("pa_expand_bc", i32, u64, u64, vp, vp)
 pa_last_error = _sig("pa_last_error", i32, ctypes.c_char_p, ctypes.c_size_t)
+pa_abi_sizes = _sig("pa_abi_sizes", i32, ctypes.POINTER(u64), ctypes.POINTER(u64))
 pa_derive_security_coefficient = _sig("pa_derive_security_coefficient", i32, ctypes.c_double, ctypes.POINTER(u64))
 pa_select_block_count = _sig("pa_select_block_count", i32, ctypes.c_double, ctypes.POINTER(u64))
 pa_select_gamma = _sig("pa_select_gamma", i32, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(i32))
@@ -119,7 +120,7 @@ EXPORTED = ["pa_ctx_create", "pa_ctx_create_ex", "pa_hash", "pa_hash_host", "pa_
             "pa_ctx_stage_times", "pa_plan", "pa_philox4x64_10", "pa_expand_a", "pa_expand_bc",
             "pa_last_error", "pa_ctx_paper_stats", "pa_derive_security_coefficient", "pa_select_block_count", "pa_select_gamma",
             "pa_derive_paper_params", "pa_mmh_acc", "pa_tail_merge", "pa_nccl_unique_id", "pa_debug_build",
-            "pa_debug_selftest"]
+            "pa_debug_selftest", "pa_abi_sizes"]
 
 
 class PAError(RuntimeError):

@@ -42,4 +42,57 @@ __global__ void __launch_bounds__(256) acc_import_u64(const uint64_t *__restrict
     }
 }
 
+// ---- P2P exchange (pa_params.p2p): the ranks' row MACs add their partial accumulators
+// straight into the root's 64-bit receive buffer over NVLink (row_mac mode 3, so the transfer
+// overlaps the multiply-accumulate), and 32-bit counters in each GPU's own memory order the
+// uses of a buffer.  A counter is incremented by a remote (or local) release atomic and
+// waited on locally; every counter has a local "expected" companion that the wait advances,
+// so every kernel argument stays the same from one use to the next (graph replay).
+constexpr int kMaxWorld = 64;
+constexpr uint32_t kFlagWords = 32;          // one counter per 128-byte line
+struct PeerFlags {
+    uint32_t *p[kMaxWorld];
+};
+
+// for i < n: wait until flags[i] >= expected[i] + 1 (wrap-safe), then expected[i] += 1.
+// A peer that never signals (a rank that stopped calling) must not hang the GPU: after
+// kP2PTimeoutNs the wait gives up and traps, which fails the stream with an error.
+constexpr uint64_t kP2PTimeoutNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void __launch_bounds__(64) p2p_wait(const uint32_t *flags, uint32_t *expected, uint32_t n) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t want = PA_AT(expected + (size_t)i * kFlagWords) + 1u;
+        const uint32_t *f = flags + (size_t)i * kFlagWords;
+        PA_CK(f, 4);
+        const uint64_t t0 = globaltimer_ns();
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if ((int32_t)(v - want) >= 0) break;
+            if (globaltimer_ns() - t0 > kP2PTimeoutNs) {
+                printf("pa p2p_wait: counter %u stuck at %u, expected %u (a rank stopped?)\n", i, v, want);
+                __trap();
+            }
+            __nanosleep(256);
+        }
+        PA_AT(expected + (size_t)i * kFlagWords) = want;
+    }
+}
+
+// for i < n: counter P.p[i] += 1, a system-scope release after everything this stream did
+// before (the preceding kernels' peer writes ended with a system fence)
+__global__ void __launch_bounds__(64) p2p_signal(PeerFlags P, uint32_t n) {
+    const uint32_t i = threadIdx.x;
+    if (i < n) {
+        __threadfence_system();
+        uint32_t old;
+        asm volatile("atom.add.release.sys.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.p[i]) : "memory");
+        (void)old;
+    }
+}
+
 }  // namespace pa

@@ -23,6 +23,7 @@ struct NcclApi {
     ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
                            cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GetVersion)(int *) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -47,6 +48,7 @@ inline NcclApi &nccl_api() {
         sym(api.CommDestroy, "ncclCommDestroy");
         sym(api.CommAbort, "ncclCommAbort");
         sym(api.Reduce, "ncclReduce");
+        sym(api.AllGather, "ncclAllGather");
         sym(api.GetVersion, "ncclGetVersion");
         sym(api.GetErrorString, "ncclGetErrorString");
         if (!all) {

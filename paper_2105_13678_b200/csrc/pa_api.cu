@@ -239,6 +239,8 @@ static int make_plan(const pa_params *prm, Plan *P) {
         return set_err(PA_E_PARAM, "multi-GPU: need 0 <= rank < world (got rank %d, world %d)", p.rank, p.world);
     if (p.world > 0 && (p.paper_k || p.mh_only || p.toeplitz))
         return set_err(PA_E_PARAM, "multi-GPU contexts hash in r-bit mode (no paper_k, mh_only or toeplitz)");
+    if (prm->p2p && (p.world < 1 || p.world > kMaxWorld))
+        return set_err(PA_E_PARAM, "p2p needs a multi-GPU context with 1 <= world <= %d", kMaxWorld);
     if (p.m < 1) return set_err(PA_E_PARAM, "m must be >= 1");
     if (p.toeplitz) {
         // comparator: Toeplitz-hashing PA, r x r blocks, one prime
@@ -787,6 +789,10 @@ static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, 
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
     const uint64_t full = (uint64_t)ki.occ * g_num_sms;
     *nslot = 1;
+    if (mode == 3) {                                     // 64-bit sums: no partial-count bound
+        *grid = (int)std::min<uint64_t>(full, (uint64_t)nunits * nvec);
+        return PA_OK;
+    }
     if (mode) {
         *grid = (int)std::min<uint64_t>(nunits, full);
         return PA_OK;
@@ -941,6 +947,17 @@ struct pa_ctx {
     ncclComm_t comm = nullptr;
     bool x_u64 = false;                       // reduce 64-bit words (world * max prime >= 2^32)
     void *xsend[2] = {}, *xrecv[2] = {};
+    // P2P exchange (pa_params.p2p, exchange.cuh): this GPU's receive region (cudaMalloc, shared
+    // by CUDA IPC): two 64-bit receive buffers [P][L] and the counters (p2p_flag_word); every
+    // rank's region as mapped in this process (own: p2p_region)
+    bool p2p = false;
+    uint8_t *p2p_region = nullptr;
+    size_t p2p_recv_bytes = 0;
+    uint8_t *p2p_peer[kMaxWorld] = {};
+    uint32_t *p2p_tmp = nullptr;              // root: the imported accumulator [P][L]
+    uint32_t p2p_uses[kMaxWorld] = {};        // keys rooted at rank q so far (the same on all ranks)
+    GraphSlot g_p2p_pre[kMaxWorld][2][2];     // [root][receive buffer][hashing buffer set]
+    GraphSlot g_p2p_post[2][2];               // [receive buffer][hashing buffer set]
     cudaEvent_t copy_ev[9] = {};
     uint8_t *out_dev = nullptr;
     uint8_t *key_dev2 = nullptr, *out_dev2 = nullptr;   // pa_hash_host_batch second staging set
@@ -1170,12 +1187,14 @@ static int stage_pack_col(pa_ctx *c, StageDev &sd, const Src &src, uint32_t nvec
 // into zeroed acc); else first / later call of a multi-call accumulation (whole units per
 // CTA, store / modular read-modify-write, no atomics).
 static int stage_mac(pa_ctx *c, StageDev &sd, uint32_t nvec, const uint32_t *scratch, const uint32_t *hat,
-                     uint32_t *acc, bool first, const char *tag, bool only = true, bool zero = true) {
+                     uint32_t *acc, bool first, const char *tag, bool only = true, bool zero = true,
+                     unsigned long long *dst64 = nullptr) {
     const int rlog = __builtin_ctz(sd.pl.n_row);
     const uint32_t P = sd.pl.nprimes;
     ProfScope ps(c, tag);
     MacArgs M{};
-    M.mode = only ? 0u : (first ? 1u : 2u);
+    M.mode = dst64 ? 3u : only ? 0u : (first ? 1u : 2u);
+    M.dst64 = dst64;
     M.nt = ntt_args(sd, 0, 1);
     M.src = scratch;
     M.ahat = hat;
@@ -1185,8 +1204,8 @@ static int stage_mac(pa_ctx *c, StageDev &sd, uint32_t nvec, const uint32_t *scr
     int grid = 0;
     TRY(mac_grid(rlog, M.nunits, nvec, M.mode, &grid, &M.nslot));
     M.slot_stride = P * sd.L;
-    if (only && zero) CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M.nslot * P * sd.L * 4, c->stream));
-    if (&sd == &c->smmh) c->mac_slots = M.nslot;
+    if (only && zero && !dst64) CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M.nslot * P * sd.L * 4, c->stream));
+    if (&sd == &c->smmh && !dst64) c->mac_slots = M.nslot;
     TRY(launch_mac(rlog, M, grid, c->stream));
     c->launches++;
     return PA_OK;
@@ -1592,6 +1611,16 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     if (!c) return;
     DevGuard dg_(c);
     cudaStreamSynchronize(c->stream);
+    if (c->p2p_region) {
+        for (int q = 0; q < kMaxWorld; q++)
+            if (c->p2p_peer[q] && c->p2p_peer[q] != c->p2p_region) cudaIpcCloseMemHandle(c->p2p_peer[q]);
+        cudaFree(c->p2p_region);
+    }
+    for (auto &row : c->g_p2p_pre)
+        for (auto &pair : row)
+            for (GraphSlot &g : pair) g.reset();
+    for (auto &pair : c->g_p2p_post)
+        for (GraphSlot &g : pair) g.reset();
     if (c->comm) nccl_api().CommDestroy(c->comm);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->evpool) cudaEventDestroy(e);
@@ -1711,6 +1740,7 @@ extern "C" int pa_ctx_query(const pa_ctx *c, pa_info *info) {
     info->graph_captures = c->graph_captures;
     info->graph_updates = c->graph_updates;
     info->graph_instantiations = c->graph_instantiations;
+    info->p2p = c->p2p ? 1u : 0u;
     info->tz_group_blocks = p.toeplitz ? p.tz_group : 0u;
     info->kernels_per_hash = c->launches;
     info->launches_total = c->launches_total;
@@ -1931,6 +1961,7 @@ static bool graphs_enabled(const pa_ctx *c) {
 }
 
 static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set);
+static int mg_hash_p2p(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set);
 static int mg_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count);
 
 // Enqueue `enqueue()` on the context stream through the graph slot `gs` (captured once per
@@ -1991,7 +2022,7 @@ extern "C" int pa_hash(pa_ctx *c, const uint8_t *key_bits, uint8_t *out_bits) {
     if (!c || !key_bits) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
     dbg_user({{key_bits, key_slice_len(c)}, {out_bits, cdiv(c->pl.m, 8)}});
-    if (c->comm) return mg_hash(c, key_bits, out_bits, 0, 0);
+    if (c->comm) return c->p2p ? mg_hash_p2p(c, key_bits, out_bits, 0, 0) : mg_hash(c, key_bits, out_bits, 0, 0);
     if (!out_bits) return set_err(PA_E_PARAM, "NULL argument");
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k)
         return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge or pa_mmh_acc + pa_tail_merge");
@@ -2171,6 +2202,119 @@ static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int se
     return PA_OK;
 }
 
+// ---- P2P exchange (pa_params.p2p; exchange.cuh).  Counter words of a region (each
+// kFlagWords apart): FREE(q, s) -- root q's receive buffer s may take new sums (written by q);
+// READY(s, r) -- rank r's sums for this GPU's buffer s are complete (written by r);
+// EXPF / EXPR -- this GPU's "expected" companions of FREE / READY (local only).
+enum { P2P_FREE = 0, P2P_READY = 2 * kMaxWorld, P2P_EXPF = 4 * kMaxWorld, P2P_EXPR = 6 * kMaxWorld,
+       P2P_NFLAG = 8 * kMaxWorld };
+static uint32_t *p2p_flag(uint8_t *region, size_t recv_bytes, uint32_t idx) {
+    return reinterpret_cast<uint32_t *>(region + 2 * recv_bytes) + (size_t)idx * kFlagWords;
+}
+
+// one key on a P2P multi-GPU context, finished on `root`, hashing buffer set `set`
+static int mg_hash_p2p(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set) {
+    const int rank = c->pl.rank, world = c->pl.world;
+    if (rank == root && !out) return set_err(PA_E_PARAM, "NULL output on the root rank");
+    const uint32_t s = c->p2p_uses[root]++ & 1u;         // receive buffer of this use of root's
+    const size_t RB = c->p2p_recv_bytes;
+    uint8_t *rreg = c->p2p_peer[root];
+    auto *dst64 = reinterpret_cast<unsigned long long *>(rreg + s * RB);
+    uint32_t launched = 0;
+    // S1-S3: transforms, then (once root has freed buffer s) the row MAC adding into it over
+    // NVLink, then READY(s, rank) += 1 on the root
+    TRY(graph_run(c, c->g_p2p_pre[root][s][set], {key, c->scratch}, [&] {
+        c->launches = 0;
+        TRY(mmh_forward(c, key, 0, c->nblk));
+        p2p_wait<<<1, 64, 0, c->stream>>>(p2p_flag(c->p2p_region, RB, P2P_FREE + 2 * root + s),
+                                          p2p_flag(c->p2p_region, RB, P2P_EXPF + 2 * root + s), 1);
+        CUDA_TRY(cudaGetLastError());
+        const size_t off = 0;
+        TRY(stage_mac(c, c->smmh, c->nblk, c->scratch + off, c->ahat + off, c->acc, true, "mmh_fwd_row_mac_p2p", true,
+                      false, dst64));
+        PeerFlags pf{};
+        pf.p[0] = p2p_flag(rreg, RB, P2P_READY + s * kMaxWorld + rank);
+        p2p_signal<<<1, 64, 0, c->stream>>>(pf, 1);
+        CUDA_TRY(cudaGetLastError());
+        c->launches += 2;
+        return PA_OK;
+    }));
+    launched += c->launches;
+    if (rank == root) {
+        // every rank's sums in: import (mod each prime), S4-S7, zero the buffer, FREE(rank, s)
+        // += 1 on every rank
+        TRY(graph_run(c, c->g_p2p_post[s][set], {out, c->scratch}, [&] {
+            c->launches = 0;
+            TRY(carry_reset(c));
+            p2p_wait<<<1, 64, 0, c->stream>>>(p2p_flag(c->p2p_region, RB, P2P_READY + s * kMaxWorld),
+                                              p2p_flag(c->p2p_region, RB, P2P_EXPR + s * kMaxWorld), (uint32_t)world);
+            CUDA_TRY(cudaGetLastError());
+            const uint64_t total = (uint64_t)c->pl.mmh.nprimes * c->smmh.L;
+            const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
+            {
+                ProfScope ps(c, "mmh_acc_import");
+                acc_import_u64<<<grid, 256, 0, c->stream>>>(reinterpret_cast<const uint64_t *>(c->p2p_region + s * RB),
+                                                             c->pl.mmh.log2_len, total, c->smmh.pks, c->p2p_tmp);
+                CUDA_TRY(cudaGetLastError());
+            }
+            CUDA_TRY(cudaMemsetAsync(c->p2p_region + s * RB, 0, RB, c->stream));
+            PeerFlags pf{};
+            for (int r = 0; r < world; r++) pf.p[r] = p2p_flag(c->p2p_peer[r], RB, P2P_FREE + 2 * rank + s);
+            p2p_signal<<<1, 64, 0, c->stream>>>(pf, (uint32_t)world);
+            CUDA_TRY(cudaGetLastError());
+            c->launches += 3;
+            uint32_t *y = nullptr;
+            TRY(mmh_tail(c, &y, c->p2p_tmp, 1, 0));
+            return run_mh(c, y, out);
+        }));
+        launched += c->launches;
+    }
+    c->launches = launched;
+    c->launches_total += launched;
+    return PA_OK;
+}
+
+// P2P setup (collective, after the communicator exists): region, IPC handles all-gathered
+// over NCCL, peers mapped, FREE counters primed; a final all-gather is the barrier after which
+// any rank may signal any other
+static int p2p_init(pa_ctx *c) {
+    const int world = c->pl.world, rank = c->pl.rank;
+    if (world > kMaxWorld) return set_err(PA_E_PARAM, "p2p: world %d > %d", world, kMaxWorld);
+    NcclApi &api = nccl_api();
+    const size_t total = (size_t)c->pl.mmh.nprimes * c->smmh.L;
+    c->p2p_recv_bytes = (total * 8 + 4095) & ~(size_t)4095;
+    const size_t bytes = 2 * c->p2p_recv_bytes + (size_t)P2P_NFLAG * kFlagWords * 4;
+    CUDA_TRY(cudaMalloc(&c->p2p_region, bytes));
+    dbg_add(c->p2p_region, bytes);
+    TRY(c->da.alloc(&c->p2p_tmp, total));
+    CUDA_TRY(cudaMemsetAsync(c->p2p_region, 0, bytes, c->stream));
+    std::vector<uint32_t> one(2 * kMaxWorld * kFlagWords, 0);
+    for (int i = 0; i < 2 * kMaxWorld; i++) one[(size_t)i * kFlagWords] = 1u;   // every buffer free for use 1
+    CUDA_TRY(cudaMemcpyAsync(p2p_flag(c->p2p_region, c->p2p_recv_bytes, P2P_FREE), one.data(), one.size() * 4,
+                             cudaMemcpyHostToDevice, c->stream));
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, c->p2p_region));
+    uint8_t *hb = nullptr;
+    TRY(c->da.alloc(&hb, (size_t)world * sizeof h));
+    CUDA_TRY(cudaMemcpyAsync(hb + (size_t)rank * sizeof h, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(api.AllGather(hb + (size_t)rank * sizeof h, hb, sizeof h, ncclUint8, c->comm, c->stream));
+    std::vector<cudaIpcMemHandle_t> all(world);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), hb, (size_t)world * sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (int q = 0; q < world; q++) {
+        if (q == rank) { c->p2p_peer[q] = c->p2p_region; continue; }
+        void *ptr = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess));
+        c->p2p_peer[q] = static_cast<uint8_t *>(ptr);
+        dbg_add(ptr, bytes);
+    }
+    // barrier: every rank has primed its counters and mapped its peers
+    NCCL_TRY(api.AllGather(hb + (size_t)rank * sizeof h, hb, sizeof h, ncclUint8, c->comm, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->p2p = true;
+    return PA_OK;
+}
+
 // stream of keys with the root rotating (key j on rank j mod world), alternating buffer sets
 // and streams so key j's reduce and tail overlap key j+1's transforms
 static int mg_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count) {
@@ -2187,7 +2331,8 @@ static int mg_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *
     for (uint32_t j = 0; j < count; j++) {
         const int set = (int)(j & 1);
         if (set) swap_bufs(c);
-        const int rc = mg_hash(c, keys[j], outs[j], (int)(j % world), set);
+        const int rc = c->p2p ? mg_hash_p2p(c, keys[j], outs[j], (int)(j % world), set)
+                              : mg_hash(c, keys[j], outs[j], (int)(j % world), set);
         total += c->launches;
         if (set) swap_bufs(c);
         TRY(rc);
@@ -2229,6 +2374,13 @@ static int mg_init(pa_ctx *c, const pa_params *prm) {
     static_assert(sizeof id.internal == sizeof prm->nccl_id, "ncclUniqueId size");
     memcpy(id.internal, prm->nccl_id, sizeof id.internal);
     NCCL_TRY(api.CommInitRank(&c->comm, c->pl.world, id, c->pl.rank));
+    if (prm->p2p) TRY(p2p_init(c));
+    return PA_OK;
+}
+
+extern "C" int pa_abi_sizes(uint64_t *params_bytes, uint64_t *info_bytes) {
+    if (params_bytes) *params_bytes = sizeof(pa_params);
+    if (info_bytes) *info_bytes = sizeof(pa_info);
     return PA_OK;
 }
 

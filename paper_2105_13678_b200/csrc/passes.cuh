@@ -988,6 +988,10 @@ struct MacArgs {
     uint32_t mode;            // 0: iterations split evenly, red.add into zeroed dst (< 4p)
                               // 1: whole units per CTA, dst = sum (canonical)
                               // 2: whole units per CTA, dst = (dst + sum) mod p (dst canonical)
+                              // 3: iterations split evenly, 64-bit red.add of the canonical
+                              //    partials into dst64 (a peer GPU's receive buffer, the
+                              //    multi-GPU P2P exchange), then a system-scope fence
+    unsigned long long *dst64;
     uint32_t nslot;           // mode 0: CTA b adds into slot b mod nslot (dst + slot * slot_stride),
     uint32_t slot_stride;     // so that no slot receives more than four partials of a unit
 };
@@ -1046,10 +1050,11 @@ row_mac(const MacArgs A) {
     const uint32_t P = a.nprimes;
     const uint32_t nvec = A.nvec;
     const uint64_t total = (uint64_t)A.nunits * nvec;
-    const uint64_t it0 = A.mode ? (uint64_t)(blockIdx.x * (uint64_t)A.nunits / gridDim.x) * nvec
-                                : blockIdx.x * total / gridDim.x;
-    const uint64_t it1 = A.mode ? (uint64_t)((blockIdx.x + 1) * (uint64_t)A.nunits / gridDim.x) * nvec
-                                : (blockIdx.x + 1) * total / gridDim.x;
+    const bool whole = A.mode == 1 || A.mode == 2;
+    const uint64_t it0 = whole ? (uint64_t)(blockIdx.x * (uint64_t)A.nunits / gridDim.x) * nvec
+                               : blockIdx.x * total / gridDim.x;
+    const uint64_t it1 = whole ? (uint64_t)((blockIdx.x + 1) * (uint64_t)A.nunits / gridDim.x) * nvec
+                               : (blockIdx.x + 1) * total / gridDim.x;
     auto sidx = [w](int pos) {
         if constexpr (PAD) return w * (S + S / 32) + pos + (pos >> 5);
         else return swz32(w * S + pos);
@@ -1101,6 +1106,11 @@ row_mac(const MacArgs A) {
         v = red1p(v, cx.p);
         PA_CK(d, 4);
         if (A.mode == 0) atomicAdd(d, v);
+        else if (A.mode == 3) {
+            const size_t e = (size_t)(d - dslot);                  // element of the [P][L] accumulator
+            PA_CK(A.dst64 + e, 8);
+            atomicAdd(A.dst64 + e, (unsigned long long)v);
+        }
         else if (A.mode == 1) *d = v;
         else *d = red1p(*d + v, cx.p);
     };
@@ -1183,6 +1193,9 @@ row_mac(const MacArgs A) {
 #pragma unroll
             for (int mm = 0; mm < R; mm++) flush_one(dst + out_pos<S_LOG, E_LOG>(v, h, mm), acc[h * R + mm]);
     }
+    // mode 3: the peer atomics are performed (system scope) before this CTA exits, so the
+    // p2p_signal kernel that follows in stream order publishes complete sums
+    if (A.mode == 3) __threadfence_system();
 }
 
 }  // namespace pa

@@ -25,9 +25,10 @@ def _words(v: int, bits: int) -> np.ndarray:
 
 def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
             stream=None, limb_bits=0, strict=False, keep=None, paper_k=0, mh_only=False,
-            toeplitz=False, world=0, rank=0, nccl_id=None, tz_group_blocks=0) -> B.pa_params:
+            toeplitz=False, world=0, rank=0, nccl_id=None, tz_group_blocks=0, p2p=False) -> B.pa_params:
     prm = B.pa_params()
     prm.tz_group_blocks = tz_group_blocks
+    prm.p2p = 1 if p2p else 0
     prm.n, prm.r, prm.m, prm.gamma, prm.seed = n, r, m, gamma, seed & (2**64 - 1)
     prm.world, prm.rank = world, rank
     if nccl_id is not None:
@@ -63,10 +64,11 @@ def _params(n, r, m, gamma=0, seed=0, block_range=None, a=None, b=None, c=None,
 
 def plan(n: int, r: int, m: int, gamma: int = 0, block_range=None, limb_bits: int = 0,
          strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False,
-         world: int = 0, rank: int = 0, tz_group_blocks: int = 0) -> dict:
+         world: int = 0, rank: int = 0, tz_group_blocks: int = 0, p2p: bool = False) -> dict:
     """Validate parameters and return the transform plan (host only, no GPU)."""
     prm = _params(n, r, m, gamma, 0, block_range, limb_bits=limb_bits, strict=strict, paper_k=paper_k,
-                  mh_only=mh_only, toeplitz=toeplitz, world=world, rank=rank, tz_group_blocks=tz_group_blocks)
+                  mh_only=mh_only, toeplitz=toeplitz, world=world, rank=rank, tz_group_blocks=tz_group_blocks,
+                  p2p=p2p)
     info = B.pa_info()
     B.check(B.pa_plan(ctypes.byref(prm), ctypes.byref(info)))
     return info.as_dict()
@@ -147,7 +149,7 @@ class PAContext:
                  block_range=None, a=None, b=None, c=None, stream=None, limb_bits: int = 0,
                  strict: bool = False, paper_k: int = 0, mh_only: bool = False, toeplitz: bool = False,
                  throughput_only: bool = False, world: int = 0, rank: int = 0, nccl_id: bytes | None = None,
-                 torch_allocator: bool = True, tz_group_blocks: int = 0):
+                 torch_allocator: bool = True, tz_group_blocks: int = 0, p2p: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise B.PAError(B.PA_E_CUDA, "no CUDA device: the library has no CPU path")
@@ -156,7 +158,8 @@ class PAContext:
         self.stream = st
         keep: list = []
         prm = _params(n, r, m, gamma, seed, block_range, a, b, c, ctypes.c_void_p(st.cuda_stream),
-                      limb_bits, strict, keep, paper_k, mh_only, toeplitz, world, rank, nccl_id, tz_group_blocks)
+                      limb_bits, strict, keep, paper_k, mh_only, toeplitz, world, rank, nccl_id, tz_group_blocks,
+                      p2p)
         self._alloc_cbs = None
         if torch_allocator:
             # the context's device memory comes from PyTorch's caching allocator; the callbacks

@@ -284,3 +284,21 @@ def test_debug_build_flag():
         pytest.skip("a development library is loaded")
     assert B.pa_debug_build() == 0
     assert B.pa_debug_selftest() == B.PA_E_STATE
+
+
+def test_struct_mirrors_match_library():
+    # the ctypes mirrors of pa_params / pa_info have the library's layout size
+    pb, ib = ctypes.c_uint64(), ctypes.c_uint64()
+    assert B.pa_abi_sizes(ctypes.byref(pb), ctypes.byref(ib)) == 0
+    assert pb.value == ctypes.sizeof(B.pa_params)
+    assert ib.value == ctypes.sizeof(B.pa_info)
+
+
+def test_plan_p2p_needs_multi_gpu_context():
+    # pa_params.p2p (peer-memory accumulator exchange) is a multi-GPU option only
+    n, r, m = 1 << 20, 1 << 16, 104_858
+    P.plan(n, r, m, world=2, rank=0, p2p=True)
+    for kw in (dict(p2p=True), dict(world=0, rank=0, p2p=True)):
+        with pytest.raises(B.PAError) as ei:
+            P.plan(n, r, m, **kw)
+        assert ei.value.code == B.PA_E_PARAM

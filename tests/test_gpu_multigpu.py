@@ -68,13 +68,16 @@ def _one_rank_ctx(P, n, r, m, seed, **kw):
 
 
 @pytest.mark.parametrize("on_stream", [False, True])
-def test_nccl_one_rank_hash_and_rotating_batch(on_stream):
+@pytest.mark.parametrize("p2p", [False, True])
+def test_nccl_one_rank_hash_and_rotating_batch(on_stream, p2p):
+    # p2p: the peer-memory exchange (row MAC mode 3 into the root's 64-bit receive buffer,
+    # counters waited on / signalled by p2p_wait / p2p_signal) with the rank as its own root
     P = _P()
     n, r, m, seed = 262_157, 2048, 30_001, 4
     s = torch.cuda.Stream() if on_stream else torch.cuda.current_stream()
     with torch.cuda.stream(s):
-        ctx = _one_rank_ctx(P, n, r, m, seed)
-        assert ctx.world == 1 and ctx.rank == 0
+        ctx = _one_rank_ctx(P, n, r, m, seed, p2p=p2p)
+        assert ctx.world == 1 and ctx.rank == 0 and ctx.query()["p2p"] == int(p2p)
         for ks in (1, 2):
             key = key_bytes(n, 0x900 + ks)
             out = ctx.hash(torch.from_numpy(key).cuda())
@@ -93,17 +96,20 @@ def test_nccl_one_rank_hash_and_rotating_batch(on_stream):
         ctx.close()
 
 
-def test_nccl_one_rank_c2_golden():
+@pytest.mark.parametrize("p2p", [False, True])
+def test_nccl_one_rank_c2_golden(p2p):
     import hashlib
     import json
     import os
     P = _P()
     w = CONFIGS["C2"]
-    ctx = _one_rank_ctx(P, w.n, w.r, w.m, w.hash_seed)
-    out = ctx.hash(torch.from_numpy(key_bytes(w.n, w.key_seed)).cuda())
-    torch.cuda.synchronize()
+    ctx = _one_rank_ctx(P, w.n, w.r, w.m, w.hash_seed, p2p=p2p)
     gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "digests.json")))
-    assert hashlib.sha256(bytes(out.cpu().numpy())).hexdigest() == gold["C2"]["out_sha256"]
+    key = torch.from_numpy(key_bytes(w.n, w.key_seed)).cuda()
+    for _ in range(3):            # the receive buffers alternate; each is zeroed and freed after use
+        out = ctx.hash(key)
+        torch.cuda.synchronize()
+        assert hashlib.sha256(bytes(out.cpu().numpy())).hexdigest() == gold["C2"]["out_sha256"]
     ctx.close()
 
 
