@@ -33,12 +33,15 @@ __global__ void __launch_bounds__(256) acc_export(const uint32_t *__restrict__ a
     }
 }
 
-// in[e] < 2^64 (a sum of canonical residues over the ranks) -> in[e] mod q_{e >> log2L}
-__global__ void __launch_bounds__(256) acc_import_u64(const uint64_t *__restrict__ in, uint32_t log2L, uint64_t total,
+// in[e] < 2^64 (a sum of canonical residues over the ranks) -> in[e] mod q_{e >> log2L};
+// ZERO: the input is cleared as it is read (the P2P receive buffer, ready for its next use)
+template <bool ZERO = false>
+__global__ void __launch_bounds__(256) acc_import_u64(uint64_t *__restrict__ in, uint32_t log2L, uint64_t total,
                                                       const PrimeSet ks, uint32_t *__restrict__ out) {
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = ks.k[e >> log2L].p;
         PA_AT(out + e) = (uint32_t)(PA_AT(in + e) % q);
+        if (ZERO) PA_AT(in + e) = 0ull;
     }
 }
 

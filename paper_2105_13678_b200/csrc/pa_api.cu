@@ -954,7 +954,7 @@ struct pa_ctx {
     uint8_t *p2p_region = nullptr;
     size_t p2p_recv_bytes = 0;
     uint8_t *p2p_peer[kMaxWorld] = {};
-    uint32_t *p2p_tmp = nullptr;              // root: the imported accumulator [P][L]
+    uint32_t *p2p_tmp[2] = {};                // root: the imported accumulator [P][L], per hashing buffer set
     uint32_t p2p_uses[kMaxWorld] = {};        // keys rooted at rank q so far (the same on all ranks)
     GraphSlot g_p2p_pre[kMaxWorld][2][2];     // [root][receive buffer][hashing buffer set]
     GraphSlot g_p2p_post[2][2];               // [receive buffer][hashing buffer set]
@@ -2162,8 +2162,8 @@ static int mg_post_enqueue(pa_ctx *c, const void *recv, uint32_t *tmp32, uint8_t
         const uint64_t total = (uint64_t)c->pl.mmh.nprimes * c->smmh.L;
         const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
         ProfScope ps(c, "mmh_acc_import");
-        acc_import_u64<<<grid, 256, 0, c->stream>>>(static_cast<const uint64_t *>(recv), c->pl.mmh.log2_len, total,
-                                                     c->smmh.pks, tmp32);
+        acc_import_u64<<<grid, 256, 0, c->stream>>>(static_cast<uint64_t *>(const_cast<void *>(recv)), c->pl.mmh.log2_len,
+                                                     total, c->smmh.pks, tmp32);
         c->launches++;
         CUDA_TRY(cudaGetLastError());
         src = tmp32;
@@ -2241,8 +2241,8 @@ static int mg_hash_p2p(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, in
     }));
     launched += c->launches;
     if (rank == root) {
-        // every rank's sums in: import (mod each prime), S4-S7, zero the buffer, FREE(rank, s)
-        // += 1 on every rank
+        // every rank's sums in: import (mod each prime; the import zeroes the buffer), S4-S7,
+        // FREE(rank, s) += 1 on every rank
         TRY(graph_run(c, c->g_p2p_post[s][set], {out, c->scratch}, [&] {
             c->launches = 0;
             TRY(carry_reset(c));
@@ -2253,18 +2253,17 @@ static int mg_hash_p2p(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, in
             const uint32_t grid = (uint32_t)std::min<uint64_t>(cdiv(total, 256), (uint64_t)g_num_sms * 8);
             {
                 ProfScope ps(c, "mmh_acc_import");
-                acc_import_u64<<<grid, 256, 0, c->stream>>>(reinterpret_cast<const uint64_t *>(c->p2p_region + s * RB),
-                                                             c->pl.mmh.log2_len, total, c->smmh.pks, c->p2p_tmp);
+                acc_import_u64<true><<<grid, 256, 0, c->stream>>>(reinterpret_cast<uint64_t *>(c->p2p_region + s * RB),
+                                                                   c->pl.mmh.log2_len, total, c->smmh.pks, c->p2p_tmp[set]);
                 CUDA_TRY(cudaGetLastError());
             }
-            CUDA_TRY(cudaMemsetAsync(c->p2p_region + s * RB, 0, RB, c->stream));
             PeerFlags pf{};
             for (int r = 0; r < world; r++) pf.p[r] = p2p_flag(c->p2p_peer[r], RB, P2P_FREE + 2 * rank + s);
             p2p_signal<<<1, 64, 0, c->stream>>>(pf, (uint32_t)world);
             CUDA_TRY(cudaGetLastError());
             c->launches += 3;
             uint32_t *y = nullptr;
-            TRY(mmh_tail(c, &y, c->p2p_tmp, 1, 0));
+            TRY(mmh_tail(c, &y, c->p2p_tmp[set], 1, 0));
             return run_mh(c, y, out);
         }));
         launched += c->launches;
@@ -2286,7 +2285,8 @@ static int p2p_init(pa_ctx *c) {
     const size_t bytes = 2 * c->p2p_recv_bytes + (size_t)P2P_NFLAG * kFlagWords * 4;
     CUDA_TRY(cudaMalloc(&c->p2p_region, bytes));
     dbg_add(c->p2p_region, bytes);
-    TRY(c->da.alloc(&c->p2p_tmp, total));
+    TRY(c->da.alloc(&c->p2p_tmp[0], total));
+    TRY(c->da.alloc(&c->p2p_tmp[1], total));
     CUDA_TRY(cudaMemsetAsync(c->p2p_region, 0, bytes, c->stream));
     std::vector<uint32_t> one(2 * kMaxWorld * kFlagWords, 0);
     for (int i = 0; i < 2 * kMaxWorld; i++) one[(size_t)i * kFlagWords] = 1u;   // every buffer free for use 1
