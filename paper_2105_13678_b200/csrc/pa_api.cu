@@ -820,7 +820,15 @@ static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, 
 template <int S_LOG>
 static int launch_mac_t(const MacArgs &A, int grid, cudaStream_t st) {
     constexpr int E_LOG = 5;
-    static KInfo kis[kMaxDevices];
+    static KInfo kis[kMaxDevices], kis3[kMaxDevices];
+    if (A.mode == 3) {                                   // P2P exchange instantiation
+        KInfo &ki = kinfo_slot(kis3);
+        auto fn = row_mac<S_LOG, E_LOG, 0, mac_pad(S_LOG), PA_MAC_NSX, 0, 1>;
+        TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
+        fn<<<grid, ki.threads, ki.smem, st>>>(A);
+        CUDA_TRY(cudaGetLastError());
+        return PA_OK;
+    }
     KInfo &ki = kinfo_slot(kis);
     auto fn = row_mac<S_LOG, E_LOG>;
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
