@@ -817,26 +817,27 @@ static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, 
     return PA_OK;
 }
 
-template <int S_LOG>
-static int launch_mac_t(const MacArgs &A, int grid, cudaStream_t st) {
+template <int S_LOG, int MODE>
+static int launch_mac_m(const MacArgs &A, int grid, cudaStream_t st) {
     constexpr int E_LOG = 5;
-    static KInfo kis[kMaxDevices], kis3[kMaxDevices];
-    if (A.mode == 3) {                                   // P2P exchange instantiation
-        KInfo &ki = kinfo_slot(kis3);
-        auto fn = row_mac<S_LOG, E_LOG, 0, mac_pad(S_LOG), PA_MAC_NSX, 0, 1>;
-        TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
-        fn<<<grid, ki.threads, ki.smem, st>>>(A);
-        CUDA_TRY(cudaGetLastError());
-        return PA_OK;
-    }
+    static KInfo kis[kMaxDevices];
     KInfo &ki = kinfo_slot(kis);
-    auto fn = row_mac<S_LOG, E_LOG>;
+    auto fn = row_mac<S_LOG, E_LOG, 0, mac_pad(S_LOG), PA_MAC_NSX, 0, MODE>;
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;
 }
-
+template <int S_LOG>
+static int launch_mac_t(const MacArgs &A, int grid, cudaStream_t st) {
+    switch (A.mode) {
+        case 0: return launch_mac_m<S_LOG, 0>(A, grid, st);
+        case 1: return launch_mac_m<S_LOG, 1>(A, grid, st);
+        case 2: return launch_mac_m<S_LOG, 2>(A, grid, st);
+        case 3: return launch_mac_m<S_LOG, 3>(A, grid, st);
+    }
+    return set_err(PA_E_PARAM, "row MAC mode %u", A.mode);
+}
 static int mac_grid(int slog, uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, uint32_t *nslot) {
     switch (slog) {
 #define PA_MG(S) case S: return mac_grid_t<S>(nunits, nvec, mode, grid, nslot);

@@ -1026,9 +1026,10 @@ __host__ __device__ constexpr int mac_threads(int slog, int elog) { return mac_v
 __host__ __device__ constexpr int mac_minb(size_t smem_bytes) {
     return (int)(232448 / (smem_bytes + 1024)) < 1 ? 1 : ((int)(232448 / (smem_bytes + 1024)) > 8 ? 8 : (int)(232448 / (smem_bytes + 1024)));
 }
-// M3: the mode-3 (P2P) instantiation; the others carry no mode-3 code (its branch cost the
-// default C4 row MAC 6 registers and 4.5 us)
-template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = PA_MAC_NSX, int AIN = 0, int M3 = 0>
+// MODE: A.mode as a template parameter, so each instantiation carries only its own flush and
+// iteration split (the P2P mode's branch in the shared kernel cost the default C4 row MAC 6
+// registers and 4.5 us)
+template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = PA_MAC_NSX, int AIN = 0, int MODE = 0>
 __global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(mac_smem_bytes<S_LOG, PAD, NSX, AIN>()))
 row_mac(const MacArgs A) {
     PA_TMARK(0x3000 | (S_LOG << 8) | (E_LOG << 4), 0);
@@ -1052,7 +1053,7 @@ row_mac(const MacArgs A) {
     const uint32_t P = a.nprimes;
     const uint32_t nvec = A.nvec;
     const uint64_t total = (uint64_t)A.nunits * nvec;
-    const bool whole = !M3 && (A.mode == 1 || A.mode == 2);
+    constexpr bool whole = MODE == 1 || MODE == 2;
     const uint64_t it0 = whole ? (uint64_t)(blockIdx.x * (uint64_t)A.nunits / gridDim.x) * nvec
                                : blockIdx.x * total / gridDim.x;
     const uint64_t it1 = whole ? (uint64_t)((blockIdx.x + 1) * (uint64_t)A.nunits / gridDim.x) * nvec
@@ -1107,12 +1108,12 @@ row_mac(const MacArgs A) {
     auto flush_one = [&](uint32_t *d, uint32_t v) {
         v = red1p(v, cx.p);
         PA_CK(d, 4);
-        if constexpr (M3) {
+        if constexpr (MODE == 3) {
             const size_t e = (size_t)(d - dslot);                  // element of the [P][L] accumulator
             PA_CK(A.dst64 + e, 8);
             atomicAdd(A.dst64 + e, (unsigned long long)v);
-        } else if (A.mode == 0) atomicAdd(d, v);
-        else if (A.mode == 1) *d = v;
+        } else if constexpr (MODE == 0) atomicAdd(d, v);
+        else if constexpr (MODE == 1) *d = v;
         else *d = red1p(*d + v, cx.p);
     };
     const uint32_t *rtw_p = nullptr;
@@ -1196,7 +1197,7 @@ row_mac(const MacArgs A) {
     }
     // mode 3: the peer atomics are performed (system scope) before this CTA exits, so the
     // p2p_signal kernel that follows in stream order publishes complete sums
-    if constexpr (M3) __threadfence_system();
+    if constexpr (MODE == 3) __threadfence_system();
 }
 
 }  // namespace pa
