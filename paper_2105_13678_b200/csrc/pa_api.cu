@@ -656,11 +656,11 @@ static int kinfo(F *fn, int threads, size_t smem, KInfo &ki) {
 #ifndef PA_COL_LANES
 #define PA_COL_LANES 1
 #endif
-template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
-static int launch_col_e(const ColArgs &A0, cudaStream_t st) {
+template <int S_LOG, int E_LOG, int N1_LOG, int MODE, bool ZH>
+static int launch_col_z(const ColArgs &A0, cudaStream_t st) {
     static KInfo kis[kMaxDevices];
     KInfo &ki = kinfo_slot(kis);
-    auto fn = col_pass<S_LOG, E_LOG, N1_LOG, MODE>;
+    auto fn = col_pass<S_LOG, E_LOG, N1_LOG, MODE, ZH>;
     TRY(kinfo(fn, 32 * (1 << (S_LOG - E_LOG)), (size_t)(1 << S_LOG) * 32 * 4, ki));
     ColArgs A = A0;
     if (E_LOG == 4)
@@ -682,6 +682,14 @@ static int launch_col_e(const ColArgs &A0, cudaStream_t st) {
 #ifndef PA_COL_E4_UNITS
 #define PA_COL_E4_UNITS 3                          // E = 16 while 2 units <= this x SMs
 #endif
+template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
+static int launch_col_e(const ColArgs &A, cudaStream_t st) {
+    // the zero-half forward instantiation when every packed row lies in the first half
+    if constexpr (MODE == COL_FWD)
+        if (2ull * A.rows <= (1ull << S_LOG)) return launch_col_z<S_LOG, E_LOG, N1_LOG, MODE, true>(A, st);
+    return launch_col_z<S_LOG, E_LOG, N1_LOG, MODE, false>(A, st);
+}
+
 template <int S_LOG, int N1_LOG, int MODE>
 static int launch_col_t(const ColArgs &A, cudaStream_t st) {
     if constexpr (S_LOG == 8) {

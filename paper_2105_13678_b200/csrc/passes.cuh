@@ -621,7 +621,9 @@ struct ColArgs {
 // One CTA = 32 adjacent columns (one lane each) x S/E threads per column.  The row
 // length N1 = 2^N1_LOG is a template parameter so every element address is a per-unit
 // base plus a compile-time offset (no per-element 64-bit index arithmetic).
-template <int S_LOG, int E_LOG, int N1_LOG, int MODE>
+// ZH (template, chosen by the launcher): the forward input's rows all lie in the first half
+// of each column (see below); each instantiation carries only its own load and first stage
+template <int S_LOG, int E_LOG, int N1_LOG, int MODE, bool ZH = false>
 #ifndef PA_COL8_MINB
 #define PA_COL8_MINB 4
 #endif
@@ -691,7 +693,7 @@ col_pass(const ColArgs A) {
         // upper half (m >= R/2 in every group) is neither loaded nor read.  Its loads are left
         // out of this branch altogether: a predicated-off load still holds its destination
         // register on the scoreboard, and a later reuse of that register waited on it.
-        const bool zh = MODE == COL_FWD && 2 * rows <= (1u << S_LOG);
+        constexpr bool zh = ZH;
         {
             constexpr int R = 1 << SP::rlog(0);
 #if defined(PA_COL_DBG) && (PA_COL_DBG & 4)
@@ -702,7 +704,7 @@ col_pass(const ColArgs A) {
                                                      : A.src + ((size_t)iv * P + pi) * ((size_t)rows * N1)) +
 #endif
                                   ((size_t)v << N1_LOG) + j1;
-            if (zh) {
+            if constexpr (zh) {
 #pragma unroll
                 for (int h = 0; h < E / R; h++) {
 #pragma unroll
@@ -727,7 +729,7 @@ col_pass(const ColArgs A) {
             }
         }
         __syncthreads();    // previous unit's last-round smem reads are done
-        if (zh)
+        if constexpr (zh)
             round0_finish<S_LOG, E_LOG, true>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
         else
             round0_finish<S_LOG, E_LOG>(x, sm, sidx, v, tw, twp, rtw_p, a, cx);
