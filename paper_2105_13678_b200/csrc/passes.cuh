@@ -261,6 +261,9 @@ constexpr int kPackT = 256;
 #define PA_PACKL 2
 #endif
 constexpr int kPackL = PA_PACKL;                               // limbs per thread in pack_key_residues
+#ifndef PA_PACK_V4
+#define PA_PACK_V4 1                           // 128-bit key loads in pack_key_residues
+#endif
 #ifndef PA_PACK_CHUNK24
 #define PA_PACK_CHUNK24 1                      // reduce limbs over 24-bit chunks (one REDC per prime)
 #endif
@@ -333,8 +336,10 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     // a tile is kPackL kPackT limbs, kPackL per thread (limbs t + q kPackT): the per-prime
     // constants, loop and addressing are shared by the limbs' reductions
     constexpr int TL = kPackL * kPackT;
-    constexpr int MAXW = TL * NW + 4;                         // staged words (LB <= 4 NW bytes per limb)
-    __shared__ uint32_t sw[MAXW];
+    // staged words (LB <= 4 NW bytes per limb), plus up to 3 words back to a 16-byte boundary
+    // and the round-up of the 16-byte loads
+    constexpr int MAXW = ((TL * NW + 4 + 6 + 3) / 4) * 4;
+    __shared__ __align__(16) uint32_t sw[MAXW];
     const uint32_t iv = blockIdx.y;
     const uint32_t jt0 = blockIdx.x * TL;
     const int64_t start = (int64_t)iv * s.blk_bytes;
@@ -343,31 +348,58 @@ __global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, cons
     const uint32_t jt1 = min(jt0 + TL, s.wx);               // limbs with data in this tile
     int64_t tlo = end - (int64_t)LB * jt1 - 4;               // lowest byte any word may touch
     if (tlo < start - 4) tlo = start - 4;
-    const int64_t gw0 = tlo >> 2;                            // floor
+    int64_t gw0 = tlo >> 2;                                  // floor
     const int64_t thi = end - (int64_t)LB * jt0;
-    const int nw = (jt0 < jt1) ? (int)(((thi + 3) >> 2) - gw0 + 1) : 0;
-    // interior tiles: plain aligned word loads; tiles touching the key's ends: key_word
+    int nw = (jt0 < jt1) ? (int)(((thi + 3) >> 2) - gw0 + 1) : 0;
+    // interior tiles: plain aligned loads; tiles touching the key's ends: key_word
     const bool interior = s.aligned && gw0 >= 0 && (gw0 + nw + 1) * 4 < (int64_t)s.nbytes;
-    const uint32_t *kw = reinterpret_cast<const uint32_t *>(s.key) + (interior ? gw0 : 0);
-    // all of a thread's loads are issued before its stores (no load->store serialisation)
-    constexpr int KU = (MAXW + kPackT - 1) / kPackT;
-    uint32_t v[KU];
-    if (interior) {
+#if PA_PACK_V4
+    // 128-bit loads (north_star (1)): the staged window starts at the 16-byte boundary at or
+    // below its first word, so every load and every shared store is one aligned uint4
+    const int dl = (int)((((uintptr_t)s.key + (uintptr_t)(gw0 * 4)) & 15) >> 2);
+    const bool vec = interior && nw > 0 && gw0 - dl >= 0 &&
+                     (gw0 - dl + 4 * (int64_t)((nw + dl + 3) >> 2) + 1) * 4 < (int64_t)s.nbytes;
+    if (vec) {
+        gw0 -= dl;
+        nw += dl;
+        const int nv = (nw + 3) >> 2;
+        const uint4 *kv = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(s.key) + gw0);
+        constexpr int KV = (MAXW / 4 + kPackT - 1) / kPackT;
+        uint4 q[KV];
+#pragma unroll
+        for (int u = 0; u < KV; u++) {
+            const int k = threadIdx.x + u * kPackT;
+            if (k < nv) q[u] = PA_LDG(kv + k);
+        }
+#pragma unroll
+        for (int u = 0; u < KV; u++) {
+            const int k = threadIdx.x + u * kPackT;
+            if (k < nv) { PA_IDX_CK(4 * k + 3, MAXW); reinterpret_cast<uint4 *>(sw)[k] = q[u]; }
+        }
+    } else
+#endif
+    {
+        const uint32_t *kw = reinterpret_cast<const uint32_t *>(s.key) + (interior ? gw0 : 0);
+        // all of a thread's loads are issued before its stores (no load->store serialisation)
+        constexpr int KU = (MAXW + kPackT - 1) / kPackT;
+        uint32_t v[KU];
+        if (interior) {
+#pragma unroll
+            for (int u = 0; u < KU; u++) {
+                const int k = threadIdx.x + u * kPackT;
+                v[u] = (k < nw) ? PA_LDG(kw + k) : 0u;
+            }
+        } else {
+            for (int u = 0; u < KU; u++) {
+                const int k = threadIdx.x + u * kPackT;
+                v[u] = (k < nw) ? key_word(s, gw0 + k) : 0u;
+            }
+        }
 #pragma unroll
         for (int u = 0; u < KU; u++) {
             const int k = threadIdx.x + u * kPackT;
-            v[u] = (k < nw) ? PA_LDG(kw + k) : 0u;
+            if (k < nw) { PA_IDX_CK(k, MAXW); sw[k] = v[u]; }
         }
-    } else {
-        for (int u = 0; u < KU; u++) {
-            const int k = threadIdx.x + u * kPackT;
-            v[u] = (k < nw) ? key_word(s, gw0 + k) : 0u;
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < KU; u++) {
-        const int k = threadIdx.x + u * kPackT;
-        if (k < nw) { PA_IDX_CK(k, MAXW); sw[k] = v[u]; }
     }
     __syncthreads();
     // limb j's NW words (big-endian bytes, readings A3/A4).  Byte offsets relative to the
