@@ -529,3 +529,46 @@ def test_context_on_other_current_device_is_used():
     assert torch.cuda.current_device() == dev_before
     assert bytes(out.cpu().numpy()) == oracle_seeded(key, n, r, m, seed)
     ctx.close()
+
+
+def test_distinct_contexts_from_concurrent_host_threads():
+    """distinct jobs may run concurrently, no shared mutable state.  Four host
+    threads, each with its own context, stream and key, hash at the same time (ctypes drops the
+    GIL during the C calls); every output equals the oracle's, on every repetition."""
+    import threading
+    shapes = [(100_003, 1024, 5_000, 11), (262_157, 2048, 30_001, 12),
+              (300_000, 4096, 4_000, 13), (1 << 20, 1 << 16, 104_858, 14)]
+    keys = [key_bytes(n, 0xC0 + i) for i, (n, _, _, _) in enumerate(shapes)]
+    want = [oracle_seeded(k, n, r, m, s) for k, (n, r, m, s) in zip(keys, shapes)]
+    got = [[] for _ in shapes]
+    errs = []
+    go = threading.Barrier(len(shapes))
+
+    def worker(i):
+        try:
+            n, r, m, s = shapes[i]
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                ctx = _pa()(n, r, m, seed=s)
+                kd = torch.from_numpy(keys[i]).cuda()
+                go.wait()
+                for _ in range(6):
+                    out = ctx.hash(kd)
+                    st.synchronize()
+                    got[i].append(bytes(out.cpu().numpy()))
+                ctx.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append((i, repr(e)))
+            try:
+                go.abort()
+            except Exception:  # noqa: BLE001
+                pass
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(len(shapes))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i in range(len(shapes)):
+        assert len(got[i]) == 6 and all(g == want[i] for g in got[i]), f"thread {i}"
