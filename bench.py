@@ -377,11 +377,20 @@ def main():
                     help="process-group backend for N>1 (gloo only to validate the multi-rank path)")
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 (validation of the N>1 host path on a 1-GPU box; not a bench)")
+    ap.add_argument("--one-rank-mg", action="store_true",
+                    help="run the N>1 code path (library NCCL context, reduce / p2p exchange, multi-GPU e2e, "
+                         "rotating-root stream) with a one-rank communicator on one GPU: validates that path, not a bench")
     ap.add_argument("--verify", action="store_true",
                     help="N>1: rank 0 checks the sharded hash against a whole-key single-GPU context")
     args = ap.parse_args()
     if args.impl != "reference":
         args.warmup = max(args.warmup, 3)
+    # stdout carries exactly one JSON line: anything native libraries write to fd 1 (NCCL prints
+    # its version banner there when NCCL_DEBUG is set) goes to stderr instead
+    sys.stdout.flush()
+    _real_stdout = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(_real_stdout, "w")
 
     from synth import CONFIGS, PAPER_CONFIGS, key_bytes
     paper = args.config in PAPER_CONFIGS
@@ -402,6 +411,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         args.gpus = world
+    multi = world > 1 or args.one_rank_mg
+    if args.one_rank_mg and world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
     if args.same_device:
         local = 0
     torch.cuda.set_device(local)
@@ -410,8 +425,8 @@ def main():
     # reduces the transform-domain accumulators; torch.distributed only broadcasts the id and
     # brackets the timing.  Validation path (--dist-backend gloo / --same-device, one GPU):
     # the same split through pa_mmh_acc / pa_tail_merge with a gloo exchange.
-    lib_nccl = world > 1 and args.dist_backend == "nccl" and not args.same_device
-    if world > 1:
+    lib_nccl = multi and args.dist_backend == "nccl" and not args.same_device
+    if multi:
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -421,7 +436,7 @@ def main():
     torch.cuda.set_stream(stream)
 
     k = w.k
-    if paper and world > 1:
+    if paper and multi:
         raise SystemExit("paper-mode configs (reload rule over the whole key) run on one GPU")
     b0, b1 = shard_ranges(k, world)[rank]
     key_full = key_bytes(w.n, w.key_seed)
@@ -437,7 +452,7 @@ def main():
         ctx = nccl_context(w.n, w.r, w.m, seed=w.hash_seed, limb_bits=args.limb_bits, throughput_only=True,
                            p2p=args.p2p)
     else:
-        ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if world > 1 else None,
+        ctx = PAContext(w.n, w.r, w.m, seed=w.hash_seed, block_range=(b0, b1) if multi else None,
                         limb_bits=args.limb_bits, throughput_only=True)
     torch.cuda.synchronize()
     ctx_create_ms = (time.perf_counter() - t_create) * 1e3
@@ -446,7 +461,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
-        if world == 1 or lib_nccl:
+        if not multi or lib_nccl:
             return ctx.hash(key_dev, out)
         return transform_merge_hash(ctx, key_dev)
 
@@ -454,7 +469,7 @@ def main():
         step()
     torch.cuda.synchronize()
     verified = None
-    if world > 1 and args.verify:
+    if multi and args.verify:
         # rank 0 checks the sharded hash against the CPU oracle (golden digest of the config's
         # key, written by scripts/gen_golden.py from oracle/ only)
         res = step()
@@ -464,12 +479,12 @@ def main():
             if not verified:
                 raise SystemExit("sharded hash differs from the CPU oracle")
     launches0 = ctx.query()["launches_total"]
-    if world > 1:
+    if multi:
         dist.barrier()
     sampler = ClockSampler(local)
     sampler.start()
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     evs = []
     for _ in range(args.steps):
@@ -481,13 +496,13 @@ def main():
         b.record(stream)
         evs.append((a, b))
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     clocks = sampler.stop()
     launches_timed = (ctx.query()["launches_total"] - launches0) % (1 << 32)
     times = [a.elapsed_time(b) for a, b in evs]
     tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if multi:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_per_step = tot.item() / args.steps
 
@@ -495,13 +510,13 @@ def main():
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": w.n / (ms_per_step * 1e-3) / 1e6, "unit": "Mbps",
                               "ms_per_step": ms_per_step, "only_device": True}), flush=True)
-        if world > 1:
+        if multi:
             dist.destroy_process_group()
         return
     # ---- N>1 stream mode (NEXT-3): G independent keys per step, the root rotating (key j
     # reduced to and finished on rank j mod G), so the tail + MH no longer serialise on rank 0
     mr_stream = None
-    if world > 1:
+    if multi:
         def roll_key(j):
             kb = np.roll(key_full, 977 * j)
             if w.n % 8:
@@ -560,7 +575,7 @@ def main():
     stages = {kname: (v[0], v[1]) for kname, v in stages.items()}
 
     e2e = None
-    if world == 1:
+    if not multi:
         host_key = torch.from_numpy(key_full).pin_memory()
         host_out = torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory()
         for _ in range(2):
@@ -625,10 +640,47 @@ def main():
                "h2d_copy_ms_interleaved": statistics.median(t_copy),
                "h2d_gbs": (w.n + 7) // 8 / (min(th2d) * 1e-3) / 1e9}
 
+    if multi and lib_nccl:
+        # e2e at N GPUs: every rank copies its own key slice from pinned host memory over its own
+        # host link (pa_hash_host on the multi-GPU context), rank 0 reads the output back
+        host_key = torch.from_numpy(key_full[lo:hi].copy()).pin_memory()
+        host_out = torch.empty(ctx.nbytes_out, dtype=torch.uint8).pin_memory() if rank == 0 else None
+        for _ in range(2):
+            ctx.hash_host(host_key, host_out)
+        e2e_ok = True
+        if args.verify and rank == 0:
+            e2e_ok = oracle_check(w, key_full, bytes(host_out.numpy()))
+        t = []
+        for _ in range(max(3, args.steps // 2)):
+            if not args.no_flush:
+                flush.fill_(1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.hash_host(host_key, host_out)
+            bb.record(stream)
+            bb.synchronize()
+            ts = torch.tensor([a.elapsed_time(bb)], dtype=torch.float64, device=dev)
+            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+            t.append(ts.item())
+        e2e_ms = statistics.median(t)
+        e2e = {"value": w.n / (e2e_ms * 1e-3) / 1e6, "unit": "Mbps", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": (w.n + 7) // 8, "d2h_bytes_per_step": (w.m + 7) // 8,
+               "h2d_bytes_this_rank": hi - lo,
+               "api": "pa_hash_host on the multi-GPU context (each rank: pinned key slice H2D + transforms + "
+                      "accumulator merge; rank 0: tail + MH + D2H + sync); max over ranks per step",
+               "samples_ms": [round(x, 4) for x in t]}
+        if args.verify:
+            e2e["verified_vs_oracle"] = e2e_ok
+            if not e2e_ok:
+                raise SystemExit("multi-GPU pa_hash_host differs from the CPU oracle")
+
     # ---- stream mode (pa_hash_batch, NEXT-3): a batch of independent keys, MH / tail of one
     # key overlapping the MMH of the next; reported beside the single-key `value`
     stream_mode = None
-    if world == 1 and args.batch > 1:
+    if not multi and args.batch > 1:
         keys_b = [key_dev] + [torch.empty_like(key_dev).copy_(key_dev.roll(j)) for j in range(1, args.batch)]
         outs_b = [torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev) for _ in range(args.batch)]
         for _ in range(2):
@@ -656,7 +708,7 @@ def main():
     # call sees a new pointer set and re-captures + updates its executable graph in place
     # (cudaGraphExecUpdate), against the same calls on one buffer (plain replay)
     graph_rebind = None
-    if world == 1 and not paper:
+    if not multi and not paper:
         outs2 = [torch.empty(ctx.nbytes_out, dtype=torch.uint8, device=dev) for _ in range(2)]
         i0 = ctx.query()
         torch.cuda.synchronize()
@@ -680,7 +732,7 @@ def main():
                         "what": "wall time of pa_hash + synchronize; new pointers re-capture and cudaGraphExecUpdate"}
 
     fresh = None
-    if world == 1:
+    if not multi:
         for j in range(2):
             ctx.rekey(w.hash_seed + 1 + j)
             ctx.hash(key_dev, out)
@@ -710,7 +762,7 @@ def main():
     # ---- comparator (NEXT-4; Table 1 / Fig. 3): MH-only PA on the same key and (n, m),
     # top m bits of (b x + c) mod 2^n over the whole key, same kernels and timing rules
     comparators = None
-    if world == 1 and not paper and args.comparators:
+    if not multi and not paper and args.comparators:
         cctx = PAContext(w.n, 0, w.m, 0, seed=w.hash_seed, mh_only=True)
         cout = torch.empty(cctx.nbytes_out, dtype=torch.uint8, device=dev)
         for _ in range(args.warmup):
@@ -763,7 +815,7 @@ def main():
         tctx.close()
 
     if rank != 0:
-        if world > 1:
+        if multi:
             dist.destroy_process_group()
         return
     peaks = load_peaks()
@@ -781,7 +833,7 @@ def main():
                    "parallelism": (f"blocks sharded over {world} ranks; transform-domain accumulators " +
                                    ("added by each rank's row MAC into rank 0's receive buffer over peer memory "
                                     "(p2p)" if args.p2p else "summed by one ncclReduce (library NCCL) to rank 0") +
-                                   ", which runs the inverse, CRT, carries, fold and MH") if lib_nccl else (f"{world} ranks, gloo exchange (validation)" if world > 1
+                                   ", which runs the inverse, CRT, carries, fold and MH") if lib_nccl else (f"{world} ranks, gloo exchange (validation)" if multi
                                                                 else "one GPU"),
                    "l2": "flushed (256 MiB write) before every timed step" if not args.no_flush else "not flushed"},
         "gpu_launches": launches_timed,
@@ -790,7 +842,7 @@ def main():
         "hbm": hbm_view(w, info, ms_per_step, peaks, paper),
         "stages_ms_per_step": {kk: v[0] / nsteps_prof for kk, v in sorted(stages.items())},
         "e2e": e2e,
-        "stream": stream_mode if world == 1 else mr_stream,
+        "stream": stream_mode if not multi else mr_stream,
         "comparators": comparators,
         "fresh_keys": fresh,
         "graph_rebind": graph_rebind,
@@ -798,12 +850,13 @@ def main():
     }
     if verified is not None:
         line["verified_vs_oracle"] = verified
-    if world > 1 and (args.same_device or args.dist_backend != "nccl"):
-        line["validation_only"] = f"{world} ranks, backend {args.dist_backend}, same_device={args.same_device}"
-    if world == 1 and not args.no_cpu_baseline and not paper:
+    if multi and (args.same_device or args.dist_backend != "nccl" or args.one_rank_mg):
+        line["validation_only"] = (f"{world} ranks, backend {args.dist_backend}, same_device={args.same_device}, "
+                                   f"one_rank_mg={args.one_rank_mg}")
+    if not multi and not args.no_cpu_baseline and not paper:
         line["cpu_baseline"] = cpu_oracle_full(w)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
 
 

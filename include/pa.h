@@ -229,7 +229,11 @@ int pa_hash_batch(pa_ctx *ctx, const uint8_t *const *keys, uint8_t *const *outs,
 /* End-to-end variant with HOST buffers: copies the key host->device, hashes,
  * copies the output device->host and synchronizes the stream before returning.
  * Pinned host memory gives full PCIe bandwidth; the copy is split in chunks that
- * overlap the first pass of the transform. */
+ * overlap the first pass of the transform.
+ * Multi-GPU contexts (world >= 1): key_host is this rank's key SLICE (the bytes of its
+ * blocks, as for pa_hash), copied over this rank's own host link; out_host is written on
+ * rank 0 only (NULL allowed elsewhere).  Collective: every rank calls it; each rank
+ * returns when its own stream has drained (rank 0: after the output has landed). */
 int pa_hash_host(pa_ctx *ctx, const uint8_t *key_host, uint8_t *out_host);
 
 /* End-to-end stream mode: `count` keys in HOST memory (keys_host[j]: ceil(n/8) bytes,

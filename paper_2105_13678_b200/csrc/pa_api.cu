@@ -959,6 +959,7 @@ struct pa_ctx {
     cudaStream_t copy_stream = nullptr;       // pa_hash_host H2D copies
     GraphSlot g_hash, g_host, g_batch;        // captured pa_hash / pa_hash_host / pa_hash_batch
     GraphSlot g_mg_pre[2], g_mg_post[2];      // multi-GPU, per buffer set: S1-S3 + export; S4-S7 (root)
+    GraphSlot g_mg_host;                      // multi-GPU pa_hash_host: grouped H2D + S1-S3 + export
     // multi-GPU (pa_params.world >= 1): the NCCL communicator and, per buffer set, the
     // exported accumulator (send) and the reduced sum (recv; significant on the root)
     ncclComm_t comm = nullptr;
@@ -1642,7 +1643,7 @@ extern "C" void pa_ctx_destroy(pa_ctx *c) {
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->evpool) cudaEventDestroy(e);
     for (GraphSlot *g : {&c->g_hash, &c->g_host, &c->g_batch, &c->g_mg_pre[0], &c->g_mg_pre[1], &c->g_mg_post[0],
-                         &c->g_mg_post[1]})
+                         &c->g_mg_post[1], &c->g_mg_host})
         g->reset();
     if (c->alt_ready) {
         cudaStreamSynchronize(c->alt.stream);
@@ -1768,7 +1769,7 @@ extern "C" int pa_ctx_set_stream(pa_ctx *c, void *stream) {
     if (!c) return set_err(PA_E_PARAM, "NULL ctx");
     DevGuard dg_(c);
     for (GraphSlot *g : {&c->g_hash, &c->g_host, &c->g_batch, &c->g_mg_pre[0], &c->g_mg_pre[1], &c->g_mg_post[0],
-                         &c->g_mg_post[1]})
+                         &c->g_mg_post[1], &c->g_mg_host})
         g->reset();
     c->stream = (cudaStream_t)stream;
     c->da.stream = c->stream;
@@ -1977,7 +1978,24 @@ static bool graphs_enabled(const pa_ctx *c) {
     return !off && c->stream != nullptr && !c->prof;
 }
 
-static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set);
+// End-to-end hash from host buffers.  The key is copied in kCopyGroups block groups on a
+// copy stream; the pack, both forward passes and the multiply-accumulate of group g start
+// as soon as group g has landed (stream-ordered by events), so the PCIe transfer overlaps
+// the MMH transforms.
+static constexpr int kCopyGroups = 8;
+
+// First block of copy group g of G: group sizes fall linearly (weights G, G-1, ..., 1), so the
+// last group -- whose transforms are all that is left to do once the last byte has arrived --
+// is the smallest (C4: 7, 6, 5, 4, 4, 2, 2, 1 blocks).  The H2D copy outruns nothing: the
+// GPU finishes each group's transforms before the next group's bytes land.
+static uint32_t group_begin(uint32_t nblk, int G, int g) {
+    const uint64_t W = (uint64_t)G * (G + 1) / 2;
+    uint64_t cum = 0;
+    for (int i = 0; i < g; i++) cum += (uint64_t)(G - i);
+    return (uint32_t)((nblk * cum + W / 2) / W);
+}
+
+static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set, const uint8_t *key_host = nullptr);
 static int mg_hash_p2p(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set);
 static int mg_hash_batch(pa_ctx *c, const uint8_t *const *keys, uint8_t *const *outs, uint32_t count);
 
@@ -2192,11 +2210,39 @@ static int mg_post_enqueue(pa_ctx *c, const void *recv, uint32_t *tmp32, uint8_t
 
 // one key on a multi-GPU context, reduced to and finished on `root`, with buffer set `set`
 // (the caller has swapped the set in: c->acc, c->stream, ... are the set's)
-static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set) {
+// key_host (pa_hash_host, pinned memory): the slice is first copied into `key` in block groups on
+// the copy stream, each group's transforms waiting only for its own bytes
+static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set, const uint8_t *key_host) {
     const int rank = c->pl.rank;
     if (rank == root && !out) return set_err(PA_E_PARAM, "NULL output on the root rank");
     const uint64_t total = (uint64_t)c->pl.mmh.nprimes * c->smmh.L;
     uint32_t launched = 0;
+    if (key_host) {
+        TRY(graph_run(c, c->g_mg_host, {key_host, key}, [&] {
+            c->launches = 0;
+            const uint64_t sb = key_slice_len(c), R = c->pl.r / 8;
+            const uint32_t nblk = c->nblk;
+            const int G = (int)std::min<uint32_t>(kCopyGroups, nblk);
+            uint8_t *kd = const_cast<uint8_t *>(key);
+            CUDA_TRY(cudaEventRecord(c->copy_ev[kCopyGroups], c->stream));
+            CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[kCopyGroups], 0));
+            for (int g = 0; g < G; g++) {
+                const uint64_t lo = std::min<uint64_t>(sb, (uint64_t)group_begin(nblk, G, g) * R);
+                const uint64_t hi = g + 1 == G ? sb : std::min<uint64_t>(sb, (uint64_t)group_begin(nblk, G, g + 1) * R);
+                if (hi > lo) CUDA_TRY(cudaMemcpyAsync(kd + lo, key_host + lo, hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
+                CUDA_TRY(cudaEventRecord(c->copy_ev[g], c->copy_stream));
+            }
+            bool first = true;
+            for (int g = 0; g < G; g++) {
+                const uint32_t v0 = group_begin(nblk, G, g), v1 = group_begin(nblk, G, g + 1);
+                CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_ev[g], 0));
+                if (v1 > v0) TRY(mmh_forward(c, key, v0, v1));
+                if (v1 > v0) TRY(mmh_mac(c, v0, v1, first, G == 1));
+                if (v1 > v0) first = false;
+            }
+            return launch_export(c, c->xsend[set], c->x_u64);
+        }));
+    } else
     TRY(graph_run(c, c->g_mg_pre[set], {key}, [&] {
         c->launches = 0;
         TRY(run_mmh_acc(c, key));
@@ -2439,23 +2485,6 @@ extern "C" int pa_tail_merge(pa_ctx *c, const uint32_t *acc_parts, uint32_t G, u
     return rc;
 }
 
-// End-to-end hash from host buffers.  The key is copied in kCopyGroups block groups on a
-// copy stream; the pack, both forward passes and the multiply-accumulate of group g start
-// as soon as group g has landed (stream-ordered by events), so the PCIe transfer overlaps
-// the MMH transforms.
-static constexpr int kCopyGroups = 8;
-
-// First block of copy group g of G: group sizes fall linearly (weights G, G-1, ..., 1), so the
-// last group -- whose transforms are all that is left to do once the last byte has arrived --
-// is the smallest (C4: 7, 6, 5, 4, 4, 2, 2, 1 blocks).  The H2D copy outruns nothing: the
-// GPU finishes each group's transforms before the next group's bytes land.
-static uint32_t group_begin(uint32_t nblk, int G, int g) {
-    const uint64_t W = (uint64_t)G * (G + 1) / 2;
-    uint64_t cum = 0;
-    for (int i = 0; i < g; i++) cum += (uint64_t)(G - i);
-    return (uint32_t)((nblk * cum + W / 2) / W);
-}
-
 static int grouped_copy_hash(pa_ctx *c, const uint8_t *key_host, uint8_t *key_dev, uint8_t *out_dev,
                              uint8_t *out_host) {
     // copy_stream is already ordered after every earlier user of key_dev
@@ -2525,10 +2554,39 @@ static int stream_poll(cudaStream_t st, const char *what) {
 }
 
 extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_host) {
-    if (!c || !key_host || !out_host) return set_err(PA_E_PARAM, "NULL argument");
+    if (!c || !key_host) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
-    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     const uint64_t nb = cdiv(c->pl.n, 8), mb = cdiv(c->pl.m, 8);
+    if (c->comm) {
+        // multi-GPU context: every rank copies in its own key slice over its own host link,
+        // the ranks' accumulators are merged as in pa_hash, the root (rank 0) copies the output back
+        const uint64_t sb = key_slice_len(c);
+        const bool root = c->pl.rank == 0;
+        if (root && !out_host) return set_err(PA_E_PARAM, "NULL output on the root rank");
+        if (!c->key_dev) TRY(c->da.alloc(&c->key_dev, std::max<uint64_t>(sb, 1)));
+        if (root && !c->out_dev) TRY(c->da.alloc(&c->out_dev, mb));
+        if (!c->p2p && c->nblk > 0 && host_pinned(key_host)) {
+            // pinned slice, NCCL reduce: the slice is copied in block groups on the copy stream and
+            // each group's transforms start as it lands (grouped_copy_hash's scheme), captured
+            // with the export as one graph
+            if (!c->copy_stream) {
+                CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+                for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
+            }
+            TRY(mg_hash(c, c->key_dev, root ? c->out_dev : nullptr, 0, 0, key_host));
+        } else {
+            // pageable memory (its copies synchronise, so they stay outside the graphs) or the
+            // peer-memory exchange: one copy, then the device path
+            if (sb) CUDA_TRY(cudaMemcpyAsync(c->key_dev, key_host, sb, cudaMemcpyHostToDevice, c->stream));
+            TRY(c->p2p ? mg_hash_p2p(c, c->key_dev, root ? c->out_dev : nullptr, 0, 0)
+                       : mg_hash(c, c->key_dev, root ? c->out_dev : nullptr, 0, 0));
+        }
+        if (root) CUDA_TRY(cudaMemcpyAsync(out_host, c->out_dev, mb, cudaMemcpyDeviceToHost, c->stream));
+        TRY(stream_poll(c->stream, "pa_hash_host"));
+        return PA_OK;
+    }
+    if (!out_host) return set_err(PA_E_PARAM, "NULL argument");
+    if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     if (!c->key_dev) TRY(c->da.alloc(&c->key_dev, nb));
     if (!c->out_dev) TRY(c->da.alloc(&c->out_dev, mb));
     if (!c->copy_stream) {

@@ -311,7 +311,12 @@ class PAContext:
         PCIe bandwidth."""
         if isinstance(key_host, (bytes, bytearray)):
             key_host = np.frombuffer(bytes(key_host), dtype=np.uint8)
-        kp = self._host_u8(key_host, self.nbytes_in, "key")
+        mg = self.world > 0
+        kp = self._host_u8(key_host, self.slice_bytes if mg else self.nbytes_in, "key")
+        if mg and self.rank != 0:
+            # multi-GPU context, not the root: this rank only feeds its key slice
+            B.check(B.pa_hash_host(self._h, ctypes.c_void_p(kp), None))
+            return None
         if out_host is None:
             out_host = np.zeros(self.nbytes_out, dtype=np.uint8)
         op = self._host_u8(out_host, self.nbytes_out, "output", True)

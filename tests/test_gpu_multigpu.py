@@ -97,6 +97,28 @@ def test_nccl_one_rank_hash_and_rotating_batch(on_stream, p2p):
 
 
 @pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_nccl_one_rank_hash_host(p2p, pinned):
+    # pa_hash_host on a multi-GPU context: the rank's key slice in from host memory, the merged
+    # hash, the output back on rank 0 (one rank: the same H2D, reduce / p2p exchange, tail, D2H)
+    P = _P()
+    n, r, m, seed = 262_157, 2048, 30_001, 6
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = _one_rank_ctx(P, n, r, m, seed, p2p=p2p)
+        for ks in (1, 2, 3):
+            key = key_bytes(n, 0xB00 + ks)
+            hk = torch.from_numpy(key)
+            ho = torch.zeros(ctx.nbytes_out, dtype=torch.uint8)
+            if pinned:
+                hk, ho = hk.pin_memory(), ho.pin_memory()
+            got = ctx.hash_host(hk, ho)
+            assert got is ho
+            assert bytes(ho.numpy()) == hashes.pa_hash_seeded(key, n, r, m, seed)
+        ctx.close()
+
+
+@pytest.mark.parametrize("p2p", [False, True])
 def test_nccl_one_rank_c2_golden(p2p):
     import hashlib
     import json
