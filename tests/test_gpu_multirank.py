@@ -33,3 +33,23 @@ def test_multirank_bench_matches_oracle(config, nproc):
     assert line["value"] > 0 and line["gpu_launches"] > 0
     # NEXT-3 rotating-root stream mode ran and was verified against the oracle too
     assert line["stream"]["keys_per_step"] == 2 * nproc and line["stream"]["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p2p", [False, True])
+def test_bench_multi_gpu_path_one_rank(p2p):
+    """The product N>1 bench path -- library NCCL context, reduce (or peer-memory exchange),
+    rotating-root pa_hash_batch, pa_hash_host on the multi-GPU context for e2e -- with a
+    one-rank communicator; single-key, stream and e2e outputs checked against the CPU oracle."""
+    cmd = [sys.executable, "bench.py", "--one-rank-mg", "--verify", "--config", "C2", "--steps", "5",
+           "--warmup", "3"] + (["--p2p"] if p2p else [])
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29650 + int(p2p)), RANK="0", WORLD_SIZE="1")
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, lines                     # exactly one JSON line on stdout
+    line = json.loads(lines[0])
+    assert line["verified_vs_oracle"] is True
+    assert line["e2e"]["verified_vs_oracle"] is True and line["e2e"]["value"] > 0
+    assert line["stream"]["value"] > 0 and line["gpu_launches"] > 0
+    assert "one_rank_mg=True" in line["validation_only"]
