@@ -2415,6 +2415,8 @@ static int mg_init(pa_ctx *c, const pa_params *prm) {
     for (uint32_t i = 0; i < c->pl.mmh.nprimes; i++) qmax = std::max(qmax, c->pl.mmh.primes[i]);
     // u32 sums must stay below 4 q (the inverse row pass reduces its input from [0, 4q))
     c->x_u64 = c->pl.world > 4 || (uint64_t)c->pl.world * (qmax - 1) >= (1ull << 32);
+    // test knob: take the 64-bit exchange (the world > 4 path) on any world size
+    if (const char *e = getenv("PA_FORCE_X64")) c->x_u64 = c->x_u64 || atoi(e) != 0;
     const size_t total = (size_t)c->pl.mmh.nprimes * c->smmh.L;
     for (int s = 0; s < 2; s++) {
         // u64 buffers also hold the u32 conversion on the root (tmp32 = xsend)

@@ -118,6 +118,32 @@ def test_nccl_one_rank_hash_host(p2p, pinned):
         ctx.close()
 
 
+def test_nccl_one_rank_u64_exchange(monkeypatch):
+    # the exchange of world > 4 jobs (64-bit sums: acc_export<u64>, ncclUint64 reduce,
+    # acc_import_u64), forced on a one-rank communicator with PA_FORCE_X64
+    monkeypatch.setenv("PA_FORCE_X64", "1")
+    P = _P()
+    n, r, m, seed = 262_157, 2048, 30_001, 8
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = _one_rank_ctx(P, n, r, m, seed)
+        for ks in (1, 2):
+            key = key_bytes(n, 0xC00 + ks)
+            out = ctx.hash(torch.from_numpy(key).cuda())
+            s.synchronize()
+            assert bytes(out.cpu().numpy()) == hashes.pa_hash_seeded(key, n, r, m, seed)
+        keys = [key_bytes(n, 0xD00 + j) for j in range(3)]
+        outs = ctx.hash_batch([torch.from_numpy(kk).cuda() for kk in keys])
+        s.synchronize()
+        for kk, o in zip(keys, outs):
+            assert bytes(o.cpu().numpy()) == hashes.pa_hash_seeded(kk, n, r, m, seed)
+        hk = torch.from_numpy(keys[0]).pin_memory()
+        ho = torch.zeros(ctx.nbytes_out, dtype=torch.uint8).pin_memory()
+        ctx.hash_host(hk, ho)
+        assert bytes(ho.numpy()) == hashes.pa_hash_seeded(keys[0], n, r, m, seed)
+        ctx.close()
+
+
 @pytest.mark.parametrize("p2p", [False, True])
 def test_nccl_one_rank_c2_golden(p2p):
     import hashlib
