@@ -787,6 +787,9 @@ static int launch_macinv(int slog, const MacInvArgs &A, cudaStream_t st) {
 // (< 4p < 2^32).  nslot = 1 while grid <= 3 nunits; few units and many vectors (C5a: 88
 // units of 2048 vectors) take up to kMacSlots slots to keep every SM busy.  Modes 1/2
 // (whole units per CTA): grid <= nunits, one slot.
+#ifndef PA_MAC_DBG
+#define PA_MAC_DBG 0     // timing-only ablations of the row MAC (1: no DFT, 2: no loads, 3: no loads, no MAC); results are wrong when set
+#endif
 static constexpr uint32_t kMacSlots = 4;
 template <int S_LOG>
 static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, uint32_t *nslot) {
@@ -830,7 +833,7 @@ static int launch_mac_m(const MacArgs &A, int grid, cudaStream_t st) {
     constexpr int E_LOG = 5;
     static KInfo kis[kMaxDevices];
     KInfo &ki = kinfo_slot(kis);
-    auto fn = row_mac<S_LOG, E_LOG, 0, mac_pad(S_LOG), PA_MAC_NSX, 0, MODE>;
+    auto fn = row_mac<S_LOG, E_LOG, PA_MAC_DBG, mac_pad(S_LOG), PA_MAC_NSX, 0, MODE>;
     TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
