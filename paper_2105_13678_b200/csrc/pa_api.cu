@@ -797,7 +797,7 @@ static int mac_grid_t(uint32_t nunits, uint32_t nvec, uint32_t mode, int *grid, 
     static KInfo kis[kMaxDevices];
     KInfo &ki = kinfo_slot(kis);
     auto fn = row_mac<S_LOG, E_LOG>;
-    TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
+    TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG, mac_pad(S_LOG), PA_MAC_NSX, mac_ain(S_LOG)>(), ki));
     const uint64_t full = (uint64_t)ki.occ * g_num_sms;
     *nslot = 1;
     if (mode == 3) {                                     // 64-bit sums: no partial-count bound
@@ -833,8 +833,8 @@ static int launch_mac_m(const MacArgs &A, int grid, cudaStream_t st) {
     constexpr int E_LOG = 5;
     static KInfo kis[kMaxDevices];
     KInfo &ki = kinfo_slot(kis);
-    auto fn = row_mac<S_LOG, E_LOG, PA_MAC_DBG, mac_pad(S_LOG), PA_MAC_NSX, 0, MODE>;
-    TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG>(), ki));
+    auto fn = row_mac<S_LOG, E_LOG, PA_MAC_DBG, mac_pad(S_LOG), PA_MAC_NSX, mac_ain(S_LOG), MODE>;
+    TRY(kinfo(fn, mac_v(S_LOG) * (1 << (S_LOG - E_LOG)), mac_smem_bytes<S_LOG, mac_pad(S_LOG), PA_MAC_NSX, mac_ain(S_LOG)>(), ki));
     fn<<<grid, ki.threads, ki.smem, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     return PA_OK;

@@ -1063,8 +1063,16 @@ __host__ __device__ constexpr int mac_minb(size_t smem_bytes) {
 // MODE: A.mode as a template parameter, so each instantiation carries only its own flush and
 // iteration split (the P2P mode's branch in the shared kernel cost the default C4 row MAC 6
 // registers and 4.5 us)
-template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = PA_MAC_NSX, int AIN = 0, int MODE = 0>
-__global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb(mac_smem_bytes<S_LOG, PAD, NSX, AIN>()))
+#ifndef PA_MAC_AIN
+#define PA_MAC_AIN 0          // A^ rows land in the X stage (needs the padded exchange buffer): two stages, not three
+#endif
+#ifndef PA_MAC_MINB_CAP
+#define PA_MAC_MINB_CAP 8     // most CTAs per SM the register budget is sized for
+#endif
+__host__ __device__ constexpr int mac_ain(int slog) { return PA_MAC_AIN && mac_pad(slog); }
+__host__ __device__ constexpr int mac_minb_cap(int b) { return b > PA_MAC_MINB_CAP ? PA_MAC_MINB_CAP : b; }
+template <int S_LOG, int E_LOG, int DBG = 0, int PAD = mac_pad(S_LOG), int NSX = PA_MAC_NSX, int AIN = mac_ain(S_LOG), int MODE = 0>
+__global__ void __launch_bounds__(mac_threads(S_LOG, E_LOG), mac_minb_cap(mac_minb(mac_smem_bytes<S_LOG, PAD, NSX, AIN>())))
 row_mac(const MacArgs A) {
     PA_TMARK(0x3000 | (S_LOG << 8) | (E_LOG << 4), 0);
     using SP = SubPlan<S_LOG, E_LOG>;
