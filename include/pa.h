@@ -239,7 +239,10 @@ int pa_hash_host(pa_ctx *ctx, const uint8_t *key_host, uint8_t *out_host);
 /* End-to-end stream mode: `count` keys in HOST memory (keys_host[j]: ceil(n/8) bytes,
  * outs_host[j]: ceil(m/8) bytes; pinned memory for full PCIe bandwidth).  Key j's H2D
  * overlaps the hash of key j-1 (two device staging buffers, the two buffer sets of
- * pa_hash_batch).  Synchronous.  Not available in paper mode or for shards. */
+ * pa_hash_batch).  Synchronous.  Not available in paper mode or for shards.
+ * Multi-GPU contexts (world >= 1): keys_host[j] is this rank's slice of key j; the root
+ * rotates as in pa_hash_batch, outs_host[j] is written on rank j mod world only (NULL
+ * allowed elsewhere).  Collective: every rank passes the same count. */
 int pa_hash_host_batch(pa_ctx *ctx, const uint8_t *const *keys_host, uint8_t *const *outs_host, uint32_t count);
 
 /* Stages S1-S5 on this context's blocks: y_part = sum_{i in shard} a_i x_i mod p,

@@ -2618,10 +2618,68 @@ extern "C" int pa_hash_host(pa_ctx *c, const uint8_t *key_host, uint8_t *out_hos
 // buffer j % 2) overlaps the hash of key j - 1 (buffer set / stream (j - 1) % 2); the copy
 // of key j waits for the hash of key j - 2 (same staging buffer) to finish; the output of
 // key j is copied back on its hash stream.  Synchronous: returns after the last D2H.
+// End-to-end stream mode on a multi-GPU context: key j's slice goes host -> device on this
+// rank's copy stream (staging buffer j % 2) while key j - 1 is hashed; the root rotates as in
+// pa_hash_batch (key j is merged and finished on rank j mod world, which copies its output back).
+static int mg_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, uint8_t *const *outs_host, uint32_t count) {
+    const int world = c->pl.world, rank = c->pl.rank;
+    for (uint32_t j = 0; j < count; j++) {
+        if (!keys_host[j]) return set_err(PA_E_PARAM, "NULL key in batch");
+        if ((int)(j % world) == rank && !outs_host[j]) return set_err(PA_E_PARAM, "NULL output of a key this rank is root of");
+    }
+    if (count == 0) return PA_OK;
+    const uint64_t sb = key_slice_len(c), mb = cdiv(c->pl.m, 8);
+    if (!c->key_dev) TRY(c->da.alloc(&c->key_dev, std::max<uint64_t>(sb, 1)));
+    if (!c->key_dev2) TRY(c->da.alloc(&c->key_dev2, std::max<uint64_t>(sb, 1)));
+    if (!c->out_dev) TRY(c->da.alloc(&c->out_dev, mb));
+    if (!c->out_dev2) TRY(c->da.alloc(&c->out_dev2, mb));
+    if (!c->copy_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int g = 0; g < kCopyGroups + 1; g++) CUDA_TRY(cudaEventCreateWithFlags(&c->copy_ev[g], cudaEventDisableTiming));
+    }
+    if (!c->hb_copy[0])
+        for (int s = 0; s < 2; s++) {
+            CUDA_TRY(cudaEventCreateWithFlags(&c->hb_copy[s], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->hb_done[s], cudaEventDisableTiming));
+        }
+    TRY(alloc_alt(c));
+    uint8_t *kbuf[2] = {c->key_dev, c->key_dev2}, *obuf[2] = {c->out_dev, c->out_dev2};
+    CUDA_TRY(cudaEventRecord(c->bev[0], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->alt.stream, c->bev[0], 0));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->bev[0], 0));
+    uint32_t total = 0;
+    int rc = PA_OK;
+    for (uint32_t j = 0; j < count && rc == PA_OK; j++) {
+        const int s = (int)(j & 1), root = (int)(j % world);
+        if (j >= 2 && cudaStreamWaitEvent(c->copy_stream, c->hb_done[s], 0) != cudaSuccess) rc = set_err(PA_E_CUDA, "event wait failed");
+        if (rc == PA_OK && sb && cudaMemcpyAsync(kbuf[s], keys_host[j], sb, cudaMemcpyHostToDevice, c->copy_stream) != cudaSuccess)
+            rc = set_err(PA_E_CUDA, "H2D copy failed");
+        if (rc == PA_OK && cudaEventRecord(c->hb_copy[s], c->copy_stream) != cudaSuccess) rc = set_err(PA_E_CUDA, "event record failed");
+        if (rc != PA_OK) break;
+        if (s) swap_bufs(c);
+        if (cudaStreamWaitEvent(c->stream, c->hb_copy[s], 0) != cudaSuccess) rc = set_err(PA_E_CUDA, "event wait failed");
+        if (rc == PA_OK)
+            rc = c->p2p ? mg_hash_p2p(c, kbuf[s], root == rank ? obuf[s] : nullptr, root, s)
+                        : mg_hash(c, kbuf[s], root == rank ? obuf[s] : nullptr, root, s);
+        total += c->launches;
+        if (rc == PA_OK && root == rank &&
+            cudaMemcpyAsync(outs_host[j], obuf[s], mb, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+            rc = set_err(PA_E_CUDA, "D2H copy failed");
+        if (rc == PA_OK && cudaEventRecord(c->hb_done[s], c->stream) != cudaSuccess) rc = set_err(PA_E_CUDA, "event record failed");
+        if (s) swap_bufs(c);
+    }
+    CUDA_TRY(cudaEventRecord(c->bev[1], c->alt.stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->bev[1], 0));
+    c->launches = total;
+    TRY(rc);
+    return stream_poll(c->stream, "pa_hash_host_batch");
+}
+
 extern "C" int pa_hash_host_batch(pa_ctx *c, const uint8_t *const *keys_host, uint8_t *const *outs_host,
                                   uint32_t count) {
     if (!c || (count && (!keys_host || !outs_host))) return set_err(PA_E_PARAM, "NULL argument");
     DevGuard dg_(c);
+    if (c->comm) return mg_hash_host_batch(c, keys_host, outs_host, count);
     if (c->pl.b0 != 0 || c->pl.b1 != c->pl.k) return set_err(PA_E_STATE, "shard context: use pa_mmh_partial + pa_mh_merge");
     if (c->pl.paper_k || c->pl.mh_only || c->pl.toeplitz)
         return set_err(PA_E_STATE, "paper mode / comparators: use pa_hash_host per key");

@@ -291,17 +291,23 @@ class PAContext:
 
     def hash_host_batch(self, keys_host, outs_host=None):
         """pa_hash_host_batch: host keys (numpy uint8 / pinned torch CPU tensors) -> host
-        outputs, H2D of key j overlapping the hash of key j-1.  Synchronous."""
+        outputs, H2D of key j overlapping the hash of key j-1.  Synchronous.  Multi-GPU
+        contexts: keys are this rank's slices; outputs[j] is None except on rank j mod world."""
         keys_host = list(keys_host)
+        mg = self.world > 0
+        mine = [(not mg) or j % self.world == self.rank for j in range(len(keys_host))]
         if outs_host is None:
-            outs_host = [np.zeros(self.nbytes_out, dtype=np.uint8) for _ in keys_host]
+            outs_host = [np.zeros(self.nbytes_out, dtype=np.uint8) if mine[j] else None
+                         for j in range(len(keys_host))]
         outs_host = list(outs_host)
         if len(outs_host) != len(keys_host):
             raise ValueError("keys and outs differ in length")
         kp = (ctypes.c_void_p * len(keys_host))(
-            *[self._host_u8(k, self.nbytes_in, f"key {j}") for j, k in enumerate(keys_host)])
+            *[self._host_u8(k, self.slice_bytes if mg else self.nbytes_in, f"key {j}") for j, k in enumerate(keys_host)])
+        # multi-GPU contexts: key j's output lands on rank j mod world only
         op = (ctypes.c_void_p * len(outs_host))(
-            *[self._host_u8(o, self.nbytes_out, f"output {j}", True) for j, o in enumerate(outs_host)])
+            *[self._host_u8(o, self.nbytes_out, f"output {j}", True) if (mine[j] or o is not None) else None
+              for j, o in enumerate(outs_host)])
         B.check(B.pa_hash_host_batch(self._h, kp, op, len(keys_host)))
         return outs_host
 

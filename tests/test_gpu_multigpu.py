@@ -118,6 +118,27 @@ def test_nccl_one_rank_hash_host(p2p, pinned):
         ctx.close()
 
 
+@pytest.mark.parametrize("p2p", [False, True])
+def test_nccl_one_rank_hash_host_batch(p2p):
+    # pa_hash_host_batch on a multi-GPU context: slices in from host memory on the copy stream
+    # (two staging buffers), rotating root, outputs back to host; five keys, twice
+    P = _P()
+    n, r, m, seed = 262_157, 2048, 30_001, 9
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = _one_rank_ctx(P, n, r, m, seed, p2p=p2p)
+        keys = [key_bytes(n, 0xE00 + j) for j in range(5)]
+        want = [hashes.pa_hash_seeded(kk, n, r, m, seed) for kk in keys]
+        hk = [torch.from_numpy(kk).pin_memory() for kk in keys]
+        for _ in range(2):
+            ho = [torch.zeros(ctx.nbytes_out, dtype=torch.uint8).pin_memory() for _ in keys]
+            ctx.hash_host_batch(hk, ho)
+            assert [bytes(o.numpy()) for o in ho] == want
+        outs = ctx.hash_host_batch(keys[:3])             # pageable numpy keys, library-made outputs
+        assert [bytes(o) for o in outs] == want[:3]
+        ctx.close()
+
+
 def test_nccl_one_rank_u64_exchange(monkeypatch):
     # the exchange of world > 4 jobs (64-bit sums: acc_export<u64>, ncclUint64 reduce,
     # acc_import_u64), forced on a one-rank communicator with PA_FORCE_X64
