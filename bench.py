@@ -212,9 +212,12 @@ def roofline(info: dict, stages: dict, peaks: dict, steps: int) -> dict:
     issue_peak = 148 * 4 * 32 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
     achieved = ops / (per_launch_ms * 1e-3) / 1e9 if ops else None
     traffic = None
+    ncu_pct = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         traffic = prof.get(name, {}).get("dram_bytes_per_launch")
+        # issue-slot and per-pipe utilisation of that kernel from the committed --set full capture
+        ncu_pct = prof.get(name, {}).get("ncu_pct_of_peak")
     except Exception:
         pass
     share = ms / sum(v[0] for v in stages.values())
@@ -223,7 +226,8 @@ def roofline(info: dict, stages: dict, peaks: dict, steps: int) -> dict:
             "ms_per_launch": per_launch_ms, "share_of_step": share, "peak_source": note,
             "issue_model_peak": issue_peak,
             "issue_model_frac": (achieved / issue_peak) if achieved else None,
-            "measured_lane_ops_per_sm_clk": pipes}
+            "measured_lane_ops_per_sm_clk": pipes,
+            "ncu_pct_of_peak": ncu_pct}
 
 
 # --------------------------------------------------------------------------- CPU oracle

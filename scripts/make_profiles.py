@@ -74,6 +74,12 @@ def full(rep: str, stage: str, tag: str) -> None:
         traffic[stage] = {"kernel": rec.get("Kernel Name"), "dram_bytes_per_launch":
                           mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
                           "dram_read": mb("dram__bytes_read.sum"), "dram_write": mb("dram__bytes_write.sum"),
+                          "ncu_pct_of_peak": {kk: float(rec[mk].split()[0]) for kk, mk in (
+                              ("issue_active", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                              ("pipe_alu", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                              ("pipe_fma", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                              ("pipe_lsu", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                              ("warps_active", "sm__warps_active.avg.pct_of_peak_sustained_active")) if mk in rec},
                           "source": f"profiles/{tag}_{names[0] if len(names) == 1 else 'kernels'}.txt"}
     open(os.path.join(PROF, f"{tag}_{names[0] if len(names) == 1 else 'kernels'}.txt"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
