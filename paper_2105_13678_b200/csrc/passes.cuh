@@ -329,8 +329,11 @@ __device__ __forceinline__ void store_residues_multi(uint32_t *o, uint32_t j0, u
     }
 }
 
+#ifndef PA_PACK_MINB
+#define PA_PACK_MINB 8        // resident CTAs per SM the key pack's register budget is sized for (limbs of <= 6
+#endif                        // words fit 32 registers without spills; wider limbs keep the default budget)
 template <int NW, int NC28 = 0>
-__global__ void __launch_bounds__(kPackT) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
+__global__ void __launch_bounds__(kPackT, ((NW <= 5 || (NW == 6 && NC28 > 0)) ? PA_PACK_MINB : 1)) pack_key_residues(const KeySrc s, const PrimeSet ks, uint32_t P,
                                                           uint32_t wxp, uint32_t *__restrict__ res) {
     PA_TMARK(0x6000 | NW, 0);
     // a tile is kPackL kPackT limbs, kPackL per thread (limbs t + q kPackT): the per-prime
