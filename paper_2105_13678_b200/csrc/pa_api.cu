@@ -1985,17 +1985,30 @@ static bool graphs_enabled(const pa_ctx *c) {
 // copy stream; the pack, both forward passes and the multiply-accumulate of group g start
 // as soon as group g has landed (stream-ordered by events), so the PCIe transfer overlaps
 // the MMH transforms.
-static constexpr int kCopyGroups = 8;
+#ifndef PA_COPY_GROUPS
+#define PA_COPY_GROUPS 8
+#endif
+static constexpr int kCopyGroups = PA_COPY_GROUPS;
 
 // First block of copy group g of G: group sizes fall linearly (weights G, G-1, ..., 1), so the
 // last group -- whose transforms are all that is left to do once the last byte has arrived --
 // is the smallest (C4: 7, 6, 5, 4, 4, 2, 2, 1 blocks).  The H2D copy outruns nothing: the
 // GPU finishes each group's transforms before the next group's bytes land.
+#ifndef PA_COPY_GEOM
+#define PA_COPY_GEOM 0        // 1: group sizes halve (weights 2^(G-1), ..., 2, 1) instead of falling linearly
+#endif
 static uint32_t group_begin(uint32_t nblk, int G, int g) {
+#if PA_COPY_GEOM
+    const uint64_t W = (1ull << G) - 1;
+    uint64_t cum = 0;
+    for (int i = 0; i < g; i++) cum += 1ull << (G - 1 - i);
+    return (uint32_t)((nblk * cum + W / 2) / W);
+#else
     const uint64_t W = (uint64_t)G * (G + 1) / 2;
     uint64_t cum = 0;
     for (int i = 0; i < g; i++) cum += (uint64_t)(G - i);
     return (uint32_t)((nblk * cum + W / 2) / W);
+#endif
 }
 
 static int mg_hash(pa_ctx *c, const uint8_t *key, uint8_t *out, int root, int set, const uint8_t *key_host = nullptr);
