@@ -536,6 +536,11 @@ def test_distinct_contexts_from_concurrent_host_threads():
     threads, each with its own context, stream and key, hash at the same time (ctypes drops the
     GIL during the C calls); every output equals the oracle's, on every repetition."""
     import threading
+    from paper_2105_13678_b200 import _binding as B
+    if B.pa_debug_build():
+        # the bounds-checking build keeps ONE process-wide table of the caller's live key / output
+        # ranges (csrc/debug.cuh), replaced by every call: concurrent calls would trip it
+        pytest.skip("debug build: the user-range table is process-wide")
     shapes = [(100_003, 1024, 5_000, 11), (262_157, 2048, 30_001, 12),
               (300_000, 4096, 4_000, 13), (1 << 20, 1 << 16, 104_858, 14)]
     keys = [key_bytes(n, 0xC0 + i) for i, (n, _, _, _) in enumerate(shapes)]
